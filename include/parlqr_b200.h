@@ -1,0 +1,157 @@
+/*
+ * parlqr_b200 -- C ABI of the B200-native horizon-partitioned Riccati solve.
+ *
+ * Drop-in for the hot path of the reference package `parlqr`
+ * (/root/reference/pkg/src/parlqr), whose Python entry point is
+ *
+ *     parlqr.solve_parallel(problem, J, workers=None, tolerances=...,
+ *                           collect_diagnostics=False, partition=None)
+ *                                                    (parallel.py:422-553)
+ *
+ * Plain pointers and sizes only; no torch types.  All arrays are float64,
+ * row-major, C-contiguous, in the reference's stacked transport layout
+ * (`_stacked_stages`, parallel.py:108,141-149) with a leading batch axis B.
+ * The library never allocates device memory persistently: callers size the
+ * workspace with plq_workspace_bytes() and own every buffer.
+ */
+#ifndef PARLQR_B200_H
+#define PARLQR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLQ_ABI_VERSION 1
+
+/* Return codes of the entry points (launch / argument errors only; numerical
+ * failures are reported per segment in plq_outputs_t.status). */
+#define PLQ_OK 0
+#define PLQ_ERR_ARG (-1)         /* invalid argument (shapes, null pointers, partition) */
+#define PLQ_ERR_CUDA (-2)        /* a CUDA launch or copy failed; see plq_last_error() */
+#define PLQ_ERR_WORKSPACE (-3)   /* workspace smaller than plq_workspace_bytes() */
+
+/* Per-(problem, segment) status values, mapped to the reference exceptions
+ * by the Python host layer (errors.py:8-51):
+ *   0          ok
+ *   1 + t      CholeskyFailure(t), t = segment-local stage (endpoint.py:243-245,
+ *              serial.py:63-66)
+ *   -1         rank-deficient constraint-to-go / leftover feasibility rows:
+ *              the degenerate-partition path (parallel.py:322-384, 452-456) is
+ *              not built on the GPU -> UnsupportedPartition
+ *   -2         LinkSingular (parallel.py:267-271); stored in segment 0's slot */
+#define PLQ_STATUS_OK 0
+#define PLQ_STATUS_DEGENERATE (-1)
+#define PLQ_STATUS_LINK_SINGULAR (-2)
+
+/* One batch of B independent problems sharing (T, n, m) and one partition.
+ * Replaces the (problem, partition, tolerances) arguments of
+ * parlqr.solve_parallel (parallel.py:422-445).  Device pointers. */
+typedef struct plq_problem {
+  int64_t B;                 /* problems in the batch */
+  int32_t T, n, m, J;        /* horizon, state dim, control dim, segments (1 <= J <= T) */
+  int32_t max_seg_len;       /* max(split_times[j+1]-split_times[j]) */
+  const int32_t* split_times;/* J+1 increasing stage indices, 0 .. T (Partition.split_times) */
+  const double* Qxx;         /* (B,T,n,n) symmetric */
+  const double* Qux;         /* (B,T,m,n) */
+  const double* Quu;         /* (B,T,m,m) symmetric */
+  const double* qx1;         /* (B,T,n) */
+  const double* qu1;         /* (B,T,m) */
+  const double* Fx;          /* (B,T,n,n) */
+  const double* Fu;          /* (B,T,n,m) */
+  const double* f1;          /* (B,T,n) */
+  const double* QxxT;        /* (B,n,n) terminal Qxx (TerminalCost) */
+  const double* qx1T;        /* (B,n) terminal qx1 */
+  const double* x_init;      /* (B,n) */
+  double rank_tol;           /* ToleranceSet.rank_tol (problem.py:53) */
+  double feas_tol;           /* ToleranceSet.feas_tol (problem.py:54) */
+} plq_problem_t;
+
+/* Caller-allocated device outputs of one solve (LqrSolution + ParallelDetails,
+ * problem.py:262-280, parallel.py:390-405). */
+typedef struct plq_outputs {
+  double* K;              /* (B,T,m,n)  policies[t].Kx */
+  double* k;              /* (B,T,m)    policies[t].k1 (folded k = Kz z + k1) */
+  double* x;              /* (B,T+1,n)  states */
+  double* u;              /* (B,T,m)    controls */
+  double* lam;            /* (B,T+1,n)  lambdas */
+  double* links;          /* (B,J-1,n)  details.link_points */
+  double* mu_left;        /* (B,J-1,n)  details.mu_left */
+  double* lambda_right;   /* (B,J-1,n)  details.lambda_right */
+  double* vf0;            /* (B,J,3n^2+2n) details.segment_values0: Vxx0,Vzx0,Vzz0,vx10,vz10
+                             (the last, serial segment fills Vxx0 and vx10 only) */
+  double* Kz;             /* (B,T,m,n)  unfolded segment gains (_solve_segment_task "Kz"); may be NULL */
+  double* k1;             /* (B,T,m)    unfolded segment offsets ("k1"); may be NULL */
+  double* objective;      /* (B) */
+  double* kkt_inf;        /* (B) kkt_residual_inf */
+  double* link_mismatch;  /* (B) details.link_mismatch */
+  double* link_residual;  /* (B) details.link_residual */
+  int32_t* status;        /* (B,J) see PLQ_STATUS_* */
+} plq_outputs_t;
+
+/* Library identification. */
+int plq_abi_version(void);
+const char* plq_last_error(void);
+
+/* Workspace for plq_solve_parallel (and the phase entry points below). */
+size_t plq_workspace_bytes(const plq_problem_t* problem);
+
+/* Full partitioned solve of every problem in the batch, stream-ordered:
+ * segment sweeps (replaces _run_tasks/_solve_segment_task, parallel.py:197-240,
+ * endpoint.backward_pass endpoint.py:168-301, serial.backward_pass
+ * serial.py:37-79), link solve (assemble_link_system + LinkSystem.solve,
+ * parallel.py:264-319, endpoint.py:410-438), reconstruction
+ * (parallel.py:478-527) and diagnostics (evaluate_objective, kkt_residual,
+ * problem.py:366-420).  `stream` is a cudaStream_t (NULL = legacy default). */
+int plq_solve_parallel(const plq_problem_t* problem, const plq_outputs_t* out, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* Same solve from HOST buffers (the end-to-end entry a ctypes/cgo binding of
+ * the reference would call): `host_problem` holds host pointers in every
+ * array field (split_times included), `host_out` host destinations (any may
+ * be NULL to skip the copy back).  Copies in, solves, copies out, returns
+ * after the stream is synchronized.  `device_arena` must hold
+ * plq_host_arena_bytes() bytes of device memory. */
+size_t plq_host_arena_bytes(const plq_problem_t* host_problem);
+int plq_solve_parallel_host(const plq_problem_t* host_problem, const plq_outputs_t* host_out, void* device_arena,
+                            size_t arena_bytes, void* stream);
+
+/* Phase entry points for horizon sharding across GPUs (one process per GPU;
+ * the caller exchanges data between phases, e.g. NCCL all-gathers).  The
+ * same `workspace` must be passed to every phase of one solve.
+ *   1. plq_sweep_segments: sweeps of segments [seg_begin, seg_end) of every
+ *      problem -> out->K, Kz/k1 (workspace if NULL), vf0, status.
+ *      [exchange: vf0 rows of all segments]
+ *   2. plq_link_solve: replicated coupling solve from the complete vf0
+ *      -> links, link_residual, status (LinkSingular).
+ *   3. plq_reconstruct_segments: fold, rollout, multipliers, per-segment
+ *      objective / interior-KKT partials for [seg_begin, seg_end) -> k, x, u,
+ *      lam, mu_left, lambda_right, partials[b][j][0..1].
+ *      [exchange: mu_left, lambda_right]
+ *   4. plq_boundary_segments: KKT rows of the link stages of [seg_begin,
+ *      seg_end) (need the right neighbour's lambda) -> partials[b][j][2].
+ *      [exchange: partials]
+ *   5. plq_finalize: fixed-order reduction of the complete `partials`
+ *      (B,J,3) into objective, kkt_inf and link_mismatch. */
+int plq_sweep_segments(const plq_problem_t* problem, const plq_outputs_t* out, int32_t seg_begin, int32_t seg_end,
+                       void* workspace, size_t workspace_bytes, void* stream);
+int plq_link_solve(const plq_problem_t* problem, const plq_outputs_t* out, void* workspace, size_t workspace_bytes,
+                   void* stream);
+int plq_reconstruct_segments(const plq_problem_t* problem, const plq_outputs_t* out, int32_t seg_begin,
+                             int32_t seg_end, double* partials, void* workspace, size_t workspace_bytes, void* stream);
+int plq_boundary_segments(const plq_problem_t* problem, const plq_outputs_t* out, int32_t seg_begin,
+                          int32_t seg_end, double* partials, void* workspace, size_t workspace_bytes, void* stream);
+int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const double* partials, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* Number of kernel launches the last plq_solve_parallel / phase call issued
+ * on this thread (evidence for bench.py's gpu_launches). */
+int plq_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARLQR_B200_H */

@@ -1,0 +1,25 @@
+"""B200-native horizon-partitioned Riccati solve (arXiv 1809.06360).
+
+Drop-in for the hot path of the reference package ``parlqr``:
+``solve_parallel`` keeps ``parlqr.solve_parallel``'s signature, partition
+rules, error contract and result types, and runs on hand-written sm_100a
+CUDA kernels (``libparlqr_b200.so``, C ABI in ``include/parlqr_b200.h``).
+"""
+
+from .errors import (CholeskyFailure, FactorizationFailure, Infeasible, LinkSingular,
+                     SingularKkt, SolverError, UnsupportedPartition)
+from .problem import (DEFAULT_TOLERANCES, AffinePolicy, LqrProblem, LqrSolution, StageCost,
+                      StageDynamics, TerminalCost, ToleranceSet)
+from .parallel import (BatchSolver, HostSolver, ParallelDetails, Partition, default_workers,
+                       make_partition, solve_parallel, solve_parallel_batch, solve_parallel_host,
+                       stack_problem)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AffinePolicy", "BatchSolver", "CholeskyFailure", "DEFAULT_TOLERANCES", "FactorizationFailure",
+    "HostSolver", "Infeasible", "LinkSingular", "LqrProblem", "LqrSolution", "ParallelDetails",
+    "Partition", "SingularKkt", "SolverError", "StageCost", "StageDynamics", "TerminalCost",
+    "ToleranceSet", "UnsupportedPartition", "default_workers", "make_partition", "solve_parallel",
+    "solve_parallel_batch", "solve_parallel_host", "stack_problem",
+]

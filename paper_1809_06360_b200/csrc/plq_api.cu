@@ -1,0 +1,392 @@
+// C-ABI layer (include/parlqr_b200.h): argument checks, workspace carving,
+// and the stream-ordered phase sequence of one partitioned solve.
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "plq_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+int fail(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+
+int cuda_fail(const char* where) {
+  const cudaError_t e = cudaGetLastError();
+  snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+  return PLQ_ERR_CUDA;
+}
+
+inline size_t up2(size_t x) { return (x + 1) & ~size_t(1); }
+
+struct Plan {
+  plq::SweepLayout lay;
+  int threads = 0;
+  size_t smem = 0;
+  int grid_max = 0;
+  size_t off_Kz = 0, off_k1 = 0, off_gh = 0, off_xend = 0, off_part = 0, off_gs = 0, off_link = 0;
+  size_t total_doubles = 0;
+};
+
+int check_problem(const plq_problem_t* p) {
+  if (!p) return fail(PLQ_ERR_ARG, "null problem");
+  if (p->B < 1 || p->T < 1 || p->n < 1 || p->m < 1) return fail(PLQ_ERR_ARG, "B, T, n, m must be >= 1");
+  if (p->J < 1 || p->J > p->T) return fail(PLQ_ERR_ARG, "J must be in [1, T]");
+  if (p->n > 128 || p->m > 128) return fail(PLQ_ERR_ARG, "n and m are limited to 128");
+  if (p->max_seg_len < 1 || p->max_seg_len > p->T) return fail(PLQ_ERR_ARG, "bad max_seg_len");
+  if (!p->split_times || !p->Qxx || !p->Qux || !p->Quu || !p->qx1 || !p->qu1 || !p->Fx || !p->Fu || !p->f1 ||
+      !p->QxxT || !p->qx1T || !p->x_init)
+    return fail(PLQ_ERR_ARG, "null problem array");
+  return PLQ_OK;
+}
+
+Plan make_plan(const plq_problem_t* p) {
+  Plan P;
+  const int64_t B = p->B, T = p->T, n = p->n, m = p->m, J = p->J;
+  P.threads = plq::sweep_threads(p->n);
+  const size_t budget = 200 * 1024;
+  P.lay = plq::plan_sweep(p->n, p->m, P.threads, budget);
+  P.smem = (size_t)P.lay.smem_doubles * sizeof(double);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = plq::sweep_max_blocks_per_sm(P.threads, P.smem);
+  if (per_sm < 1) per_sm = 1;
+  P.grid_max = sms * per_sm;
+  size_t off = 0;
+  P.off_Kz = off;
+  off += up2(B * T * m * n);
+  P.off_k1 = off;
+  off += up2(B * T * m);
+  P.off_gh = off;
+  off += up2(B * T * (n + m));
+  P.off_xend = off;
+  off += up2(B * J * n);
+  P.off_part = off;
+  off += up2(B * J * 3);
+  P.off_gs = off;
+  off += up2((size_t)P.grid_max * P.lay.gmem_doubles);
+  P.off_link = off;
+  off += up2(plq::link_workspace_doubles(B, p->J, p->n));
+  P.total_doubles = off;
+  return P;
+}
+
+struct Ctx {
+  Plan P;
+  double* ws;
+  double* Kz;
+  double* k1;
+  cudaStream_t s;
+};
+
+int setup(const plq_problem_t* p, const plq_outputs_t* o, void* ws, size_t bytes, void* stream, Ctx* c) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (!o) return fail(PLQ_ERR_ARG, "null outputs");
+  if (!ws) return fail(PLQ_ERR_ARG, "null workspace");
+  c->P = make_plan(p);
+  if (bytes < c->P.total_doubles * sizeof(double)) return fail(PLQ_ERR_WORKSPACE, "workspace too small");
+  c->ws = static_cast<double*>(ws);
+  c->Kz = o->Kz ? o->Kz : c->ws + c->P.off_Kz;
+  c->k1 = o->k1 ? o->k1 : c->ws + c->P.off_k1;
+  c->s = static_cast<cudaStream_t>(stream);
+  return PLQ_OK;
+}
+
+int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, int j1) {
+  if (!o->K || !o->vf0 || !o->status) return fail(PLQ_ERR_ARG, "null sweep output");
+  if (j0 < 0 || j1 > p->J || j0 >= j1) return fail(PLQ_ERR_ARG, "bad segment range");
+  plq::SweepArgs a{};
+  a.p = *p;
+  a.Kx = o->K;
+  a.Kz = c.Kz;
+  a.k1 = c.k1;
+  a.vf0 = o->vf0;
+  a.status = o->status;
+  a.gscratch = c.ws + c.P.off_gs;
+  a.lay = c.P.lay;
+  a.seg_begin = j0;
+  a.seg_end = j1;
+  const int64_t tasks = p->B * (int64_t)(j1 - j0);
+  const int grid = (int)std::min<int64_t>(tasks, c.P.grid_max);
+  if (plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s)) return cuda_fail("sweep launch");
+  ++g_launches;
+  return PLQ_OK;
+}
+
+int phase_link(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c) {
+  if (!o->links || !o->link_residual || !o->vf0 || !o->status) return fail(PLQ_ERR_ARG, "null link output");
+  int nl = 0;
+  if (plq::launch_link_solve(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s, &nl))
+    return cuda_fail("link launch");
+  g_launches += nl;
+  return PLQ_OK;
+}
+
+plq::ReconArgs recon_args(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, int j1, double* part) {
+  plq::ReconArgs a{};
+  a.p = *p;
+  a.Kx = o->K;
+  a.Kz = c.Kz;
+  a.k1 = c.k1;
+  a.vf0 = o->vf0;
+  a.links = o->links;
+  a.k = o->k;
+  a.x = o->x;
+  a.u = o->u;
+  a.lam = o->lam;
+  a.mu_left = o->mu_left;
+  a.lambda_right = o->lambda_right;
+  a.gh = c.ws + c.P.off_gh;
+  a.xend = c.ws + c.P.off_xend;
+  a.part = part ? part : c.ws + c.P.off_part;
+  a.seg_begin = j0;
+  a.seg_end = j1;
+  return a;
+}
+
+int check_recon_out(const plq_outputs_t* o) {
+  if (!o->K || !o->k || !o->x || !o->u || !o->lam || !o->links || !o->mu_left || !o->lambda_right || !o->vf0)
+    return fail(PLQ_ERR_ARG, "null reconstruction output");
+  return PLQ_OK;
+}
+
+int phase_recon(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, int j1, double* part) {
+  int rc = check_recon_out(o);
+  if (rc) return rc;
+  if (j0 < 0 || j1 > p->J || j0 >= j1) return fail(PLQ_ERR_ARG, "bad segment range");
+  if (plq::launch_recon(recon_args(p, o, c, j0, j1, part), c.s)) return cuda_fail("recon launch");
+  ++g_launches;
+  return PLQ_OK;
+}
+
+int phase_boundary(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, int j1, double* part) {
+  int rc = check_recon_out(o);
+  if (rc) return rc;
+  if (j0 < 0 || j1 > p->J || j0 >= j1) return fail(PLQ_ERR_ARG, "bad segment range");
+  if (plq::launch_boundary(recon_args(p, o, c, j0, j1, part), nullptr, c.s)) return cuda_fail("boundary launch");
+  ++g_launches;
+  return PLQ_OK;
+}
+
+int phase_finalize(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, const double* part) {
+  if (!o->objective || !o->kkt_inf || !o->link_mismatch || !o->mu_left || !o->lambda_right)
+    return fail(PLQ_ERR_ARG, "null finalize output");
+  if (plq::launch_finalize(*p, part ? part : c.ws + c.P.off_part, nullptr, o->mu_left, o->lambda_right, nullptr,
+                           o->objective, o->kkt_inf, o->link_mismatch, nullptr, c.s))
+    return cuda_fail("finalize launch");
+  ++g_launches;
+  return PLQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int plq_abi_version(void) { return PLQ_ABI_VERSION; }
+
+const char* plq_last_error(void) { return g_err; }
+
+int plq_last_launch_count(void) { return g_launches; }
+
+size_t plq_workspace_bytes(const plq_problem_t* problem) {
+  if (check_problem(problem)) return 0;
+  return make_plan(problem).total_doubles * sizeof(double);
+}
+
+int plq_solve_parallel(const plq_problem_t* problem, const plq_outputs_t* out, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, out, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  const int J = problem->J;
+  if ((rc = phase_sweep(problem, out, c, 0, J))) return rc;
+  if ((rc = phase_link(problem, out, c))) return rc;
+  if ((rc = phase_recon(problem, out, c, 0, J, nullptr))) return rc;
+  if ((rc = phase_boundary(problem, out, c, 0, J, nullptr))) return rc;
+  if ((rc = phase_finalize(problem, out, c, nullptr))) return rc;
+  return PLQ_OK;
+}
+
+int plq_sweep_segments(const plq_problem_t* problem, const plq_outputs_t* out, int32_t seg_begin, int32_t seg_end,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, out, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  return phase_sweep(problem, out, c, seg_begin, seg_end);
+}
+
+int plq_link_solve(const plq_problem_t* problem, const plq_outputs_t* out, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, out, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  return phase_link(problem, out, c);
+}
+
+int plq_reconstruct_segments(const plq_problem_t* problem, const plq_outputs_t* out, int32_t seg_begin,
+                             int32_t seg_end, double* partials, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, out, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  return phase_recon(problem, out, c, seg_begin, seg_end, partials);
+}
+
+int plq_boundary_segments(const plq_problem_t* problem, const plq_outputs_t* out, int32_t seg_begin,
+                          int32_t seg_end, double* partials, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, out, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  return phase_boundary(problem, out, c, seg_begin, seg_end, partials);
+}
+
+int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const double* partials, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, out, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  return phase_finalize(problem, out, c, partials);
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer entry
+
+namespace {
+
+void host_sizes(const plq_problem_t* p, size_t* in_sz, size_t* out_sz) {
+  const size_t B = p->B, T = p->T, n = p->n, m = p->m, J = p->J;
+  // order: split_times(int32), Qxx, Qux, Quu, qx1, qu1, Fx, Fu, f1, QxxT, qx1T, x_init (bytes)
+  in_sz[0] = (J + 1) * sizeof(int32_t);
+  in_sz[1] = B * T * n * n * 8;
+  in_sz[2] = B * T * m * n * 8;
+  in_sz[3] = B * T * m * m * 8;
+  in_sz[4] = B * T * n * 8;
+  in_sz[5] = B * T * m * 8;
+  in_sz[6] = B * T * n * n * 8;
+  in_sz[7] = B * T * n * m * 8;
+  in_sz[8] = B * T * n * 8;
+  in_sz[9] = B * n * n * 8;
+  in_sz[10] = B * n * 8;
+  in_sz[11] = B * n * 8;
+  // order: K, k, x, u, lam, links, mu_left, lambda_right, vf0, Kz, k1, objective, kkt, mismatch, link_res, status
+  out_sz[0] = B * T * m * n * 8;
+  out_sz[1] = B * T * m * 8;
+  out_sz[2] = B * (T + 1) * n * 8;
+  out_sz[3] = B * T * m * 8;
+  out_sz[4] = B * (T + 1) * n * 8;
+  out_sz[5] = B * (J - 1) * n * 8;
+  out_sz[6] = B * (J - 1) * n * 8;
+  out_sz[7] = B * (J - 1) * n * 8;
+  out_sz[8] = B * J * (3 * n * n + 2 * n) * 8;
+  out_sz[9] = B * T * m * n * 8;
+  out_sz[10] = B * T * m * 8;
+  out_sz[11] = B * 8;
+  out_sz[12] = B * 8;
+  out_sz[13] = B * 8;
+  out_sz[14] = B * 8;
+  out_sz[15] = B * J * sizeof(int32_t);
+}
+
+inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+size_t plq_host_arena_bytes(const plq_problem_t* hp) {
+  if (check_problem(hp)) return 0;
+  size_t in_sz[12], out_sz[16], total = 0;
+  host_sizes(hp, in_sz, out_sz);
+  for (size_t s : in_sz) total += up256(s);
+  for (size_t s : out_sz) total += up256(s);
+  return total + up256(plq_workspace_bytes(hp));
+}
+
+int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, void* arena, size_t arena_bytes,
+                            void* stream) {
+  int rc = check_problem(hp);
+  if (rc) return rc;
+  if (!ho || !arena) return fail(PLQ_ERR_ARG, "null outputs or arena");
+  const size_t need = plq_host_arena_bytes(hp);
+  if (arena_bytes < need) return fail(PLQ_ERR_WORKSPACE, "arena too small");
+  // partition sanity on the host copy (parallel.py:434-440)
+  for (int j = 0; j < hp->J; ++j)
+    if (hp->split_times[j + 1] <= hp->split_times[j]) return fail(PLQ_ERR_ARG, "split times must be increasing");
+  if (hp->split_times[0] != 0 || hp->split_times[hp->J] != hp->T)
+    return fail(PLQ_ERR_ARG, "partition does not cover the horizon");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  size_t in_sz[12], out_sz[16];
+  host_sizes(hp, in_sz, out_sz);
+  char* cur = static_cast<char*>(arena);
+  const void* hin[12] = {hp->split_times, hp->Qxx, hp->Qux, hp->Quu, hp->qx1, hp->qu1,
+                         hp->Fx, hp->Fu, hp->f1, hp->QxxT, hp->qx1T, hp->x_init};
+  void* din[12];
+  for (int i = 0; i < 12; ++i) {
+    din[i] = cur;
+    cur += up256(in_sz[i]);
+    if (cudaMemcpyAsync(din[i], hin[i], in_sz[i], cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return cuda_fail("H2D copy");
+  }
+  void* dout[16];
+  for (int i = 0; i < 16; ++i) {
+    dout[i] = cur;
+    cur += up256(out_sz[i]);
+  }
+  plq_problem_t dp = *hp;
+  dp.split_times = static_cast<const int32_t*>(din[0]);
+  dp.Qxx = static_cast<const double*>(din[1]);
+  dp.Qux = static_cast<const double*>(din[2]);
+  dp.Quu = static_cast<const double*>(din[3]);
+  dp.qx1 = static_cast<const double*>(din[4]);
+  dp.qu1 = static_cast<const double*>(din[5]);
+  dp.Fx = static_cast<const double*>(din[6]);
+  dp.Fu = static_cast<const double*>(din[7]);
+  dp.f1 = static_cast<const double*>(din[8]);
+  dp.QxxT = static_cast<const double*>(din[9]);
+  dp.qx1T = static_cast<const double*>(din[10]);
+  dp.x_init = static_cast<const double*>(din[11]);
+  plq_outputs_t dout_s;
+  dout_s.K = (double*)dout[0];
+  dout_s.k = (double*)dout[1];
+  dout_s.x = (double*)dout[2];
+  dout_s.u = (double*)dout[3];
+  dout_s.lam = (double*)dout[4];
+  dout_s.links = (double*)dout[5];
+  dout_s.mu_left = (double*)dout[6];
+  dout_s.lambda_right = (double*)dout[7];
+  dout_s.vf0 = (double*)dout[8];
+  dout_s.Kz = (double*)dout[9];
+  dout_s.k1 = (double*)dout[10];
+  dout_s.objective = (double*)dout[11];
+  dout_s.kkt_inf = (double*)dout[12];
+  dout_s.link_mismatch = (double*)dout[13];
+  dout_s.link_residual = (double*)dout[14];
+  dout_s.status = (int32_t*)dout[15];
+  void* wsp = cur;
+  rc = plq_solve_parallel(&dp, &dout_s, wsp, plq_workspace_bytes(hp), s);
+  if (rc) return rc;
+  void* hout[16] = {ho->K, ho->k, ho->x, ho->u, ho->lam, ho->links, ho->mu_left, ho->lambda_right,
+                    ho->vf0, ho->Kz, ho->k1, ho->objective, ho->kkt_inf, ho->link_mismatch, ho->link_residual,
+                    ho->status};
+  for (int i = 0; i < 16; ++i) {
+    if (!hout[i]) continue;
+    if (cudaMemcpyAsync(hout[i], dout[i], out_sz[i], cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return cuda_fail("D2H copy");
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail("stream sync");
+  return PLQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// Internal (non-ABI) declarations shared by the kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/parlqr_b200.h"
+
+namespace plq {
+
+// Per-CTA scratch buffers of the segment sweep.  Each one is placed in
+// shared memory or in a per-CTA slice of global scratch by plan_sweep().
+enum SweepBuf {
+  SB_V = 0,   // [Vxx; Vzx; Vzz] (3n x n) then vx1 (n), vz1 (n)
+  SB_IN,      // stage inputs: F=[Fx|Fu|f1] (n x (n+m+1)), Qxx, Qux, Quu, qx1, qu1
+  SB_PGY,     // P, G, Y (each m x W, W = 2n+1)
+  SB_MUU,     // Muu (m x m) then its Cholesky factor (m x m)
+  SB_MISC,    // tau (m), rdiag (m), reduction scratch (32), flags
+  SB_VF,      // Vxx*F (n x (n+m+1)); reused as the N = Hx*F temp in tail stages
+  SB_Z,       // Vzx*F (n x (n+m+1)) = [Mzx | Mzu | Vzx f1 + vz1]
+  SB_MX,      // [Mxx | mx1] (n x (n+1))
+  SB_H,       // constraint rows [Hx | Hz | h1] (n x W)
+  SB_WIDE,    // mixed-branch scratch (only when n % m != 0)
+  SB_COUNT
+};
+
+struct SweepLayout {
+  int64_t off[SB_COUNT];     // offset in doubles within its space
+  int in_smem[SB_COUNT];
+  int64_t smem_doubles;
+  int64_t gmem_doubles;      // per CTA
+};
+
+struct SweepArgs {
+  plq_problem_t p;
+  double* Kx;      // (B,T,m,n)
+  double* Kz;      // (B,T,m,n)
+  double* k1;      // (B,T,m)
+  double* vf0;     // (B,J,3n^2+2n)
+  int32_t* status; // (B,J)
+  double* gscratch;
+  SweepLayout lay;
+  int seg_begin, seg_end;  // segment range [seg_begin, seg_end) of every problem
+};
+
+struct ReconArgs {
+  plq_problem_t p;
+  const double* Kx;
+  const double* Kz;
+  const double* k1;
+  const double* vf0;
+  const double* links;   // (B,J-1,n)
+  double* k;             // (B,T,m)
+  double* x;             // (B,T+1,n)
+  double* u;             // (B,T,m)
+  double* lam;           // (B,T+1,n)
+  double* mu_left;       // (B,J-1,n)
+  double* lambda_right;  // (B,J-1,n)
+  double* gh;            // (B,T,n+m) per-stage g = Qxx x + Qux' u + qx1, h = Qux x + Quu u + qu1
+  double* xend;          // (B,J,n) rollout end state of each segment
+  double* part;          // (B,J,3) objective partial, interior KKT, link-stage KKT
+  int seg_begin, seg_end;
+};
+
+int launch_sweep(const SweepArgs& a, int grid, int threads, size_t smem, cudaStream_t s);
+int sweep_threads(int n);
+int sweep_max_blocks_per_sm(int threads, size_t smem);
+SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget);
+
+int launch_recon(const ReconArgs& a, cudaStream_t s);
+int launch_boundary(const ReconArgs& a, double* bpart, cudaStream_t s);
+int launch_finalize(const plq_problem_t& p, const double* part, const double* bpart, const double* mu_left,
+                    const double* lambda_right, const double* link_res, double* objective, double* kkt,
+                    double* mismatch, double* link_residual, cudaStream_t s);
+
+// Link (coupling) solve by block cyclic reduction.
+size_t link_workspace_doubles(int64_t B, int J, int n);
+int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
+                      int32_t* status, double* ws, cudaStream_t s, int* launches);
+
+}  // namespace plq

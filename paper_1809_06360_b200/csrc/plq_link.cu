@@ -1,0 +1,327 @@
+// K2: the link-point coupling solve.
+//
+// The reference assembles the multiplier-matching equations over the J-1
+// interior links (parallel.py:286-319) and solves the SPD block-tridiagonal
+// system (-diag, -sub) x = rhs by sequential block Cholesky
+// (LinkSystem.solve parallel.py:264-283 -> endpoint.solve_block_tridiagonal
+// endpoint.py:410-438).  A J-1 = 1023-deep sequential chain is the GPU's
+// sequential-depth risk, so here it is solved by block cyclic reduction:
+// each level eliminates the odd blocks in parallel (one CTA each), leaving a
+// half-size SPD block-tridiagonal system on the even blocks; log2(J) levels
+// down, back-substitution climbs up again.  Per eliminated block i with
+// Cholesky D_i = L L' and W = L^{-1} [A(i,i-1) | A(i,i+1) | b_i]:
+//   D_{i-1} -= W_L'W_L,  D_{i+1} -= W_R'W_R,  A'(i+1,i-1) = -W_R'W_L,
+//   b_{i-1} -= W_L'W_b,  b_{i+1} -= W_R'W_b,  x_i = L^{-T}(W_b - W_L x_{i-1} - W_R x_{i+1}).
+// A pivot block that is not positive-definite raises LinkSingular, as the
+// reference does (parallel.py:267-271).
+#include "plq_device.cuh"
+#include "plq_internal.h"
+
+#include <vector>
+
+namespace plq {
+
+namespace {
+
+struct LinkLevel {
+  double* D;     // (B,K,n,n)   SPD diagonal blocks
+  double* S;     // (B,K-1,n,n) S[i] = A(i+1,i)
+  double* rhs;   // (B,K,n)
+  double* x;     // (B,K,n)     solution of this level's system
+  double* Lc;    // (B,E,n,n)   Cholesky factors of eliminated blocks
+  double* Wm;    // (B,E,n,2n+1)
+  double* CL;    // (B,E,n,n)
+  double* CR;    // (B,E,n,n)
+  double* X;     // (B,E,n,n)
+  double* cL;    // (B,E,n)
+  double* cR;    // (B,E,n)
+  int K, E, top;
+};
+
+struct LinkPlan {
+  std::vector<LinkLevel> lv;
+  double* rpart;   // (B, K0) link-residual partials
+  size_t doubles;
+};
+
+LinkPlan plan_link(int64_t B, int J, int n, double* base) {
+  LinkPlan P;
+  P.rpart = nullptr;
+  P.doubles = 0;
+  if (J < 2) return P;   // a single segment has no links
+  const int64_t nn = (int64_t)n * n, w = 2 * n + 1;
+  size_t off = 0;
+  auto take = [&](int64_t count) {
+    double* p = base ? base + off : nullptr;
+    off += (size_t)((count + 1) & ~1LL);
+    return p;
+  };
+  int K = J - 1;
+  while (true) {
+    LinkLevel L{};
+    L.K = K;
+    L.top = (K == 1);
+    L.E = L.top ? 1 : K / 2;
+    L.D = take(B * K * nn);
+    L.S = take(B * (K > 1 ? K - 1 : 0) * nn);
+    L.rhs = take(B * K * n);
+    L.x = take(B * K * n);
+    L.Lc = take(B * L.E * nn);
+    L.Wm = take(B * L.E * n * w);
+    L.CL = take(B * L.E * nn);
+    L.CR = take(B * L.E * nn);
+    L.X = take(B * L.E * nn);
+    L.cL = take(B * L.E * n);
+    L.cR = take(B * L.E * n);
+    P.lv.push_back(L);
+    if (L.top) break;
+    K = (K + 1) / 2;
+  }
+  P.rpart = take(B * (J - 1));
+  P.doubles = off;
+  return P;
+}
+
+// level-0 system from the segment-start value blocks (parallel.py:286-319):
+// D_i = Vzz0_i + Vxx0_{i+1},  A(i+1,i) = Vzx0_{i+1},
+// b_i = -vz1_i - vx1_{i+1} (- Vzx0_0 x_init for i = 0).
+__global__ void link_assemble0(plq_problem_t p, const double* vf0, LinkLevel L) {
+  const int n = p.n, J = p.J, K = L.K;
+  const int64_t nn = (int64_t)n * n, vsz = 3 * nn + 2 * n;
+  const int64_t b = blockIdx.x / K;
+  const int i = blockIdx.x % K;
+  const double* left = vf0 + (b * J + i) * vsz;
+  const double* right = vf0 + (b * J + i + 1) * vsz;
+  double* D = L.D + (b * K + i) * nn;
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) D[idx] = left[2 * nn + idx] + right[idx];
+  if (i + 1 < K) {
+    double* S = L.S + (b * (K - 1) + i) * nn;
+    const double* rr = vf0 + (b * J + i + 1) * vsz;   // segment i+1 is an endpoint segment here
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) S[idx] = rr[nn + idx];
+  }
+  double* rhs = L.rhs + (b * K + i) * n;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    double v = -left[3 * nn + n + r] + -right[3 * nn + r];
+    if (i == 0) {
+      double s = 0.0;
+      for (int c = 0; c < n; ++c) s += left[nn + r * n + c] * p.x_init[b * n + c];
+      v += -s;
+    }
+    rhs[r] = v;
+  }
+}
+
+__device__ __forceinline__ void flag_singular(plq_problem_t& p, int32_t* status, int64_t b) {
+  if (threadIdx.x == 0 && status[b * p.J] == 0) status[b * p.J] = PLQ_STATUS_LINK_SINGULAR;
+}
+
+// eliminate the odd blocks of one level (or the single top block)
+__global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
+  __shared__ int flag;
+  const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t b = blockIdx.x / E;
+  const int o = blockIdx.x % E;
+  const int i = L.top ? 0 : 2 * o + 1;
+  double* Lc = L.Lc + (b * E + o) * nn;
+  double* Wm = L.Wm + (b * E + o) * n * w;
+  const double* D = L.D + (b * K + i) * nn;
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[idx] = D[idx];
+  const bool has_l = i >= 1, has_r = i + 1 < K;
+  const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;   // A(i,i-1)
+  const double* Sr = has_r ? L.S + (b * (K - 1) + i) * nn : nullptr;         // A(i+1,i) -> A(i,i+1) = Sr'
+  for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) {
+    const int r = idx / w, c = idx % w;
+    double v;
+    if (c < n)
+      v = has_l ? Sl[r * n + c] : 0.0;
+    else if (c < 2 * n)
+      v = has_r ? Sr[(c - n) * n + r] : 0.0;
+    else
+      v = L.rhs[(b * K + i) * n + r];
+    Wm[idx] = v;
+  }
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  if (!cta_cholesky(Lc, n, n, &flag)) {
+    flag_singular(p, status, b);
+    return;
+  }
+  cta_trsm_lower(Lc, n, n, Wm, w, w);
+  if (L.top) return;
+  double* CL = L.CL + (b * E + o) * nn;
+  double* CR = L.CR + (b * E + o) * nn;
+  double* X = L.X + (b * E + o) * nn;
+  double* cL = L.cL + (b * E + o) * n;
+  double* cR = L.cR + (b * E + o) * n;
+  cta_gemm<true, false, 1, 1>(2 * n, w, n, Wm, w, Wm, w, [&](int r, int c, double acc) {
+    if (r < n) {
+      if (c < n)
+        CL[r * n + c] = acc;
+      else if (c == 2 * n)
+        cL[r] = acc;
+    } else {
+      const int rr = r - n;
+      if (c < n)
+        X[rr * n + c] = acc;
+      else if (c < 2 * n)
+        CR[rr * n + (c - n)] = acc;
+      else
+        cR[rr] = acc;
+    }
+  });
+}
+
+// next level's system on the even blocks
+__global__ void link_assemble_next(plq_problem_t p, LinkLevel L, LinkLevel N) {
+  const int n = p.n, K = L.K, E = L.E, K2 = N.K;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t b = blockIdx.x / K2;
+  const int e2 = blockIdx.x % K2;
+  const int e = 2 * e2;
+  const bool has_l = e >= 2, has_r = e + 1 < K;
+  const double* D = L.D + (b * K + e) * nn;
+  double* Dn = N.D + (b * K2 + e2) * nn;
+  const double* CRl = has_l ? L.CR + (b * E + (e2 - 1)) * nn : nullptr;
+  const double* CLr = has_r ? L.CL + (b * E + e2) * nn : nullptr;
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+    double v = D[idx];
+    if (has_l) v -= CRl[idx];
+    if (has_r) v -= CLr[idx];
+    Dn[idx] = v;
+  }
+  if (e2 >= 1) {
+    const double* X = L.X + (b * E + (e2 - 1)) * nn;
+    double* Sn = N.S + (b * (K2 - 1) + (e2 - 1)) * nn;
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Sn[idx] = -X[idx];
+  }
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    double v = L.rhs[(b * K + e) * n + r];
+    if (has_l) v -= L.cR[(b * E + (e2 - 1)) * n + r];
+    if (has_r) v -= L.cL[(b * E + e2) * n + r];
+    N.rhs[(b * K2 + e2) * n + r] = v;
+  }
+}
+
+// back-substitution of one level: x_i = L^{-T} (W_b - W_L x_{i-1} - W_R x_{i+1})
+// for eliminated blocks, copy from the coarser level for kept blocks.
+__global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_coarse) {
+  extern __shared__ __align__(16) double v[];
+  const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t b = blockIdx.x / K;
+  const int i = blockIdx.x % K;
+  double* x = L.x + (b * K + i) * n;
+  const bool elim = L.top ? true : (i & 1);
+  if (!elim) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = C.x[(b * C.K + i / 2) * n + r];
+    return;
+  }
+  const int o = L.top ? 0 : (i - 1) / 2;
+  const double* Lc = L.Lc + (b * E + o) * nn;
+  const double* Wm = L.Wm + (b * E + o) * n * w;
+  const bool has_l = !L.top && i >= 1, has_r = !L.top && i + 1 < K;
+  const double* xl = has_l ? C.x + (b * C.K + (i - 1) / 2) * n : nullptr;
+  const double* xr = has_r ? C.x + (b * C.K + (i + 1) / 2) * n : nullptr;
+  (void)has_coarse;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    double s = Wm[r * w + 2 * n];
+    double t = 0.0;
+    if (has_l)
+      for (int c = 0; c < n; ++c) t += Wm[r * w + c] * xl[c];
+    if (has_r)
+      for (int c = 0; c < n; ++c) t += Wm[r * w + n + c] * xr[c];
+    v[r] = s - t;
+  }
+  __syncthreads();
+  // x = L^{-T} v : column-oriented back substitution
+  for (int r = n - 1; r >= 0; --r) {
+    if (threadIdx.x == 0) v[r] /= Lc[r * n + r];
+    __syncthreads();
+    const double xr_ = v[r];
+    for (int k = threadIdx.x; k < r; k += blockDim.x) v[k] -= Lc[r * n + k] * xr_;
+    __syncthreads();
+  }
+  for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = v[r];
+}
+
+// residual of the level-0 equations at the solved links (parallel.py:273-282)
+__global__ void link_residual_part(plq_problem_t p, LinkLevel L, double* rpart) {
+  __shared__ double red[32];
+  const int n = p.n, K = L.K;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t b = blockIdx.x / K;
+  const int i = blockIdx.x % K;
+  const double* D = L.D + (b * K + i) * nn;
+  const double* x = L.x + b * K * n;
+  double worst = 0.0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) s += D[r * n + c] * x[i * n + c];
+    if (i >= 1) {
+      const double* S = L.S + (b * (K - 1) + (i - 1)) * nn;
+      for (int c = 0; c < n; ++c) s += S[r * n + c] * x[(i - 1) * n + c];
+    }
+    if (i + 1 < K) {
+      const double* S = L.S + (b * (K - 1) + i) * nn;
+      for (int c = 0; c < n; ++c) s += S[c * n + r] * x[(i + 1) * n + c];
+    }
+    worst = fmax(worst, fabs(s - L.rhs[(b * K + i) * n + r]));
+  }
+  worst = block_max(worst, red);
+  if (threadIdx.x == 0) rpart[b * K + i] = worst;
+}
+
+__global__ void link_residual_reduce(plq_problem_t p, const double* rpart, const double* x0, double* links,
+                                     double* link_residual) {
+  const int64_t b = blockIdx.x;
+  const int K = p.J - 1, n = p.n;
+  for (int64_t idx = threadIdx.x; idx < (int64_t)K * n; idx += blockDim.x) links[b * K * n + idx] = x0[b * K * n + idx];
+  if (threadIdx.x == 0) {
+    double w = 0.0;
+    for (int i = 0; i < K; ++i) w = fmax(w, rpart[b * K + i]);
+    link_residual[b] = w;
+  }
+}
+
+int link_threads(int n) {
+  if (n <= 16) return 32;
+  if (n <= 32) return 128;
+  return 256;
+}
+
+}  // namespace
+
+size_t link_workspace_doubles(int64_t B, int J, int n) { return plan_link(B, J, n, nullptr).doubles; }
+
+int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
+                      int32_t* status, double* ws, cudaStream_t s, int* launches) {
+  if (p.J < 2) return 0;
+  LinkPlan P = plan_link(p.B, p.J, p.n, ws);
+  const int threads = link_threads(p.n);
+  const unsigned B = (unsigned)p.B;
+  int nl = 0;
+  link_assemble0<<<B * P.lv[0].K, threads, 0, s>>>(p, vf0, P.lv[0]);
+  ++nl;
+  for (size_t l = 0; l < P.lv.size(); ++l) {
+    link_eliminate<<<B * P.lv[l].E, threads, 0, s>>>(p, P.lv[l], status);
+    ++nl;
+    if (!P.lv[l].top) {
+      link_assemble_next<<<B * P.lv[l + 1].K, threads, 0, s>>>(p, P.lv[l], P.lv[l + 1]);
+      ++nl;
+    }
+  }
+  for (int l = (int)P.lv.size() - 1; l >= 0; --l) {
+    const LinkLevel& C = P.lv[l + 1 < (int)P.lv.size() ? l + 1 : l];
+    link_backsub<<<B * P.lv[l].K, threads, sizeof(double) * (p.n + 2), s>>>(p, P.lv[l], C,
+                                                                              l + 1 < (int)P.lv.size());
+    ++nl;
+  }
+  link_residual_part<<<B * P.lv[0].K, threads, 0, s>>>(p, P.lv[0], P.rpart);
+  link_residual_reduce<<<B, 128, 0, s>>>(p, P.rpart, P.lv[0].x, links, link_residual);
+  nl += 2;
+  if (launches) *launches += nl;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace plq

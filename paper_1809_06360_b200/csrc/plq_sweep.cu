@@ -1,0 +1,483 @@
+// K1: per-segment backward sweeps of the horizon-partitioned Riccati solve.
+//
+// One CTA owns one segment of one problem and walks its stages backwards.
+//   * endpoint segments (j < J-1): endpoint-explicit sweep with zero terminal
+//     cost and terminal rows Hx=I, Hz=-I -- endpoint.backward_pass
+//     (/root/reference/pkg/src/parlqr/endpoint.py:168-301) as called by
+//     parallel._solve_segment_task (parallel.py:228-240);
+//   * the last segment: plain Riccati sweep from the terminal cost --
+//     serial.backward_pass (serial.py:37-79).
+//
+// Per stage, with F = [Fx | Fu | f1]:
+//   GEMM1  [VF; Z] = [Vxx; Vzx] F            (+ vx1 / vz1 in the last column)
+//   GEMM2  [Mxx mx1; Mux Muu mu1] = [Fx Fu]' VF + Q-blocks
+//   gains  G = [Kx | Kz | k1]:  r = 0: G = -Muu^{-1} [Mux | Mzu' | mu1]
+//          tail (r >= m): Householder QR of Nu = Hx Fu replaces the SVD of
+//          endpoint.py:226 -- G = -R^{-1} Q1' [Nx Nz n1], rows <- Q2'[Nx Nz n1]
+//          (pinv, projector and compressed rows are invariant to the row
+//          basis); 0 < r < m: mixed range/null branch.
+//   value  Y = P + Muu G;  [Vxx Vzx' vx1; Vzx Vzz vz1] = M + P'G + G'Y
+//          which is term-for-term endpoint.py:285-294.
+#include "plq_device.cuh"
+#include "plq_internal.h"
+
+#include <algorithm>
+
+namespace plq {
+
+namespace {
+
+struct Bufs {
+  double *V, *IN, *PGY, *MUU, *MISC, *VF, *Z, *MX, *H, *WIDE;
+};
+
+__device__ void wide_branch(const plq_problem_t& p, int n, int m, int r, int W, int ldw, int Fw, double* VF,
+                            double* H, double* P, double* G, double* Muu, double* WIDE, double* tau, double* rdiag,
+                            double* red, int* iflag, double thr_scale, int* status_out, int stage) {
+  // Mixed branch 0 < p = r < m (endpoint.py:234-250): Nu (r x m) has full
+  // row rank.  QR of Nu' = Q [R; 0]; pinv(Nu) = Q1 R^{-T}; null basis Q2.
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* X = WIDE;              // m x r   (Nu')
+  double* Qm = X + m * r;        // m x m   (Q' Muu Q)
+  double* BASE = Qm + m * m;     // m x ldw
+  double* C = BASE + m * ldw;    // m x ldw
+  for (int idx = tid; idx < m * r; idx += nt) {
+    const int c = idx / r, i = idx % r;
+    X[c * r + i] = VF[i * Fw + n + c];
+  }
+  __syncthreads();
+  cta_householder_qr(X, m, r, r, nullptr, 0, 1, tau, rdiag, red);
+  double rmax = 0.0, rmin = 1e308;
+  for (int i = 0; i < r; ++i) {
+    rmax = fmax(rmax, fabs(rdiag[i]));
+    rmin = fmin(rmin, fabs(rdiag[i]));
+  }
+  if (!(rmin > p.rank_tol * fmax(thr_scale, rmax))) {
+    if (tid == 0) *status_out = PLQ_STATUS_DEGENERATE;
+    __syncthreads();
+    return;
+  }
+  // y = R^{-T} stack (forward substitution), BASE = Q [y; 0]
+  for (int c = tid; c < W; c += nt) {
+    for (int i = 0; i < r; ++i) {
+      double s = H[i * ldw + c];
+      for (int k = 0; k < i; ++k) s -= X[k * r + i] * BASE[k * ldw + c];
+      BASE[i * ldw + c] = s / rdiag[i];
+    }
+    for (int i = r; i < m; ++i) BASE[i * ldw + c] = 0.0;
+  }
+  __syncthreads();
+  cta_apply_q(X, m, r, r, tau, BASE, W, ldw, true);
+  // C = P - Muu BASE
+  cta_gemm<false, false, 1, 1>(m, W, m, Muu, m, BASE, ldw,
+                               [&](int i, int j, double acc) { C[i * ldw + j] = P[i * ldw + j] - acc; });
+  // Qm = Muu, then Q' Muu, transpose, Q' (Muu Q) -> Q' Muu Q
+  for (int idx = tid; idx < m * m; idx += nt) Qm[idx] = Muu[idx];
+  __syncthreads();
+  cta_apply_q(X, m, r, r, tau, Qm, m, m, false);
+  for (int idx = tid; idx < m * m; idx += nt) {
+    const int i = idx / m, j = idx % m;
+    if (i < j) {
+      const double a = Qm[i * m + j];
+      Qm[i * m + j] = Qm[j * m + i];
+      Qm[j * m + i] = a;
+    }
+  }
+  __syncthreads();
+  cta_apply_q(X, m, r, r, tau, Qm, m, m, false);
+  cta_apply_q(X, m, r, r, tau, C, W, ldw, false);   // C <- Q' C
+  // chol of W = Q2' Muu Q2 (the (m-r) x (m-r) trailing block)
+  const int q = m - r;
+  double* Wn = Qm + r * m + r;
+  if (tid == 0) *iflag = 0;
+  __syncthreads();
+  if (!cta_cholesky(Wn, q, m, iflag)) {
+    if (tid == 0) *status_out = 1 + stage;
+    __syncthreads();
+    return;
+  }
+  cta_cho_solve(Wn, q, m, C + r * ldw, W, ldw);
+  for (int idx = tid; idx < r * W; idx += nt) C[(idx / W) * ldw + idx % W] = 0.0;
+  __syncthreads();
+  cta_apply_q(X, m, r, r, tau, C, W, ldw, true);   // Q [0; x]
+  for (int idx = tid; idx < m * W; idx += nt) {
+    const int i = idx / W, j = idx % W;
+    G[i * ldw + j] = -(BASE[i * ldw + j] + C[i * ldw + j]);
+  }
+  __syncthreads();
+}
+
+__device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int j) {
+  const plq_problem_t& p = a.p;
+  const int n = p.n, m = p.m, J = p.J, T = p.T;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
+  const bool serial = (j == J - 1);
+  const int nz = serial ? 0 : n;
+  const int cc = n + nz;            // constant column of G
+  const int W = cc + 1;             // logical width of P/G/Y
+  const int ldw = 2 * n + 1;        // storage stride of P/G/Y/H
+  const int Fw = n + m + 1;
+  const int nn = n * n;
+
+  double* Vxx = bf.V;
+  double* Vzx = bf.V + nn;
+  double* Vzz = bf.V + 2 * nn;
+  double* vx1 = bf.V + 3 * nn;
+  double* vz1 = vx1 + n;
+  double* F = bf.IN;
+  double* Qxx = F + n * Fw;
+  double* Qux = Qxx + nn;
+  double* Quu = Qux + m * n;
+  double* qx1 = Quu + m * m;
+  double* qu1 = qx1 + n;
+  double* P = bf.PGY;
+  double* G = P + m * ldw;
+  double* Y = G + m * ldw;
+  double* Muu = bf.MUU;
+  double* Lm = Muu + m * m;
+  double* tau = bf.MISC;
+  double* rdiag = tau + m;
+  double* red = rdiag + m;
+  int* iflag = reinterpret_cast<int*>(red + 32);
+  int* sflag = iflag + 1;
+  double* VF = bf.VF;
+  double* Z = bf.Z;
+  double* MX = bf.MX;
+  double* H = bf.H;
+
+  // ---- initial value function and constraint rows (endpoint.py:182-199, serial.py:46-48)
+  for (int idx = tid; idx < 3 * nn + 2 * n; idx += nt) bf.V[idx] = 0.0;
+  if (tid == 0) *sflag = 0;
+  __syncthreads();
+  if (serial) {
+    for (int idx = tid; idx < nn; idx += nt) Vxx[idx] = p.QxxT[b * nn + idx];
+    for (int i = tid; i < n; i += nt) vx1[i] = p.qx1T[b * n + i];
+  } else {
+    for (int idx = tid; idx < n * ldw; idx += nt) {
+      const int i = idx / ldw, c = idx % ldw;
+      H[idx] = (c == i) ? 1.0 : ((c == n + i) ? -1.0 : 0.0);
+    }
+  }
+  int r = serial ? 0 : n;
+  __syncthreads();
+
+  for (int s = L - 1; s >= 0; --s) {
+    const int64_t st = b * T + (lo + s);
+    // ---- stage inputs -> shared/scratch (coalesced global reads)
+    for (int idx = tid; idx < nn; idx += nt) {
+      F[(idx / n) * Fw + idx % n] = p.Fx[st * nn + idx];
+      Qxx[idx] = p.Qxx[st * nn + idx];
+    }
+    for (int idx = tid; idx < n * m; idx += nt) {
+      F[(idx / m) * Fw + n + idx % m] = p.Fu[st * n * m + idx];
+      Qux[idx] = p.Qux[st * m * n + idx];
+    }
+    for (int i = tid; i < n; i += nt) {
+      F[i * Fw + n + m] = p.f1[st * n + i];
+      qx1[i] = p.qx1[st * n + i];
+    }
+    for (int idx = tid; idx < m * m; idx += nt) Quu[idx] = p.Quu[st * m * m + idx];
+    for (int i = tid; i < m; i += nt) qu1[i] = p.qu1[st * m + i];
+    __syncthreads();
+
+    // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217)
+    cta_gemm<false, false, 1, 1>(n + nz, Fw, n, bf.V, n, F, Fw, [&](int i, int c, double acc) {
+      if (i < n) {
+        VF[i * Fw + c] = (c == n + m) ? vx1[i] + acc : acc;
+      } else {
+        Z[(i - n) * Fw + c] = (c == n + m) ? vz1[i - n] + acc : acc;
+      }
+    });
+    __syncthreads();
+    // ---- GEMM2: M-terms (endpoint.py:209-211, 215-216)
+    cta_gemm<true, false, 1, 1>(n + m, Fw, n, F, Fw, VF, Fw, [&](int i, int c, double acc) {
+      if (i < n) {
+        if (c < n) {
+          MX[i * (n + 1) + c] = Qxx[i * n + c] + acc;
+        } else if (c == n + m) {
+          MX[i * (n + 1) + n] = qx1[i] + acc;
+        }
+      } else {
+        const int u = i - n;
+        if (c < n) {
+          P[u * ldw + c] = Qux[u * n + c] + acc;
+        } else if (c < n + m) {
+          Muu[u * m + (c - n)] = Quu[u * m + (c - n)] + acc;
+        } else {
+          P[u * ldw + cc] = qu1[u] + acc;
+        }
+      }
+    });
+    // P z-block = Mzu' (Mzu = Vzx Fu lives in Z's middle columns)
+    for (int idx = tid; idx < m * nz; idx += nt) {
+      const int u = idx / nz, c = idx % nz;
+      P[u * ldw + n + c] = Z[c * Fw + n + u];
+    }
+    __syncthreads();
+
+    // ---- gains
+    if (r == 0) {
+      // unconstrained stage: G = -Muu^{-1} P (endpoint.py:239-250 with p = 0;
+      // serial.py:63-70)
+      for (int idx = tid; idx < m * m; idx += nt) Lm[idx] = Muu[idx];
+      for (int idx = tid; idx < m * W; idx += nt) {
+        const int u = idx / W, c = idx % W;
+        G[u * ldw + c] = P[u * ldw + c];
+      }
+      if (tid == 0) *iflag = 0;
+      __syncthreads();
+      if (!cta_cholesky(Lm, m, m, iflag)) {
+        if (tid == 0) *sflag = 1 + s;
+        __syncthreads();
+        break;
+      }
+      cta_cho_solve(Lm, m, m, G, W, ldw);
+      for (int idx = tid; idx < m * W; idx += nt) {
+        const int u = idx / W, c = idx % W;
+        G[u * ldw + c] = -G[u * ldw + c];
+      }
+      __syncthreads();
+    } else {
+      // constrained tail stage (endpoint.py:219-238, 251-252, 267-281)
+      double part_h = 0.0, part_u = 0.0;
+      for (int idx = tid; idx < r * n; idx += nt) {
+        const double v = H[(idx / n) * ldw + idx % n];
+        part_h += v * v;
+      }
+      for (int idx = tid; idx < n * m; idx += nt) {
+        const double v = F[(idx / m) * Fw + n + idx % m];
+        part_u += v * v;
+      }
+      const double hx2 = block_sum(part_h, red);
+      const double fu2 = block_sum(part_u, red);
+      const double nu_scale = sqrt(hx2) * sqrt(fu2);
+      // N = Hx F -> VF (r x Fw): [Nx | Nu | Hx f1]
+      cta_gemm<false, false, 1, 1>(r, Fw, n, H, ldw, F, Fw,
+                                   [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
+      __syncthreads();
+      // stack [Nx | Nz=Hz | n1 = Hx f1 + h1] in place in H
+      for (int idx = tid; idx < r * n; idx += nt) {
+        const int i = idx / n, c = idx % n;
+        H[i * ldw + c] = VF[i * Fw + c];
+      }
+      for (int i = tid; i < r; i += nt) H[i * ldw + cc] += VF[i * Fw + n + m];
+      __syncthreads();
+      if (r >= m) {
+        cta_householder_qr(VF + n, r, m, Fw, H, W, ldw, tau, rdiag, red);
+        double rmax = 0.0, rmin = 1e308;
+        for (int i = 0; i < m; ++i) {
+          rmax = fmax(rmax, fabs(rdiag[i]));
+          rmin = fmin(rmin, fabs(rdiag[i]));
+        }
+        if (!(rmin > p.rank_tol * fmax(nu_scale, rmax))) {
+          if (tid == 0) *sflag = PLQ_STATUS_DEGENERATE;
+          __syncthreads();
+          break;
+        }
+        // G = -R^{-1} (Q1' stack): back substitution, thread per column
+        for (int c = tid; c < W; c += nt) {
+          for (int i = m - 1; i >= 0; --i) {
+            double v = H[i * ldw + c];
+            for (int k = i + 1; k < m; ++k) v -= VF[i * Fw + n + k] * G[k * ldw + c];
+            G[i * ldw + c] = v / rdiag[i];
+          }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < m * W; idx += nt) {
+          const int u = idx / W, c = idx % W;
+          G[u * ldw + c] = -G[u * ldw + c];
+        }
+        // surviving rows Q2' stack: shift rows m..r-1 up by m, one block of
+        // m rows at a time so sources and destinations never overlap
+        for (int blk = 0; blk < r - m; blk += m) {
+          const int rows = min(m, r - m - blk);
+          for (int idx = tid; idx < rows * W; idx += nt) {
+            const int i = blk + idx / W, c = idx % W;
+            H[i * ldw + c] = H[(i + m) * ldw + c];
+          }
+          __syncthreads();
+        }
+        r -= m;
+        __syncthreads();
+      } else {
+        wide_branch(p, n, m, r, W, ldw, Fw, VF, H, P, G, Muu, bf.WIDE, tau, rdiag, red, iflag, nu_scale, sflag, s);
+        if (*sflag) break;
+        r = 0;
+      }
+    }
+
+    // ---- policy outputs (parallel.py:224-236 stacking)
+    for (int idx = tid; idx < m * n; idx += nt) {
+      const int u = idx / n, c = idx % n;
+      a.Kx[st * m * n + idx] = G[u * ldw + c];
+      a.Kz[st * m * n + idx] = serial ? 0.0 : G[u * ldw + n + c];   // serial segment: Kz = 0
+    }
+    for (int u = tid; u < m; u += nt) a.k1[st * m + u] = G[u * ldw + cc];
+
+    // ---- value update (endpoint.py:285-294; serial.py:75-77)
+    cta_gemm<false, false, 1, 1>(m, W, m, Muu, m, G, ldw,
+                                 [&](int i, int c, double acc) { Y[i * ldw + c] = P[i * ldw + c] + acc; });
+    __syncthreads();
+    cta_gemm<true, false, 1, 1>(n + nz, W, 2 * m, P, ldw, G, ldw, [&](int i, int c, double acc) {
+      if (i < n) {
+        if (c < n) {
+          Vxx[i * n + c] = MX[i * (n + 1) + c] + acc;
+        } else if (c == cc) {
+          vx1[i] = MX[i * (n + 1) + n] + acc;
+        }
+      } else {
+        const int zi = i - n;
+        if (c < n) {
+          Vzx[zi * n + c] = Z[zi * Fw + c] + acc;
+        } else if (c < cc) {
+          Vzz[zi * n + (c - n)] += acc;
+        } else {
+          vz1[zi] = Z[zi * Fw + n + m] + acc;
+        }
+      }
+    });
+    __syncthreads();
+    // symmetrize Vxx (and Vzz): 0.5 * (V + V')
+    for (int idx = tid; idx < nn; idx += nt) {
+      const int i = idx / n, c = idx % n;
+      if (i < c) {
+        const double v = 0.5 * (Vxx[i * n + c] + Vxx[c * n + i]);
+        Vxx[i * n + c] = v;
+        Vxx[c * n + i] = v;
+        if (!serial) {
+          const double w = 0.5 * (Vzz[i * n + c] + Vzz[c * n + i]);
+          Vzz[i * n + c] = w;
+          Vzz[c * n + i] = w;
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- segment-start value blocks (parallel.py:230-237) and status
+  const int vsz = 3 * nn + 2 * n;
+  double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
+  for (int idx = tid; idx < vsz; idx += nt) dst[idx] = bf.V[idx];
+  if (tid == 0) {
+    int st = *sflag;
+    if (st == 0 && !serial && r > 0) st = PLQ_STATUS_DEGENERATE;   // feasibility rows left
+    a.status[b * J + j] = st;
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  Bufs bf;
+  double* ptrs[SB_COUNT];
+  double* g = a.gscratch + (int64_t)blockIdx.x * a.lay.gmem_doubles;
+#pragma unroll
+  for (int i = 0; i < SB_COUNT; ++i) ptrs[i] = a.lay.in_smem[i] ? smem + a.lay.off[i] : g + a.lay.off[i];
+  bf.V = ptrs[SB_V];
+  bf.IN = ptrs[SB_IN];
+  bf.PGY = ptrs[SB_PGY];
+  bf.MUU = ptrs[SB_MUU];
+  bf.MISC = ptrs[SB_MISC];
+  bf.VF = ptrs[SB_VF];
+  bf.Z = ptrs[SB_Z];
+  bf.MX = ptrs[SB_MX];
+  bf.H = ptrs[SB_H];
+  bf.WIDE = ptrs[SB_WIDE];
+  const int nloc = a.seg_end - a.seg_begin;
+  const int64_t total = a.p.B * nloc;
+  for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
+    const int64_t b = task / nloc;
+    const int j = a.seg_begin + (int)(task % nloc);
+    sweep_segment(a, bf, b, j);
+  }
+}
+
+}  // namespace
+
+int sweep_threads(int n) {
+  if (n <= 16) return 32;
+  if (n <= 32) return 128;
+  if (n <= 64) return 256;
+  return 512;
+}
+
+SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
+  (void)threads;
+  const int64_t Fw = n + m + 1, W = 2 * n + 1;
+  int64_t sz[SB_COUNT];
+  sz[SB_V] = 3LL * n * n + 2 * n;
+  sz[SB_IN] = n * Fw + (int64_t)n * n + (int64_t)m * n + (int64_t)m * m + n + m;
+  sz[SB_PGY] = 3 * m * W;
+  sz[SB_MUU] = 2LL * m * m;
+  sz[SB_MISC] = 2LL * m + 32 + 2;
+  sz[SB_VF] = n * Fw;
+  sz[SB_Z] = n * Fw;
+  sz[SB_MX] = (int64_t)n * (n + 1);
+  sz[SB_H] = n * W;
+  const bool wide = (n % m) != 0;
+  sz[SB_WIDE] = wide ? ((int64_t)m * std::min(n, m) + (int64_t)m * m + 2 * m * W) : 0;
+  SweepLayout L{};
+  int64_t so = 0, go = 0;
+  const int64_t budget = (int64_t)(smem_budget / sizeof(double));
+  for (int i = 0; i < SB_COUNT; ++i) {
+    const int64_t s = (sz[i] + 1) & ~1LL;   // 16-byte granules
+    if (so + s <= budget) {
+      L.off[i] = so;
+      L.in_smem[i] = 1;
+      so += s;
+    } else {
+      L.off[i] = go;
+      L.in_smem[i] = 0;
+      go += s;
+    }
+  }
+  L.smem_doubles = so;
+  L.gmem_doubles = go;
+  return L;
+}
+
+int launch_sweep(const SweepArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
+  switch (threads) {
+    case 32:
+      sweep_kernel<32><<<grid, 32, smem, s>>>(a);
+      break;
+    case 128:
+      sweep_kernel<128><<<grid, 128, smem, s>>>(a);
+      break;
+    case 256:
+      sweep_kernel<256><<<grid, 256, smem, s>>>(a);
+      break;
+    default:
+      sweep_kernel<512><<<grid, 512, smem, s>>>(a);
+      break;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// Occupancy helper used by the C-ABI layer to size the persistent grid.
+int sweep_max_blocks_per_sm(int threads, size_t smem) {
+  int nb = 0;
+  switch (threads) {
+    case 32:
+      cudaFuncSetAttribute(sweep_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel<32>, 32, smem);
+      break;
+    case 128:
+      cudaFuncSetAttribute(sweep_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel<128>, 128, smem);
+      break;
+    case 256:
+      cudaFuncSetAttribute(sweep_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel<256>, 256, smem);
+      break;
+    default:
+      cudaFuncSetAttribute(sweep_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel<512>, 512, smem);
+      break;
+  }
+  return nb;
+}
+
+}  // namespace plq

@@ -1,0 +1,244 @@
+"""Generate golden fixtures from the REFERENCE implementation itself.
+
+Run in the build container only (it imports ``parlqr`` from
+``/root/reference/pkg/src``, which does not exist on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Each ``*.npz`` holds the inputs (or the seeded-config recipe plus a sha256 of
+the inputs), the outputs of ``parlqr.solve_parallel`` on them, the unfolded
+per-segment ``_solve_segment_task`` outputs, and the reference's numerical
+floor: the relative change of each output when the inputs are perturbed by
+~1 ulp (SURVEY.md Appendix C protocol).  Outputs are data, not source.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import parlqr  # noqa: E402  (the reference)
+from parlqr import parallel as ref_parallel  # noqa: E402
+from parlqr.generate import generate as ref_generate  # noqa: E402
+from parlqr.problem import (LqrProblem, StageCost, StageDynamics,  # noqa: E402
+                            TerminalCost)
+
+from paper_1809_06360_b200 import synth  # noqa: E402
+
+FIELDS = synth.STAGE_FIELDS
+OUTS = ("states", "controls", "lambdas", "K", "k")
+
+
+def to_problem(a):
+    stages = [(StageCost(a["Qxx"][t], a["Qux"][t], a["Quu"][t], a["qx1"][t], a["qu1"][t]),
+               StageDynamics(a["Fx"][t], a["Fu"][t], a["f1"][t]))
+              for t in range(a["qx1"].shape[0])]
+    return LqrProblem(stages, TerminalCost(a["QxxT"], a["qx1T"]), a["x_init"])
+
+
+def from_problem(p):
+    a = {f: np.stack([getattr(c if f[0] in "Qq" else d, f) for c, d in p.stages])
+         for f in FIELDS}
+    a["QxxT"] = np.array(p.terminal.Qxx)
+    a["qx1T"] = np.array(p.terminal.qx1)
+    a["x_init"] = np.array(p.x_init)
+    return a
+
+
+def digest(a):
+    h = hashlib.sha256()
+    for k in sorted(a):
+        h.update(k.encode())
+        h.update(np.ascontiguousarray(a[k], dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def ref_solve(a, J, splits=None):
+    prob = to_problem(a)
+    part = None if splits is None else ref_parallel.Partition(len(splits) - 1, tuple(splits))
+    sol = parlqr.solve_parallel(prob, J=J, workers=1, partition=part)
+    d = sol.details
+    out = {
+        "states": sol.states, "controls": sol.controls, "lambdas": sol.lambdas,
+        "K": np.stack([p.Kx for p in sol.policies]),
+        "k": np.stack([p.k1 for p in sol.policies]),
+        "objective": np.float64(sol.objective),
+        "kkt": np.float64(sol.kkt_residual_inf),
+        "degenerate": np.bool_(d.degenerate),
+        "splits": np.array(d.partition.split_times),
+    }
+    if d.degenerate:
+        return out
+    out.update({
+        "links": d.link_points, "mu_left": d.mu_left, "lambda_right": d.lambda_right,
+        "link_mismatch": np.float64(d.link_mismatch),
+        "link_residual": np.float64(d.link_residual),
+    })
+    vf = d.segment_values0
+    out["Vxx0"] = np.stack([v[0] for v in vf])
+    out["vx10"] = np.stack([v[3] if len(v) == 5 else v[1] for v in vf])
+    if len(vf) > 1:
+        out["Vzx0"] = np.stack([v[1] for v in vf[:-1]])
+        out["Vzz0"] = np.stack([v[2] for v in vf[:-1]])
+        out["vz10"] = np.stack([v[4] for v in vf[:-1]])
+    # unfolded per-segment gains through the reference's own task seam
+    payloads = ref_parallel._segment_payloads(prob, d.partition, parlqr.DEFAULT_TOLERANCES, False)
+    segs = [ref_parallel._solve_segment_task(ref_parallel._copy_payload(p)) for p in payloads]
+    T, m, n = out["K"].shape
+    Kz = np.zeros((T, m, n))
+    k1 = np.empty((T, m))
+    for j, seg in enumerate(segs):
+        lo, hi = d.partition.split_times[j], d.partition.split_times[j + 1]
+        k1[lo:hi] = seg["k1"]
+        if seg["kind"] == "endpoint":
+            Kz[lo:hi] = seg["Kz"]
+    out["Kz"] = Kz
+    out["k1"] = k1
+    return out
+
+
+def rel(a, b):
+    den = float(np.abs(b).max())
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max()) / (den if den else 1.0)
+
+
+def floors(a, J, base, splits=None, eps=1e-15, trials=3):
+    """Relative output change under ~1-ulp input perturbation (App. C)."""
+    fl = {}
+    for s in range(trials):
+        rng = np.random.default_rng(777 + s)
+        pa = {}
+        for k, v in a.items():
+            p = v * (1.0 + eps * rng.standard_normal(v.shape))
+            if k in ("Qxx", "Quu", "QxxT"):
+                p = 0.5 * (p + np.swapaxes(p, -1, -2))
+            pa[k] = p
+        o = ref_solve(pa, J, splits)
+        for key in OUTS + ("objective", "links", "Kz", "k1"):
+            if key in base and key in o:
+                fl[key] = max(fl.get(key, 0.0), rel(o[key], base[key]))
+    return {f"floor_{k}": np.float64(v) for k, v in fl.items()}
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"{name}: {os.path.getsize(path) / 1024:.1f} KiB")
+
+
+def synth_case(name, cfg_id, seed, count=1, **over):
+    cfg = synth.CONFIGS[cfg_id].scaled(**over) if over else synth.CONFIGS[cfg_id]
+    batch = synth.generate_batch(cfg, seed=seed, count=count)
+    rec = {"cfg_id": np.int64(cfg_id), "n": np.int64(cfg.n), "m": np.int64(cfg.m),
+           "T": np.int64(cfg.T), "J": np.int64(cfg.J), "seed": np.int64(seed),
+           "count": np.int64(count), "a_scale": np.float64(cfg.a_scale),
+           "q_eps": np.float64(cfg.q_eps), "r_eps": np.float64(cfg.r_eps),
+           "input_sha256": np.array(digest(batch))}
+    for i in range(count):
+        a = {k: v[i] for k, v in batch.items()}
+        base = ref_solve(a, cfg.J)
+        fl = floors(a, cfg.J, base)
+        for k, v in {**base, **fl}.items():
+            rec.setdefault(k, []).append(v)
+    out = {k: (np.stack(v) if isinstance(v, list) else v) for k, v in rec.items()}
+    save(name, **out)
+
+
+def stored_case(name, problems, Js, splits_list=None):
+    """Small instances stored with their inputs (ragged, so one entry per
+    problem with an index prefix)."""
+    rec = {"num": np.int64(len(problems))}
+    for i, (a, J) in enumerate(zip(problems, Js)):
+        splits = None if splits_list is None else splits_list[i]
+        o = ref_solve(a, J, splits)
+        for k, v in a.items():
+            rec[f"{i}/in/{k}"] = v
+        for k, v in o.items():
+            rec[f"{i}/out/{k}"] = v
+        rec[f"{i}/J"] = np.int64(J)
+    save(name, **rec)
+
+
+def scalar_problem(T):
+    cost = StageCost([[0.0]], [[0.0]], [[1.0]], [0.0], [0.0])
+    dyn = StageDynamics([[1.0]], [[1.0]], [0.0])
+    return LqrProblem([(cost, dyn)] * T, TerminalCost([[1.0]], [0.0]), [1.0])
+
+
+def main():
+    # 1. hand example of test_parallel.py:48-54 (J=2 scalar problem)
+    stored_case("hand_scalar", [from_problem(scalar_problem(2))], [2])
+    # 2. the reference's small random pool (conftest.py:53-63) for J=2,3,4
+    probs, Js = [], []
+    for k in range(40):
+        dims = np.random.default_rng(1_000 + k)
+        n = int(dims.integers(1, 7))
+        m = int(dims.integers(1, 4))
+        T = int(dims.integers(1, 21))
+        a = from_problem(ref_generate(n, m, T, seed=2_000 + k))
+        for J in (2, 3, 4):
+            if J <= T:
+                probs.append(a)
+                Js.append(J)
+    stored_case("small_random", probs, Js)
+    # 3. random custom partitions (test_parallel.py:95-112)
+    rng = np.random.default_rng(9)
+    probs, Js, splits = [], [], []
+    for trial in range(40):
+        dims = np.random.default_rng(5_000 + trial)
+        n = int(dims.integers(1, 6))
+        m = int(dims.integers(1, 4))
+        T = int(dims.integers(2, 18))
+        a = from_problem(ref_generate(n, m, T, seed=6_000 + trial))
+        J = int(rng.integers(2, T + 1))
+        interior = np.sort(rng.choice(np.arange(1, T), size=J - 1, replace=False))
+        probs.append(a)
+        Js.append(J)
+        splits.append((0, *map(int, interior), T))
+    stored_case("random_splits", probs, Js, splits)
+    # 4. BASELINE configs: cfg0 in full, a cfg1 subset, reduced-T cfg2/3/4 shapes
+    synth_case("cfg0_seed0", 0, seed=0)
+    synth_case("cfg1_first4", 1, seed=0, count=4)
+    synth_case("cfg2_shape_T256_J4", 2, seed=0, T=256, J=4)
+    synth_case("cfg3_shape_T16_J2", 3, seed=0, T=16, J=2)
+    synth_case("cfg4_shape_T64_J2", 4, seed=0, T=64, J=2)
+    # 5. the double-integrator demo's J=3 partitioned solve (demo.py:52-62,
+    #    102-112) plus its stored rollouts (demos/out/double_integrator)
+    from parlqr import demo
+    cfg = demo.DemoConfig()
+    prob = demo.double_integrator_problem(cfg)
+    a = from_problem(prob)
+    o = ref_solve(a, demo.DEMO_SPLITS)
+    ddir = "/root/reference/pkg/demos/out/double_integrator"
+
+    def read_csv(fname):
+        rows = open(os.path.join(ddir, fname)).read().strip().splitlines()[1:]
+        vals = []
+        for r in rows:
+            cells = r.split(",")[1:]
+            vals.append([float(c.replace("np.float64(", "").rstrip(")")) if c else np.nan
+                         for c in cells])
+        return np.array(vals)
+
+    und = read_csv("parallel_undisturbed.csv")
+    dis = read_csv("parallel_disturbed.csv")
+    summ = open(os.path.join(ddir, "summary.csv")).read().strip().splitlines()[1].split(",")
+    rec = {f"in/{k}": v for k, v in a.items()}
+    rec.update({f"out/{k}": v for k, v in o.items()})
+    rec.update({"J": np.int64(demo.DEMO_SPLITS), "csv_undisturbed": und,
+                "csv_disturbed": dis, "cost_p": np.float64(float(summ[1])),
+                "disturbance_smoothing": np.float64(demo.DISTURBANCE_SMOOTHING)})
+    save("demo_double_integrator", **rec)
+
+
+if __name__ == "__main__":
+    main()
