@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 partitioned Riccati solve (BASELINE.json metric:
+solved knot-points/s, fp64, including the K_t, k_t policies).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = one full ``solve_parallel`` of the configured batch (sweeps, link
+solve, reconstruction, objective and KKT diagnostics) with inputs resident in
+HBM.  Default workload: BASELINE config 1 (4096 independent problems, n=12,
+m=4, T=64, J=8), the config the metric is quoted on; the batch is sharded
+across ranks (``torchrun``), no collective on the data path.  Rank 0 prints
+one JSON line.  ``--impl reference`` times the CPU oracle port of the
+reference's path on the host cores instead (rank 0 only).
+"""
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import statistics  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1809_06360_b200 import perfmodel, synth  # noqa: E402
+
+METRIC = "solved knot-points/sec (fp64, incl. K_t,k_t policies)"
+L2_BYTES = 126 * 1024 * 1024
+
+NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                0x100: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1, choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler(threading.Thread):
+    """NVML clocks / throttle reasons sampled every ~5 ms during the timed region."""
+
+    def __init__(self, index):
+        super().__init__(daemon=True)
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._halt = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.nv = None
+
+    def run(self):
+        while self.ok and not self._halt.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def stop(self):
+        self._halt.set()
+        self.join(timeout=1.0)
+
+    def report(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        names = [v for k, v in NVML_REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port of the reference path (bench's cpu_baseline leg
+# and the --impl reference arm; the only places bench.py runs oracle/)
+
+def cpu_sample(cfg, cores, seed):
+    """A bounded sample of ``cfg`` for the CPU oracle and how to time it."""
+    from oracle import parlqr_oracle as O
+    if cfg.B > 1:
+        S = max(1, (8 if cfg.n <= 16 else 1) * cores)
+        batch = synth.generate_batch(cfg, seed=seed, count=S)
+        desc = (f"first {S} of {cfg.B} problems (T={cfg.T}, J={cfg.J}), problem-level fork pool "
+                f"of {cores} workers around the reference's per-problem solve (it has no batch API)")
+        return (lambda: O.solve_batch(batch, J=cfg.J, workers=cores)), S * cfg.T, desc, cores
+    if cfg.T <= 4096 and cfg.n <= 16:
+        prob = synth.generate_batch(cfg, seed=seed, count=1)
+        prob = O.problem_slice(prob, 0)
+        w = min(cfg.J, cores)
+        desc = f"full problem, segment fork pool of {w} workers (reference default min(J, cores))"
+        return (lambda: O.solve(prob, J=cfg.J, workers=w)), cfg.T, desc, w
+    L = cfg.T // cfg.J
+    Js = 2 * cores
+    sub = cfg.scaled(T=L * Js, J=Js)
+    prob = O.problem_slice(synth.generate_batch(sub, seed=seed, count=1), 0)
+    desc = (f"sub-horizon T={sub.T} with the config's segment length L={L} (J={Js}), segment fork pool "
+            f"of {cores} workers (reference default)")
+    return (lambda: O.solve(prob, J=Js, workers=cores)), sub.T, desc, cores
+
+
+def time_cpu(cfg, seed, steps, warmup):
+    from oracle import parlqr_oracle as O
+    cores = O.host_cores()
+    fn, knots, desc, used = cpu_sample(cfg, cores, seed)
+    for _ in range(warmup):
+        fn()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    return {"value": knots / statistics.mean(times), "unit": "knots/s", "cores": used, "kind": "port",
+            "sample": desc, "sample_seconds_mean": statistics.mean(times), "steps": steps}
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    cb = time_cpu(cfg, args.seed, max(1, args.steps), max(0, args.warmup))
+    line = {
+        "metric": METRIC, "value": cb["value"], "unit": "knots/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * cb["sample_seconds_mean"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json recipe, seeded)", "impl": "reference",
+        "config": {"workload": cfg.name, "B": cfg.B, "n": cfg.n, "m": cfg.m, "T": cfg.T, "J": cfg.J},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "knots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_1809_06360_b200 import BatchSolver, HostSolver, _native
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg = synth.CONFIGS[args.config]
+    if cfg.B % world and cfg.B > 1:
+        raise SystemExit(f"batch {cfg.B} does not shard over {world} ranks")
+    if cfg.B > 1:
+        B_loc = cfg.B // world
+        first = rank * B_loc
+        scaling = "strong"
+    else:
+        B_loc, first = 1, 0          # single horizon: replicas only in this round
+        scaling = "replicas"
+    host = synth.generate_batch(cfg, seed=args.seed, count=B_loc, first=first)
+    inputs = {k: torch.from_numpy(v).to(dev) for k, v in host.items()}
+    solver = BatchSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 1)):
+        solver.run(inputs)
+    solver.raise_for_status()
+    in_bytes = sum(v.numel() * 8 for v in inputs.values())
+    flush = None
+    if in_bytes < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    sampler = ClockSampler(dev.index if world == 1 else local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        ev[i][0].record(stream)
+        solver.run(inputs)
+        ev[i][1].record(stream)
+        launches += solver.launches
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    knots = cfg.B * cfg.T if cfg.B > 1 else world * cfg.T
+    value = knots / (ms_per_step / 1000.0)
+    solver.raise_for_status()
+
+    # ---- dominant kernel (the segment sweep) timed on its own stream, and the other phases
+    import ctypes
+    lib = _native.lib()
+    prob = solver._problem_struct(inputs)
+    phase_ms = {}
+    phases = {
+        "sweep": lambda: lib.plq_sweep_segments(ctypes.byref(prob), ctypes.byref(solver._outs), 0, cfg.J,
+                                                ctypes.c_void_p(solver.workspace.data_ptr()), solver.ws_bytes,
+                                                ctypes.c_void_p(stream.cuda_stream)),
+        "link": lambda: lib.plq_link_solve(ctypes.byref(prob), ctypes.byref(solver._outs),
+                                           ctypes.c_void_p(solver.workspace.data_ptr()), solver.ws_bytes,
+                                           ctypes.c_void_p(stream.cuda_stream)),
+        "recon": lambda: lib.plq_reconstruct_segments(ctypes.byref(prob), ctypes.byref(solver._outs), 0, cfg.J,
+                                                      None, ctypes.c_void_p(solver.workspace.data_ptr()),
+                                                      solver.ws_bytes, ctypes.c_void_p(stream.cuda_stream)),
+    }
+    reps = max(3, min(args.steps, 20))
+    for name, fn in phases.items():
+        es = []
+        for _ in range(reps):
+            if flush is not None:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _native.check(fn(), name)
+            b.record(stream)
+            es.append((a, b))
+        torch.cuda.synchronize()
+        phase_ms[name] = statistics.mean(x.elapsed_time(y) for x, y in es)
+    _, sweep_fl = perfmodel.problem_flops(cfg.n, cfg.m, cfg.T, cfg.J)
+    peak_f64 = perfmodel.fp64_peak_tflops()
+    achieved = B_loc * sweep_fl / (phase_ms["sweep"] / 1000.0) / 1e12
+    hbm_peak, hbm_src = perfmodel.hbm_peak_gbs(ROOT)
+    sweep_b = B_loc * perfmodel.sweep_bytes(cfg.n, cfg.m, cfg.T, cfg.J)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(cfg.name)
+    total_fl, _ = perfmodel.problem_flops(cfg.n, cfg.m, cfg.T, cfg.J)
+    bin_, bout = perfmodel.knot_bytes(cfg.n, cfg.m)
+    whole = {
+        "fp64_tflops": B_loc * total_fl / (ms_per_step / 1000.0) / 1e12,
+        "fp64_frac": B_loc * total_fl / (ms_per_step / 1000.0) / 1e12 / peak_f64,
+        "hbm_gbs": B_loc * cfg.T * (bin_ + bout) / (ms_per_step / 1000.0) / 1e9,
+    }
+    whole["hbm_frac"] = whole["hbm_gbs"] / hbm_peak
+
+    # ---- end-to-end: host buffers through plq_solve_parallel_host
+    e2e = None
+    if not args.no_e2e:
+        hs = HostSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev, pin=True)
+        pinned = {k: torch.from_numpy(v).pin_memory() for k, v in host.items()}
+        for _ in range(max(1, min(args.warmup, 3))):
+            hs.run(pinned)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e_steps = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            hs.run(pinned)                 # synchronizes on the result copy
+        el = (time.perf_counter() - t0) / e_steps
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        e2e = {"value": knots / el, "unit": "knots/s", "h2d_bytes_per_step": int(hs.h2d_bytes) * world,
+               "d2h_bytes_per_step": int(hs.d2h_bytes) * world, "ms_per_step": el * 1000.0,
+               "api": "plq_solve_parallel_host (pinned host inputs -> host LqrSolution arrays)"}
+        del hs, pinned
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = time_cpu(cfg, args.seed, steps=3, warmup=1)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "knots/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE.json recipe, seeded numpy generator, see synth.py)",
+            "config": {"workload": cfg.name, "B": cfg.B, "n": cfg.n, "m": cfg.m, "T": cfg.T, "J": cfg.J,
+                       "global_batch": cfg.B, "parallelism": f"batch-shard x{world}" if cfg.B > 1 else "replica",
+                       "l2": "inputs exceed L2" if flush is None else "L2 flushed between steps"},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "sweep_kernel (K1, DMMA.8x8x4 fp64)",
+                         "achieved": achieved, "peak": peak_f64, "unit": "TFLOP/s",
+                         "frac": achieved / peak_f64, "traffic": traffic,
+                         "peak_source": "measured fp64 (tools/fp64_peak.cu, profiles/fp64_peak.json)",
+                         "algorithmic_flops_per_launch": B_loc * sweep_fl,
+                         "algorithmic_bytes_per_launch": sweep_b,
+                         "hbm_frac": sweep_b / (phase_ms["sweep"] / 1000.0) / 1e9 / hbm_peak,
+                         "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src},
+            "whole_solve": whole,
+            "phases_ms": phase_ms,
+            "clocks": sampler.report(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
