@@ -1,6 +1,7 @@
 // C-ABI layer (include/parlqr_b200.h): argument checks, workspace carving,
 // and the stream-ordered phase sequence of one partitioned solve.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -11,6 +12,16 @@ namespace {
 
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
+
+// PLQ_FORCE_GENERIC=1 routes every shape through the generic kernels (tests
+// use it to keep the generic path covered on the config shapes).
+bool force_generic() {
+  const char* e = getenv("PLQ_FORCE_GENERIC");
+  return e && e[0] == '1';
+}
+bool use_small_sweep(const plq_problem_t* p) { return !force_generic() && plq::sweep_small_supported(p->n, p->m); }
+bool use_small_recon(const plq_problem_t* p) { return !force_generic() && plq::recon_small_supported(p->n, p->m); }
+bool use_seq_link(const plq_problem_t* p) { return !force_generic() && plq::link_seq_supported(p->n, p->J); }
 
 int fail(int code, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -73,7 +84,8 @@ Plan make_plan(const plq_problem_t* p) {
   P.off_gs = off;
   off += up2((size_t)P.grid_max * P.lay.gmem_doubles);
   P.off_link = off;
-  off += up2(plq::link_workspace_doubles(B, p->J, p->n));
+  off += up2(std::max(plq::link_workspace_doubles(B, p->J, p->n),
+                      use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0)));
   P.total_doubles = off;
   return P;
 }
@@ -116,7 +128,8 @@ int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
   a.seg_end = j1;
   const int64_t tasks = p->B * (int64_t)(j1 - j0);
   const int grid = (int)std::min<int64_t>(tasks, c.P.grid_max);
-  if (plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s)) return cuda_fail("sweep launch");
+  const int rc = use_small_sweep(p) ? plq::launch_sweep_small(a, c.s) : plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s);
+  if (rc) return cuda_fail("sweep launch");
   ++g_launches;
   return PLQ_OK;
 }
@@ -124,8 +137,15 @@ int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
 int phase_link(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c) {
   if (!o->links || !o->link_residual || !o->vf0 || !o->status) return fail(PLQ_ERR_ARG, "null link output");
   int nl = 0;
-  if (plq::launch_link_solve(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s, &nl))
+  if (p->J < 2) return PLQ_OK;
+  if (use_seq_link(p)) {
+    if (plq::launch_link_seq(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s))
+      return cuda_fail("link launch");
+    nl = 1;
+  } else if (plq::launch_link_solve(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s,
+                                    &nl)) {
     return cuda_fail("link launch");
+  }
   g_launches += nl;
   return PLQ_OK;
 }
@@ -162,7 +182,9 @@ int phase_recon(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
   int rc = check_recon_out(o);
   if (rc) return rc;
   if (j0 < 0 || j1 > p->J || j0 >= j1) return fail(PLQ_ERR_ARG, "bad segment range");
-  if (plq::launch_recon(recon_args(p, o, c, j0, j1, part), c.s)) return cuda_fail("recon launch");
+  const plq::ReconArgs ra = recon_args(p, o, c, j0, j1, part);
+  if (use_small_recon(p) ? plq::launch_recon_small(ra, c.s) : plq::launch_recon(ra, c.s))
+    return cuda_fail("recon launch");
   ++g_launches;
   return PLQ_OK;
 }

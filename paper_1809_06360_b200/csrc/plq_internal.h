@@ -74,6 +74,16 @@ int launch_finalize(const plq_problem_t& p, const double* part, const double* bp
                     const double* lambda_right, const double* link_res, double* objective, double* kkt,
                     double* mismatch, double* link_residual, cudaStream_t s);
 
+// Specialized small-state kernels (compile-time n, m).
+bool sweep_small_supported(int n, int m);
+int launch_sweep_small(const SweepArgs& a, cudaStream_t s);
+bool recon_small_supported(int n, int m);
+int launch_recon_small(const ReconArgs& a, cudaStream_t s);
+bool link_seq_supported(int n, int J);
+size_t link_seq_workspace_doubles(int64_t B, int J, int n);
+int launch_link_seq(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
+                    int32_t* status, double* ws, cudaStream_t s);
+
 // Link (coupling) solve by block cyclic reduction.
 size_t link_workspace_doubles(int64_t B, int J, int n);
 int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,

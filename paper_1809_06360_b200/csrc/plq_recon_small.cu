@@ -1,0 +1,491 @@
+// K2/K3 specialized for the small-state configs (compile-time n, m; one warp
+// per segment / per problem):
+//   * link_seq_kernel: the reference's sequential block Cholesky of the link
+//     system (endpoint.solve_block_tridiagonal, endpoint.py:410-438, on
+//     (-diag, -sub, rhs) from parallel.py:264-319), one warp per problem --
+//     the right shape when J-1 is small (BASELINE configs 0, 1);
+//   * recon_small_kernel: the reconstruction loop of parallel.py:485-525 plus
+//     the objective / KKT rows of problem.py:366-420, one warp per segment,
+//     lane = state row, stage matrices staged in shared memory (odd strides:
+//     row-per-lane reads are bank-conflict free) with the next stage
+//     prefetched into registers.
+#include "plq_internal.h"
+#include "plq_small.cuh"
+
+namespace plq {
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// reconstruction
+
+template <int N, int M>
+struct RL {
+  static constexpr int LN = N + 1, LM = M + 1;   // odd strides (N, M even here)
+  static constexpr int FX = 0;                  // N x LN
+  static constexpr int FU = FX + N * LN;        // N x LM
+  static constexpr int F1 = FU + N * LM;        // N
+  static constexpr int QXX = F1 + N;            // N x LN
+  static constexpr int QUX = QXX + N * LN;      // M x LN
+  static constexpr int QUU = QUX + M * LN;      // M x LM
+  static constexpr int QX1 = QUU + M * LM;      // N
+  static constexpr int QU1 = QX1 + N;           // M
+  static constexpr int KX = QU1 + M;            // M x LN
+  static constexpr int KZ = KX + M * LN;        // M x LN
+  static constexpr int K1 = KZ + M * LN;        // M
+  static constexpr int STAGE = K1 + M;
+  // vectors
+  static constexpr int X = STAGE, XN = X + N, U = XN + N, KV = U + M, Z = KV + M, A = Z + N, LAM = A + N;
+  static constexpr int TOTAL = (LAM + N + 1) & ~1;
+  // stage element count (global order Fx|Fu|f1|Qxx|Qux|Quu|qx1|qu1|Kx|Kz|k1)
+  static constexpr int SE = 2 * N * N + 2 * N * M + M * M + 2 * N + M + 2 * M * N + M;
+};
+
+template <int N, int M>
+__device__ __forceinline__ const double* recon_elem(const ReconArgs& A, int64_t st, int e, int& dst, bool last) {
+  using S = RL<N, M>;
+  constexpr int NN = N * N, NM = N * M;
+  const plq_problem_t& p = A.p;
+  if (e < NN) { dst = S::FX + (e / N) * S::LN + e % N; return p.Fx + st * NN + e; }
+  e -= NN;
+  if (e < NM) { dst = S::FU + (e / M) * S::LM + e % M; return p.Fu + st * NM + e; }
+  e -= NM;
+  if (e < N) { dst = S::F1 + e; return p.f1 + st * N + e; }
+  e -= N;
+  if (e < NN) { dst = S::QXX + (e / N) * S::LN + e % N; return p.Qxx + st * NN + e; }
+  e -= NN;
+  if (e < NM) { dst = S::QUX + (e / N) * S::LN + e % N; return p.Qux + st * NM + e; }
+  e -= NM;
+  if (e < M * M) { dst = S::QUU + (e / M) * S::LM + e % M; return p.Quu + st * M * M + e; }
+  e -= M * M;
+  if (e < N) { dst = S::QX1 + e; return p.qx1 + st * N + e; }
+  e -= N;
+  if (e < M) { dst = S::QU1 + e; return p.qu1 + st * M + e; }
+  e -= M;
+  if (e < NM) { dst = S::KX + (e / N) * S::LN + e % N; return A.Kx + st * NM + e; }
+  e -= NM;
+  if (e < NM) { dst = S::KZ + (e / N) * S::LN + e % N; return last ? nullptr : A.Kz + st * NM + e; }
+  e -= NM;
+  dst = S::K1 + e;
+  return A.k1 + st * M + e;
+}
+
+template <int N, int M>
+struct RPrefetch {
+  static constexpr int PF = (RL<N, M>::SE + 31) / 32;
+  double v[PF];
+  __device__ __forceinline__ void load(const ReconArgs& A, int64_t st, int lane, bool last) {
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int e = lane + 32 * k;
+      if (e < RL<N, M>::SE) {
+        int d;
+        const double* src = recon_elem<N, M>(A, st, e, d, last);
+        v[k] = src ? __ldg(src) : 0.0;
+      }
+    }
+  }
+  __device__ __forceinline__ void store(const ReconArgs& A, double* sm, int lane) {
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int e = lane + 32 * k;
+      if (e < RL<N, M>::SE) {
+        int d;
+        recon_elem<N, M>(A, 0, e, d, false);
+        sm[d] = v[k];
+      }
+    }
+  }
+};
+
+template <int N, int M>
+__global__ void __launch_bounds__(32) recon_small_kernel(ReconArgs A) {
+  static_assert(N <= 32 && M <= 32, "lane = row");
+  using S = RL<N, M>;
+  extern __shared__ __align__(16) double sm[];
+  const plq_problem_t& p = A.p;
+  const int J = p.J, T = p.T, NN = N * N;
+  const int lane = threadIdx.x;
+  double* x = sm + S::X;
+  double* xn = sm + S::XN;
+  double* uu = sm + S::U;
+  double* kv = sm + S::KV;
+  double* z = sm + S::Z;
+  double* av = sm + S::A;
+  double* lam = sm + S::LAM;
+  const int nloc = A.seg_end - A.seg_begin;
+  const int64_t total = p.B * nloc;
+  for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
+    const int64_t b = task / nloc;
+    const int j = A.seg_begin + (int)(task % nloc);
+    const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
+    const bool last = (j == J - 1);
+    if (lane < N) {
+      const double a0 = (j == 0) ? p.x_init[b * N + lane] : A.links[(b * (J - 1) + (j - 1)) * N + lane];
+      av[lane] = a0;
+      x[lane] = a0;
+      z[lane] = last ? 0.0 : A.links[(b * (J - 1) + j) * N + lane];
+    }
+    RPrefetch<N, M> pf;
+    pf.load(A, b * T + lo, lane, last);
+    pf.store(A, sm, lane);
+    __syncwarp();
+    double obj = 0.0;      // per-lane partial objective
+    double worst = 0.0;    // per-lane KKT partial
+    // ---- forward: fold, rollout, stage cost, g/h (parallel.py:495-502)
+#pragma unroll 1
+    for (int s = 0; s < L; ++s) {
+      const int64_t st = b * T + lo + s;
+      if (s + 1 < L) pf.load(A, st + 1, lane, last);
+      if (lane < M) {
+        double kk = sm[S::K1 + lane];
+        if (!last) {
+          double t = 0.0;
+#pragma unroll
+          for (int c = 0; c < N; ++c) t += sm[S::KZ + lane * S::LN + c] * z[c];
+          kk = t + kk;
+        }
+        kv[lane] = kk;
+        double t = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) t += sm[S::KX + lane * S::LN + c] * x[c];
+        uu[lane] = t + kk;
+      }
+      __syncwarp();
+      if (lane < M) {
+        A.k[st * M + lane] = kv[lane];
+        A.u[st * M + lane] = uu[lane];
+      }
+      if (lane < N) {
+        A.x[(b * (T + 1) + lo + s) * N + lane] = x[lane];
+        const double xi = x[lane];
+        double t0 = 0.0, t1 = 0.0, fx = 0.0, fu = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          t0 += sm[S::QXX + lane * S::LN + c] * x[c];
+          fx += sm[S::FX + lane * S::LN + c] * x[c];
+        }
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          t1 += sm[S::QUX + q * S::LN + lane] * uu[q];
+          fu += sm[S::FU + lane * S::LM + q] * uu[q];
+        }
+        const double qx = sm[S::QX1 + lane];
+        obj += 0.5 * xi * t0 + qx * xi;
+        A.gh[st * (N + M) + lane] = (t0 + t1) + qx;
+        xn[lane] = (fx + fu) + sm[S::F1 + lane];
+      }
+      if (lane < M) {
+        double t2 = 0.0, t3 = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) t2 += sm[S::QUX + lane * S::LN + c] * x[c];
+#pragma unroll
+        for (int q = 0; q < M; ++q) t3 += sm[S::QUU + lane * S::LM + q] * uu[q];
+        const double ui = uu[lane], qu = sm[S::QU1 + lane];
+        obj += 0.5 * ui * t3 + ui * t2 + qu * ui;
+        A.gh[st * (N + M) + N + lane] = (t2 + t3) + qu;
+      }
+      __syncwarp();
+      if (lane < N) x[lane] = xn[lane];
+      if (s + 1 < L) pf.store(A, sm, lane);
+      __syncwarp();
+    }
+    // ---- multiplier seed (parallel.py:505-515)
+    if (last) {
+      if (lane < N) {
+        A.x[(b * (T + 1) + T) * N + lane] = x[lane];
+        double t = 0.0;
+        const double* QT = p.QxxT + b * NN + lane * N;
+#pragma unroll
+        for (int c = 0; c < N; ++c) t += QT[c] * x[c];
+        const double q1 = p.qx1T[b * N + lane];
+        obj += 0.5 * x[lane] * t + q1 * x[lane];
+        const double g = t + q1;
+        lam[lane] = -g;
+        A.lam[(b * (T + 1) + T) * N + lane] = -g;
+        worst = fmax(worst, fabs(g + -g));
+      }
+    } else {
+      if (lane < N) {
+        A.xend[(b * J + j) * N + lane] = x[lane];
+        const double* vf = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          t0 += vf[NN + lane * N + c] * av[c];
+          t1 += vf[2 * NN + lane * N + c] * z[c];
+        }
+        const double mu = -((t0 + t1) + vf[3 * NN + N + lane]);
+        A.mu_left[(b * (J - 1) + j) * N + lane] = mu;
+        lam[lane] = -mu;
+      }
+    }
+    __syncwarp();
+    // ---- backward multiplier recursion (parallel.py:518-523) + interior KKT rows
+#pragma unroll 1
+    for (int s = L - 1; s >= 0; --s) {
+      const int64_t st = b * T + lo + s;
+      const bool interior = last || (s < L - 1);
+      double ln = 0.0;
+      if (lane < N) {
+        const double* Fx = p.Fx + st * NN;
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) t += __ldg(Fx + k * N + lane) * lam[k];
+        const double g = A.gh[st * (N + M) + lane];
+        ln = t - g;
+        A.lam[(b * (T + 1) + lo + s) * N + lane] = ln;
+        if (interior) worst = fmax(worst, fabs((g + ln) - t));
+      }
+      if (lane < M && interior) {
+        const double* Fu = p.Fu + st * N * M;
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) t += __ldg(Fu + k * M + lane) * lam[k];
+        worst = fmax(worst, fabs(A.gh[st * (N + M) + N + lane] - t));
+      }
+      __syncwarp();
+      if (lane < N) lam[lane] = ln;
+      __syncwarp();
+    }
+    if (j > 0 && lane < N) A.lambda_right[(b * (J - 1) + (j - 1)) * N + lane] = lam[lane];
+    obj = warp_sum(obj);
+    worst = warp_max(worst);
+    if (lane == 0) {
+      A.part[(b * J + j) * 3 + 0] = obj;
+      A.part[(b * J + j) * 3 + 1] = worst;
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// sequential link solve, one warp per problem
+
+template <int N>
+struct LL {
+  static constexpr int LD = N + 1;
+  static constexpr int P = 0;              // N x LD   pivot block / its Cholesky factor
+  static constexpr int R = P + N * LD;     // N x (N+1) right-hand sides [S_i' | g]
+  static constexpr int SP = R + N * LD;    // N x LD   S_{i-1} = A(i, i-1)
+  static constexpr int D = SP + N * LD;    // N        d_{i-1}
+  static constexpr int TOTAL = (D + N + 1) & ~1;
+};
+
+template <int N>
+__device__ __forceinline__ void warp_chol(double* A, int* fail) {
+  constexpr int LD = N + 1;
+  const int lane = threadIdx.x & 31;
+  int bad = 0;
+  for (int k = 0; k < N; ++k) {
+    const double dkk = A[k * LD + k];
+    if (!(dkk > 0.0)) bad = 1;
+    const double d = sqrt(dkk > 0.0 ? dkk : 1.0);
+    __syncwarp();
+    if (lane == k) A[k * LD + k] = d;
+    if (lane > k && lane < N) A[lane * LD + k] /= d;
+    __syncwarp();
+    if (lane > k && lane < N) {
+      const double lik = A[lane * LD + k];
+      for (int jj = k + 1; jj <= lane; ++jj) A[lane * LD + jj] -= lik * A[jj * LD + k];
+    }
+    __syncwarp();
+  }
+  *fail = bad;
+}
+
+// X <- L^{-T} L^{-1} X for the N x C block X (stride N+1), lane per column
+template <int N, int C>
+__device__ __forceinline__ void warp_cho_solve(const double* Lc, double* X) {
+  constexpr int LD = N + 1;
+  const int lane = threadIdx.x & 31;
+  for (int col = lane; col < C; col += 32) {
+    double x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double v = X[i * LD + col];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v -= Lc[i * LD + k] * x[k];
+      x[i] = v / Lc[i * LD + i];
+    }
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) {
+      double v = x[i];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) v -= Lc[k * LD + i] * x[k];
+      x[i] = v / Lc[i * LD + i];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) X[i * LD + col] = x[i];
+  }
+  __syncwarp();
+}
+
+template <int N>
+__global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const double* vf0, double* links,
+                                                     double* link_residual, int32_t* status, double* Xs,
+                                                     double* ds) {
+  using S = LL<N>;
+  constexpr int LD = S::LD, NN = N * N, VS = 3 * NN + 2 * N;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x;
+  const int J = p.J, K = J - 1;
+  double* Pm = sm + S::P;
+  double* R = sm + S::R;
+  double* Sp = sm + S::SP;
+  double* dprev = sm + S::D;
+  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+    const double* vf = vf0 + b * (int64_t)J * VS;
+    double* X = Xs + b * (int64_t)K * NN;
+    double* d = ds + b * (int64_t)K * N;
+    int bad = 0;
+    for (int i = 0; i < K; ++i) {
+      const double* left = vf + i * VS;         // segment i (endpoint)
+      const double* right = vf + (i + 1) * VS;  // segment i+1
+      // P = Vzz0_i + Vxx0_{i+1}  (- S_{i-1} X_{i-1});  R = [S_i' | b_i]
+      for (int idx = lane; idx < NN; idx += 32) {
+        const int r = idx / N, c = idx % N;
+        Pm[r * LD + c] = left[2 * NN + idx] + right[idx];
+        R[r * LD + c] = (i + 1 < K) ? right[NN + c * N + r] : 0.0;   // S_i' = Vzx0_{i+1}'
+      }
+      if (lane < N) {
+        double v = -left[3 * NN + N + lane] + -right[3 * NN + lane];
+        if (i == 0) {
+          double s = 0.0;
+          for (int c = 0; c < N; ++c) s += left[NN + lane * N + c] * p.x_init[b * N + c];
+          v += -s;
+        }
+        R[lane * LD + N] = v;
+      }
+      __syncwarp();
+      if (i > 0) {
+        // P -= S_{i-1} X_{i-1};  g = b_i - S_{i-1} d_{i-1}   (S_{i-1} = Vzx0_i in Sp)
+        for (int idx = lane; idx < NN; idx += 32) {
+          const int r = idx / N, c = idx % N;
+          double t = 0.0;
+          for (int k = 0; k < N; ++k) t += Sp[r * LD + k] * X[(i - 1) * NN + k * N + c];
+          Pm[r * LD + c] -= t;
+        }
+        if (lane < N) {
+          double t = 0.0;
+          for (int k = 0; k < N; ++k) t += Sp[lane * LD + k] * dprev[k];
+          R[lane * LD + N] -= t;
+        }
+        __syncwarp();
+      }
+      int f;
+      warp_chol<N>(Pm, &f);
+      bad |= f;
+      warp_cho_solve<N, N + 1>(Pm, R);
+      // store X_i = P^{-1} S_i' and d_i; keep S_i = Vzx0_{i+1} for the next block
+      for (int idx = lane; idx < NN; idx += 32) {
+        const int r = idx / N, c = idx % N;
+        X[i * NN + idx] = R[r * LD + c];
+        Sp[r * LD + c] = (i + 1 < K) ? right[NN + idx] : 0.0;
+      }
+      if (lane < N) {
+        d[i * N + lane] = R[lane * LD + N];
+        dprev[lane] = R[lane * LD + N];
+      }
+      __syncwarp();
+    }
+    // back substitution: out_{K-1} = d_{K-1}; out_i = d_i - X_i out_{i+1}
+    double* out = links + b * (int64_t)K * N;
+    if (lane < N) out[(K - 1) * N + lane] = d[(K - 1) * N + lane];
+    __syncwarp();
+    for (int i = K - 2; i >= 0; --i) {
+      if (lane < N) {
+        double t = 0.0;
+        for (int c = 0; c < N; ++c) t += X[i * NN + lane * N + c] * out[(i + 1) * N + c];
+        out[i * N + lane] = d[i * N + lane] - t;
+      }
+      __syncwarp();
+    }
+    // residual of the link equations at the solution (parallel.py:273-282)
+    double worst = 0.0;
+    for (int i = 0; i < K; ++i) {
+      if (lane < N) {
+        const double* left = vf + i * VS;
+        const double* right = vf + (i + 1) * VS;
+        double s = 0.0;
+        for (int c = 0; c < N; ++c) s += (left[2 * NN + lane * N + c] + right[lane * N + c]) * out[i * N + c];
+        if (i >= 1)
+          for (int c = 0; c < N; ++c) s += left[NN + lane * N + c] * out[(i - 1) * N + c];
+        if (i + 1 < K)
+          for (int c = 0; c < N; ++c) s += right[NN + c * N + lane] * out[(i + 1) * N + c];
+        double rhs = -left[3 * NN + N + lane] + -right[3 * NN + lane];
+        if (i == 0) {
+          double t = 0.0;
+          for (int c = 0; c < N; ++c) t += left[NN + lane * N + c] * p.x_init[b * N + c];
+          rhs += -t;
+        }
+        worst = fmax(worst, fabs(s - rhs));
+      }
+    }
+    worst = warp_max(worst);
+    if (lane == 0) {
+      link_residual[b] = worst;
+      if (bad && status[b * J] == 0) status[b * J] = PLQ_STATUS_LINK_SINGULAR;
+    }
+    __syncwarp();
+  }
+}
+
+int sms_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+template <int N, int M>
+int launch_recon_t(const ReconArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * RL<N, M>::TOTAL;
+  const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
+  const int64_t cap = (int64_t)sms_count() * 32;
+  const int grid = (int)(tasks < cap ? tasks : cap);
+  if (grid <= 0) return 0;
+  recon_small_kernel<N, M><<<grid, 32, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+template <int N>
+int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, double* link_residual, int32_t* status,
+                  double* ws, cudaStream_t s) {
+  const size_t smem = sizeof(double) * LL<N>::TOTAL;
+  const int64_t cap = (int64_t)sms_count() * 32;
+  const int grid = (int)(p.B < cap ? p.B : cap);
+  double* Xs = ws;
+  double* ds = ws + p.B * (int64_t)(p.J - 1) * N * N;
+  link_seq_kernel<N><<<grid, 32, smem, s>>>(p, vf0, links, link_residual, status, Xs, ds);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace
+
+// n = 32 would need ~100 prefetch registers per lane with one warp per
+// segment; it stays on the generic reconstruction for now
+bool recon_small_supported(int n, int m) { return n == 12 && m == 4; }
+
+int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
+  if (a.p.n == 12 && a.p.m == 4) return launch_recon_t<12, 4>(a, s);
+  return -1;
+}
+
+// the sequential link solve is used while the chain is short
+bool link_seq_supported(int n, int J) { return (n == 12 || n == 32) && J - 1 <= 64; }
+
+size_t link_seq_workspace_doubles(int64_t B, int J, int n) { return (size_t)B * (J - 1) * (n * n + n) + 2; }
+
+int launch_link_seq(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
+                    int32_t* status, double* ws, cudaStream_t s) {
+  if (p.J < 2) return 0;
+  if (p.n == 12) return launch_link_t<12>(p, vf0, links, link_residual, status, ws, s);
+  if (p.n == 32) return launch_link_t<32>(p, vf0, links, link_residual, status, ws, s);
+  return -1;
+}
+
+}  // namespace plq

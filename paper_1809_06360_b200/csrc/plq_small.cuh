@@ -1,0 +1,85 @@
+// Compile-time-shape building blocks for the specialized kernels: a "group"
+// of NWG warps cooperates on one segment (NWG = 1 for n <= 16), synchronized
+// with __syncwarp (NWG = 1) or a named barrier, so CTAs can hold several
+// independent segments without CTA-wide barriers.
+#pragma once
+
+#include "plq_device.cuh"
+
+namespace plq {
+
+// smallest v >= x with v % 8 == 4: row strides (in doubles) for which the
+// DMMA fragment loads A[g][q] / B[q][g] (g = lane/4, q = lane%4) hit 16
+// distinct 8-byte banks per half-warp, i.e. are shared-memory conflict-free
+__host__ __device__ constexpr int pad_ld(int x) { return ((x + 3) / 8) * 8 + 4; }
+
+static_assert(pad_ld(12) == 12 && pad_ld(17) == 20 && pad_ld(25) == 28 && pad_ld(32) == 36 && pad_ld(41) == 44 &&
+                  pad_ld(65) == 68 && pad_ld(13) == 20 && pad_ld(4) == 4 && pad_ld(5) == 12,
+              "pad_ld");
+
+template <int NWG>
+__device__ __forceinline__ void gsync(int grp) {
+  if constexpr (NWG == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(NWG * 32) : "memory");
+  }
+}
+
+// Group sum over NWG warps; `red` holds NWG doubles of this group's scratch.
+template <int NWG>
+__device__ __forceinline__ double gsum(double v, double* red, int grp, int gw) {
+  v = warp_sum(v);
+  if constexpr (NWG == 1) {
+    return v;
+  } else {
+    gsync<NWG>(grp);
+    if ((threadIdx.x & 31) == 0) red[gw] = v;
+    gsync<NWG>(grp);
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWG; ++w) t += red[w];
+    return t;
+  }
+}
+
+// C(M x N) = op(A) (M x K) * B (K x N) on the FP64 tensor pipe (DMMA 8x8x4),
+// compile-time shapes and strides.  Rows are processed in 8-row bands, band
+// tm by warp (tm % NWG) of the group; `rows` <= M trims the band loop at run
+// time (constraint-row GEMMs).  epi(i, j, acc) receives each element once.
+template <int M, int N, int K, bool TA, int LDA, int LDB, int NWG, class Epi>
+__device__ __forceinline__ void ggemm(const double* __restrict__ A, const double* __restrict__ B, int gw, Epi epi,
+                                      int rows = M) {
+  constexpr int TM = (M + 7) / 8, TN = (N + 7) / 8, KS = (K + 3) / 4;
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+#pragma unroll 1
+  for (int tm = gw; tm < TM; tm += NWG) {
+    if (tm * 8 >= rows) break;
+    double acc[TN][2];
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn) acc[tn][0] = acc[tn][1] = 0.0;
+    const int i = tm * 8 + g;
+    const bool iok = (M % 8 == 0) ? (i < rows) : (i < M && i < rows);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = ks * 4 + q;
+      const bool kok = (K % 4 == 0) || (k < K);
+      const double a = (iok && kok) ? (TA ? A[k * LDA + i] : A[i * LDA + k]) : 0.0;
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn) {
+        const int j = tn * 8 + g;
+        const double b = (((N % 8 == 0) || (j < N)) && kok) ? B[k * LDB + j] : 0.0;
+        dmma884(acc[tn][0], acc[tn][1], a, b);
+      }
+    }
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tn * 8 + 2 * q + e;
+        if (i < M && i < rows && j < N) epi(i, j, acc[tn][e]);
+      }
+  }
+}
+
+}  // namespace plq

@@ -76,8 +76,18 @@ def test_reference_goldens_small(name):
     assert checked >= 1
 
 
+@pytest.fixture(params=["specialized", "generic"])
+def kernel_path(request, monkeypatch):
+    # PLQ_FORCE_GENERIC=1 routes the config shapes through the generic kernels
+    if request.param == "generic":
+        monkeypatch.setenv("PLQ_FORCE_GENERIC", "1")
+    else:
+        monkeypatch.delenv("PLQ_FORCE_GENERIC", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("name", SYNTH_FIXTURES)
-def test_reference_goldens_configs(name):
+def test_reference_goldens_configs(name, kernel_path):
     cfg, batch, z = load_synth(name)
     g, _ = _gpu_batch(batch, J=cfg.J)
     for i in range(int(z["count"])):
@@ -92,8 +102,8 @@ def test_reference_goldens_configs(name):
 
 
 @pytest.mark.parametrize("cfg_id,T,J,count", [(0, 256, 4, 1), (1, 64, 8, 16), (2, 512, 8, 1),
-                                              (3, 32, 4, 1), (4, 128, 4, 2)])
-def test_gpu_vs_oracle_fresh_seeds(cfg_id, T, J, count):
+                                              (2, 4096, 64, 1), (3, 32, 4, 1), (4, 128, 4, 2)])
+def test_gpu_vs_oracle_fresh_seeds(cfg_id, T, J, count, kernel_path):
     from paper_1809_06360_b200 import synth
     cfg = synth.CONFIGS[cfg_id].scaled(T=T, J=J)
     batch = synth.generate_batch(cfg, seed=4242, count=count)
