@@ -11,6 +11,7 @@
 //     prefetched into registers.
 #include "plq_internal.h"
 #include "plq_small.cuh"
+#include "plq_tma.cuh"
 
 namespace plq {
 
@@ -260,16 +261,216 @@ __global__ void __launch_bounds__(32) recon_small_kernel(ReconArgs A) {
 }
 
 // ----------------------------------------------------------------------------
+// whole-segment variant: the segment's 11 per-stage fields are contiguous
+// L-stage blocks in global memory, so one bulk copy per field (TMA 1-D,
+// cp.async.bulk) stages the entire segment in shared memory; the forward
+// rollout and the backward multiplier recursion then run from smem, and g/h
+// stay on chip.
+
+template <int N, int M, int LMAX>
+struct SegL {
+  static constexpr int NN = N * N, NM = N * M, MM = M * M;
+  static constexpr int FX = 0, FU = FX + LMAX * NN, F1 = FU + LMAX * NM, QXX = F1 + LMAX * N,
+                       QUX = QXX + LMAX * NN, QUU = QUX + LMAX * NM, QX1 = QUU + LMAX * MM, QU1 = QX1 + LMAX * N,
+                       KX = QU1 + LMAX * M, KZ = KX + LMAX * NM, K1 = KZ + LMAX * NM, GH = K1 + LMAX * M,
+                       X = GH + LMAX * (N + M), XN = X + N, U = XN + N, KV = U + M, Z = KV + M, A = Z + N,
+                       LAM = A + N, BAR = (LAM + N + 1) & ~1, TOTAL = BAR + 2;
+  static_assert((FU | F1 | QXX | QUX | QUU | QX1 | QU1 | KX | KZ | K1) % 2 == 0, "16-byte aligned fields");
+};
+
+template <int N, int M, int LMAX>
+__global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
+  using S = SegL<N, M, LMAX>;
+  constexpr int NN = N * N, NM = N * M, MM = M * M;
+  extern __shared__ __align__(16) double sm[];
+  const plq_problem_t& p = A.p;
+  const int J = p.J, T = p.T;
+  const int lane = threadIdx.x;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
+  double* x = sm + S::X;
+  double* xn = sm + S::XN;
+  double* uu = sm + S::U;
+  double* kv = sm + S::KV;
+  double* z = sm + S::Z;
+  double* av = sm + S::A;
+  double* lam = sm + S::LAM;
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  uint32_t phase = 0;
+  const int nloc = A.seg_end - A.seg_begin;
+  const int64_t total = p.B * nloc;
+  for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
+    const int64_t b = task / nloc;
+    const int j = A.seg_begin + (int)(task % nloc);
+    const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
+    const bool last = (j == J - 1);
+    const int64_t s0 = b * T + lo;
+    if (lane == 0) {
+      fence_proxy_async();
+      const uint32_t l8 = (uint32_t)L * 8u;
+      mbar_arrive_tx(bar, l8 * (2 * NN + 4 * NM + MM + 2 * N + 2 * M));   // the 11 fields below
+      bulk_g2s(sm + S::FX, p.Fx + s0 * NN, l8 * NN, bar);
+      bulk_g2s(sm + S::FU, p.Fu + s0 * NM, l8 * NM, bar);
+      bulk_g2s(sm + S::F1, p.f1 + s0 * N, l8 * N, bar);
+      bulk_g2s(sm + S::QXX, p.Qxx + s0 * NN, l8 * NN, bar);
+      bulk_g2s(sm + S::QUX, p.Qux + s0 * NM, l8 * NM, bar);
+      bulk_g2s(sm + S::QUU, p.Quu + s0 * MM, l8 * MM, bar);
+      bulk_g2s(sm + S::QX1, p.qx1 + s0 * N, l8 * N, bar);
+      bulk_g2s(sm + S::QU1, p.qu1 + s0 * M, l8 * M, bar);
+      bulk_g2s(sm + S::KX, A.Kx + s0 * NM, l8 * NM, bar);
+      bulk_g2s(sm + S::KZ, A.Kz + s0 * NM, l8 * NM, bar);   // zeros for the last segment
+      bulk_g2s(sm + S::K1, A.k1 + s0 * M, l8 * M, bar);
+    }
+    if (lane < N) {
+      const double a0 = (j == 0) ? p.x_init[b * N + lane] : A.links[(b * (J - 1) + (j - 1)) * N + lane];
+      av[lane] = a0;
+      x[lane] = a0;
+      z[lane] = last ? 0.0 : A.links[(b * (J - 1) + j) * N + lane];
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    __syncwarp();
+    double obj = 0.0, worst = 0.0;
+    // ---- forward (parallel.py:495-502) + stage costs (problem.py:375-379)
+#pragma unroll 1
+    for (int s = 0; s < L; ++s) {
+      const int64_t st = s0 + s;
+      if (lane < M) {
+        const double* kz = sm + S::KZ + s * NM + lane * N;
+        const double* kx = sm + S::KX + s * NM + lane * N;
+        double t = 0.0, tu = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          t += kz[c] * z[c];
+          tu += kx[c] * x[c];
+        }
+        const double kk = t + sm[S::K1 + s * M + lane];
+        kv[lane] = kk;
+        uu[lane] = tu + kk;
+      }
+      __syncwarp();
+      if (lane < M) {
+        A.k[st * M + lane] = kv[lane];
+        A.u[st * M + lane] = uu[lane];
+      }
+      if (lane < N) {
+        const double xi = x[lane];
+        A.x[(b * (T + 1) + lo + s) * N + lane] = xi;
+        const double* qxx = sm + S::QXX + s * NN + lane * N;
+        const double* fx = sm + S::FX + s * NN + lane * N;
+        double t0 = 0.0, tf = 0.0, t1 = 0.0, tfu = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          t0 += qxx[c] * x[c];
+          tf += fx[c] * x[c];
+        }
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          t1 += sm[S::QUX + s * NM + q * N + lane] * uu[q];
+          tfu += sm[S::FU + s * NM + lane * M + q] * uu[q];
+        }
+        const double qx = sm[S::QX1 + s * N + lane];
+        obj += 0.5 * xi * t0 + qx * xi;
+        sm[S::GH + s * (N + M) + lane] = (t0 + t1) + qx;
+        xn[lane] = (tf + tfu) + sm[S::F1 + s * N + lane];
+      }
+      if (lane < M) {
+        const double* qux = sm + S::QUX + s * NM + lane * N;
+        const double* quu = sm + S::QUU + s * MM + lane * M;
+        double t2 = 0.0, t3 = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) t2 += qux[c] * x[c];
+#pragma unroll
+        for (int q = 0; q < M; ++q) t3 += quu[q] * uu[q];
+        const double ui = uu[lane], qu = sm[S::QU1 + s * M + lane];
+        obj += 0.5 * ui * t3 + ui * t2 + qu * ui;
+        sm[S::GH + s * (N + M) + N + lane] = (t2 + t3) + qu;
+      }
+      __syncwarp();
+      if (lane < N) x[lane] = xn[lane];
+      __syncwarp();
+    }
+    // g/h of the link stage feed the boundary kernel
+    if (lane < N + M) A.gh[(s0 + L - 1) * (N + M) + lane] = sm[S::GH + (L - 1) * (N + M) + lane];
+    // ---- multiplier seed (parallel.py:505-515)
+    if (lane < N) {
+      if (last) {
+        A.x[(b * (T + 1) + T) * N + lane] = x[lane];
+        double t = 0.0;
+        const double* QT = p.QxxT + b * NN + lane * N;
+#pragma unroll
+        for (int c = 0; c < N; ++c) t += QT[c] * x[c];
+        const double q1 = p.qx1T[b * N + lane];
+        obj += 0.5 * x[lane] * t + q1 * x[lane];
+        const double g = t + q1;
+        lam[lane] = -g;
+        A.lam[(b * (T + 1) + T) * N + lane] = -g;
+        worst = fmax(worst, fabs(g + -g));
+      } else {
+        A.xend[(b * J + j) * N + lane] = x[lane];
+        const double* vf = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          t0 += vf[NN + lane * N + c] * av[c];
+          t1 += vf[2 * NN + lane * N + c] * z[c];
+        }
+        const double mu = -((t0 + t1) + vf[3 * NN + N + lane]);
+        A.mu_left[(b * (J - 1) + j) * N + lane] = mu;
+        lam[lane] = -mu;
+      }
+    }
+    __syncwarp();
+    // ---- backward multipliers (parallel.py:518-523) + interior KKT rows
+#pragma unroll 1
+    for (int s = L - 1; s >= 0; --s) {
+      const bool interior = last || (s < L - 1);
+      double ln = 0.0;
+      if (lane < N) {
+        const double* fx = sm + S::FX + s * NN + lane;
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) t += fx[k * N] * lam[k];
+        const double g = sm[S::GH + s * (N + M) + lane];
+        ln = t - g;
+        A.lam[(b * (T + 1) + lo + s) * N + lane] = ln;
+        if (interior) worst = fmax(worst, fabs((g + ln) - t));
+      }
+      if (lane < M && interior) {
+        const double* fu = sm + S::FU + s * NM + lane;
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) t += fu[k * M] * lam[k];
+        worst = fmax(worst, fabs(sm[S::GH + s * (N + M) + N + lane] - t));
+      }
+      __syncwarp();
+      if (lane < N) lam[lane] = ln;
+      __syncwarp();
+    }
+    if (j > 0 && lane < N) A.lambda_right[(b * (J - 1) + (j - 1)) * N + lane] = lam[lane];
+    obj = warp_sum(obj);
+    worst = warp_max(worst);
+    if (lane == 0) {
+      A.part[(b * J + j) * 3 + 0] = obj;
+      A.part[(b * J + j) * 3 + 1] = worst;
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------------------
 // sequential link solve, one warp per problem
 
-template <int N>
+template <int N, int KMAX>
 struct LL {
-  static constexpr int LD = N + 1;
-  static constexpr int P = 0;              // N x LD   pivot block / its Cholesky factor
-  static constexpr int R = P + N * LD;     // N x (N+1) right-hand sides [S_i' | g]
-  static constexpr int SP = R + N * LD;    // N x LD   S_{i-1} = A(i, i-1)
-  static constexpr int D = SP + N * LD;    // N        d_{i-1}
-  static constexpr int TOTAL = (D + N + 1) & ~1;
+  static constexpr int LD = N + 1, NN = N * N;
+  static constexpr int P = 0;               // N x LD   pivot block -> Cholesky factor
+  static constexpr int R = P + N * LD;      // N x LD   [S_i' | g] -> [X_i | d_i]
+  static constexpr int RP = R + N * LD;     // N x LD   [X_{i-1} | d_{i-1}]
+  static constexpr int SR = RP + N * LD;    // N x N    S_i   = Vzx0_{i+1}
+  static constexpr int SP = SR + NN;        // N x N    S_{i-1}
+  static constexpr int D = SP + NN;         // KMAX x N d_i, then the solution
+  static constexpr int TOTAL = (D + KMAX * N + 1) & ~1;
 };
 
 template <int N>
@@ -321,106 +522,127 @@ __device__ __forceinline__ void warp_cho_solve(const double* Lc, double* X) {
   __syncwarp();
 }
 
-template <int N>
+// One warp per problem: the reference's block Cholesky (endpoint.py:410-438)
+// with every vf0 block staged through shared memory in coalesced rows.
+template <int N, int KMAX>
 __global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const double* vf0, double* links,
-                                                     double* link_residual, int32_t* status, double* Xs,
-                                                     double* ds) {
-  using S = LL<N>;
+                                                     double* link_residual, int32_t* status, double* Xs) {
+  using S = LL<N, KMAX>;
   constexpr int LD = S::LD, NN = N * N, VS = 3 * NN + 2 * N;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x;
   const int J = p.J, K = J - 1;
   double* Pm = sm + S::P;
   double* R = sm + S::R;
-  double* Sp = sm + S::SP;
-  double* dprev = sm + S::D;
+  double* RP = sm + S::RP;
+  double* SR = sm + S::SR;
+  double* SP = sm + S::SP;
+  double* dv = sm + S::D;
   for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
     const double* vf = vf0 + b * (int64_t)J * VS;
     double* X = Xs + b * (int64_t)K * NN;
-    double* d = ds + b * (int64_t)K * N;
     int bad = 0;
     for (int i = 0; i < K; ++i) {
-      const double* left = vf + i * VS;         // segment i (endpoint)
-      const double* right = vf + (i + 1) * VS;  // segment i+1
-      // P = Vzz0_i + Vxx0_{i+1}  (- S_{i-1} X_{i-1});  R = [S_i' | b_i]
+      const double* left = vf + i * VS;
+      const double* right = vf + (i + 1) * VS;
       for (int idx = lane; idx < NN; idx += 32) {
-        const int r = idx / N, c = idx % N;
-        Pm[r * LD + c] = left[2 * NN + idx] + right[idx];
-        R[r * LD + c] = (i + 1 < K) ? right[NN + c * N + r] : 0.0;   // S_i' = Vzx0_{i+1}'
+        Pm[(idx / N) * LD + idx % N] = left[2 * NN + idx] + right[idx];
+        SR[idx] = (i + 1 < K) ? right[NN + idx] : 0.0;
       }
       if (lane < N) {
         double v = -left[3 * NN + N + lane] + -right[3 * NN + lane];
         if (i == 0) {
-          double s = 0.0;
-          for (int c = 0; c < N; ++c) s += left[NN + lane * N + c] * p.x_init[b * N + c];
-          v += -s;
+          double t = 0.0;
+          for (int c = 0; c < N; ++c) t += left[NN + lane * N + c] * p.x_init[b * N + c];
+          v += -t;
         }
         R[lane * LD + N] = v;
       }
       __syncwarp();
+      for (int idx = lane; idx < NN; idx += 32) {
+        const int r = idx / N, c = idx % N;
+        R[r * LD + c] = SR[c * N + r];   // S_i'
+      }
       if (i > 0) {
-        // P -= S_{i-1} X_{i-1};  g = b_i - S_{i-1} d_{i-1}   (S_{i-1} = Vzx0_i in Sp)
+        // P -= S_{i-1} X_{i-1} ; g -= S_{i-1} d_{i-1}
         for (int idx = lane; idx < NN; idx += 32) {
           const int r = idx / N, c = idx % N;
           double t = 0.0;
-          for (int k = 0; k < N; ++k) t += Sp[r * LD + k] * X[(i - 1) * NN + k * N + c];
+#pragma unroll
+          for (int k = 0; k < N; ++k) t += SP[r * N + k] * RP[k * LD + c];
           Pm[r * LD + c] -= t;
         }
         if (lane < N) {
           double t = 0.0;
-          for (int k = 0; k < N; ++k) t += Sp[lane * LD + k] * dprev[k];
+#pragma unroll
+          for (int k = 0; k < N; ++k) t += SP[lane * N + k] * RP[k * LD + N];
           R[lane * LD + N] -= t;
         }
-        __syncwarp();
       }
+      __syncwarp();
       int f;
       warp_chol<N>(Pm, &f);
       bad |= f;
       warp_cho_solve<N, N + 1>(Pm, R);
-      // store X_i = P^{-1} S_i' and d_i; keep S_i = Vzx0_{i+1} for the next block
       for (int idx = lane; idx < NN; idx += 32) {
         const int r = idx / N, c = idx % N;
         X[i * NN + idx] = R[r * LD + c];
-        Sp[r * LD + c] = (i + 1 < K) ? right[NN + idx] : 0.0;
+        RP[r * LD + c] = R[r * LD + c];
+        SP[idx] = SR[idx];
       }
       if (lane < N) {
-        d[i * N + lane] = R[lane * LD + N];
-        dprev[lane] = R[lane * LD + N];
+        dv[i * N + lane] = R[lane * LD + N];
+        RP[lane * LD + N] = R[lane * LD + N];
       }
       __syncwarp();
     }
-    // back substitution: out_{K-1} = d_{K-1}; out_i = d_i - X_i out_{i+1}
-    double* out = links + b * (int64_t)K * N;
-    if (lane < N) out[(K - 1) * N + lane] = d[(K - 1) * N + lane];
-    __syncwarp();
+    // back substitution: out_{K-1} = d_{K-1}; out_i = d_i - X_i out_{i+1}  (in place in dv)
     for (int i = K - 2; i >= 0; --i) {
+      for (int idx = lane; idx < NN; idx += 32) Pm[(idx / N) * LD + idx % N] = X[i * NN + idx];
+      __syncwarp();
       if (lane < N) {
         double t = 0.0;
-        for (int c = 0; c < N; ++c) t += X[i * NN + lane * N + c] * out[(i + 1) * N + c];
-        out[i * N + lane] = d[i * N + lane] - t;
+#pragma unroll
+        for (int c = 0; c < N; ++c) t += Pm[lane * LD + c] * dv[(i + 1) * N + c];
+        dv[i * N + lane] -= t;
       }
       __syncwarp();
     }
+    double* out = links + b * (int64_t)K * N;
+    for (int idx = lane; idx < K * N; idx += 32) out[idx] = dv[idx];
     // residual of the link equations at the solution (parallel.py:273-282)
     double worst = 0.0;
     for (int i = 0; i < K; ++i) {
+      const double* left = vf + i * VS;
+      const double* right = vf + (i + 1) * VS;
+      for (int idx = lane; idx < NN; idx += 32) {
+        Pm[(idx / N) * LD + idx % N] = left[2 * NN + idx] + right[idx];   // D_i
+        SP[idx] = left[NN + idx];                                          // S_{i-1} = Vzx0_i
+        SR[idx] = (i + 1 < K) ? right[NN + idx] : 0.0;                     // S_i = Vzx0_{i+1}
+      }
+      __syncwarp();
       if (lane < N) {
-        const double* left = vf + i * VS;
-        const double* right = vf + (i + 1) * VS;
         double s = 0.0;
-        for (int c = 0; c < N; ++c) s += (left[2 * NN + lane * N + c] + right[lane * N + c]) * out[i * N + c];
-        if (i >= 1)
-          for (int c = 0; c < N; ++c) s += left[NN + lane * N + c] * out[(i - 1) * N + c];
-        if (i + 1 < K)
-          for (int c = 0; c < N; ++c) s += right[NN + c * N + lane] * out[(i + 1) * N + c];
+#pragma unroll
+        for (int c = 0; c < N; ++c) s += Pm[lane * LD + c] * dv[i * N + c];
+        if (i >= 1) {
+#pragma unroll
+          for (int c = 0; c < N; ++c) s += SP[lane * N + c] * dv[(i - 1) * N + c];
+        }
+        if (i + 1 < K) {
+#pragma unroll
+          for (int c = 0; c < N; ++c) s += SR[c * N + lane] * dv[(i + 1) * N + c];
+        }
         double rhs = -left[3 * NN + N + lane] + -right[3 * NN + lane];
         if (i == 0) {
           double t = 0.0;
-          for (int c = 0; c < N; ++c) t += left[NN + lane * N + c] * p.x_init[b * N + c];
+#pragma unroll
+          for (int c = 0; c < N; ++c) t += SP[lane * N + c] * p.x_init[b * N + c];
           rhs += -t;
         }
         worst = fmax(worst, fabs(s - rhs));
       }
+      __syncwarp();
     }
     worst = warp_max(worst);
     if (lane == 0) {
@@ -441,6 +663,24 @@ int sms_count() {
   return sms;
 }
 
+template <int N, int M, int LMAX>
+int launch_recon_seg(const ReconArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * SegL<N, M, LMAX>::TOTAL;
+  auto kern = recon_seg_kernel<N, M, LMAX>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
+  const int per_sm = (int)((227 * 1024) / (smem + 1024));
+  const int64_t cap = (int64_t)sms_count() * (per_sm > 0 ? per_sm : 1);
+  const int grid = (int)(tasks < cap ? tasks : cap);
+  if (grid <= 0) return 0;
+  kern<<<grid, 32, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 template <int N, int M>
 int launch_recon_t(const ReconArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(double) * RL<N, M>::TOTAL;
@@ -455,12 +695,17 @@ int launch_recon_t(const ReconArgs& a, cudaStream_t s) {
 template <int N>
 int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, double* link_residual, int32_t* status,
                   double* ws, cudaStream_t s) {
-  const size_t smem = sizeof(double) * LL<N>::TOTAL;
+  constexpr int KMAX = 64;
+  const size_t smem = sizeof(double) * LL<N, KMAX>::TOTAL;
+  auto kern = link_seq_kernel<N, KMAX>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   const int64_t cap = (int64_t)sms_count() * 32;
   const int grid = (int)(p.B < cap ? p.B : cap);
-  double* Xs = ws;
-  double* ds = ws + p.B * (int64_t)(p.J - 1) * N * N;
-  link_seq_kernel<N><<<grid, 32, smem, s>>>(p, vf0, links, link_residual, status, Xs, ds);
+  kern<<<grid, 32, smem, s>>>(p, vf0, links, link_residual, status, ws);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -471,20 +716,23 @@ int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, doub
 bool recon_small_supported(int n, int m) { return n == 12 && m == 4; }
 
 int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
-  if (a.p.n == 12 && a.p.m == 4) return launch_recon_t<12, 4>(a, s);
+  if (a.p.n == 12 && a.p.m == 4) {
+    // whole segment on chip when it fits (BASELINE config 1: L = 8)
+    if (a.p.max_seg_len <= 8) return launch_recon_seg<12, 4, 8>(a, s);
+    return launch_recon_t<12, 4>(a, s);
+  }
   return -1;
 }
 
 // the sequential link solve is used while the chain is short
-bool link_seq_supported(int n, int J) { return (n == 12 || n == 32) && J - 1 <= 64; }
+bool link_seq_supported(int n, int J) { return n == 12 && J - 1 <= 64; }
 
-size_t link_seq_workspace_doubles(int64_t B, int J, int n) { return (size_t)B * (J - 1) * (n * n + n) + 2; }
+size_t link_seq_workspace_doubles(int64_t B, int J, int n) { return (size_t)B * (J - 1) * n * n + 2; }
 
 int launch_link_seq(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
                     int32_t* status, double* ws, cudaStream_t s) {
   if (p.J < 2) return 0;
   if (p.n == 12) return launch_link_t<12>(p, vf0, links, link_residual, status, ws, s);
-  if (p.n == 32) return launch_link_t<32>(p, vf0, links, link_residual, status, ws, s);
   return -1;
 }
 

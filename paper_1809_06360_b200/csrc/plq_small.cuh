@@ -43,32 +43,32 @@ __device__ __forceinline__ double gsum(double v, double* red, int grp, int gw) {
   }
 }
 
-// C(M x N) = op(A) (M x K) * B (K x N) on the FP64 tensor pipe (DMMA 8x8x4),
-// compile-time shapes and strides.  Rows are processed in 8-row bands, band
-// tm by warp (tm % NWG) of the group; `rows` <= M trims the band loop at run
-// time (constraint-row GEMMs).  epi(i, j, acc) receives each element once.
-template <int M, int N, int K, bool TA, int LDA, int LDB, int NWG, class Epi>
-__device__ __forceinline__ void ggemm(const double* __restrict__ A, const double* __restrict__ B, int gw, Epi epi,
-                                      int rows = M) {
+// C(M x N) = A (M x K) * B (K x N) on the FP64 tensor pipe (DMMA 8x8x4),
+// compile-time shapes, operands supplied by loader functors aload(i, k) /
+// bload(k, j) (only called in range).  Rows are processed in 8-row bands,
+// band tm by warp (tm % NWG) of the group; `rows` <= M trims the bands at
+// run time (constraint-row GEMMs).  With a single-warp group the band loop
+// is unrolled so independent DMMA chains of different bands interleave.
+// epi(i, j, acc) receives each element once.
+template <int M, int N, int K, int NWG, class AL, class BL, class Epi>
+__device__ __forceinline__ void ggemm_f(AL aload, BL bload, int gw, Epi epi, int rows = M) {
   constexpr int TM = (M + 7) / 8, TN = (N + 7) / 8, KS = (K + 3) / 4;
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-#pragma unroll 1
-  for (int tm = gw; tm < TM; tm += NWG) {
-    if (tm * 8 >= rows) break;
+  auto band = [&](int tm) {
     double acc[TN][2];
 #pragma unroll
     for (int tn = 0; tn < TN; ++tn) acc[tn][0] = acc[tn][1] = 0.0;
     const int i = tm * 8 + g;
-    const bool iok = (M % 8 == 0) ? (i < rows) : (i < M && i < rows);
+    const bool iok = (i < M) && (i < rows);
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int k = ks * 4 + q;
       const bool kok = (K % 4 == 0) || (k < K);
-      const double a = (iok && kok) ? (TA ? A[k * LDA + i] : A[i * LDA + k]) : 0.0;
+      const double a = (iok && kok) ? aload(i, k) : 0.0;
 #pragma unroll
       for (int tn = 0; tn < TN; ++tn) {
         const int j = tn * 8 + g;
-        const double b = (((N % 8 == 0) || (j < N)) && kok) ? B[k * LDB + j] : 0.0;
+        const double b = (((N % 8 == 0) || (j < N)) && kok) ? bload(k, j) : 0.0;
         dmma884(acc[tn][0], acc[tn][1], a, b);
       }
     }
@@ -77,9 +77,28 @@ __device__ __forceinline__ void ggemm(const double* __restrict__ A, const double
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = tn * 8 + 2 * q + e;
-        if (i < M && i < rows && j < N) epi(i, j, acc[tn][e]);
+        if (iok && j < N) epi(i, j, acc[tn][e]);
       }
+  };
+  if constexpr (NWG == 1) {
+#pragma unroll
+    for (int tm = 0; tm < TM; ++tm)
+      if (tm * 8 < rows) band(tm);
+  } else {
+#pragma unroll 1
+    for (int tm = gw; tm < TM; tm += NWG) {
+      if (tm * 8 >= rows) break;
+      band(tm);
+    }
   }
+}
+
+// pointer-operand form: A row-major (or transposed, TA) with stride LDA, B row-major stride LDB
+template <int M, int N, int K, bool TA, int LDA, int LDB, int NWG, class Epi>
+__device__ __forceinline__ void ggemm(const double* __restrict__ A, const double* __restrict__ B, int gw, Epi epi,
+                                      int rows = M) {
+  ggemm_f<M, N, K, NWG>([&](int i, int k) { return TA ? A[k * LDA + i] : A[i * LDA + k]; },
+                        [&](int k, int j) { return B[k * LDB + j]; }, gw, epi, rows);
 }
 
 }  // namespace plq

@@ -4,15 +4,21 @@
 // Same recurrences as the generic sweep (plq_sweep.cu; endpoint.py:168-301,
 // serial.py:37-79), restructured for latency:
 //   * one group of NWG warps per segment, group barriers only;
-//   * every buffer in shared memory with strides = 4 (mod 8) doubles so the
-//     DMMA fragment loads are bank-conflict free;
+//   * each stage's inputs arrive by bulk asynchronous copy (TMA 1-D,
+//     cp.async.bulk) into a shared staging buffer; the copy for stage s-1 is
+//     issued as soon as stage s has consumed its inputs, so it overlaps the
+//     gain / value-update half of the stage;
+//   * GEMM operands are read straight from the staged fields ([Fx|Fu|f1] by a
+//     loader functor) -- no re-layout pass; other buffers use strides = 4
+//     (mod 8) doubles so the DMMA fragment loads are bank-conflict free;
 //   * GEMM epilogues write in place: GEMM1 puts Mzx straight into Vzx (band
 //     by band -- a band only reads its own rows) and Mzu' into P, GEMM2 puts
 //     Mxx/mx1 into Vxx/vx1, and the value update accumulates into V;
-//   * the next stage's inputs are loaded into registers while the current
-//     stage computes (software pipelining over the stage loop).
+//   * the m x m Cholesky of Muu is computed redundantly in every lane's
+//     registers (m <= 8), so the gain solve needs no barrier.
 #include "plq_internal.h"
 #include "plq_small.cuh"
+#include "plq_tma.cuh"
 
 namespace plq {
 
@@ -20,109 +26,82 @@ namespace {
 
 template <int N, int M>
 struct SL {
-  static constexpr int NN = N * N;
+  static constexpr int NN = N * N, NM = N * M, MM = M * M;
   static constexpr int LDN = pad_ld(N);
   static constexpr int FW = N + M + 1;
   static constexpr int LDF = pad_ld(FW);
   static constexpr int WE = 2 * N + 1;
   static constexpr int LDW = pad_ld(WE);
-  static constexpr int SE = 2 * NN + 2 * N * M + M * M + 2 * N + M;   // stage input doubles
+  // Fx rows are staged row by row with a padded stride when N is not already
+  // conflict-free (N % 8 != 4)
+  static constexpr bool FX_ROWS = (N % 8) != 4;
+  static constexpr int LFX = FX_ROWS ? pad_ld(N) : N;
+  static constexpr bool FU_ROWS = (M % 8) != 4 && M > 4;
+  static constexpr int LFU = FU_ROWS ? pad_ld(M) : M;
   static constexpr int V = 0;                    // Vxx, Vzx, Vzz: 3 x (N x LDN)
   static constexpr int VX1 = V + 3 * N * LDN;
   static constexpr int VZ1 = VX1 + N;
-  static constexpr int F = (VZ1 + N + 1) & ~1;   // [Fx | Fu | f1]  N x LDF
-  static constexpr int QXX = F + N * LDF;        // flat N x N
-  static constexpr int QUX = QXX + NN;           // M x N
-  static constexpr int QUU = QUX + M * N;        // M x M
-  static constexpr int QX1 = QUU + M * M;        // N
-  static constexpr int QU1 = QX1 + N;            // M
-  static constexpr int VF = (QU1 + M + 1) & ~1;  // N x LDF (also N = Hx F)
-  static constexpr int P = VF + N * LDF;         // P, G, Y: M x LDW each, contiguous
+  // staged stage inputs (16-byte aligned fields)
+  static constexpr int SFX = (VZ1 + N + 1) & ~1;        // N x LFX
+  static constexpr int SFU = SFX + N * LFX;             // N x LFU
+  static constexpr int SF1 = SFU + N * LFU;             // N
+  static constexpr int SQXX = SF1 + N;                  // N x N
+  static constexpr int SQUX = SQXX + NN;                // M x N
+  static constexpr int SQUU = SQUX + NM;                // M x M
+  static constexpr int SQX1 = SQUU + MM;                // N
+  static constexpr int SQU1 = SQX1 + N;                 // M
+  static constexpr int VF = (SQU1 + M + 1) & ~1;        // N x LDF (also N = Hx F)
+  static constexpr int P = VF + N * LDF;                // P, G, Y: M x LDW each, contiguous
   static constexpr int G = P + M * LDW;
   static constexpr int Y = G + M * LDW;
-  static constexpr int MUU = Y + M * LDW;        // M x M
-  static constexpr int LM = MUU + M * M;         // M x M Cholesky factor
-  static constexpr int IDG = LM + M * M;         // M   1 / L_ii
-  static constexpr int H = IDG + M;              // N x LDW constraint rows [Hx | Hz | h1]
-  static constexpr int TAU = H + N * LDW;        // M
-  static constexpr int RD = TAU + M;             // M
-  static constexpr int RED = RD + M;             // 8
-  static constexpr int FLG = RED + 8;            // ints
-  static constexpr int TOTAL = (FLG + 2 + 1) & ~1;
+  static constexpr int MUU = Y + M * LDW;               // M x M
+  static constexpr int H = MUU + MM;                    // N x LDW constraint rows [Hx | Hz | h1]
+  static constexpr int TAU = H + N * LDW;               // M
+  static constexpr int RD = TAU + M;                    // M
+  static constexpr int RED = RD + M;                    // 8
+  static constexpr int BAR = (RED + 8 + 1) & ~1;        // mbarrier (8 bytes)
+  static constexpr int TOTAL = BAR + 2;
+  static constexpr uint32_t STAGE_BYTES = 8u * (2 * NN + 2 * NM + MM + 2 * N + M);
+  static_assert(SFX % 2 == 0 && SFU % 2 == 0 && SF1 % 2 == 0 && SQXX % 2 == 0 && SQUX % 2 == 0 &&
+                    SQUU % 2 == 0 && SQX1 % 2 == 0 && SQU1 % 2 == 0 && (N * 8) % 16 == 0 && (M * 8) % 16 == 0,
+                "bulk copies need 16-byte alignment");
 };
 
-// stage element e (concatenation Fx|Fu|f1|Qxx|Qux|Quu|qx1|qu1) -> source
-// address in global memory and destination offset in the group's smem
+// issue the bulk copies of stage `st` into the staging fields (one thread)
 template <int N, int M>
-__device__ __forceinline__ const double* stage_elem(const plq_problem_t& p, int64_t st, int e, int& dst) {
+__device__ __forceinline__ void stage_issue(const plq_problem_t& p, int64_t st, double* sm, uint64_t* bar) {
   using S = SL<N, M>;
-  constexpr int NN = N * N, NM = N * M;
-  if (e < NN) {
-    dst = S::F + (e / N) * S::LDF + e % N;
-    return p.Fx + st * NN + e;
+  constexpr int NN = N * N, NM = N * M, MM = M * M;
+  fence_proxy_async();
+  mbar_arrive_tx(bar, S::STAGE_BYTES);
+  if constexpr (S::FX_ROWS) {
+#pragma unroll 1
+    for (int r = 0; r < N; ++r) bulk_g2s(sm + S::SFX + r * S::LFX, p.Fx + st * NN + r * N, 8u * N, bar);
+  } else {
+    bulk_g2s(sm + S::SFX, p.Fx + st * NN, 8u * NN, bar);
   }
-  e -= NN;
-  if (e < NM) {
-    dst = S::F + (e / M) * S::LDF + N + e % M;
-    return p.Fu + st * NM + e;
+  if constexpr (S::FU_ROWS) {
+#pragma unroll 1
+    for (int r = 0; r < N; ++r) bulk_g2s(sm + S::SFU + r * S::LFU, p.Fu + st * NM + r * M, 8u * M, bar);
+  } else {
+    bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
   }
-  e -= NM;
-  if (e < N) {
-    dst = S::F + e * S::LDF + N + M;
-    return p.f1 + st * N + e;
-  }
-  e -= N;
-  if (e < NN) {
-    dst = S::QXX + e;
-    return p.Qxx + st * NN + e;
-  }
-  e -= NN;
-  if (e < NM) {
-    dst = S::QUX + e;
-    return p.Qux + st * NM + e;
-  }
-  e -= NM;
-  if (e < M * M) {
-    dst = S::QUU + e;
-    return p.Quu + st * (M * M) + e;
-  }
-  e -= M * M;
-  if (e < N) {
-    dst = S::QX1 + e;
-    return p.qx1 + st * N + e;
-  }
-  e -= N;
-  dst = S::QU1 + e;
-  return p.qu1 + st * M + e;
+  bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
+  bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
+  bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
+  bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
+  bulk_g2s(sm + S::SQX1, p.qx1 + st * N, 8u * N, bar);
+  bulk_g2s(sm + S::SQU1, p.qu1 + st * M, 8u * M, bar);
 }
 
-template <int N, int M, int NWG>
-struct Prefetch {
-  static constexpr int NT = NWG * 32;
-  static constexpr int PF = (SL<N, M>::SE + NT - 1) / NT;
-  double v[PF];
-  __device__ __forceinline__ void load(const plq_problem_t& p, int64_t st, int gt) {
-#pragma unroll
-    for (int k = 0; k < PF; ++k) {
-      const int e = gt + k * NT;
-      if (e < SL<N, M>::SE) {
-        int d;
-        v[k] = __ldg(stage_elem<N, M>(p, st, e, d));
-      }
-    }
-  }
-  __device__ __forceinline__ void store(const plq_problem_t& p, double* sm, int gt) {
-#pragma unroll
-    for (int k = 0; k < PF; ++k) {
-      const int e = gt + k * NT;
-      if (e < SL<N, M>::SE) {
-        int d;
-        stage_elem<N, M>(p, 0, e, d);
-        sm[d] = v[k];
-      }
-    }
-  }
-};
+// F(k, j) = [Fx | Fu | f1](k, j) from the staged fields
+template <int N, int M>
+__device__ __forceinline__ double fload(const double* sm, int k, int j) {
+  using S = SL<N, M>;
+  if (j < N) return sm[S::SFX + k * S::LFX + j];
+  if (j < N + M) return sm[S::SFU + k * S::LFU + (j - N)];
+  return sm[S::SF1 + k];
+}
 
 // Householder QR of the r x M panel A (stride LDA) applied to the r x W block
 // X (stride LDX) -- group version of cta_householder_qr (LAPACK dlarfg
@@ -177,7 +156,8 @@ __device__ __forceinline__ void gqr(double* A, int r, double* X, double* tau, do
 }
 
 template <int N, int M, int NWG, bool SERIAL>
-__device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, int grp, int gt, int64_t b, int j) {
+__device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, int grp, int gt, int64_t b, int j,
+                                              uint32_t& phase) {
   using S = SL<N, M>;
   constexpr int NT = NWG * 32;
   constexpr int NZ = SERIAL ? 0 : N;
@@ -185,6 +165,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   constexpr int W = CC + 1;
   constexpr int LDN = S::LDN, LDF = S::LDF, LDW = S::LDW, FW = S::FW, NN = N * N;
   const int gw = gt >> 5;
+  const int lane = threadIdx.x & 31;
   const plq_problem_t& p = a.p;
   const int T = p.T, J = p.J;
   const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
@@ -193,25 +174,23 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   double* Vzz = Vzx + N * LDN;
   double* vx1 = sm + S::VX1;
   double* vz1 = sm + S::VZ1;
-  double* F = sm + S::F;
-  const double* Qxx = sm + S::QXX;
-  const double* Qux = sm + S::QUX;
-  const double* Quu = sm + S::QUU;
-  const double* qx1 = sm + S::QX1;
-  const double* qu1 = sm + S::QU1;
+  const double* Qxx = sm + S::SQXX;
+  const double* Qux = sm + S::SQUX;
+  const double* Quu = sm + S::SQUU;
+  const double* qx1 = sm + S::SQX1;
+  const double* qu1 = sm + S::SQU1;
   double* VF = sm + S::VF;
   double* P = sm + S::P;
   double* G = sm + S::G;
   double* Y = sm + S::Y;
   double* Muu = sm + S::MUU;
-  double* Lm = sm + S::LM;
-  double* idg = sm + S::IDG;
   double* H = sm + S::H;
   double* tau = sm + S::TAU;
   double* rdiag = sm + S::RD;
   double* red = sm + S::RED;
-  int* flg = reinterpret_cast<int*>(sm + S::FLG);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
 
+  if (gt == 0) stage_issue<N, M>(p, b * T + lo + L - 1, sm, bar);
   for (int idx = gt; idx < S::VZ1 + N; idx += NT) sm[idx] = 0.0;
   gsync<NWG>(grp);
   if (SERIAL) {
@@ -225,76 +204,80 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   }
   int r = SERIAL ? 0 : N;
   int status = 0;
-  Prefetch<N, M, NWG> pf;
-  pf.load(p, b * T + lo + L - 1, gt);
-  pf.store(p, sm, gt);
   gsync<NWG>(grp);
 
 #pragma unroll 1
   for (int s = L - 1; s >= 0; --s) {
     const int64_t st = b * T + lo + s;
-    if (s > 0) pf.load(p, st - 1, gt);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
 
     // GEMM1: [VF; Z] = [Vxx; Vzx] F; Z lands in place: Mzx -> Vzx, Mzu' -> P, mz1 -> vz1
-    ggemm<N + NZ, FW, N, false, LDN, LDF, NWG>(Vxx, F, gw, [&](int i, int c, double acc) {
-      if (i < N) {
-        VF[i * LDF + c] = (c == N + M) ? vx1[i] + acc : acc;
-      } else {
-        const int zi = i - N;
-        if (c < N)
-          Vzx[zi * LDN + c] = acc;
-        else if (c < N + M)
-          P[(c - N) * LDW + N + zi] = acc;
-        else
-          vz1[zi] += acc;
-      }
-    });
+    ggemm_f<N + NZ, FW, N, NWG>(
+        [&](int i, int k) { return Vxx[i * LDN + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
+        [&](int i, int c, double acc) {
+          if (i < N) {
+            VF[i * LDF + c] = (c == N + M) ? vx1[i] + acc : acc;
+          } else {
+            const int zi = i - N;
+            if (c < N)
+              Vzx[zi * LDN + c] = acc;
+            else if (c < N + M)
+              P[(c - N) * LDW + N + zi] = acc;
+            else
+              vz1[zi] += acc;
+          }
+        });
     gsync<NWG>(grp);
     // GEMM2: [Mxx mx1; Mux Muu mu1] = [Fx Fu]' [VFx VFu w] + Q-blocks
-    ggemm<N + M, FW, N, true, LDF, LDF, NWG>(F, VF, gw, [&](int i, int c, double acc) {
-      if (i < N) {
-        if (c < N)
-          Vxx[i * LDN + c] = Qxx[i * N + c] + acc;
-        else if (c == N + M)
-          vx1[i] = qx1[i] + acc;
-      } else {
-        const int u = i - N;
-        if (c < N)
-          P[u * LDW + c] = Qux[u * N + c] + acc;
-        else if (c < N + M)
-          Muu[u * M + (c - N)] = Quu[u * M + (c - N)] + acc;
-        else
-          P[u * LDW + CC] = qu1[u] + acc;
-      }
-    });
+    ggemm_f<N + M, FW, N, NWG>(
+        [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
+        [&](int i, int c, double acc) {
+          if (i < N) {
+            if (c < N)
+              Vxx[i * LDN + c] = Qxx[i * N + c] + acc;
+            else if (c == N + M)
+              vx1[i] = qx1[i] + acc;
+          } else {
+            const int u = i - N;
+            if (c < N)
+              P[u * LDW + c] = Qux[u * N + c] + acc;
+            else if (c < N + M)
+              Muu[u * M + (c - N)] = Quu[u * M + (c - N)] + acc;
+            else
+              P[u * LDW + CC] = qu1[u] + acc;
+          }
+        });
     gsync<NWG>(grp);
 
     if (r == 0) {
-      // ---- unconstrained stage: G = -Muu^{-1} P
-      if (gt == 0) {
-        int fail = 0;
-        for (int k = 0; k < M; ++k) {
-          for (int i = k; i < M; ++i) {
-            double v = Muu[i * M + k];
-            for (int q = 0; q < k; ++q) v -= Lm[i * M + q] * Lm[k * M + q];
-            if (i == k) {
-              if (!(v > 0.0)) {
-                fail = 1;
-                v = 1.0;
-              }
-              v = sqrt(v);
-              Lm[k * M + k] = v;
-              idg[k] = 1.0 / v;
-            } else {
-              Lm[i * M + k] = v * idg[k];
-            }
+      // ---- unconstrained stage: G = -Muu^{-1} P, Cholesky in every lane's registers
+      if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);
+      double Lr[M][M], id[M];
+      int fail = 0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+#pragma unroll
+        for (int i = k; i < M; ++i) {
+          double v = Muu[i * M + k];
+#pragma unroll
+          for (int q = 0; q < k; ++q) v -= Lr[i][q] * Lr[k][q];
+          if (i == k) {
+            fail |= !(v > 0.0);
+            v = sqrt(v > 0.0 ? v : 1.0);
+            Lr[k][k] = v;
+            id[k] = 1.0 / v;
+          } else {
+            Lr[i][k] = v * id[k];
           }
         }
-        flg[0] = fail;
       }
-      gsync<NWG>(grp);
-      if (flg[0]) {
+      if (fail) {
         status = 1 + s;
+        if (s > 0) {   // drain the copy in flight so the barrier phase stays in step
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
         break;
       }
       for (int c = gt; c < W; c += NT) {
@@ -303,15 +286,15 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         for (int i = 0; i < M; ++i) {
           double v = P[i * LDW + c];
 #pragma unroll
-          for (int k = 0; k < i; ++k) v -= Lm[i * M + k] * x[k];
-          x[i] = v * idg[i];
+          for (int k = 0; k < i; ++k) v -= Lr[i][k] * x[k];
+          x[i] = v * id[i];
         }
 #pragma unroll
         for (int i = M - 1; i >= 0; --i) {
           double v = x[i];
 #pragma unroll
-          for (int k = i + 1; k < M; ++k) v -= Lm[k * M + i] * x[k];
-          x[i] = v * idg[i];
+          for (int k = i + 1; k < M; ++k) v -= Lr[k][i] * x[k];
+          x[i] = v * id[i];
         }
 #pragma unroll
         for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
@@ -325,7 +308,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         ph += v * v;
       }
       for (int idx = gt; idx < N * M; idx += NT) {
-        const double v = F[(idx / M) * LDF + N + idx % M];
+        const double v = sm[S::SFU + (idx / M) * S::LFU + idx % M];
         pu += v * v;
       }
       const double hx2 = gsum<NWG>(ph, red, grp, gw);
@@ -333,9 +316,11 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       const double fu2 = gsum<NWG>(pu, red, grp, gw);
       const double nu_scale = sqrt(hx2) * sqrt(fu2);
       // N = Hx F -> VF rows 0..r-1
-      ggemm<N, FW, N, false, LDW, LDF, NWG>(
-          H, F, gw, [&](int i, int c, double acc) { VF[i * LDF + c] = acc; }, r);
+      ggemm_f<N, FW, N, NWG>(
+          [&](int i, int k) { return H[i * LDW + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
+          [&](int i, int c, double acc) { VF[i * LDF + c] = acc; }, r);
       gsync<NWG>(grp);
+      if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
       for (int idx = gt; idx < r * N; idx += NT) {
         const int i = idx / N, c = idx % N;
         H[i * LDW + c] = VF[i * LDF + c];
@@ -351,6 +336,10 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       }
       if (!(rmin > p.rank_tol * fmax(nu_scale, rmax))) {
         status = PLQ_STATUS_DEGENERATE;
+        if (s > 0) {
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
         break;
       }
       for (int c = gt; c < W; c += NT) {
@@ -406,9 +395,10 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       }
     });
     gsync<NWG>(grp);
-    for (int idx = gt; idx < NN; idx += NT) {
-      const int i = idx / N, c = idx % N;
-      if (i < c) {
+    // symmetrize Vxx (and Vzz): lane per row, upper-triangle partner
+    for (int i = gt; i < N; i += NT) {
+#pragma unroll 4
+      for (int c = i + 1; c < N; ++c) {
         const double v = 0.5 * (Vxx[i * LDN + c] + Vxx[c * LDN + i]);
         Vxx[i * LDN + c] = v;
         Vxx[c * LDN + i] = v;
@@ -419,9 +409,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         }
       }
     }
-    if (s > 0) pf.store(p, sm, gt);
     gsync<NWG>(grp);
   }
+  (void)lane;
 
   const int vsz = 3 * NN + 2 * N;
   double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
@@ -443,15 +433,19 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS) sweep_small_kernel(SweepArg
   const int grp = threadIdx.x / (NWG * 32);
   const int gt = threadIdx.x % (NWG * 32);
   double* sm = smem + grp * SL<N, M>::TOTAL;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SL<N, M>::BAR);
+  if (gt == 0) mbar_init(bar, 1);
+  gsync<NWG>(grp);
+  uint32_t phase = 0;
   const int nloc = a.seg_end - a.seg_begin;
   const int64_t total = a.p.B * nloc;
   for (int64_t task = (int64_t)blockIdx.x * GROUPS + grp; task < total; task += (int64_t)gridDim.x * GROUPS) {
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
     if (j == a.p.J - 1)
-      small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j);
+      small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j, phase);
     else
-      small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j);
+      small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j, phase);
   }
 }
 
@@ -459,11 +453,14 @@ template <int N, int M, int NWG, int GROUPS>
 int launch_small(const SweepArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(double) * SL<N, M>::TOTAL * GROUPS;
   auto kern = sweep_small_kernel<N, M, NWG, GROUPS>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0, dev = 0, sms = 148;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWG * 32 * GROUPS, smem);
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int per_sm = -1, sms = 148;
+  if (per_sm < 0) {
+    int dev = 0;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWG * 32 * GROUPS, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
   const int64_t blocks_needed = (tasks + GROUPS - 1) / GROUPS;
   const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
