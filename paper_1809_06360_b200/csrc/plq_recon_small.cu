@@ -267,33 +267,63 @@ __global__ void __launch_bounds__(32) recon_small_kernel(ReconArgs A) {
 // rollout and the backward multiplier recursion then run from smem, and g/h
 // stay on chip.
 
-template <int N, int M, int LMAX>
-struct SegL {
-  static constexpr int NN = N * N, NM = N * M, MM = M * M;
-  static constexpr int FX = 0, FU = FX + LMAX * NN, F1 = FU + LMAX * NM, QXX = F1 + LMAX * N,
-                       QUX = QXX + LMAX * NN, QUU = QUX + LMAX * NM, QX1 = QUU + LMAX * MM, QU1 = QX1 + LMAX * N,
-                       KX = QU1 + LMAX * M, KZ = KX + LMAX * NM, K1 = KZ + LMAX * NM, GH = K1 + LMAX * M,
-                       X = GH + LMAX * (N + M), XN = X + N, U = XN + N, KV = U + M, Z = KV + M, A = Z + N,
-                       LAM = A + N, BAR = (LAM + N + 1) & ~1, TOTAL = BAR + 2;
-  static_assert((FU | F1 | QXX | QUX | QUU | QX1 | QU1 | KX | KZ | K1) % 2 == 0, "16-byte aligned fields");
-};
+template <int N, int M>
+__device__ __forceinline__ void seg_issue(const ReconArgs& A, double* buf, uint64_t* bar, int64_t s0, int L,
+                                          const double* vf, bool endpoint) {
+  constexpr int NN = N * N, NM = N * M, MM = M * M;
+  const plq_problem_t& p = A.p;
+  fence_proxy_async();
+  const uint32_t l8 = (uint32_t)L * 8u;
+  const uint32_t vbytes = endpoint ? 8u * (2 * NN + 2 * N) : 0u;
+  mbar_arrive_tx(bar, l8 * (2 * NN + 4 * NM + MM + 2 * N + 2 * M) + vbytes);   // the fields below
+  double* d = buf;
+  bulk_g2s(d, p.Fx + s0 * NN, l8 * NN, bar);
+  d += L * NN;
+  bulk_g2s(d, p.Fu + s0 * NM, l8 * NM, bar);
+  d += L * NM;
+  bulk_g2s(d, p.f1 + s0 * N, l8 * N, bar);
+  d += L * N;
+  bulk_g2s(d, p.Qxx + s0 * NN, l8 * NN, bar);
+  d += L * NN;
+  bulk_g2s(d, p.Qux + s0 * NM, l8 * NM, bar);
+  d += L * NM;
+  bulk_g2s(d, p.Quu + s0 * MM, l8 * MM, bar);
+  d += L * MM;
+  bulk_g2s(d, p.qx1 + s0 * N, l8 * N, bar);
+  d += L * N;
+  bulk_g2s(d, p.qu1 + s0 * M, l8 * M, bar);
+  d += L * M;
+  bulk_g2s(d, A.Kx + s0 * NM, l8 * NM, bar);
+  d += L * NM;
+  bulk_g2s(d, A.Kz + s0 * NM, l8 * NM, bar);   // zeros for the last segment
+  d += L * NM;
+  bulk_g2s(d, A.k1 + s0 * M, l8 * M, bar);
+  d += L * M;
+  if (endpoint) bulk_g2s(d, vf + NN, vbytes, bar);   // Vzx0, Vzz0, vx10, vz10
+}
 
+// Row-fused reconstruction for 2n + 2m = 32 (n = 12, m = 4): in each
+// dot-product pass every lane owns one row of a different matrix, e.g. pass 1
+// computes Fx x | Kx x | Qxx x | Qux x on lanes 0-11 | 12-15 | 16-27 | 28-31.
 template <int N, int M, int LMAX>
 __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
-  using S = SegL<N, M, LMAX>;
+  static_assert(2 * N + 2 * M == 32, "row-fused lane map");
   constexpr int NN = N * N, NM = N * M, MM = M * M;
+  constexpr int BUF = LMAX * (2 * NN + 4 * NM + MM + 2 * N + 2 * M) + 2 * NN + 2 * N;
   extern __shared__ __align__(16) double sm[];
   const plq_problem_t& p = A.p;
   const int J = p.J, T = p.T;
   const int lane = threadIdx.x;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
-  double* x = sm + S::X;
-  double* xn = sm + S::XN;
-  double* uu = sm + S::U;
-  double* kv = sm + S::KV;
-  double* z = sm + S::Z;
-  double* av = sm + S::A;
-  double* lam = sm + S::LAM;
+  double* buf = sm;
+  double* gh = sm + BUF;                 // LMAX x (N+M)
+  double* kv = gh + LMAX * (N + M);      // LMAX x M folded offsets
+  double* x = kv + LMAX * M;             // N
+  double* xn = x + N;                    // N
+  double* uu = xn + N;                   // M
+  double* z = uu + M;                    // N
+  double* av = z + N;                    // N
+  double* lam = av + N;                  // N
+  uint64_t* bar = reinterpret_cast<uint64_t*>(lam + N);
   if (lane == 0) mbar_init(bar, 1);
   __syncwarp();
   uint32_t phase = 0;
@@ -302,25 +332,25 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
   for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
-    const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
+    const int lo = p.split_times[j], L = p.split_times[j + 1] - lo;
     const bool last = (j == J - 1);
     const int64_t s0 = b * T + lo;
-    if (lane == 0) {
-      fence_proxy_async();
-      const uint32_t l8 = (uint32_t)L * 8u;
-      mbar_arrive_tx(bar, l8 * (2 * NN + 4 * NM + MM + 2 * N + 2 * M));   // the 11 fields below
-      bulk_g2s(sm + S::FX, p.Fx + s0 * NN, l8 * NN, bar);
-      bulk_g2s(sm + S::FU, p.Fu + s0 * NM, l8 * NM, bar);
-      bulk_g2s(sm + S::F1, p.f1 + s0 * N, l8 * N, bar);
-      bulk_g2s(sm + S::QXX, p.Qxx + s0 * NN, l8 * NN, bar);
-      bulk_g2s(sm + S::QUX, p.Qux + s0 * NM, l8 * NM, bar);
-      bulk_g2s(sm + S::QUU, p.Quu + s0 * MM, l8 * MM, bar);
-      bulk_g2s(sm + S::QX1, p.qx1 + s0 * N, l8 * N, bar);
-      bulk_g2s(sm + S::QU1, p.qu1 + s0 * M, l8 * M, bar);
-      bulk_g2s(sm + S::KX, A.Kx + s0 * NM, l8 * NM, bar);
-      bulk_g2s(sm + S::KZ, A.Kz + s0 * NM, l8 * NM, bar);   // zeros for the last segment
-      bulk_g2s(sm + S::K1, A.k1 + s0 * M, l8 * M, bar);
-    }
+    const double* vfg = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);
+    if (lane == 0) seg_issue<N, M>(A, buf, bar, s0, L, vfg, !last);
+    const double* FX = buf;
+    const double* FU = FX + L * NN;
+    const double* F1 = FU + L * NM;
+    const double* QXX = F1 + L * N;
+    const double* QUX = QXX + L * NN;
+    const double* QUU = QUX + L * NM;
+    const double* QX1 = QUU + L * MM;
+    const double* QU1 = QX1 + L * N;
+    const double* KX = QU1 + L * M;
+    const double* KZ = KX + L * NM;
+    const double* K1 = KZ + L * NM;
+    const double* VZX = K1 + L * M;      // endpoint segments only
+    const double* VZZ = VZX + NN;
+    const double* VZ1 = VZZ + NN + N;
     if (lane < N) {
       const double a0 = (j == 0) ? p.x_init[b * N + lane] : A.links[(b * (J - 1) + (j - 1)) * N + lane];
       av[lane] = a0;
@@ -330,118 +360,126 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
     mbar_wait(bar, phase);
     phase ^= 1u;
     __syncwarp();
+    // fold k = Kz z + k1 for every stage at once (parallel.py:495)
+    for (int r = lane; r < L * M; r += 32) {
+      const double* kz = KZ + r * N;
+      double t = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) t += kz[c] * z[c];
+      kv[r] = t + K1[r];
+    }
+    __syncwarp();
     double obj = 0.0, worst = 0.0;
-    // ---- forward (parallel.py:495-502) + stage costs (problem.py:375-379)
+    // lane roles of the two forward passes
+    const int grp = lane < N ? 0 : (lane < N + M ? 1 : (lane < 2 * N + M ? 2 : 3));
+    const int row = grp == 0 ? lane : (grp == 1 ? lane - N : (grp == 2 ? lane - N - M : lane - 2 * N - M));
 #pragma unroll 1
     for (int s = 0; s < L; ++s) {
       const int64_t st = s0 + s;
-      if (lane < M) {
-        const double* kz = sm + S::KZ + s * NM + lane * N;
-        const double* kx = sm + S::KX + s * NM + lane * N;
-        double t = 0.0, tu = 0.0;
+      // pass 1: Fx x | Kx x | Qxx x | Qux x
+      const double* r1 = grp == 0 ? FX + s * NN + row * N
+                                  : (grp == 1 ? KX + s * NM + row * N
+                                              : (grp == 2 ? QXX + s * NN + row * N : QUX + s * NM + row * N));
+      double t = 0.0, t_ = 0.0;
 #pragma unroll
-        for (int c = 0; c < N; ++c) {
-          t += kz[c] * z[c];
-          tu += kx[c] * x[c];
-        }
-        const double kk = t + sm[S::K1 + s * M + lane];
-        kv[lane] = kk;
-        uu[lane] = tu + kk;
+      for (int c = 0; c < N; c += 2) {
+        t += r1[c] * x[c];
+        t_ += r1[c + 1] * x[c + 1];
+      }
+      t += t_;
+      if (grp == 1) {
+        const double kk = kv[s * M + row];
+        const double uv = t + kk;
+        uu[row] = uv;
+        A.k[st * M + row] = kk;
+        A.u[st * M + row] = uv;
       }
       __syncwarp();
-      if (lane < M) {
-        A.k[st * M + lane] = kv[lane];
-        A.u[st * M + lane] = uu[lane];
-      }
-      if (lane < N) {
-        const double xi = x[lane];
-        A.x[(b * (T + 1) + lo + s) * N + lane] = xi;
-        const double* qxx = sm + S::QXX + s * NN + lane * N;
-        const double* fx = sm + S::FX + s * NN + lane * N;
-        double t0 = 0.0, tf = 0.0, t1 = 0.0, tfu = 0.0;
+      // pass 2: Fu u | - | Qux' u | Quu u
+      double t2 = 0.0;
+      if (grp == 0) {
 #pragma unroll
-        for (int c = 0; c < N; ++c) {
-          t0 += qxx[c] * x[c];
-          tf += fx[c] * x[c];
-        }
+        for (int q = 0; q < M; ++q) t2 += FU[s * NM + row * M + q] * uu[q];
+        xn[row] = (t + t2) + F1[s * N + row];
+      } else if (grp == 2) {
 #pragma unroll
-        for (int q = 0; q < M; ++q) {
-          t1 += sm[S::QUX + s * NM + q * N + lane] * uu[q];
-          tfu += sm[S::FU + s * NM + lane * M + q] * uu[q];
-        }
-        const double qx = sm[S::QX1 + s * N + lane];
-        obj += 0.5 * xi * t0 + qx * xi;
-        sm[S::GH + s * (N + M) + lane] = (t0 + t1) + qx;
-        xn[lane] = (tf + tfu) + sm[S::F1 + s * N + lane];
-      }
-      if (lane < M) {
-        const double* qux = sm + S::QUX + s * NM + lane * N;
-        const double* quu = sm + S::QUU + s * MM + lane * M;
-        double t2 = 0.0, t3 = 0.0;
+        for (int q = 0; q < M; ++q) t2 += QUX[s * NM + q * N + row] * uu[q];
+        const double xi = x[row], qx = QX1[s * N + row];
+        gh[s * (N + M) + row] = (t + t2) + qx;
+        obj += 0.5 * xi * t + qx * xi;
+        A.x[(b * (T + 1) + lo + s) * N + row] = xi;
+      } else if (grp == 3) {
 #pragma unroll
-        for (int c = 0; c < N; ++c) t2 += qux[c] * x[c];
-#pragma unroll
-        for (int q = 0; q < M; ++q) t3 += quu[q] * uu[q];
-        const double ui = uu[lane], qu = sm[S::QU1 + s * M + lane];
-        obj += 0.5 * ui * t3 + ui * t2 + qu * ui;
-        sm[S::GH + s * (N + M) + N + lane] = (t2 + t3) + qu;
+        for (int q = 0; q < M; ++q) t2 += QUU[s * MM + row * M + q] * uu[q];
+        const double ui = uu[row], qu = QU1[s * M + row];
+        gh[s * (N + M) + N + row] = (t + t2) + qu;
+        obj += 0.5 * ui * t2 + ui * t + qu * ui;
       }
       __syncwarp();
       if (lane < N) x[lane] = xn[lane];
       __syncwarp();
     }
     // g/h of the link stage feed the boundary kernel
-    if (lane < N + M) A.gh[(s0 + L - 1) * (N + M) + lane] = sm[S::GH + (L - 1) * (N + M) + lane];
+    if (lane < N + M) A.gh[(s0 + L - 1) * (N + M) + lane] = gh[(L - 1) * (N + M) + lane];
     // ---- multiplier seed (parallel.py:505-515)
-    if (lane < N) {
-      if (last) {
+    if (last) {
+      if (lane < N) {
         A.x[(b * (T + 1) + T) * N + lane] = x[lane];
-        double t = 0.0;
+        double tt = 0.0;
         const double* QT = p.QxxT + b * NN + lane * N;
 #pragma unroll
-        for (int c = 0; c < N; ++c) t += QT[c] * x[c];
+        for (int c = 0; c < N; ++c) tt += QT[c] * x[c];
         const double q1 = p.qx1T[b * N + lane];
-        obj += 0.5 * x[lane] * t + q1 * x[lane];
-        const double g = t + q1;
+        obj += 0.5 * x[lane] * tt + q1 * x[lane];
+        const double g = tt + q1;
         lam[lane] = -g;
         A.lam[(b * (T + 1) + T) * N + lane] = -g;
         worst = fmax(worst, fabs(g + -g));
-      } else {
-        A.xend[(b * J + j) * N + lane] = x[lane];
-        const double* vf = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);
-        double t0 = 0.0, t1 = 0.0;
+      }
+    } else {
+      // mu = -(Vzx0 a + Vzz0 z + vz10): lanes 0-11 Vzx0 a, lanes 16-27 Vzz0 z
+      double tv = 0.0;
+      const bool hi = lane >= 16 && lane < 16 + N;
+      const int rr = hi ? lane - 16 : lane;
+      if (lane < N || hi) {
+        const double* mrow = hi ? VZZ + rr * N : VZX + rr * N;
+        const double* vec = hi ? z : av;
 #pragma unroll
-        for (int c = 0; c < N; ++c) {
-          t0 += vf[NN + lane * N + c] * av[c];
-          t1 += vf[2 * NN + lane * N + c] * z[c];
-        }
-        const double mu = -((t0 + t1) + vf[3 * NN + N + lane]);
+        for (int c = 0; c < N; ++c) tv += mrow[c] * vec[c];
+      }
+      const double tz = __shfl_down_sync(0xffffffffu, tv, 16);
+      if (lane < N) {
+        A.xend[(b * J + j) * N + lane] = x[lane];
+        const double mu = -((tv + tz) + VZ1[lane]);
         A.mu_left[(b * (J - 1) + j) * N + lane] = mu;
         lam[lane] = -mu;
       }
     }
     __syncwarp();
-    // ---- backward multipliers (parallel.py:518-523) + interior KKT rows
+    // ---- backward multipliers (parallel.py:518-523) + interior KKT rows:
+    // lanes 0-11 Fx' lam, lanes 12-15 Fu' lam
 #pragma unroll 1
     for (int s = L - 1; s >= 0; --s) {
       const bool interior = last || (s < L - 1);
+      double tb = 0.0, tb_ = 0.0;
+      if (lane < N + M) {
+        const double* col = lane < N ? FX + s * NN + lane : FU + s * NM + (lane - N);
+        const int stride = lane < N ? N : M;
+#pragma unroll
+        for (int k = 0; k < N; k += 2) {
+          tb += col[k * stride] * lam[k];
+          tb_ += col[(k + 1) * stride] * lam[k + 1];
+        }
+        tb += tb_;
+      }
       double ln = 0.0;
       if (lane < N) {
-        const double* fx = sm + S::FX + s * NN + lane;
-        double t = 0.0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) t += fx[k * N] * lam[k];
-        const double g = sm[S::GH + s * (N + M) + lane];
-        ln = t - g;
+        const double g = gh[s * (N + M) + lane];
+        ln = tb - g;
         A.lam[(b * (T + 1) + lo + s) * N + lane] = ln;
-        if (interior) worst = fmax(worst, fabs((g + ln) - t));
-      }
-      if (lane < M && interior) {
-        const double* fu = sm + S::FU + s * NM + lane;
-        double t = 0.0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) t += fu[k * M] * lam[k];
-        worst = fmax(worst, fabs(sm[S::GH + s * (N + M) + N + lane] - t));
+        if (interior) worst = fmax(worst, fabs((g + ln) - tb));
+      } else if (lane < N + M && interior) {
+        worst = fmax(worst, fabs(gh[s * (N + M) + lane] - tb));
       }
       __syncwarp();
       if (lane < N) lam[lane] = ln;
@@ -461,149 +499,129 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
 // ----------------------------------------------------------------------------
 // sequential link solve, one warp per problem
 
-template <int N, int KMAX>
-struct LL {
-  static constexpr int LD = N + 1, NN = N * N;
-  static constexpr int P = 0;               // N x LD   pivot block -> Cholesky factor
-  static constexpr int R = P + N * LD;      // N x LD   [S_i' | g] -> [X_i | d_i]
-  static constexpr int RP = R + N * LD;     // N x LD   [X_{i-1} | d_{i-1}]
-  static constexpr int SR = RP + N * LD;    // N x N    S_i   = Vzx0_{i+1}
-  static constexpr int SP = SR + NN;        // N x N    S_{i-1}
-  static constexpr int D = SP + NN;         // KMAX x N d_i, then the solution
-  static constexpr int TOTAL = (D + KMAX * N + 1) & ~1;
-};
-
+// One warp per problem: the reference's block Cholesky (endpoint.py:410-438).
+// The problem's segment-start value blocks (J x (3n^2+2n) doubles, contiguous)
+// arrive in shared memory by one bulk copy; pivot / right-hand-side blocks
+// ping-pong in smem, pivots are inverted once, only X_i goes to global.
 template <int N>
-__device__ __forceinline__ void warp_chol(double* A, int* fail) {
-  constexpr int LD = N + 1;
-  const int lane = threadIdx.x & 31;
-  int bad = 0;
-  for (int k = 0; k < N; ++k) {
-    const double dkk = A[k * LD + k];
-    if (!(dkk > 0.0)) bad = 1;
-    const double d = sqrt(dkk > 0.0 ? dkk : 1.0);
-    __syncwarp();
-    if (lane == k) A[k * LD + k] = d;
-    if (lane > k && lane < N) A[lane * LD + k] /= d;
-    __syncwarp();
-    if (lane > k && lane < N) {
-      const double lik = A[lane * LD + k];
-      for (int jj = k + 1; jj <= lane; ++jj) A[lane * LD + jj] -= lik * A[jj * LD + k];
-    }
-    __syncwarp();
-  }
-  *fail = bad;
-}
-
-// X <- L^{-T} L^{-1} X for the N x C block X (stride N+1), lane per column
-template <int N, int C>
-__device__ __forceinline__ void warp_cho_solve(const double* Lc, double* X) {
-  constexpr int LD = N + 1;
-  const int lane = threadIdx.x & 31;
-  for (int col = lane; col < C; col += 32) {
-    double x[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double v = X[i * LD + col];
-#pragma unroll
-      for (int k = 0; k < i; ++k) v -= Lc[i * LD + k] * x[k];
-      x[i] = v / Lc[i * LD + i];
-    }
-#pragma unroll
-    for (int i = N - 1; i >= 0; --i) {
-      double v = x[i];
-#pragma unroll
-      for (int k = i + 1; k < N; ++k) v -= Lc[k * LD + i] * x[k];
-      x[i] = v / Lc[i * LD + i];
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) X[i * LD + col] = x[i];
-  }
-  __syncwarp();
-}
-
-// One warp per problem: the reference's block Cholesky (endpoint.py:410-438)
-// with every vf0 block staged through shared memory in coalesced rows.
-template <int N, int KMAX>
 __global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const double* vf0, double* links,
                                                      double* link_residual, int32_t* status, double* Xs) {
-  using S = LL<N, KMAX>;
-  constexpr int LD = S::LD, NN = N * N, VS = 3 * NN + 2 * N;
+  constexpr int LD = N + 1, NN = N * N, VS = 3 * NN + 2 * N;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x;
   const int J = p.J, K = J - 1;
-  double* Pm = sm + S::P;
-  double* R = sm + S::R;
-  double* RP = sm + S::RP;
-  double* SR = sm + S::SR;
-  double* SP = sm + S::SP;
-  double* dv = sm + S::D;
+  double* VF = sm;                       // J x VS
+  double* Pm = VF + J * VS;              // N x LD
+  double* R0 = Pm + N * LD;              // N x LD  ping
+  double* R1 = R0 + N * LD;              // N x LD  pong
+  double* dv = R1 + N * LD;              // K x N
+  double* idg = dv + K * N;              // N
+  uint64_t* bar = reinterpret_cast<uint64_t*>(idg + N + 1);
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  uint32_t phase = 0;
   for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
-    const double* vf = vf0 + b * (int64_t)J * VS;
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_arrive_tx(bar, (uint32_t)(J * VS * 8));
+      bulk_g2s(VF, vf0 + b * (int64_t)J * VS, (uint32_t)(J * VS * 8), bar);
+    }
     double* X = Xs + b * (int64_t)K * NN;
+    const double* xi = p.x_init + b * N;
+    mbar_wait(bar, phase);
+    phase ^= 1u;
     int bad = 0;
+    double* R = R0;
+    double* RP = R1;
     for (int i = 0; i < K; ++i) {
-      const double* left = vf + i * VS;
-      const double* right = vf + (i + 1) * VS;
+      const double* left = VF + i * VS;
+      const double* right = VF + (i + 1) * VS;
+      // P = Vzz0_i + Vxx0_{i+1};  R = [S_i' | b_i],  S_i = Vzx0_{i+1}
       for (int idx = lane; idx < NN; idx += 32) {
-        Pm[(idx / N) * LD + idx % N] = left[2 * NN + idx] + right[idx];
-        SR[idx] = (i + 1 < K) ? right[NN + idx] : 0.0;
+        const int r = idx / N, c = idx % N;
+        Pm[r * LD + c] = left[2 * NN + idx] + right[idx];
+        R[r * LD + c] = (i + 1 < K) ? right[NN + c * N + r] : 0.0;
       }
       if (lane < N) {
         double v = -left[3 * NN + N + lane] + -right[3 * NN + lane];
         if (i == 0) {
           double t = 0.0;
-          for (int c = 0; c < N; ++c) t += left[NN + lane * N + c] * p.x_init[b * N + c];
+#pragma unroll
+          for (int c = 0; c < N; ++c) t += left[NN + lane * N + c] * xi[c];
           v += -t;
         }
         R[lane * LD + N] = v;
       }
       __syncwarp();
-      for (int idx = lane; idx < NN; idx += 32) {
-        const int r = idx / N, c = idx % N;
-        R[r * LD + c] = SR[c * N + r];   // S_i'
-      }
       if (i > 0) {
-        // P -= S_{i-1} X_{i-1} ; g -= S_{i-1} d_{i-1}
+        // P -= S_{i-1} X_{i-1};  g -= S_{i-1} d_{i-1}   (S_{i-1} = Vzx0_i, left block)
         for (int idx = lane; idx < NN; idx += 32) {
           const int r = idx / N, c = idx % N;
           double t = 0.0;
 #pragma unroll
-          for (int k = 0; k < N; ++k) t += SP[r * N + k] * RP[k * LD + c];
+          for (int k = 0; k < N; ++k) t += left[NN + r * N + k] * RP[k * LD + c];
           Pm[r * LD + c] -= t;
         }
         if (lane < N) {
           double t = 0.0;
 #pragma unroll
-          for (int k = 0; k < N; ++k) t += SP[lane * N + k] * RP[k * LD + N];
+          for (int k = 0; k < N; ++k) t += left[NN + lane * N + k] * RP[k * LD + N];
           R[lane * LD + N] -= t;
         }
+        __syncwarp();
+      }
+      // Cholesky of P (lane = row), reciprocal pivots in idg
+      for (int k = 0; k < N; ++k) {
+        const double dkk = Pm[k * LD + k];
+        bad |= !(dkk > 0.0);
+        const double d = sqrt(dkk > 0.0 ? dkk : 1.0);
+        const double inv = 1.0 / d;
+        if (lane == k) {
+          Pm[k * LD + k] = d;
+          idg[k] = inv;
+        }
+        if (lane > k && lane < N) Pm[lane * LD + k] *= inv;
+        __syncwarp();
+        if (lane > k && lane < N) {
+          const double lik = Pm[lane * LD + k];
+          for (int jj = k + 1; jj <= lane; ++jj) Pm[lane * LD + jj] -= lik * Pm[jj * LD + k];
+        }
+        __syncwarp();
+      }
+      // R <- P^{-1} R (lane per column; N+1 columns)
+      for (int col = lane; col < N + 1; col += 32) {
+        double xv[N];
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          double v = R[r * LD + col];
+#pragma unroll
+          for (int k = 0; k < r; ++k) v -= Pm[r * LD + k] * xv[k];
+          xv[r] = v * idg[r];
+        }
+#pragma unroll
+        for (int r = N - 1; r >= 0; --r) {
+          double v = xv[r];
+#pragma unroll
+          for (int k = r + 1; k < N; ++k) v -= Pm[k * LD + r] * xv[k];
+          xv[r] = v * idg[r];
+        }
+#pragma unroll
+        for (int r = 0; r < N; ++r) R[r * LD + col] = xv[r];
       }
       __syncwarp();
-      int f;
-      warp_chol<N>(Pm, &f);
-      bad |= f;
-      warp_cho_solve<N, N + 1>(Pm, R);
-      for (int idx = lane; idx < NN; idx += 32) {
-        const int r = idx / N, c = idx % N;
-        X[i * NN + idx] = R[r * LD + c];
-        RP[r * LD + c] = R[r * LD + c];
-        SP[idx] = SR[idx];
-      }
-      if (lane < N) {
-        dv[i * N + lane] = R[lane * LD + N];
-        RP[lane * LD + N] = R[lane * LD + N];
-      }
+      for (int idx = lane; idx < NN; idx += 32) X[i * NN + idx] = R[(idx / N) * LD + idx % N];
+      if (lane < N) dv[i * N + lane] = R[lane * LD + N];
+      double* t = R;
+      R = RP;
+      RP = t;
       __syncwarp();
     }
     // back substitution: out_{K-1} = d_{K-1}; out_i = d_i - X_i out_{i+1}  (in place in dv)
     for (int i = K - 2; i >= 0; --i) {
-      for (int idx = lane; idx < NN; idx += 32) Pm[(idx / N) * LD + idx % N] = X[i * NN + idx];
-      __syncwarp();
       if (lane < N) {
         double t = 0.0;
 #pragma unroll
-        for (int c = 0; c < N; ++c) t += Pm[lane * LD + c] * dv[(i + 1) * N + c];
+        for (int c = 0; c < N; ++c) t += X[i * NN + lane * N + c] * dv[(i + 1) * N + c];
         dv[i * N + lane] -= t;
       }
       __syncwarp();
@@ -612,37 +630,30 @@ __global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const dou
     for (int idx = lane; idx < K * N; idx += 32) out[idx] = dv[idx];
     // residual of the link equations at the solution (parallel.py:273-282)
     double worst = 0.0;
-    for (int i = 0; i < K; ++i) {
-      const double* left = vf + i * VS;
-      const double* right = vf + (i + 1) * VS;
-      for (int idx = lane; idx < NN; idx += 32) {
-        Pm[(idx / N) * LD + idx % N] = left[2 * NN + idx] + right[idx];   // D_i
-        SP[idx] = left[NN + idx];                                          // S_{i-1} = Vzx0_i
-        SR[idx] = (i + 1 < K) ? right[NN + idx] : 0.0;                     // S_i = Vzx0_{i+1}
-      }
-      __syncwarp();
-      if (lane < N) {
+    if (lane < N) {
+      for (int i = 0; i < K; ++i) {
+        const double* left = VF + i * VS;
+        const double* right = VF + (i + 1) * VS;
         double s = 0.0;
 #pragma unroll
-        for (int c = 0; c < N; ++c) s += Pm[lane * LD + c] * dv[i * N + c];
+        for (int c = 0; c < N; ++c) s += (left[2 * NN + lane * N + c] + right[lane * N + c]) * dv[i * N + c];
         if (i >= 1) {
 #pragma unroll
-          for (int c = 0; c < N; ++c) s += SP[lane * N + c] * dv[(i - 1) * N + c];
+          for (int c = 0; c < N; ++c) s += left[NN + lane * N + c] * dv[(i - 1) * N + c];
         }
         if (i + 1 < K) {
 #pragma unroll
-          for (int c = 0; c < N; ++c) s += SR[c * N + lane] * dv[(i + 1) * N + c];
+          for (int c = 0; c < N; ++c) s += right[NN + c * N + lane] * dv[(i + 1) * N + c];
         }
         double rhs = -left[3 * NN + N + lane] + -right[3 * NN + lane];
         if (i == 0) {
           double t = 0.0;
 #pragma unroll
-          for (int c = 0; c < N; ++c) t += SP[lane * N + c] * p.x_init[b * N + c];
+          for (int c = 0; c < N; ++c) t += left[NN + lane * N + c] * xi[c];
           rhs += -t;
         }
         worst = fmax(worst, fabs(s - rhs));
       }
-      __syncwarp();
     }
     worst = warp_max(worst);
     if (lane == 0) {
@@ -665,7 +676,8 @@ int sms_count() {
 
 template <int N, int M, int LMAX>
 int launch_recon_seg(const ReconArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * SegL<N, M, LMAX>::TOTAL;
+  constexpr int BUF = LMAX * (2 * N * N + 4 * N * M + M * M + 2 * N + 2 * M) + 2 * N * N + 2 * N;
+  const size_t smem = sizeof(double) * (BUF + LMAX * (N + M) + LMAX * M + 5 * N + M + 4);
   auto kern = recon_seg_kernel<N, M, LMAX>;
   static bool attr = false;
   if (!attr) {
@@ -695,13 +707,13 @@ int launch_recon_t(const ReconArgs& a, cudaStream_t s) {
 template <int N>
 int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, double* link_residual, int32_t* status,
                   double* ws, cudaStream_t s) {
-  constexpr int KMAX = 64;
-  const size_t smem = sizeof(double) * LL<N, KMAX>::TOTAL;
-  auto kern = link_seq_kernel<N, KMAX>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  const int J = p.J, K = J - 1;
+  const size_t smem = sizeof(double) * ((size_t)J * (3 * N * N + 2 * N) + 3 * N * (N + 1) + K * N + N + 4);
+  auto kern = link_seq_kernel<N>;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = 200 * 1024;
   }
   const int64_t cap = (int64_t)sms_count() * 32;
   const int grid = (int)(p.B < cap ? p.B : cap);
@@ -725,7 +737,8 @@ int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
 }
 
 // the sequential link solve is used while the chain is short
-bool link_seq_supported(int n, int J) { return n == 12 && J - 1 <= 64; }
+// the whole problem's vf0 must fit in shared memory (J <= 64 at n = 12)
+bool link_seq_supported(int n, int J) { return n == 12 && J <= 64; }
 
 size_t link_seq_workspace_doubles(int64_t B, int J, int n) { return (size_t)B * (J - 1) * n * n + 2; }
 
