@@ -1,0 +1,199 @@
+// Large-shape fp64 building blocks (n >= 64): a tiled CTA GEMM on the FP64
+// tensor pipe and a blocked triangular solve built on it.
+//
+// cta_gemm_tiled: C(MxN) = op(A) B with operands in GLOBAL memory (L2 for the
+// per-segment scratch), staged through shared memory in BM x 16 / 16 x 64
+// tiles by cp.async (double-buffered, zero-filled at the ragged edges); the
+// NW warps form an (NW/2) x 2 grid, each warp owning a 16 x 32 block = 2 x 4
+// DMMA.8x8x4 fragments, so every k-step issues 8 DMMAs for 6 fragment loads.
+#pragma once
+
+#include "plq_device.cuh"
+
+namespace plq {
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int NW>
+struct TileCfg {
+  static constexpr int BM = 8 * NW, BN = 64, BK = 16;
+  static constexpr int LDA = 20, LDB = 68;   // = 4 (mod 8): conflict-free fragment loads
+  static constexpr int DOUBLES = 2 * (BM * LDA + BK * LDB);
+};
+
+template <bool TA, int NW, class Epi>
+__device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double* __restrict__ A, int lda,
+                                               const double* __restrict__ B, int ldb, double* tiles, Epi epi) {
+  using C = TileCfg<NW>;
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, LDA = C::LDA, LDB = C::LDB, NT = NW * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;
+  double* As0 = tiles;
+  double* As1 = tiles + BM * LDA;
+  double* Bs0 = tiles + 2 * BM * LDA;
+  double* Bs1 = Bs0 + BK * LDB;
+  const int tmc = (M + BM - 1) / BM, tnc = (N + BN - 1) / BN, kc = (K + BK - 1) / BK;
+  for (int tile = 0; tile < tmc * tnc; ++tile) {
+    const int m0 = (tile / tnc) * BM, n0 = (tile % tnc) * BN;
+    double acc[2][4][2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[r][t][0] = acc[r][t][1] = 0.0;
+    auto load = [&](int c, int buf) {
+      const int k0 = c * BK;
+      double* as = buf ? As1 : As0;
+      double* bs = buf ? Bs1 : Bs0;
+      for (int e = tid; e < BM * BK; e += NT) {
+        int i, k;
+        if (TA) {
+          i = e % BM;
+          k = e / BM;
+        } else {
+          k = e % BK;
+          i = e / BK;
+        }
+        const int gi = m0 + i, gk = k0 + k;
+        const bool v = gi < M && gk < K;
+        const double* src = v ? (TA ? A + (size_t)gk * lda + gi : A + (size_t)gi * lda + gk) : A;
+        cp_async8(as + i * LDA + k, src, v);
+      }
+      for (int e = tid; e < BK * BN; e += NT) {
+        const int k = e / BN, j = e % BN;
+        const int gk = k0 + k, gj = n0 + j;
+        const bool v = gk < K && gj < N;
+        cp_async8(bs + k * LDB + j, v ? B + (size_t)gk * ldb + gj : B, v);
+      }
+      cp_async_commit();
+    };
+    load(0, 0);
+    for (int c = 0; c < kc; ++c) {
+      if (c + 1 < kc) {
+        load(c + 1, (c + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* as = (c & 1) ? As1 : As0;
+      const double* bs = (c & 1) ? Bs1 : Bs0;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        double af[2], bf[4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) af[r] = as[(wr * 16 + r * 8 + g) * LDA + kk + q];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bf[t] = bs[(kk + q) * LDB + wc * 32 + t * 8 + g];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) dmma884(acc[r][t][0], acc[r][t][1], af[r], bf[t]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = m0 + wr * 16 + r * 8 + g, j = n0 + wc * 32 + t * 8 + 2 * q + e;
+          if (i < M && j < N) epi(i, j, acc[r][t][e]);
+        }
+  }
+}
+
+// X <- (L L')^{-1} X for the m x W block X (cho_solve), blocked by 8 rows:
+// the off-diagonal updates are DMMA GEMMs over all W columns, the 8 x 8
+// diagonal solves go thread per column.  `L` and `X` may be global or shared.
+__device__ __forceinline__ void cta_cho_solve_blocked(const double* L, int m, int ldl, double* X, int W, int ldx) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // forward: L y = x
+  for (int r0 = 0; r0 < m; r0 += 8) {
+    const int rb = min(8, m - r0);
+    if (r0 > 0) {
+      cta_gemm<false, false, 1, 1>(rb, W, r0, L + (size_t)r0 * ldl, ldl, X, ldx,
+                                   [&](int i, int j, double acc) { X[(size_t)(r0 + i) * ldx + j] -= acc; });
+      __syncthreads();
+    }
+    for (int c = tid; c < W; c += nt) {
+      double y[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < rb) {
+          double v = X[(size_t)(r0 + i) * ldx + c];
+#pragma unroll
+          for (int k = 0; k < i; ++k) v -= L[(size_t)(r0 + i) * ldl + r0 + k] * y[k];
+          y[i] = v / L[(size_t)(r0 + i) * ldl + r0 + i];
+          X[(size_t)(r0 + i) * ldx + c] = y[i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // backward: L' x = y
+  const int nb = (m + 7) / 8;
+  for (int bb = nb - 1; bb >= 0; --bb) {
+    const int r0 = bb * 8, rb = min(8, m - r0), r1 = r0 + rb;
+    if (r1 < m) {
+      // X[r0:r1] -= (L')[r0:r1, r1:m] X[r1:m] ; (L')(i,k) = L[r1+k][r0+i]
+      cta_gemm<true, false, 1, 1>(rb, W, m - r1, L + (size_t)r1 * ldl + r0, ldl, X + (size_t)r1 * ldx, ldx,
+                                  [&](int i, int j, double acc) { X[(size_t)(r0 + i) * ldx + j] -= acc; });
+      __syncthreads();
+    }
+    for (int c = tid; c < W; c += nt) {
+      double y[8];
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        if (i < rb) {
+          double v = X[(size_t)(r0 + i) * ldx + c];
+#pragma unroll
+          for (int k = i + 1; k < 8; ++k)
+            if (k < rb) v -= L[(size_t)(r0 + k) * ldl + r0 + i] * y[k];
+          y[i] = v / L[(size_t)(r0 + i) * ldl + r0 + i];
+          X[(size_t)(r0 + i) * ldx + c] = y[i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// forward substitution only: X <- L^{-1} X, blocked
+__device__ __forceinline__ void cta_trsm_lower_blocked(const double* L, int m, int ldl, double* X, int W, int ldx) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int r0 = 0; r0 < m; r0 += 8) {
+    const int rb = min(8, m - r0);
+    if (r0 > 0) {
+      cta_gemm<false, false, 1, 1>(rb, W, r0, L + (size_t)r0 * ldl, ldl, X, ldx,
+                                   [&](int i, int j, double acc) { X[(size_t)(r0 + i) * ldx + j] -= acc; });
+      __syncthreads();
+    }
+    for (int c = tid; c < W; c += nt) {
+      double y[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < rb) {
+          double v = X[(size_t)(r0 + i) * ldx + c];
+#pragma unroll
+          for (int k = 0; k < i; ++k) v -= L[(size_t)(r0 + i) * ldl + r0 + k] * y[k];
+          y[i] = v / L[(size_t)(r0 + i) * ldl + r0 + i];
+          X[(size_t)(r0 + i) * ldx + c] = y[i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace plq

@@ -30,6 +30,8 @@ struct SweepLayout {
   int in_smem[SB_COUNT];
   int64_t smem_doubles;
   int64_t gmem_doubles;      // per CTA
+  int large;                 // n >= 48: buffers in global scratch, smem holds GEMM tiles
+  int64_t tiles_off;         // smem offset of the tiled-GEMM staging area
 };
 
 struct SweepArgs {

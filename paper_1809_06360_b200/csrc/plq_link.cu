@@ -15,6 +15,7 @@
 // A pivot block that is not positive-definite raises LinkSingular, as the
 // reference does (parallel.py:267-271).
 #include "plq_device.cuh"
+#include "plq_gemm.cuh"
 #include "plq_internal.h"
 
 #include <vector>
@@ -147,14 +148,18 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
     flag_singular(p, status, b);
     return;
   }
-  cta_trsm_lower(Lc, n, n, Wm, w, w);
+  if (n >= 16)
+    cta_trsm_lower_blocked(Lc, n, n, Wm, w, w);
+  else
+    cta_trsm_lower(Lc, n, n, Wm, w, w);
   if (L.top) return;
   double* CL = L.CL + (b * E + o) * nn;
   double* CR = L.CR + (b * E + o) * nn;
   double* X = L.X + (b * E + o) * nn;
   double* cL = L.cL + (b * E + o) * n;
   double* cR = L.cR + (b * E + o) * n;
-  cta_gemm<true, false, 1, 1>(2 * n, w, n, Wm, w, Wm, w, [&](int r, int c, double acc) {
+  extern __shared__ __align__(16) double tiles[];
+  auto gram = [&](int r, int c, double acc) {
     if (r < n) {
       if (c < n)
         CL[r * n + c] = acc;
@@ -169,7 +174,11 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
       else
         cR[rr] = acc;
     }
-  });
+  };
+  if (n >= 32 && blockDim.x == 256)
+    cta_gemm_tiled<true, 8>(2 * n, w, n, Wm, w, Wm, w, tiles, gram);
+  else
+    cta_gemm<true, false, 1, 1>(2 * n, w, n, Wm, w, Wm, w, gram);
 }
 
 // next level's system on the even blocks
@@ -304,7 +313,9 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   link_assemble0<<<B * P.lv[0].K, threads, 0, s>>>(p, vf0, P.lv[0]);
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
-    link_eliminate<<<B * P.lv[l].E, threads, 0, s>>>(p, P.lv[l], status);
+    const size_t tsm = (p.n >= 32 && threads == 256) ? sizeof(double) * TileCfg<8>::DOUBLES : 0;
+    if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    link_eliminate<<<B * P.lv[l].E, threads, tsm, s>>>(p, P.lv[l], status);
     ++nl;
     if (!P.lv[l].top) {
       link_assemble_next<<<B * P.lv[l + 1].K, threads, 0, s>>>(p, P.lv[l], P.lv[l + 1]);

@@ -19,6 +19,7 @@
 //   value  Y = P + Muu G;  [Vxx Vzx' vx1; Vzx Vzz vz1] = M + P'G + G'Y
 //          which is term-for-term endpoint.py:285-294.
 #include "plq_device.cuh"
+#include "plq_gemm.cuh"
 #include "plq_internal.h"
 
 #include <algorithm>
@@ -29,7 +30,29 @@ namespace {
 
 struct Bufs {
   double *V, *IN, *PGY, *MUU, *MISC, *VF, *Z, *MX, *H, *WIDE;
+  double* tiles;   // tiled-GEMM staging (large mode) or nullptr
 };
+
+// large GEMMs go through the tiled DMMA kernel when the operands live in
+// global scratch (large mode), small ones through the direct-fragment GEMM
+template <bool TA, int NT, class Epi>
+__device__ __forceinline__ void gemm_x(int M, int N, int K, const double* A, int lda, const double* B, int ldb,
+                                       double* tiles, Epi epi) {
+  if constexpr (NT >= 256) {
+    if (tiles != nullptr && (long long)M * N * K >= 16384) {
+      cta_gemm_tiled<TA, NT / 32>(M, N, K, A, lda, B, ldb, tiles, epi);
+      return;
+    }
+  }
+  cta_gemm<TA, false, 1, 1>(M, N, K, A, lda, B, ldb, epi);
+}
+
+__device__ __forceinline__ void cho_solve_x(const double* L, int m, int ldl, double* X, int W, int ldx) {
+  if (m >= 16)
+    cta_cho_solve_blocked(L, m, ldl, X, W, ldx);
+  else
+    cta_cho_solve(L, m, ldl, X, W, ldx);
+}
 
 __device__ void wide_branch(const plq_problem_t& p, int n, int m, int r, int W, int ldw, int Fw, double* VF,
                             double* H, double* P, double* G, double* Muu, double* WIDE, double* tau, double* rdiag,
@@ -107,6 +130,7 @@ __device__ void wide_branch(const plq_problem_t& p, int n, int m, int r, int W, 
   __syncthreads();
 }
 
+template <int NT>
 __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int j) {
   const plq_problem_t& p = a.p;
   const int n = p.n, m = p.m, J = p.J, T = p.T;
@@ -182,7 +206,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     __syncthreads();
 
     // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217)
-    cta_gemm<false, false, 1, 1>(n + nz, Fw, n, bf.V, n, F, Fw, [&](int i, int c, double acc) {
+    gemm_x<false, NT>(n + nz, Fw, n, bf.V, n, F, Fw, bf.tiles, [&](int i, int c, double acc) {
       if (i < n) {
         VF[i * Fw + c] = (c == n + m) ? vx1[i] + acc : acc;
       } else {
@@ -191,7 +215,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     });
     __syncthreads();
     // ---- GEMM2: M-terms (endpoint.py:209-211, 215-216)
-    cta_gemm<true, false, 1, 1>(n + m, Fw, n, F, Fw, VF, Fw, [&](int i, int c, double acc) {
+    gemm_x<true, NT>(n + m, Fw, n, F, Fw, VF, Fw, bf.tiles, [&](int i, int c, double acc) {
       if (i < n) {
         if (c < n) {
           MX[i * (n + 1) + c] = Qxx[i * n + c] + acc;
@@ -232,7 +256,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         __syncthreads();
         break;
       }
-      cta_cho_solve(Lm, m, m, G, W, ldw);
+      cho_solve_x(Lm, m, m, G, W, ldw);
       for (int idx = tid; idx < m * W; idx += nt) {
         const int u = idx / W, c = idx % W;
         G[u * ldw + c] = -G[u * ldw + c];
@@ -253,8 +277,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       const double fu2 = block_sum(part_u, red);
       const double nu_scale = sqrt(hx2) * sqrt(fu2);
       // N = Hx F -> VF (r x Fw): [Nx | Nu | Hx f1]
-      cta_gemm<false, false, 1, 1>(r, Fw, n, H, ldw, F, Fw,
-                                   [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
+      gemm_x<false, NT>(r, Fw, n, H, ldw, F, Fw, bf.tiles, [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
       __syncthreads();
       // stack [Nx | Nz=Hz | n1 = Hx f1 + h1] in place in H
       for (int idx = tid; idx < r * n; idx += nt) {
@@ -316,10 +339,10 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     for (int u = tid; u < m; u += nt) a.k1[st * m + u] = G[u * ldw + cc];
 
     // ---- value update (endpoint.py:285-294; serial.py:75-77)
-    cta_gemm<false, false, 1, 1>(m, W, m, Muu, m, G, ldw,
-                                 [&](int i, int c, double acc) { Y[i * ldw + c] = P[i * ldw + c] + acc; });
+    gemm_x<false, NT>(m, W, m, Muu, m, G, ldw, bf.tiles,
+                  [&](int i, int c, double acc) { Y[i * ldw + c] = P[i * ldw + c] + acc; });
     __syncthreads();
-    cta_gemm<true, false, 1, 1>(n + nz, W, 2 * m, P, ldw, G, ldw, [&](int i, int c, double acc) {
+    gemm_x<true, NT>(n + nz, W, 2 * m, P, ldw, G, ldw, bf.tiles, [&](int i, int c, double acc) {
       if (i < n) {
         if (c < n) {
           Vxx[i * n + c] = MX[i * (n + 1) + c] + acc;
@@ -368,7 +391,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(16) double smem[];
   Bufs bf;
   double* ptrs[SB_COUNT];
@@ -385,12 +408,13 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
   bf.MX = ptrs[SB_MX];
   bf.H = ptrs[SB_H];
   bf.WIDE = ptrs[SB_WIDE];
+  bf.tiles = a.lay.large ? smem + a.lay.tiles_off : nullptr;
   const int nloc = a.seg_end - a.seg_begin;
   const int64_t total = a.p.B * nloc;
   for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
-    sweep_segment(a, bf, b, j);
+    sweep_segment<NT>(a, bf, b, j);
   }
 }
 
@@ -404,7 +428,6 @@ int sweep_threads(int n) {
 }
 
 SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
-  (void)threads;
   const int64_t Fw = n + m + 1, W = 2 * n + 1;
   int64_t sz[SB_COUNT];
   sz[SB_V] = 3LL * n * n + 2 * n;
@@ -420,10 +443,19 @@ SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
   sz[SB_WIDE] = wide ? ((int64_t)m * std::min(n, m) + (int64_t)m * m + 2 * m * W) : 0;
   SweepLayout L{};
   int64_t so = 0, go = 0;
-  const int64_t budget = (int64_t)(smem_budget / sizeof(double));
+  int64_t budget = (int64_t)(smem_budget / sizeof(double));
+  if (n >= 48) {
+    // large mode: GEMM operands stay in (L2-resident) global scratch and are
+    // streamed through shared-memory tiles; only MISC lives in smem
+    L.large = 1;
+    const int nw = threads / 32;
+    L.tiles_off = 0;
+    so = nw >= 16 ? TileCfg<16>::DOUBLES : (nw >= 8 ? TileCfg<8>::DOUBLES : TileCfg<4>::DOUBLES);
+    budget = so + ((sz[SB_MISC] + 1) & ~1LL);
+  }
   for (int i = 0; i < SB_COUNT; ++i) {
     const int64_t s = (sz[i] + 1) & ~1LL;   // 16-byte granules
-    if (so + s <= budget) {
+    if (i == SB_MISC || (!L.large && so + s <= budget)) {
       L.off[i] = so;
       L.in_smem[i] = 1;
       so += s;
