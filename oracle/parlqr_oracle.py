@@ -376,46 +376,25 @@ def solve(prob, J=None, splits=None, rank_tol=RANK_TOL, workers=1):
     k1u = np.empty((T, m))
     mu_left = np.empty((J - 1, n))
     lambda_right = np.empty((J - 1, n))
-    bounds = [x_init] + [links[i] for i in range(J - 1)]
-    # reconstruction (parallel.py:485-525)
+    # reconstruction (parallel.py:485-525), segment by segment
     for j, seg in enumerate(segs):
         lo, hi = splits[j], splits[j + 1]
-        a = bounds[j]
-        last = j == J - 1
-        if last:
-            fold = seg["k1"]
-            xs = states[lo:]
-            us = controls[lo:]
-        else:
-            z = links[j]
-            fold = seg["Kz"] @ z + seg["k1"]
-            Kz[lo:hi] = seg["Kz"]
-            xs = np.empty((hi - lo + 1, n))
-            us = controls[lo:hi]
+        r = reconstruct_segment(prob, splits, j, seg, links)
         K[lo:hi] = seg["Kx"]
-        k[lo:hi] = fold
+        k[lo:hi] = r["fold"]
         k1u[lo:hi] = seg["k1"]
-        xs[0] = a
-        for s in range(hi - lo):
-            us[s] = seg["Kx"][s] @ xs[s] + fold[s]
-            xs[s + 1] = prob["Fx"][lo + s] @ xs[s] + prob["Fu"][lo + s] @ us[s] + prob["f1"][lo + s]
-        if last:
-            lam = -(prob["QxxT"] @ xs[-1] + prob["qx1T"])
-            lambdas[T] = lam
+        if "Kz" in seg:
+            Kz[lo:hi] = seg["Kz"]
+        controls[lo:hi] = r["us"]
+        states[lo:hi] = r["xs"][:-1]
+        lambdas[lo:hi] = r["lam"]
+        if j == J - 1:
+            states[T] = r["xs"][-1]
+            lambdas[T] = r["lam_T"]
         else:
-            states[lo:hi] = xs[:-1]
-            Vxx0, Vzx0, Vzz0, vx10, vz10 = seg["vf0"]
-            mu = -(Vzx0 @ a + Vzz0 @ z + vz10)
-            mu_left[j] = mu
-            lam = -mu
-        for s in range(hi - lo - 1, -1, -1):
-            t = lo + s
-            lam = prob["Fx"][t].T @ lam - (prob["Qxx"][t] @ states[t]
-                                           + prob["Qux"][t].T @ controls[t]
-                                           + prob["qx1"][t])
-            lambdas[t] = lam
+            mu_left[j] = r["mu"]
         if j:
-            lambda_right[j - 1] = lam
+            lambda_right[j - 1] = r["lam"][0]
     mismatch = float(np.abs(mu_left + lambda_right).max())
     return {
         "states": states, "controls": controls, "lambdas": lambdas,
@@ -427,6 +406,47 @@ def solve(prob, J=None, splits=None, rank_tol=RANK_TOL, workers=1):
         "kkt": kkt_residual(prob, states, controls, lambdas),
         "splits": tuple(splits),
     }
+
+
+def reconstruct_segment(prob, splits, j, seg, links):
+    """The reconstruction of one segment (parallel.py:485-525): fold
+    ``k = Kz z + k1`` (:495), rollout (:498-502), multiplier seed (:505-515)
+    and backward multiplier recursion (:518-523).  Returns the segment's
+    rollout ``xs`` (L+1 states, the last one the rollout end), ``us``,
+    ``fold``, multipliers ``lam`` at stages lo..hi-1 and the seed values."""
+    J = len(splits) - 1
+    lo, hi = splits[j], splits[j + 1]
+    n = prob["x_init"].shape[0]
+    m = prob["qu1"].shape[1]
+    a = prob["x_init"] if j == 0 else links[j - 1]
+    last = j == J - 1
+    if last:
+        fold = seg["k1"]
+    else:
+        z = links[j]
+        fold = seg["Kz"] @ z + seg["k1"]
+    xs = np.empty((hi - lo + 1, n))
+    us = np.empty((hi - lo, m))
+    xs[0] = a
+    for s in range(hi - lo):
+        us[s] = seg["Kx"][s] @ xs[s] + fold[s]
+        xs[s + 1] = prob["Fx"][lo + s] @ xs[s] + prob["Fu"][lo + s] @ us[s] + prob["f1"][lo + s]
+    out = {"xs": xs, "us": us, "fold": fold}
+    if last:
+        lam = -(prob["QxxT"] @ xs[-1] + prob["qx1T"])
+        out["lam_T"] = lam
+    else:
+        Vxx0, Vzx0, Vzz0, vx10, vz10 = seg["vf0"]
+        mu = -(Vzx0 @ a + Vzz0 @ z + vz10)
+        out["mu"] = mu
+        lam = -mu
+    lams = np.empty((hi - lo, n))
+    for s in range(hi - lo - 1, -1, -1):
+        t = lo + s
+        lam = prob["Fx"][t].T @ lam - (prob["Qxx"][t] @ xs[s] + prob["Qux"][t].T @ us[s] + prob["qx1"][t])
+        lams[s] = lam
+    out["lam"] = lams
+    return out
 
 
 def _solve_one(args):

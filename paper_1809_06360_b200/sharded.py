@@ -1,0 +1,191 @@
+"""Horizon sharding of one (batch of) partitioned solve(s) across ranks.
+
+One process per GPU (``torch.distributed``, NCCL over NVLink for the GPU
+backend).  Rank r owns a contiguous range of segments; the phases of the C ABI
+(``include/parlqr_b200.h``) run on it with three exchanges:
+
+1. sweeps of the local segments (``plq_sweep_segments``), then ONE all-gather
+   of the segment-start value blocks ``vf0`` (the only data the coupling needs
+   -- the reference ships the same blocks back from its worker pool,
+   ``parallel.py:230-240``) and of the per-segment status;
+2. the link solve, replicated: every rank factors the same system from the
+   same bytes, so the links are bitwise identical on all ranks;
+3. local reconstruction, an all-gather of the ``mu_left / lambda_right`` rows
+   (the link-stage KKT rows need the right neighbour's multiplier), the
+   link-stage rows, and an all-gather of the per-segment partials followed by
+   a fixed-order reduction -- objective / KKT / mismatch are identical for any
+   rank count.
+
+The orchestration is backend-agnostic: :class:`DeviceBackend` drives the CUDA
+library; the tests drive the same code with a CPU (oracle) backend over gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _native
+from .parallel import BatchSolver, raise_for_status
+
+
+def shard_range(J, world, rank):
+    """Balanced contiguous segment range of ``rank`` (remainder to early ranks)."""
+    base, extra = divmod(J, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _gather_rows(dist, group, local, J, world, torch):
+    """All-gather per-segment rows.
+
+    ``local``: tensor (B, S_r, X) holding this rank's segments' rows.  Returns
+    a (B, J, X) tensor with every rank's rows in segment order.  Ranks own
+    unequal counts, so rows are padded to the largest shard for the
+    equal-size collective.
+    """
+    B, _, X = local.shape
+    smax = -(-J // world)
+    send = torch.zeros((B, smax, X), dtype=local.dtype, device=local.device)
+    send[:, :local.shape[1]] = local
+    flat = torch.empty((world * B, smax, X), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(flat, send.contiguous(), group=group)   # concatenation form (NCCL and gloo)
+    recv = flat.view(world, B, smax, X)
+    out = torch.empty((B, J, X), dtype=local.dtype, device=local.device)
+    for r in range(world):
+        lo, hi = shard_range(J, world, r)
+        out[:, lo:hi] = recv[r, :, :hi - lo]
+    return out
+
+
+def solve_sharded(backend, dist, group=None):
+    """Run one sharded solve; every rank returns the same scalar results."""
+    torch = backend.torch
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    J = backend.J
+    j0, j1 = shard_range(J, world, rank)
+    # 1. local sweeps, exchange of segment-start value blocks and status
+    if j1 > j0:
+        backend.sweep(j0, j1)
+    vf0 = _gather_rows(dist, group, backend.vf0_rows(j0, j1), J, world, torch)
+    status = _gather_rows(dist, group, backend.status_rows(j0, j1), J, world, torch)
+    backend.set_vf0(vf0)
+    raise_for_status(status[:, :, 0].cpu().numpy())
+    # 2. replicated coupling solve
+    backend.link()
+    raise_for_status(backend.status_all())
+    # 3. local reconstruction, multiplier rows, link-stage KKT rows, partials
+    if j1 > j0:
+        backend.recon(j0, j1)
+    ml = _gather_rows(dist, group, backend.multiplier_rows(j0, j1), J, world, torch)
+    backend.set_multiplier_rows(ml)
+    if j1 > j0:
+        backend.boundary(j0, j1)
+    parts = _gather_rows(dist, group, backend.partial_rows(j0, j1), J, world, torch)
+    backend.set_partials(parts)
+    backend.finalize()
+    return backend.results()
+
+
+class DeviceBackend:
+    """GPU backend: a :class:`BatchSolver`'s buffers driven phase by phase."""
+
+    def __init__(self, solver: BatchSolver, inputs):
+        self.solver = solver
+        self.torch = solver.torch
+        self.lib = solver.lib
+        self.J = solver.J
+        self.n = solver.n
+        solver.check_inputs(inputs)
+        self.prob = solver._problem_struct(inputs)
+        torch = self.torch
+        self.partials = torch.zeros((solver.B, solver.J, 3), dtype=torch.float64, device=solver.device)
+        self.stream = torch.cuda.current_stream(solver.device)
+
+    def _call(self, name, *args):
+        fn = getattr(self.lib, name)
+        s = self.solver
+        head = (ctypes.byref(self.prob), ctypes.byref(s._outs))
+        rc = fn(*head, *args)
+        _native.check(rc, name)
+
+    def _ws(self):
+        s = self.solver
+        return ctypes.c_void_p(s.workspace.data_ptr()), s.ws_bytes, ctypes.c_void_p(self.stream.cuda_stream)
+
+    def sweep(self, j0, j1):
+        self._call("plq_sweep_segments", j0, j1, *self._ws())
+
+    def vf0_rows(self, j0, j1):
+        return self.solver.out["vf0"][:, j0:j1]
+
+    def status_rows(self, j0, j1):
+        return self.solver.out["status"][:, j0:j1, None].to(self.torch.float64)
+
+    def set_vf0(self, vf0):
+        self.solver.out["vf0"].copy_(vf0)
+        # status rows gathered separately; keep the local copy in sync for link flags
+        self.solver.out["status"].zero_()
+
+    def status_all(self):
+        return self.solver.out["status"].cpu().numpy()
+
+    def link(self):
+        self._call("plq_link_solve", *self._ws())
+
+    def recon(self, j0, j1):
+        ws = self._ws()
+        self._call("plq_reconstruct_segments", j0, j1, ctypes.c_void_p(self.partials.data_ptr()), *ws)
+
+    def multiplier_rows(self, j0, j1):
+        # row j: [mu_left[j] (j < J-1) | lambda_right[j-1] (j > 0)]
+        torch = self.torch
+        s = self.solver
+        B, n, J = s.B, s.n, s.J
+        rows = torch.zeros((B, j1 - j0, 2 * n), dtype=torch.float64, device=s.device)
+        a, b = j0, min(j1, J - 1)
+        if b > a:
+            rows[:, a - j0:b - j0, :n] = s.out["mu_left"][:, a:b]
+        a, b = max(j0, 1), j1
+        if b > a:
+            rows[:, a - j0:b - j0, n:] = s.out["lambda_right"][:, a - 1:b - 1]
+        return rows
+
+    def set_multiplier_rows(self, rows):
+        s = self.solver
+        n, J = s.n, s.J
+        if J > 1:
+            s.out["mu_left"][:, :J - 1] = rows[:, :J - 1, :n]
+            s.out["lambda_right"][:, :J - 1] = rows[:, 1:, n:]
+
+    def boundary(self, j0, j1):
+        self._call("plq_boundary_segments", j0, j1, ctypes.c_void_p(self.partials.data_ptr()), *self._ws())
+
+    def partial_rows(self, j0, j1):
+        return self.partials[:, j0:j1]
+
+    def set_partials(self, parts):
+        self.partials.copy_(parts)
+
+    def finalize(self):
+        self._call("plq_finalize", ctypes.c_void_p(self.partials.data_ptr()), *self._ws())
+
+    def results(self):
+        o = self.solver.out
+        return {k: o[k] for k in ("objective", "kkt_inf", "link_mismatch", "link_residual", "links")}
+
+
+def sharded_solve_device(inputs, J=None, partition=None, dist=None, group=None, device=None, tolerances=None):
+    """Convenience wrapper: a horizon-sharded solve of device ``inputs`` (each
+    rank holds the full stacked inputs; it only reads its segments')."""
+    from .problem import DEFAULT_TOLERANCES
+    B, T, n = (int(s) for s in inputs["qx1"].shape)
+    m = int(inputs["qu1"].shape[2])
+    solver = BatchSolver(B, T, n, m, J=J, partition=partition, device=device,
+                         tolerances=tolerances or DEFAULT_TOLERANCES)
+    backend = DeviceBackend(solver, inputs)
+    res = solve_sharded(backend, dist, group)
+    return solver, res
+
+
+__all__ = ["shard_range", "solve_sharded", "DeviceBackend", "sharded_solve_device"]
