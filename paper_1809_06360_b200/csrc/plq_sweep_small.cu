@@ -56,8 +56,8 @@ struct SL {
   static constexpr int Y = G + M * LDW;
   static constexpr int MUU = Y + M * LDW;               // M x M
   static constexpr int H = MUU + MM;                    // N x LDW constraint rows [Hx | Hz | h1]
-  static constexpr int TAU = H + N * LDW;               // M
-  static constexpr int RD = TAU + M;                    // M
+  static constexpr int TAU = H + N * LDW;               // M x M (tau, or the WY factor T)
+  static constexpr int RD = TAU + M * M;                // M
   static constexpr int RED = RD + M;                    // 8
   static constexpr int BAR = (RED + 8 + 1) & ~1;        // mbarrier (8 bytes)
   static constexpr int TOTAL = BAR + 2;
@@ -155,9 +155,112 @@ __device__ __forceinline__ void gqr(double* A, int r, double* X, double* tau, do
   gsync<NWG>(grp);
 }
 
+// Householder QR of the r x M panel (r <= 32, M <= 8) held one row per lane
+// in registers (LAPACK dlarfg convention, as cta_householder_qr), then
+// Q' X for the r x W block X via the compact WY form Q' = I - V T' V'
+// (dlarft): y = V'x, z = T'y, x -= V z per column -- independent
+// dot products instead of M sequential reflector sweeps.  R (upper) and V
+// (strictly lower, unit diagonal implicit) are written back LAPACK-style to
+// A; rdiag gets diag(R).
+template <int M, int W, int LDA, int LDX>
+__device__ __forceinline__ void warp_qr_wy(double* A, int r, double* X, double* Tm, double* rdiag) {
+  const int lane = threadIdx.x & 31;
+  const bool row = lane < r;
+  double a[M], v[M], tau[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) a[k] = row ? A[lane * LDA + k] : 0.0;
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const double x = (lane > j && row) ? a[j] : 0.0;
+    const double sig = warp_sum(x * x);
+    const double alpha = __shfl_sync(0xffffffffu, a[j], j);
+    double t = 0.0, beta = alpha, scale = 0.0;
+    if (sig > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + sig), alpha);
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    const double vj = (lane == j) ? 1.0 : ((lane > j && row) ? a[j] * scale : 0.0);
+    v[j] = vj;
+    tau[j] = t;
+#pragma unroll
+    for (int k = j + 1; k < M; ++k) {
+      const double sk = warp_sum(vj * a[k]);
+      if (lane >= j) a[k] -= t * sk * vj;
+    }
+    if (lane == j) a[j] = beta;
+    if (lane == 0) rdiag[j] = beta;
+  }
+  // write R (upper) and V (strictly lower) back in place
+  if (row) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) A[lane * LDA + k] = (k >= lane) ? a[k] : v[k];
+  }
+  // T (upper triangular, M x M): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j,0:j] V[:,0:j]' v_j
+  double vtv[M][M];
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+#pragma unroll
+    for (int j = i + 1; j < M; ++j) vtv[i][j] = warp_sum(v[i] * v[j]);
+  if (lane == 0) {
+    double T[M][M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) T[i][j] = 0.0;
+      T[j][j] = tau[j];
+#pragma unroll
+      for (int i = 0; i < j; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = i; k < j; ++k) t += T[i][k] * vtv[k][j];
+        T[i][j] = -tau[j] * t;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+      for (int j = 0; j < M; ++j) Tm[i * M + j] = T[i][j];
+  }
+  __syncwarp();
+  // X <- (I - V T' V') X, lane per column; V read back from A (unit diagonal)
+  for (int c = lane; c < W; c += 32) {
+    double y[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) y[j] = 0.0;
+    for (int i = 0; i < r; ++i) {
+      const double xi = X[i * LDX + c];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const double vij = (i == j) ? 1.0 : (i > j ? A[i * LDA + j] : 0.0);
+        y[j] += vij * xi;
+      }
+    }
+    double z[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i <= j; ++i) t += Tm[i * M + j] * y[i];   // (T' y)_j
+      z[j] = t;
+    }
+    for (int i = 0; i < r; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const double vij = (i == j) ? 1.0 : (i > j ? A[i * LDA + j] : 0.0);
+        t += vij * z[j];
+      }
+      X[i * LDX + c] -= t;
+    }
+  }
+  __syncwarp();
+}
+
 template <int N, int M, int NWG, bool SERIAL>
 __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, int grp, int gt, int64_t b, int j,
-                                              uint32_t& phase) {
+                                              uint32_t& phase, const unsigned short* pairs) {
+  constexpr int NP = N * (N - 1) / 2;
   using S = SL<N, M>;
   constexpr int NT = NWG * 32;
   constexpr int NZ = SERIAL ? 0 : N;
@@ -212,44 +315,65 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     mbar_wait(bar, phase);
     phase ^= 1u;
 
-    // GEMM1: [VF; Z] = [Vxx; Vzx] F; Z lands in place: Mzx -> Vzx, Mzu' -> P, mz1 -> vz1
-    ggemm_f<N + NZ, FW, N, NWG>(
+    // GEMM1: [VF; Z] = [Vxx; Vzx] [Fx | Fu]; Z lands in place: Mzx -> Vzx, Mzu' -> P.
+    // The f1 column (w = vx1 + Vxx f1, mz1 = vz1 + Vzx f1) is a lane-parallel
+    // dot product instead of a mostly empty 8-wide DMMA tile; it reads Vzx
+    // before the in-place epilogue overwrites it.
+    double wcol = 0.0;
+    const bool wrow = gt < N + NZ;
+    if (wrow) {
+      const double* vr = Vxx + gt * LDN;
+#pragma unroll 4
+      for (int k = 0; k < N; ++k) wcol += vr[k] * sm[S::SF1 + k];
+    }
+    gsync<NWG>(grp);
+    ggemm_f<N + NZ, N + M, N, NWG>(
         [&](int i, int k) { return Vxx[i * LDN + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
         [&](int i, int c, double acc) {
           if (i < N) {
-            VF[i * LDF + c] = (c == N + M) ? vx1[i] + acc : acc;
+            VF[i * LDF + c] = acc;
           } else {
             const int zi = i - N;
             if (c < N)
               Vzx[zi * LDN + c] = acc;
-            else if (c < N + M)
-              P[(c - N) * LDW + N + zi] = acc;
             else
-              vz1[zi] += acc;
+              P[(c - N) * LDW + N + zi] = acc;
           }
         });
+    if (wrow) {
+      if (gt < N)
+        VF[gt * LDF + N + M] = vx1[gt] + wcol;
+      else
+        vz1[gt - N] += wcol;
+    }
     gsync<NWG>(grp);
-    // GEMM2: [Mxx mx1; Mux Muu mu1] = [Fx Fu]' [VFx VFu w] + Q-blocks
-    ggemm_f<N + M, FW, N, NWG>(
+    // GEMM2: [Mxx ; Mux Muu] = [Fx Fu]' [VFx VFu] + Q-blocks; the w column
+    // (mx1 = qx1 + Fx' w, mu1 = qu1 + Fu' w) lane-parallel
+    ggemm_f<N + M, N + M, N, NWG>(
         [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
         [&](int i, int c, double acc) {
           if (i < N) {
-            if (c < N)
-              Vxx[i * LDN + c] = Qxx[i * N + c] + acc;
-            else if (c == N + M)
-              vx1[i] = qx1[i] + acc;
+            if (c < N) Vxx[i * LDN + c] = Qxx[i * N + c] + acc;
           } else {
             const int u = i - N;
             if (c < N)
               P[u * LDW + c] = Qux[u * N + c] + acc;
-            else if (c < N + M)
-              Muu[u * M + (c - N)] = Quu[u * M + (c - N)] + acc;
             else
-              P[u * LDW + CC] = qu1[u] + acc;
+              Muu[u * M + (c - N)] = Quu[u * M + (c - N)] + acc;
           }
         });
+    if (gt < N + M) {
+      double t = 0.0;
+#pragma unroll 4
+      for (int k = 0; k < N; ++k) t += fload<N, M>(sm, k, gt) * VF[k * LDF + N + M];
+      if (gt < N)
+        vx1[gt] = qx1[gt] + t;
+      else
+        P[(gt - N) * LDW + CC] = qu1[gt - N] + t;
+    }
     gsync<NWG>(grp);
 
+    const bool constrained = (r != 0);
     if (r == 0) {
       // ---- unconstrained stage: G = -Muu^{-1} P, Cholesky in every lane's registers
       if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);
@@ -264,9 +388,10 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           for (int q = 0; q < k; ++q) v -= Lr[i][q] * Lr[k][q];
           if (i == k) {
             fail |= !(v > 0.0);
-            v = sqrt(v > 0.0 ? v : 1.0);
-            Lr[k][k] = v;
-            id[k] = 1.0 / v;
+            const double vv = v > 0.0 ? v : 1.0;
+            const double rs = rsqrt(vv);
+            Lr[k][k] = vv * rs;
+            id[k] = rs;
           } else {
             Lr[i][k] = v * id[k];
           }
@@ -327,7 +452,11 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       }
       for (int i = gt; i < r; i += NT) H[i * LDW + CC] += VF[i * LDF + N + M];
       gsync<NWG>(grp);
-      gqr<M, W, LDF, LDW, NWG>(VF + N, r, H, tau, rdiag, red, grp, gw, gt);
+      if constexpr (NWG == 1) {
+        warp_qr_wy<M, W, LDF, LDW>(VF + N, r, H, tau, rdiag);   // tau slot holds T (M*M <= TAU+RD+RED)
+      } else {
+        gqr<M, W, LDF, LDW, NWG>(VF + N, r, H, tau, rdiag, red, grp, gw, gt);
+      }
       double rmax = 0.0, rmin = 1e308;
 #pragma unroll
       for (int i = 0; i < M; ++i) {
@@ -374,39 +503,55 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     }
     for (int u = gt; u < M; u += NT) a.k1[st * M + u] = G[u * LDW + CC];
 
-    // ---- value update: Y = P + Muu G ; V += P'G + G'Y
-    ggemm<M, W, M, false, M, LDW, NWG>(Muu, G, gw,
-                                       [&](int i, int c, double acc) { Y[i * LDW + c] = P[i * LDW + c] + acc; });
-    gsync<NWG>(grp);
-    ggemm<N + NZ, W, 2 * M, true, LDW, LDW, NWG>(P, G, gw, [&](int i, int c, double acc) {
+    // ---- value update.  Tail stages: Y = P + Muu G, V += P'G + G'Y (the
+    // reference's terms, endpoint.py:285-294).  Unconstrained stages have
+    // G = -Muu^{-1} P, so Y = 0 in exact arithmetic and the update is the
+    // standard Riccati form V += P'G (K = m instead of 2m, no Y GEMM).
+    auto vupd = [&](int i, int c, double acc) {
       if (i < N) {
-        if (c < N)
-          Vxx[i * LDN + c] += acc;
-        else if (c == CC)
-          vx1[i] += acc;
+        if (c < N) Vxx[i * LDN + c] += acc;
       } else {
         const int zi = i - N;
         if (c < N)
           Vzx[zi * LDN + c] += acc;
-        else if (c < CC)
-          Vzz[zi * LDN + (c - N)] += acc;
         else
-          vz1[zi] += acc;
+          Vzz[zi * LDN + (c - N)] += acc;
       }
-    });
+    };
+    if (constrained) {
+      ggemm<M, W, M, false, M, LDW, NWG>(Muu, G, gw,
+                                         [&](int i, int c, double acc) { Y[i * LDW + c] = P[i * LDW + c] + acc; });
+      gsync<NWG>(grp);
+      ggemm<N + NZ, W - 1, 2 * M, true, LDW, LDW, NWG>(P, G, gw, vupd);
+    } else {
+      ggemm<N + NZ, W - 1, M, true, LDW, LDW, NWG>(P, G, gw, vupd);
+    }
+    // constant column (vx1, vz1) lane-parallel
+    if (gt < N + NZ) {
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < M; ++u) t += P[u * LDW + gt] * G[u * LDW + CC];
+      if (constrained) {
+#pragma unroll
+        for (int u = 0; u < M; ++u) t += G[u * LDW + gt] * Y[u * LDW + CC];
+      }
+      if (gt < N)
+        vx1[gt] += t;
+      else
+        vz1[gt - N] += t;
+    }
     gsync<NWG>(grp);
-    // symmetrize Vxx (and Vzz): lane per row, upper-triangle partner
-    for (int i = gt; i < N; i += NT) {
-#pragma unroll 4
-      for (int c = i + 1; c < N; ++c) {
-        const double v = 0.5 * (Vxx[i * LDN + c] + Vxx[c * LDN + i]);
-        Vxx[i * LDN + c] = v;
-        Vxx[c * LDN + i] = v;
-        if (!SERIAL) {
-          const double w = 0.5 * (Vzz[i * LDN + c] + Vzz[c * LDN + i]);
-          Vzz[i * LDN + c] = w;
-          Vzz[c * LDN + i] = w;
-        }
+    // symmetrize Vxx (and Vzz) as 0.5 (V + V'): all N(N-1)/2 pairs in parallel
+    for (int pp = gt; pp < NP; pp += NT) {
+      const int pr = pairs[pp];
+      const int i = pr >> 8, c = pr & 255;
+      const double v = 0.5 * (Vxx[i * LDN + c] + Vxx[c * LDN + i]);
+      Vxx[i * LDN + c] = v;
+      Vxx[c * LDN + i] = v;
+      if (!SERIAL) {
+        const double w = 0.5 * (Vzz[i * LDN + c] + Vzz[c * LDN + i]);
+        Vzz[i * LDN + c] = w;
+        Vzz[c * LDN + i] = w;
       }
     }
     gsync<NWG>(grp);
@@ -434,8 +579,14 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS) sweep_small_kernel(SweepArg
   const int gt = threadIdx.x % (NWG * 32);
   double* sm = smem + grp * SL<N, M>::TOTAL;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SL<N, M>::BAR);
+  // (i, c) pairs of the strict upper triangle, for the symmetrization
+  __shared__ unsigned short pairs[N * (N - 1) / 2];
+  for (int p = threadIdx.x; p < N * N; p += blockDim.x) {
+    const int i = p / N, c = p % N;
+    if (i < c) pairs[i * (2 * N - i - 1) / 2 + (c - i - 1)] = (unsigned short)((i << 8) | c);
+  }
   if (gt == 0) mbar_init(bar, 1);
-  gsync<NWG>(grp);
+  __syncthreads();
   uint32_t phase = 0;
   const int nloc = a.seg_end - a.seg_begin;
   const int64_t total = a.p.B * nloc;
@@ -443,9 +594,9 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS) sweep_small_kernel(SweepArg
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
     if (j == a.p.J - 1)
-      small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j, phase);
+      small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j, phase, pairs);
     else
-      small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j, phase);
+      small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j, phase, pairs);
   }
 }
 
