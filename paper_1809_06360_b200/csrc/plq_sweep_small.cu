@@ -59,7 +59,8 @@ struct SL {
   static constexpr int TAU = H + N * LDW;               // M x M (tau, or the WY factor T)
   static constexpr int RD = TAU + M * M;                // M
   static constexpr int RED = RD + M;                    // 8
-  static constexpr int BAR = (RED + 8 + 1) & ~1;        // mbarrier (8 bytes)
+  static constexpr int DUM = RED + 8;                   // 32 per-lane dummy slots (branch-free epilogues)
+  static constexpr int BAR = (DUM + 32 + 1) & ~1;       // mbarrier (8 bytes)
   static constexpr int TOTAL = BAR + 2;
   static constexpr uint32_t STAGE_BYTES = 8u * (2 * NN + 2 * NM + MM + 2 * N + M);
   static_assert(SFX % 2 == 0 && SFU % 2 == 0 && SF1 % 2 == 0 && SQXX % 2 == 0 && SQUX % 2 == 0 &&
@@ -291,6 +292,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   double* tau = sm + S::TAU;
   double* rdiag = sm + S::RD;
   double* red = sm + S::RED;
+  double* dum = sm + S::DUM + lane;   // per-lane sink for skipped epilogue elements
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
 
   if (gt == 0) stage_issue<N, M>(p, b * T + lo + L - 1, sm, bar);
@@ -323,22 +325,21 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     const bool wrow = gt < N + NZ;
     if (wrow) {
       const double* vr = Vxx + gt * LDN;
-#pragma unroll 4
-      for (int k = 0; k < N; ++k) wcol += vr[k] * sm[S::SF1 + k];
+      double w2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; k += 2) {
+        wcol += vr[k] * sm[S::SF1 + k];
+        w2 += vr[k + 1] * sm[S::SF1 + k + 1];
+      }
+      wcol += w2;
     }
     gsync<NWG>(grp);
     ggemm_f<N + NZ, N + M, N, NWG>(
         [&](int i, int k) { return Vxx[i * LDN + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
         [&](int i, int c, double acc) {
-          if (i < N) {
-            VF[i * LDF + c] = acc;
-          } else {
-            const int zi = i - N;
-            if (c < N)
-              Vzx[zi * LDN + c] = acc;
-            else
-              P[(c - N) * LDW + N + zi] = acc;
-          }
+          const int zi = i - N;
+          double* d = (i < N) ? VF + i * LDF + c : ((c < N) ? Vzx + zi * LDN + c : P + (c - N) * LDW + N + zi);
+          *d = acc;
         });
     if (wrow) {
       if (gt < N)
@@ -352,20 +353,20 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     ggemm_f<N + M, N + M, N, NWG>(
         [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
         [&](int i, int c, double acc) {
-          if (i < N) {
-            if (c < N) Vxx[i * LDN + c] = Qxx[i * N + c] + acc;
-          } else {
-            const int u = i - N;
-            if (c < N)
-              P[u * LDW + c] = Qux[u * N + c] + acc;
-            else
-              Muu[u * M + (c - N)] = Quu[u * M + (c - N)] + acc;
-          }
+          const int u = i - N;
+          const bool xr = i < N, xc = c < N;
+          const double* q = xr ? Qxx + i * N + (xc ? c : 0) : (xc ? Qux + u * N + c : Quu + u * M + (c - N));
+          double* d = xr ? (xc ? Vxx + i * LDN + c : dum) : (xc ? P + u * LDW + c : Muu + u * M + (c - N));
+          *d = *q + acc;
         });
     if (gt < N + M) {
-      double t = 0.0;
-#pragma unroll 4
-      for (int k = 0; k < N; ++k) t += fload<N, M>(sm, k, gt) * VF[k * LDF + N + M];
+      double t = 0.0, t2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; k += 2) {
+        t += fload<N, M>(sm, k, gt) * VF[k * LDF + N + M];
+        t2 += fload<N, M>(sm, k + 1, gt) * VF[(k + 1) * LDF + N + M];
+      }
+      t += t2;
       if (gt < N)
         vx1[gt] = qx1[gt] + t;
       else
@@ -508,15 +509,10 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     // G = -Muu^{-1} P, so Y = 0 in exact arithmetic and the update is the
     // standard Riccati form V += P'G (K = m instead of 2m, no Y GEMM).
     auto vupd = [&](int i, int c, double acc) {
-      if (i < N) {
-        if (c < N) Vxx[i * LDN + c] += acc;
-      } else {
-        const int zi = i - N;
-        if (c < N)
-          Vzx[zi * LDN + c] += acc;
-        else
-          Vzz[zi * LDN + (c - N)] += acc;
-      }
+      const int zi = i - N;
+      double* d = (i < N) ? ((c < N) ? Vxx + i * LDN + c : dum)
+                          : ((c < N) ? Vzx + zi * LDN + c : Vzz + zi * LDN + (c - N));
+      *d += acc;
     };
     if (constrained) {
       ggemm<M, W, M, false, M, LDW, NWG>(Muu, G, gw,
