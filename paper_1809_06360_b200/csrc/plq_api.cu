@@ -327,13 +327,28 @@ inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+// Batches are processed in chunks of problems on three streams so the upload
+// of chunk c+1, the solve of chunk c and the download of chunk c-1 overlap
+// (PCIe / C2C is full duplex); a single problem is one chunk.
+static void host_chunking(const plq_problem_t* hp, int* nchunks, int64_t* chunk_b, int* nstreams) {
+  const int nc = hp->B >= 64 ? 8 : (hp->B >= 4 ? 4 : 1);
+  *chunk_b = (hp->B + nc - 1) / nc;
+  *nchunks = (int)((hp->B + *chunk_b - 1) / *chunk_b);
+  *nstreams = *nchunks < 3 ? *nchunks : 3;
+}
+
 size_t plq_host_arena_bytes(const plq_problem_t* hp) {
   if (check_problem(hp)) return 0;
   size_t in_sz[12], out_sz[16], total = 0;
   host_sizes(hp, in_sz, out_sz);
   for (size_t s : in_sz) total += up256(s);
   for (size_t s : out_sz) total += up256(s);
-  return total + up256(plq_workspace_bytes(hp));
+  int nc, ns;
+  int64_t cb;
+  host_chunking(hp, &nc, &cb, &ns);
+  plq_problem_t c = *hp;
+  c.B = cb;
+  return total + (size_t)ns * up256(plq_workspace_bytes(&c));
 }
 
 int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, void* arena, size_t arena_bytes,
@@ -348,67 +363,85 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
     if (hp->split_times[j + 1] <= hp->split_times[j]) return fail(PLQ_ERR_ARG, "split times must be increasing");
   if (hp->split_times[0] != 0 || hp->split_times[hp->J] != hp->T)
     return fail(PLQ_ERR_ARG, "partition does not cover the horizon");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s0 = static_cast<cudaStream_t>(stream);
   size_t in_sz[12], out_sz[16];
   host_sizes(hp, in_sz, out_sz);
+  int nc, ns;
+  int64_t cb;
+  host_chunking(hp, &nc, &cb, &ns);
   char* cur = static_cast<char*>(arena);
   const void* hin[12] = {hp->split_times, hp->Qxx, hp->Qux, hp->Quu, hp->qx1, hp->qu1,
                          hp->Fx, hp->Fu, hp->f1, hp->QxxT, hp->qx1T, hp->x_init};
-  void* din[12];
+  char* din[12];
   for (int i = 0; i < 12; ++i) {
     din[i] = cur;
     cur += up256(in_sz[i]);
-    if (cudaMemcpyAsync(din[i], hin[i], in_sz[i], cudaMemcpyHostToDevice, s) != cudaSuccess)
-      return cuda_fail("H2D copy");
   }
-  void* dout[16];
+  char* dout[16];
   for (int i = 0; i < 16; ++i) {
     dout[i] = cur;
     cur += up256(out_sz[i]);
   }
-  plq_problem_t dp = *hp;
-  dp.split_times = static_cast<const int32_t*>(din[0]);
-  dp.Qxx = static_cast<const double*>(din[1]);
-  dp.Qux = static_cast<const double*>(din[2]);
-  dp.Quu = static_cast<const double*>(din[3]);
-  dp.qx1 = static_cast<const double*>(din[4]);
-  dp.qu1 = static_cast<const double*>(din[5]);
-  dp.Fx = static_cast<const double*>(din[6]);
-  dp.Fu = static_cast<const double*>(din[7]);
-  dp.f1 = static_cast<const double*>(din[8]);
-  dp.QxxT = static_cast<const double*>(din[9]);
-  dp.qx1T = static_cast<const double*>(din[10]);
-  dp.x_init = static_cast<const double*>(din[11]);
-  plq_outputs_t dout_s;
-  dout_s.K = (double*)dout[0];
-  dout_s.k = (double*)dout[1];
-  dout_s.x = (double*)dout[2];
-  dout_s.u = (double*)dout[3];
-  dout_s.lam = (double*)dout[4];
-  dout_s.links = (double*)dout[5];
-  dout_s.mu_left = (double*)dout[6];
-  dout_s.lambda_right = (double*)dout[7];
-  dout_s.vf0 = (double*)dout[8];
-  dout_s.Kz = (double*)dout[9];
-  dout_s.k1 = (double*)dout[10];
-  dout_s.objective = (double*)dout[11];
-  dout_s.kkt_inf = (double*)dout[12];
-  dout_s.link_mismatch = (double*)dout[13];
-  dout_s.link_residual = (double*)dout[14];
-  dout_s.status = (int32_t*)dout[15];
-  void* wsp = cur;
-  rc = plq_solve_parallel(&dp, &dout_s, wsp, plq_workspace_bytes(hp), s);
-  if (rc) return rc;
+  plq_problem_t cp = *hp;
+  cp.B = cb;
+  const size_t wsb = plq_workspace_bytes(&cp);
+  char* wsp[3];
+  for (int k = 0; k < ns; ++k) {
+    wsp[k] = cur;
+    cur += up256(wsb);
+  }
   void* hout[16] = {ho->K, ho->k, ho->x, ho->u, ho->lam, ho->links, ho->mu_left, ho->lambda_right,
                     ho->vf0, ho->Kz, ho->k1, ho->objective, ho->kkt_inf, ho->link_mismatch, ho->link_residual,
                     ho->status};
-  for (int i = 0; i < 16; ++i) {
-    if (!hout[i]) continue;
-    if (cudaMemcpyAsync(hout[i], dout[i], out_sz[i], cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return cuda_fail("D2H copy");
+  cudaStream_t st[3] = {s0, nullptr, nullptr};
+  cudaEvent_t ready = nullptr;
+  for (int k = 1; k < ns; ++k)
+    if (cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking) != cudaSuccess) return cuda_fail("stream create");
+  if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess) return cuda_fail("event create");
+  // the partition is shared by every chunk
+  if (cudaMemcpyAsync(din[0], hin[0], in_sz[0], cudaMemcpyHostToDevice, s0) != cudaSuccess) rc = cuda_fail("H2D copy");
+  cudaEventRecord(ready, s0);
+  for (int k = 1; k < ns && !rc; ++k) cudaStreamWaitEvent(st[k], ready, 0);
+  int launches = 0;
+  for (int c = 0; c < nc && !rc; ++c) {
+    cudaStream_t s = st[c % ns];
+    const int64_t b0 = c * cb, bc = (b0 + cb <= hp->B) ? cb : hp->B - b0;
+    // per-problem slice of every batched array: bytes per problem = total / B
+    for (int i = 1; i < 12 && !rc; ++i) {
+      const size_t per = in_sz[i] / (size_t)hp->B;
+      if (cudaMemcpyAsync(din[i] + b0 * per, (const char*)hin[i] + b0 * per, bc * per, cudaMemcpyHostToDevice, s) !=
+          cudaSuccess)
+        rc = cuda_fail("H2D copy");
+    }
+    if (rc) break;
+    plq_problem_t dp = *hp;
+    dp.B = bc;
+    dp.split_times = reinterpret_cast<const int32_t*>(din[0]);
+    const double** fields[11] = {&dp.Qxx, &dp.Qux, &dp.Quu, &dp.qx1, &dp.qu1, &dp.Fx,
+                                 &dp.Fu, &dp.f1, &dp.QxxT, &dp.qx1T, &dp.x_init};
+    for (int i = 1; i < 12; ++i) *fields[i - 1] = reinterpret_cast<const double*>(din[i] + b0 * (in_sz[i] / hp->B));
+    plq_outputs_t o;
+    double** ofields[15] = {&o.K, &o.k, &o.x, &o.u, &o.lam, &o.links, &o.mu_left, &o.lambda_right,
+                            &o.vf0, &o.Kz, &o.k1, &o.objective, &o.kkt_inf, &o.link_mismatch, &o.link_residual};
+    for (int i = 0; i < 15; ++i) *ofields[i] = reinterpret_cast<double*>(dout[i] + b0 * (out_sz[i] / hp->B));
+    o.status = reinterpret_cast<int32_t*>(dout[15] + b0 * (out_sz[15] / hp->B));
+    rc = plq_solve_parallel(&dp, &o, wsp[c % ns], wsb, s);
+    launches += g_launches;
+    if (rc) break;
+    for (int i = 0; i < 16 && !rc; ++i) {
+      if (!hout[i]) continue;
+      const size_t per = out_sz[i] / (size_t)hp->B;
+      if (cudaMemcpyAsync((char*)hout[i] + b0 * per, dout[i] + b0 * per, bc * per, cudaMemcpyDeviceToHost, s) !=
+          cudaSuccess)
+        rc = cuda_fail("D2H copy");
+    }
   }
-  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail("stream sync");
-  return PLQ_OK;
+  for (int k = 0; k < ns; ++k)
+    if (cudaStreamSynchronize(st[k]) != cudaSuccess && !rc) rc = cuda_fail("stream sync");
+  for (int k = 1; k < ns; ++k) cudaStreamDestroy(st[k]);
+  cudaEventDestroy(ready);
+  g_launches = launches;
+  return rc;
 }
 
 }  // extern "C"
