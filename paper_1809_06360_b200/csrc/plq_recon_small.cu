@@ -497,6 +497,252 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
 }
 
 // ----------------------------------------------------------------------------
+// ring variant for longer segments / larger n (BASELINE config 2: n = 32,
+// m = 8, L = 64): a CTA per segment, stages streamed through an RS-slot ring
+// of bulk copies (forward: all 11 fields; backward: Fx, Fu only), g/h kept on
+// chip for the whole segment, row-fused passes over the CTA's threads.
+
+template <int N, int M>
+struct RingL {
+  static constexpr int NN = N * N, NM = N * M, MM = M * M;
+  static constexpr int SLOT = 2 * NN + 4 * NM + MM + 2 * N + 2 * M;   // one stage, forward fields
+  static constexpr int FX = 0, FU = NN, F1 = FU + NM, QXX = F1 + N, QUX = QXX + NN, QUU = QUX + NM,
+                       QX1 = QUU + MM, QU1 = QX1 + N, KX = QU1 + M, KZ = KX + NM, K1 = KZ + NM;
+  static constexpr uint32_t FWD_BYTES = 8u * SLOT, BWD_BYTES = 8u * (NN + NM);
+};
+
+template <int N, int M>
+__device__ __forceinline__ void ring_issue_fwd(const ReconArgs& A, double* slot, uint64_t* bar, int64_t st) {
+  using R = RingL<N, M>;
+  constexpr int NN = N * N, NM = N * M, MM = M * M;
+  const plq_problem_t& p = A.p;
+  fence_proxy_async();
+  mbar_arrive_tx(bar, R::FWD_BYTES);
+  bulk_g2s(slot + R::FX, p.Fx + st * NN, 8u * NN, bar);
+  bulk_g2s(slot + R::FU, p.Fu + st * NM, 8u * NM, bar);
+  bulk_g2s(slot + R::F1, p.f1 + st * N, 8u * N, bar);
+  bulk_g2s(slot + R::QXX, p.Qxx + st * NN, 8u * NN, bar);
+  bulk_g2s(slot + R::QUX, p.Qux + st * NM, 8u * NM, bar);
+  bulk_g2s(slot + R::QUU, p.Quu + st * MM, 8u * MM, bar);
+  bulk_g2s(slot + R::QX1, p.qx1 + st * N, 8u * N, bar);
+  bulk_g2s(slot + R::QU1, p.qu1 + st * M, 8u * M, bar);
+  bulk_g2s(slot + R::KX, A.Kx + st * NM, 8u * NM, bar);
+  bulk_g2s(slot + R::KZ, A.Kz + st * NM, 8u * NM, bar);
+  bulk_g2s(slot + R::K1, A.k1 + st * M, 8u * M, bar);
+}
+
+template <int N, int M>
+__device__ __forceinline__ void ring_issue_bwd(const ReconArgs& A, double* slot, uint64_t* bar, int64_t st) {
+  using R = RingL<N, M>;
+  constexpr int NN = N * N, NM = N * M;
+  fence_proxy_async();
+  mbar_arrive_tx(bar, R::BWD_BYTES);
+  bulk_g2s(slot + R::FX, A.p.Fx + st * NN, 8u * NN, bar);
+  bulk_g2s(slot + R::FU, A.p.Fu + st * NM, 8u * NM, bar);
+}
+
+template <int N, int M, int NT, int RS>
+__global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
+  using R = RingL<N, M>;
+  constexpr int NN = N * N, NM = N * M, MM = M * M;
+  static_assert(2 * N + 3 * M <= NT, "row-fused passes need one thread per row");
+  extern __shared__ __align__(16) double sm[];
+  const plq_problem_t& p = A.p;
+  const int J = p.J, T = p.T, tid = threadIdx.x;
+  const int LMAX = p.max_seg_len;
+  double* ring = sm;                                  // RS x SLOT
+  double* vfb = ring + RS * R::SLOT;                  // Vzx0, Vzz0, vx10, vz10 (2NN + 2N)
+  double* gh = vfb + 2 * NN + 2 * N;                  // LMAX x (N+M)
+  double* x = gh + (size_t)LMAX * (N + M);
+  double* xn = x + N;
+  double* uu = xn + N;
+  double* z = uu + M;
+  double* av = z + N;
+  double* lam = av + N;
+  double* tf = lam + N;    // pass-1 results
+  double* tu = tf + N;
+  double* t0 = tu + M;
+  double* t2 = t0 + N;
+  double* tk = t2 + M;
+  double* red = tk + M;    // NT / 32 doubles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + NT / 32 + ((N + M) & 1));
+  uint64_t* vbar = bars + RS;
+  if (tid == 0) {
+    for (int k = 0; k <= RS; ++k) mbar_init(bars + k, 1);
+  }
+  __syncthreads();
+  uint32_t ph[RS + 1];
+#pragma unroll
+  for (int k = 0; k <= RS; ++k) ph[k] = 0u;
+  // thread roles of pass 1: Fx x | Kx x | Qxx x | Qux x | Kz z
+  const int role = tid < N ? 0 : (tid < N + M ? 1 : (tid < 2 * N + M ? 2 : (tid < 2 * N + 2 * M ? 3 : (tid < 2 * N + 3 * M ? 4 : 5))));
+  const int row = role == 0 ? tid : (role == 1 ? tid - N : (role == 2 ? tid - N - M : (role == 3 ? tid - 2 * N - M : tid - 2 * N - 2 * M)));
+  const int nloc = A.seg_end - A.seg_begin;
+  const int64_t total = p.B * nloc;
+  for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
+    const int64_t b = task / nloc;
+    const int j = A.seg_begin + (int)(task % nloc);
+    const int lo = p.split_times[j], L = p.split_times[j + 1] - lo;
+    const bool last = (j == J - 1);
+    const int64_t s0 = b * T + lo;
+    const double* vfg = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);
+    if (tid == 0) {
+      for (int k = 0; k < RS && k < L; ++k) ring_issue_fwd<N, M>(A, ring + k * R::SLOT, bars + k, s0 + k);
+      if (!last) {
+        fence_proxy_async();
+        mbar_arrive_tx(vbar, 8u * (2 * NN + 2 * N));
+        bulk_g2s(vfb, vfg + NN, 8u * (2 * NN + 2 * N), vbar);
+      }
+    }
+    if (tid < N) {
+      const double a0 = (j == 0) ? p.x_init[b * N + tid] : A.links[(b * (J - 1) + (j - 1)) * N + tid];
+      av[tid] = a0;
+      x[tid] = a0;
+      z[tid] = last ? 0.0 : A.links[(b * (J - 1) + j) * N + tid];
+    }
+    __syncthreads();
+    double obj = 0.0, worst = 0.0;
+    // ---- forward
+#pragma unroll 1
+    for (int s = 0; s < L; ++s) {
+      const int slot = s % RS;
+      const double* sl = ring + slot * R::SLOT;
+      mbar_wait(bars + slot, ph[slot]);
+      ph[slot] ^= 1u;
+      const int64_t st = s0 + s;
+      if (role < 5) {
+        const double* rp = role == 0 ? sl + R::FX + row * N
+                                     : (role == 1 ? sl + R::KX + row * N
+                                                  : (role == 2 ? sl + R::QXX + row * N
+                                                               : (role == 3 ? sl + R::QUX + row * N : sl + R::KZ + row * N)));
+        const double* vec = role == 4 ? z : x;
+        double t = 0.0, t_ = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < N; c += 2) {
+          t += rp[c] * vec[c];
+          t_ += rp[c + 1] * vec[c + 1];
+        }
+        t += t_;
+        double* dst = role == 0 ? tf : (role == 1 ? tu : (role == 2 ? t0 : (role == 3 ? t2 : tk)));
+        dst[row] = t;
+      }
+      __syncthreads();
+      if (tid < M) {
+        const double kk = tk[tid] + sl[R::K1 + tid];
+        const double uv = tu[tid] + kk;
+        uu[tid] = uv;
+        A.k[st * M + tid] = kk;
+        A.u[st * M + tid] = uv;
+      }
+      __syncthreads();
+      if (tid < N) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < M; ++q) t += sl[R::FU + tid * M + q] * uu[q];
+        xn[tid] = (tf[tid] + t) + sl[R::F1 + tid];
+      } else if (tid < 2 * N) {
+        const int i = tid - N;
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < M; ++q) t += sl[R::QUX + q * N + i] * uu[q];
+        const double xi = x[i], qx = sl[R::QX1 + i];
+        gh[s * (N + M) + i] = (t0[i] + t) + qx;
+        obj += 0.5 * xi * t0[i] + qx * xi;
+        A.x[(b * (T + 1) + lo + s) * N + i] = xi;
+      } else if (tid < 2 * N + M) {
+        const int u = tid - 2 * N;
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < M; ++q) t += sl[R::QUU + u * M + q] * uu[q];
+        const double ui = uu[u], qu = sl[R::QU1 + u];
+        gh[s * (N + M) + N + u] = (t2[u] + t) + qu;
+        obj += 0.5 * ui * t + ui * t2[u] + qu * ui;
+      }
+      __syncthreads();
+      if (tid == 0 && s + RS < L) ring_issue_fwd<N, M>(A, ring + slot * R::SLOT, bars + slot, st + RS);
+      if (tid < N) x[tid] = xn[tid];
+      __syncthreads();
+    }
+    if (tid < N + M) A.gh[(s0 + L - 1) * (N + M) + tid] = gh[(L - 1) * (N + M) + tid];
+    // backward prologue: Fx, Fu of the last RS stages
+    if (tid == 0)
+      for (int k = 0; k < RS && k < L; ++k) ring_issue_bwd<N, M>(A, ring + k * R::SLOT, bars + k, s0 + L - 1 - k);
+    // ---- multiplier seed
+    if (last) {
+      if (tid < N) {
+        A.x[(b * (T + 1) + T) * N + tid] = x[tid];
+        double t = 0.0;
+        const double* QT = p.QxxT + b * NN + tid * N;
+        for (int c = 0; c < N; ++c) t += QT[c] * x[c];
+        const double q1 = p.qx1T[b * N + tid];
+        obj += 0.5 * x[tid] * t + q1 * x[tid];
+        const double g = t + q1;
+        lam[tid] = -g;
+        A.lam[(b * (T + 1) + T) * N + tid] = -g;
+        worst = fmax(worst, fabs(g + -g));
+      }
+    } else {
+      mbar_wait(vbar, ph[RS]);
+      ph[RS] ^= 1u;
+      if (tid < N) {
+        A.xend[(b * J + j) * N + tid] = x[tid];
+        double t0v = 0.0, t1v = 0.0;
+        for (int c = 0; c < N; ++c) {
+          t0v += vfb[tid * N + c] * av[c];
+          t1v += vfb[NN + tid * N + c] * z[c];
+        }
+        const double mu = -((t0v + t1v) + vfb[2 * NN + N + tid]);
+        A.mu_left[(b * (J - 1) + j) * N + tid] = mu;
+        lam[tid] = -mu;
+      }
+    }
+    __syncthreads();
+    // ---- backward multipliers + interior KKT rows: threads < N Fx' lam, N..N+M-1 Fu' lam
+#pragma unroll 1
+    for (int k = 0; k < L; ++k) {
+      const int s = L - 1 - k;
+      const int slot = k % RS;
+      const double* sl = ring + slot * R::SLOT;
+      mbar_wait(bars + slot, ph[slot]);
+      ph[slot] ^= 1u;
+      const bool interior = last || (s < L - 1);
+      double tb = 0.0, ln = 0.0;
+      if (tid < N + M) {
+        const double* col = tid < N ? sl + R::FX + tid : sl + R::FU + (tid - N);
+        const int stride = tid < N ? N : M;
+        double t_ = 0.0;
+#pragma unroll 8
+        for (int q = 0; q < N; q += 2) {
+          tb += col[q * stride] * lam[q];
+          t_ += col[(q + 1) * stride] * lam[q + 1];
+        }
+        tb += t_;
+      }
+      if (tid < N) {
+        const double g = gh[s * (N + M) + tid];
+        ln = tb - g;
+        A.lam[(b * (T + 1) + lo + s) * N + tid] = ln;
+        if (interior) worst = fmax(worst, fabs((g + ln) - tb));
+      } else if (tid < N + M && interior) {
+        worst = fmax(worst, fabs(gh[s * (N + M) + tid] - tb));
+      }
+      __syncthreads();
+      if (tid == 0 && k + RS < L) ring_issue_bwd<N, M>(A, ring + slot * R::SLOT, bars + slot, s0 + s - RS);
+      if (tid < N) lam[tid] = ln;
+      __syncthreads();
+    }
+    if (j > 0 && tid < N) A.lambda_right[(b * (J - 1) + (j - 1)) * N + tid] = lam[tid];
+    obj = block_sum(obj, red);
+    worst = block_max(worst, red);
+    if (tid == 0) {
+      A.part[(b * J + j) * 3 + 0] = obj;
+      A.part[(b * J + j) * 3 + 1] = worst;
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------
 // sequential link solve, one warp per problem
 
 // One warp per problem: the reference's block Cholesky (endpoint.py:410-438).
@@ -723,11 +969,29 @@ int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, doub
 
 }  // namespace
 
-// n = 32 would need ~100 prefetch registers per lane with one warp per
-// segment; it stays on the generic reconstruction for now
-bool recon_small_supported(int n, int m) { return n == 12 && m == 4; }
+template <int N, int M, int NT, int RS>
+int launch_recon_ring(const ReconArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * ((size_t)RS * RingL<N, M>::SLOT + 2 * N * N + 2 * N +
+                                        (size_t)a.p.max_seg_len * (N + M) + 10 * N + 6 * M + NT / 32 + 16);
+  auto kern = recon_ring_kernel<N, M, NT, RS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+  const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
+  const int64_t cap = (int64_t)sms_count() * (per_sm > 0 ? per_sm : 1);
+  const int grid = (int)(tasks < cap ? tasks : cap);
+  if (grid <= 0) return 0;
+  kern<<<grid, NT, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+bool recon_small_supported(int n, int m) { return (n == 12 && m == 4) || (n == 32 && m == 8); }
 
 int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
+  if (a.p.n == 32 && a.p.m == 8) {
+    if (a.p.max_seg_len <= 512) return launch_recon_ring<32, 8, 128, 3>(a, s);
+    return -1;
+  }
   if (a.p.n == 12 && a.p.m == 4) {
     // whole segment on chip when it fits (BASELINE config 1: L = 8)
     if (a.p.max_seg_len <= 8) return launch_recon_seg<12, 4, 8>(a, s);
