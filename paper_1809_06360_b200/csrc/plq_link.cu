@@ -116,18 +116,50 @@ __device__ __forceinline__ void flag_singular(plq_problem_t& p, int32_t* status,
   if (threadIdx.x == 0 && status[b * p.J] == 0) status[b * p.J] = PLQ_STATUS_LINK_SINGULAR;
 }
 
-// eliminate the odd blocks of one level (or the single top block)
+// lane-per-row Cholesky of an n x n block (n <= 32) by one warp, in place in
+// shared memory (stride ld); returns false on a non-positive pivot
+__device__ __forceinline__ bool warp_cholesky_smem(double* A, int n, int ld) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  for (int k = 0; k < n; ++k) {
+    const double dkk = A[k * ld + k];
+    ok = ok && (dkk > 0.0);
+    const double d = sqrt(dkk > 0.0 ? dkk : 1.0);
+    const double inv = 1.0 / d;
+    __syncwarp();
+    if (lane == k) A[k * ld + k] = d;
+    if (lane > k && lane < n) A[lane * ld + k] *= inv;
+    __syncwarp();
+    if (lane > k && lane < n) {
+      const double lik = A[lane * ld + k];
+      for (int jj = k + 1; jj <= lane; ++jj) A[lane * ld + jj] -= lik * A[jj * ld + k];
+    }
+    __syncwarp();
+  }
+  return ok;
+}
+
+// eliminate the odd blocks of one level (or the single top block).  For
+// n <= 64 the pivot block and W live in shared memory; the factor and W are
+// written back to global once for the back-substitution.
 __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
   __shared__ int flag;
+  extern __shared__ __align__(16) double dsm[];
   const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1;
   const int64_t nn = (int64_t)n * n;
   const int64_t b = blockIdx.x / E;
   const int o = blockIdx.x % E;
   const int i = L.top ? 0 : 2 * o + 1;
-  double* Lc = L.Lc + (b * E + o) * nn;
-  double* Wm = L.Wm + (b * E + o) * n * w;
+  const bool sm = n <= 64;
+  const int ldl = sm ? n + 1 : n;
+  const int ldw = sm ? ((w + 3) / 8) * 8 + 4 : w;
+  double* gLc = L.Lc + (b * E + o) * nn;
+  double* gWm = L.Wm + (b * E + o) * n * w;
+  double* Lc = sm ? dsm : gLc;
+  double* Wm = sm ? dsm + n * ldl : gWm;
+  double* tiles = sm ? nullptr : dsm;
   const double* D = L.D + (b * K + i) * nn;
-  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[idx] = D[idx];
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[(idx / n) * ldl + idx % n] = D[idx];
   const bool has_l = i >= 1, has_r = i + 1 < K;
   const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;   // A(i,i-1)
   const double* Sr = has_r ? L.S + (b * (K - 1) + i) * nn : nullptr;         // A(i+1,i) -> A(i,i+1) = Sr'
@@ -140,25 +172,39 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
       v = has_r ? Sr[(c - n) * n + r] : 0.0;
     else
       v = L.rhs[(b * K + i) * n + r];
-    Wm[idx] = v;
+    Wm[r * ldw + c] = v;
   }
   if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  if (!cta_cholesky(Lc, n, n, &flag)) {
+  bool ok;
+  if (n <= 32) {
+    if (threadIdx.x < 32) {
+      ok = warp_cholesky_smem(Lc, n, ldl);
+      if (threadIdx.x == 0 && !ok) flag = 1;
+    }
+    __syncthreads();
+    ok = !flag;
+  } else {
+    ok = cta_cholesky(Lc, n, ldl, &flag);
+  }
+  if (!ok) {
     flag_singular(p, status, b);
     return;
   }
   if (n >= 16)
-    cta_trsm_lower_blocked(Lc, n, n, Wm, w, w);
+    cta_trsm_lower_blocked(Lc, n, ldl, Wm, w, ldw);
   else
-    cta_trsm_lower(Lc, n, n, Wm, w, w);
+    cta_trsm_lower(Lc, n, ldl, Wm, w, ldw);
+  if (sm) {
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) gLc[idx] = Lc[(idx / n) * ldl + idx % n];
+    for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) gWm[idx] = Wm[(idx / w) * ldw + idx % w];
+  }
   if (L.top) return;
   double* CL = L.CL + (b * E + o) * nn;
   double* CR = L.CR + (b * E + o) * nn;
   double* X = L.X + (b * E + o) * nn;
   double* cL = L.cL + (b * E + o) * n;
   double* cR = L.cR + (b * E + o) * n;
-  extern __shared__ __align__(16) double tiles[];
   auto gram = [&](int r, int c, double acc) {
     if (r < n) {
       if (c < n)
@@ -175,10 +221,10 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
         cR[rr] = acc;
     }
   };
-  if (n >= 32 && blockDim.x == 256)
+  if (!sm && blockDim.x == 256)
     cta_gemm_tiled<true, 8>(2 * n, w, n, Wm, w, Wm, w, tiles, gram);
   else
-    cta_gemm<true, false, 1, 1>(2 * n, w, n, Wm, w, Wm, w, gram);
+    cta_gemm<true, false, 1, 1>(2 * n, w, n, Wm, ldw, Wm, ldw, gram);
 }
 
 // next level's system on the even blocks
@@ -233,6 +279,11 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
   const double* xl = has_l ? C.x + (b * C.K + (i - 1) / 2) * n : nullptr;
   const double* xr = has_r ? C.x + (b * C.K + (i + 1) / 2) * n : nullptr;
   (void)has_coarse;
+  const bool sm = n <= 64;
+  double* Ls = v + n + 2;   // n x (n+1) when staged
+  const int ldl = n + 1;
+  if (sm)
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Ls[(idx / n) * ldl + idx % n] = Lc[idx];
   for (int r = threadIdx.x; r < n; r += blockDim.x) {
     double s = Wm[r * w + 2 * n];
     double t = 0.0;
@@ -243,12 +294,27 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
     v[r] = s - t;
   }
   __syncthreads();
-  // x = L^{-T} v : column-oriented back substitution
+  if (n <= 32) {
+    // lane-per-row back substitution, x = L^{-T} v, one warp
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      double vi = lane < n ? v[lane] : 0.0;
+      for (int r = n - 1; r >= 0; --r) {
+        const double xr_ = __shfl_sync(0xffffffffu, vi / (lane == r ? Ls[r * ldl + r] : 1.0), r);
+        if (lane == r) vi = xr_;
+        if (lane < r) vi -= Ls[r * ldl + lane] * xr_;
+      }
+      if (lane < n) x[lane] = vi;
+    }
+    return;
+  }
+  const double* Lp = sm ? Ls : Lc;
+  const int lp = sm ? ldl : n;
   for (int r = n - 1; r >= 0; --r) {
-    if (threadIdx.x == 0) v[r] /= Lc[r * n + r];
+    if (threadIdx.x == 0) v[r] /= Lp[r * lp + r];
     __syncthreads();
     const double xr_ = v[r];
-    for (int k = threadIdx.x; k < r; k += blockDim.x) v[k] -= Lc[r * n + k] * xr_;
+    for (int k = threadIdx.x; k < r; k += blockDim.x) v[k] -= Lp[r * lp + k] * xr_;
     __syncthreads();
   }
   for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = v[r];
@@ -313,7 +379,9 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   link_assemble0<<<B * P.lv[0].K, threads, 0, s>>>(p, vf0, P.lv[0]);
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
-    const size_t tsm = (p.n >= 32 && threads == 256) ? sizeof(double) * TileCfg<8>::DOUBLES : 0;
+    const int w = 2 * p.n + 1, ldw = ((w + 3) / 8) * 8 + 4;
+    const size_t tsm = p.n <= 64 ? sizeof(double) * ((size_t)p.n * (p.n + 1) + (size_t)p.n * ldw)
+                                 : (threads == 256 ? sizeof(double) * TileCfg<8>::DOUBLES : 0);
     if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     link_eliminate<<<B * P.lv[l].E, threads, tsm, s>>>(p, P.lv[l], status);
     ++nl;
@@ -324,8 +392,9 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   }
   for (int l = (int)P.lv.size() - 1; l >= 0; --l) {
     const LinkLevel& C = P.lv[l + 1 < (int)P.lv.size() ? l + 1 : l];
-    link_backsub<<<B * P.lv[l].K, threads, sizeof(double) * (p.n + 2), s>>>(p, P.lv[l], C,
-                                                                              l + 1 < (int)P.lv.size());
+    const size_t bsm = sizeof(double) * (p.n + 2 + (p.n <= 64 ? (size_t)p.n * (p.n + 1) : 0));
+    if (bsm > 48 * 1024) cudaFuncSetAttribute(link_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+    link_backsub<<<B * P.lv[l].K, threads, bsm, s>>>(p, P.lv[l], C, l + 1 < (int)P.lv.size());
     ++nl;
   }
   link_residual_part<<<B * P.lv[0].K, threads, 0, s>>>(p, P.lv[0], P.rpart);
