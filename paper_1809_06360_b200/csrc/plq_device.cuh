@@ -113,29 +113,30 @@ __device__ __forceinline__ void cta_gemm(int M, int N, int K, const double* __re
 // overwritten; the strict upper triangle is left untouched).  Returns false
 // on a non-positive (or NaN) pivot, the LAPACK dpotrf failure condition that
 // numpy.linalg.cholesky reports as LinAlgError.
-__device__ __forceinline__ bool cta_cholesky(double* A, int m, int lda, int* flag) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+//
+// Right-looking with the unscaled pivot column, A_ij -= A_ik A_jk / A_kk
+// (rows by warp, columns by lane: one barrier per column, no index division);
+// the columns are scaled by 1/sqrt(pivot) in one pass at the end.  Every
+// thread reads the same pivot, so the failure exit is uniform.
+__device__ __forceinline__ bool cta_cholesky(double* A, int m, int lda, int* /*flag*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
   for (int k = 0; k < m; ++k) {
-    if (tid == 0) {
-      const double d = A[k * lda + k];
-      if (!(d > 0.0)) {
-        *flag = 1;
-      } else {
-        A[k * lda + k] = sqrt(d);
-      }
-    }
-    __syncthreads();
-    if (*flag) return false;
-    const double dk = A[k * lda + k];
-    for (int i = k + 1 + tid; i < m; i += nt) A[i * lda + k] /= dk;
-    __syncthreads();
-    const int rem = m - k - 1;
-    for (int idx = tid; idx < rem * rem; idx += nt) {
-      const int i = k + 1 + idx / rem, j = k + 1 + idx % rem;
-      if (j <= i) A[i * lda + j] -= A[i * lda + k] * A[j * lda + k];
+    const double dkk = A[k * lda + k];
+    if (!(dkk > 0.0)) return false;
+    const double inv = 1.0 / dkk;
+    for (int i = k + 1 + warp; i < m; i += nw) {
+      const double aik = A[i * lda + k] * inv;
+      for (int j = k + 1 + lane; j <= i; j += 32) A[i * lda + j] -= aik * A[j * lda + k];
     }
     __syncthreads();
   }
+  // off-diagonal entries first (they read the unscaled pivots), then the diagonal
+  for (int i = warp; i < m; i += nw)
+    for (int k = lane; k < i; k += 32) A[i * lda + k] /= sqrt(A[k * lda + k]);
+  __syncthreads();
+  for (int k = threadIdx.x; k < m; k += blockDim.x) A[k * lda + k] = sqrt(A[k * lda + k]);
+  __syncthreads();
   return true;
 }
 

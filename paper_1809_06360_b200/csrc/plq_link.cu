@@ -17,6 +17,7 @@
 #include "plq_device.cuh"
 #include "plq_gemm.cuh"
 #include "plq_internal.h"
+#include "plq_tma.cuh"
 
 #include <vector>
 
@@ -81,6 +82,47 @@ LinkPlan plan_link(int64_t B, int J, int n, double* base) {
   P.rpart = take(B * (J - 1));
   P.doubles = off;
   return P;
+}
+
+
+// Stage contiguous global blocks into shared memory with one bulk copy each
+// (one memory latency for the whole set instead of one per loop trip).
+// Falls back to a plain cooperative copy when a block is not a multiple of
+// 16 bytes or not 16-byte aligned (odd n).
+struct BulkSet {
+  static constexpr int MAXB = 6;
+  double* dst[MAXB];
+  const double* src[MAXB];
+  int count[MAXB];
+  int nb = 0;
+  __device__ void add(double* d, const double* s, int c) {
+    dst[nb] = d;
+    src[nb] = s;
+    count[nb] = c;
+    ++nb;
+  }
+};
+
+__device__ __forceinline__ void bulk_stage(BulkSet& bs, uint64_t* bar, uint32_t& phase) {
+  bool ok = true;
+  for (int k = 0; k < bs.nb; ++k)
+    ok = ok && ((bs.count[k] * 8) % 16 == 0) && ((reinterpret_cast<uintptr_t>(bs.src[k]) & 15) == 0) &&
+         ((reinterpret_cast<uintptr_t>(bs.dst[k]) & 15) == 0);
+  if (ok) {
+    if (threadIdx.x == 0) {
+      uint32_t bytes = 0;
+      for (int k = 0; k < bs.nb; ++k) bytes += 8u * bs.count[k];
+      fence_proxy_async();
+      mbar_arrive_tx(bar, bytes);
+      for (int k = 0; k < bs.nb; ++k) bulk_g2s(bs.dst[k], bs.src[k], 8u * bs.count[k], bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+  } else {
+    for (int k = 0; k < bs.nb; ++k)
+      for (int i = threadIdx.x; i < bs.count[k]; i += blockDim.x) bs.dst[k][i] = bs.src[k][i];
+  }
+  __syncthreads();
 }
 
 // level-0 system from the segment-start value blocks (parallel.py:286-319):
@@ -159,34 +201,52 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
   double* Wm = sm ? dsm + n * ldl : gWm;
   double* tiles = sm ? nullptr : dsm;
   const double* D = L.D + (b * K + i) * nn;
-  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[(idx / n) * ldl + idx % n] = D[idx];
   const bool has_l = i >= 1, has_r = i + 1 < K;
   const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;   // A(i,i-1)
   const double* Sr = has_r ? L.S + (b * (K - 1) + i) * nn : nullptr;         // A(i+1,i) -> A(i,i+1) = Sr'
-  for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) {
-    const int r = idx / w, c = idx % w;
-    double v;
-    if (c < n)
-      v = has_l ? Sl[r * n + c] : 0.0;
-    else if (c < 2 * n)
-      v = has_r ? Sr[(c - n) * n + r] : 0.0;
-    else
-      v = L.rhs[(b * K + i) * n + r];
-    Wm[r * ldw + c] = v;
+  const double* rh = L.rhs + (b * K + i) * n;
+  if (sm) {
+    // bulk-stage D, S_l, S_r, rhs behind the factor / W buffers, assemble in smem
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    double* st = dsm + ((n * ldl + n * ldw + 1) & ~1);
+    BulkSet bs;
+    bs.add(st, D, (int)nn);
+    if (has_l) bs.add(st + nn, Sl, (int)nn);
+    if (has_r) bs.add(st + 2 * nn, Sr, (int)nn);
+    bs.add(st + 3 * nn, rh, n);
+    bulk_stage(bs, &bar, phase);
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[(idx / n) * ldl + idx % n] = st[idx];
+    for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) {
+      const int r = idx / w, c = idx % w;
+      double v;
+      if (c < n)
+        v = has_l ? st[nn + r * n + c] : 0.0;
+      else if (c < 2 * n)
+        v = has_r ? st[2 * nn + (c - n) * n + r] : 0.0;
+      else
+        v = st[3 * nn + r];
+      Wm[r * ldw + c] = v;
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[(idx / n) * ldl + idx % n] = D[idx];
+    for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) {
+      const int r = idx / w, c = idx % w;
+      double v;
+      if (c < n)
+        v = has_l ? Sl[r * n + c] : 0.0;
+      else if (c < 2 * n)
+        v = has_r ? Sr[(c - n) * n + r] : 0.0;
+      else
+        v = rh[r];
+      Wm[r * ldw + c] = v;
+    }
   }
   if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  bool ok;
-  if (n <= 32) {
-    if (threadIdx.x < 32) {
-      ok = warp_cholesky_smem(Lc, n, ldl);
-      if (threadIdx.x == 0 && !ok) flag = 1;
-    }
-    __syncthreads();
-    ok = !flag;
-  } else {
-    ok = cta_cholesky(Lc, n, ldl, &flag);
-  }
+  const bool ok = cta_cholesky(Lc, n, ldl, &flag);
   if (!ok) {
     flag_singular(p, status, b);
     return;
@@ -282,16 +342,40 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
   const bool sm = n <= 64;
   double* Ls = v + n + 2;   // n x (n+1) when staged
   const int ldl = n + 1;
-  if (sm)
-    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Ls[(idx / n) * ldl + idx % n] = Lc[idx];
-  for (int r = threadIdx.x; r < n; r += blockDim.x) {
-    double s = Wm[r * w + 2 * n];
-    double t = 0.0;
-    if (has_l)
-      for (int c = 0; c < n; ++c) t += Wm[r * w + c] * xl[c];
-    if (has_r)
-      for (int c = 0; c < n; ++c) t += Wm[r * w + n + c] * xr[c];
-    v[r] = s - t;
+  if (sm) {
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    double* st = Ls + ((n * ldl + 1) & ~1);        // raw L (nn), W (n*w), xl, xr
+    BulkSet bs;
+    bs.add(st, Lc, (int)nn);
+    bs.add(st + nn, Wm, n * w);
+    if (has_l) bs.add(st + nn + n * w + (n * w & 1), xl, n);
+    if (has_r) bs.add(st + nn + n * w + (n * w & 1) + n, xr, n);
+    bulk_stage(bs, &bar, phase);
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Ls[(idx / n) * ldl + idx % n] = st[idx];
+    const double* Ws = st + nn;
+    const double* xls = st + nn + n * w + (n * w & 1);
+    const double* xrs = xls + n;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double t = 0.0;
+      if (has_l)
+        for (int c = 0; c < n; ++c) t += Ws[r * w + c] * xls[c];
+      if (has_r)
+        for (int c = 0; c < n; ++c) t += Ws[r * w + n + c] * xrs[c];
+      v[r] = Ws[r * w + 2 * n] - t;
+    }
+  } else {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double s = Wm[r * w + 2 * n];
+      double t = 0.0;
+      if (has_l)
+        for (int c = 0; c < n; ++c) t += Wm[r * w + c] * xl[c];
+      if (has_r)
+        for (int c = 0; c < n; ++c) t += Wm[r * w + n + c] * xr[c];
+      v[r] = s - t;
+    }
   }
   __syncthreads();
   if (n <= 32) {
@@ -349,14 +433,14 @@ __global__ void link_residual_part(plq_problem_t p, LinkLevel L, double* rpart) 
 
 __global__ void link_residual_reduce(plq_problem_t p, const double* rpart, const double* x0, double* links,
                                      double* link_residual) {
+  __shared__ double red[32];
   const int64_t b = blockIdx.x;
   const int K = p.J - 1, n = p.n;
   for (int64_t idx = threadIdx.x; idx < (int64_t)K * n; idx += blockDim.x) links[b * K * n + idx] = x0[b * K * n + idx];
-  if (threadIdx.x == 0) {
-    double w = 0.0;
-    for (int i = 0; i < K; ++i) w = fmax(w, rpart[b * K + i]);
-    link_residual[b] = w;
-  }
+  double w = 0.0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) w = fmax(w, rpart[b * K + i]);
+  w = block_max(w, red);
+  if (threadIdx.x == 0) link_residual[b] = w;
 }
 
 int link_threads(int n) {
@@ -380,7 +464,8 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
     const int w = 2 * p.n + 1, ldw = ((w + 3) / 8) * 8 + 4;
-    const size_t tsm = p.n <= 64 ? sizeof(double) * ((size_t)p.n * (p.n + 1) + (size_t)p.n * ldw)
+    const size_t tsm = p.n <= 64 ? sizeof(double) * ((size_t)p.n * (p.n + 1) + (size_t)p.n * ldw + 2 +
+                                                     3 * (size_t)p.n * p.n + p.n)
                                  : (threads == 256 ? sizeof(double) * TileCfg<8>::DOUBLES : 0);
     if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     link_eliminate<<<B * P.lv[l].E, threads, tsm, s>>>(p, P.lv[l], status);
@@ -392,13 +477,14 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   }
   for (int l = (int)P.lv.size() - 1; l >= 0; --l) {
     const LinkLevel& C = P.lv[l + 1 < (int)P.lv.size() ? l + 1 : l];
-    const size_t bsm = sizeof(double) * (p.n + 2 + (p.n <= 64 ? (size_t)p.n * (p.n + 1) : 0));
+    const size_t bsm = sizeof(double) * (p.n + 2 + (p.n <= 64 ? (size_t)p.n * (p.n + 1) + 4 + (size_t)p.n * p.n +
+                                                              (size_t)p.n * (2 * p.n + 1) + 2 * p.n + 2 : 0));
     if (bsm > 48 * 1024) cudaFuncSetAttribute(link_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     link_backsub<<<B * P.lv[l].K, threads, bsm, s>>>(p, P.lv[l], C, l + 1 < (int)P.lv.size());
     ++nl;
   }
   link_residual_part<<<B * P.lv[0].K, threads, 0, s>>>(p, P.lv[0], P.rpart);
-  link_residual_reduce<<<B, 128, 0, s>>>(p, P.rpart, P.lv[0].x, links, link_residual);
+  link_residual_reduce<<<B, 1024, 0, s>>>(p, P.rpart, P.lv[0].x, links, link_residual);
   nl += 2;
   if (launches) *launches += nl;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;

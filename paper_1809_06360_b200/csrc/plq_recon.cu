@@ -234,22 +234,28 @@ __global__ void __launch_bounds__(NT) boundary_kernel(ReconArgs A) {
 }
 
 // objective = fixed-order sum of segment partials; kkt = max of all rows;
-// link_mismatch = max |mu_left + lambda_right| (parallel.py:527).
+// link_mismatch = max |mu_left + lambda_right| (parallel.py:527).  The sum is
+// deterministic: thread t adds a fixed contiguous run of segments, then a
+// fixed butterfly / warp-order combine (independent of how segments were
+// sharded across ranks).
 __global__ void finalize_kernel(plq_problem_t p, const double* part, const double* mu_left, const double* lambda_right,
                                 double* objective, double* kkt, double* mismatch) {
   __shared__ double red[32];
   const int64_t b = blockIdx.x;
-  const int J = p.J, n = p.n;
+  const int J = p.J, n = p.n, nt = blockDim.x, t = threadIdx.x;
   double worst = 0.0;
-  for (int64_t idx = threadIdx.x; idx < (int64_t)(J - 1) * n; idx += blockDim.x)
+  for (int64_t idx = t; idx < (int64_t)(J - 1) * n; idx += nt)
     worst = fmax(worst, fabs(mu_left[b * (J - 1) * n + idx] + lambda_right[b * (J - 1) * n + idx]));
   worst = block_max(worst, red);
-  if (threadIdx.x == 0) {
-    double obj = 0.0, kk = 0.0;
-    for (int j = 0; j < J; ++j) {
-      obj += part[(b * J + j) * 3 + 0];
-      kk = fmax(kk, fmax(part[(b * J + j) * 3 + 1], part[(b * J + j) * 3 + 2]));
-    }
+  const int per = (J + nt - 1) / nt;
+  double obj = 0.0, kk = 0.0;
+  for (int j = t * per; j < (t + 1) * per && j < J; ++j) {
+    obj += part[(b * J + j) * 3 + 0];
+    kk = fmax(kk, fmax(part[(b * J + j) * 3 + 1], part[(b * J + j) * 3 + 2]));
+  }
+  obj = block_sum(obj, red);
+  kk = block_max(kk, red);
+  if (t == 0) {
     objective[b] = obj;
     kkt[b] = kk;
     mismatch[b] = worst;
@@ -316,7 +322,8 @@ int launch_boundary(const ReconArgs& a, double* /*unused*/, cudaStream_t s) {
 int launch_finalize(const plq_problem_t& p, const double* part, const double* /*bpart*/, const double* mu_left,
                     const double* lambda_right, const double* /*link_res*/, double* objective, double* kkt,
                     double* mismatch, double* /*link_residual*/, cudaStream_t s) {
-  finalize_kernel<<<(unsigned)p.B, 128, 0, s>>>(p, part, mu_left, lambda_right, objective, kkt, mismatch);
+  finalize_kernel<<<(unsigned)p.B, p.J > 64 ? 1024 : 128, 0, s>>>(p, part, mu_left, lambda_right, objective, kkt,
+                                                                   mismatch);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
