@@ -82,7 +82,8 @@ Plan make_plan(const plq_problem_t* p) {
   P.off_part = off;
   off += up2(B * J * 3);
   P.off_gs = off;
-  off += up2((size_t)P.grid_max * P.lay.gmem_doubles);
+  off += up2(std::max((size_t)P.grid_max * P.lay.gmem_doubles,
+                      (size_t)sms * 2 * plq::sweep_small_gscratch_doubles(p->n, p->m)));
   P.off_link = off;
   off += up2(std::max(plq::link_workspace_doubles(B, p->J, p->n),
                       use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0)));

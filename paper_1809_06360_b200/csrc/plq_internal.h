@@ -78,6 +78,7 @@ int launch_finalize(const plq_problem_t& p, const double* part, const double* bp
 
 // Specialized small-state kernels (compile-time n, m).
 bool sweep_small_supported(int n, int m);
+size_t sweep_small_gscratch_doubles(int n, int m);   // per CTA (n >= 64 variants)
 int launch_sweep_small(const SweepArgs& a, cudaStream_t s);
 bool recon_small_supported(int n, int m);
 int launch_recon_small(const ReconArgs& a, cudaStream_t s);

@@ -16,6 +16,7 @@
 //     Mxx/mx1 into Vxx/vx1, and the value update accumulates into V;
 //   * the m x m Cholesky of Muu is computed redundantly in every lane's
 //     registers (m <= 8), so the gain solve needs no barrier.
+#include "plq_gemm.cuh"
 #include "plq_internal.h"
 #include "plq_small.cuh"
 #include "plq_tma.cuh"
@@ -26,43 +27,52 @@ namespace {
 
 template <int N, int M>
 struct SL {
+  // BIG (n >= 64): only the GEMM operands stay in shared memory ([Vxx;Vzx],
+  // staged [Fx|Fu|f1], VF / G, P, Muu); Vzz, the constraint rows H, Y and the
+  // tail temporaries live in a per-CTA slice of (L2-resident) global scratch,
+  // and the Q blocks are read from global memory in the GEMM2 epilogue.
+  static constexpr bool BIG = N >= 64;
   static constexpr int NN = N * N, NM = N * M, MM = M * M;
   static constexpr int LDN = pad_ld(N);
   static constexpr int FW = N + M + 1;
   static constexpr int LDF = pad_ld(FW);
   static constexpr int WE = 2 * N + 1;
   static constexpr int LDW = pad_ld(WE);
+  static constexpr int LDM = pad_ld(M);
   // Fx rows are staged row by row with a padded stride when N is not already
   // conflict-free (N % 8 != 4)
   static constexpr bool FX_ROWS = (N % 8) != 4;
   static constexpr int LFX = FX_ROWS ? pad_ld(N) : N;
   static constexpr bool FU_ROWS = (M % 8) != 4 && M > 4;
   static constexpr int LFU = FU_ROWS ? pad_ld(M) : M;
-  static constexpr int V = 0;                    // Vxx, Vzx, Vzz: 3 x (N x LDN)
-  static constexpr int VX1 = V + 3 * N * LDN;
+  static constexpr int V = 0;                    // Vxx, Vzx (, Vzz): (BIG ? 2 : 3) x (N x LDN)
+  static constexpr int VX1 = V + (BIG ? 2 : 3) * N * LDN;
   static constexpr int VZ1 = VX1 + N;
   // staged stage inputs (16-byte aligned fields)
   static constexpr int SFX = (VZ1 + N + 1) & ~1;        // N x LFX
   static constexpr int SFU = SFX + N * LFX;             // N x LFU
   static constexpr int SF1 = SFU + N * LFU;             // N
-  static constexpr int SQXX = SF1 + N;                  // N x N
-  static constexpr int SQUX = SQXX + NN;                // M x N
-  static constexpr int SQUU = SQUX + NM;                // M x M
-  static constexpr int SQX1 = SQUU + MM;                // N
-  static constexpr int SQU1 = SQX1 + N;                 // M
-  static constexpr int VF = (SQU1 + M + 1) & ~1;        // N x LDF (also N = Hx F)
-  static constexpr int P = VF + N * LDF;                // P, G, Y: M x LDW each, contiguous
-  static constexpr int G = P + M * LDW;
-  static constexpr int Y = G + M * LDW;
-  static constexpr int MUU = Y + M * LDW;               // M x M
-  static constexpr int H = MUU + MM;                    // N x LDW constraint rows [Hx | Hz | h1]
-  static constexpr int TAU = H + N * LDW;               // M x M (tau, or the WY factor T)
+  static constexpr int SQXX = SF1 + N;                  // N x N  (not BIG)
+  static constexpr int SQUX = SQXX + (BIG ? 0 : NN);    // M x N
+  static constexpr int SQUU = SQUX + (BIG ? 0 : NM);    // M x M
+  static constexpr int SQX1 = SQUU + (BIG ? 0 : MM);    // N
+  static constexpr int SQU1 = SQX1 + (BIG ? 0 : N);     // M
+  static constexpr int VF = (SQU1 + (BIG ? 0 : M) + 1) & ~1;   // N x LDF (also N = Hx F when not BIG)
+  static constexpr int P = VF + N * LDF;                // P (then G, Y when not BIG): M x LDW each
+  static constexpr int G = BIG ? VF : P + M * LDW;      // BIG: G overlays VF (dead after GEMM2)
+  static constexpr int Y = BIG ? -1 : G + M * LDW;
+  static constexpr int MUU = (BIG ? P + M * LDW : Y + M * LDW);   // M x LDM
+  static constexpr int H = MUU + M * LDM;               // N x LDW constraint rows (not BIG)
+  static constexpr int TAU = H + (BIG ? 0 : N * LDW);   // M x M (tau, or the WY factor T)
   static constexpr int RD = TAU + M * M;                // M
   static constexpr int RED = RD + M;                    // 8
   static constexpr int DUM = RED + 8;                   // 32 per-lane dummy slots (branch-free epilogues)
   static constexpr int BAR = (DUM + 32 + 1) & ~1;       // mbarrier (8 bytes)
   static constexpr int TOTAL = BAR + 2;
-  static constexpr uint32_t STAGE_BYTES = 8u * (2 * NN + 2 * NM + MM + 2 * N + M);
+  // global scratch per CTA (BIG): Vzz (N x LDN), H (N x LDW), Y (M x LDW), NT (N x LDF)
+  static constexpr int GVZZ = 0, GH = GVZZ + N * LDN, GY = GH + N * LDW, GNT = GY + M * LDW;
+  static constexpr int GTOTAL = BIG ? GNT + N * LDF : 0;
+  static constexpr uint32_t STAGE_BYTES = BIG ? 8u * (NN + NM + N) : 8u * (2 * NN + 2 * NM + MM + 2 * N + M);
   static_assert(SFX % 2 == 0 && SFU % 2 == 0 && SF1 % 2 == 0 && SQXX % 2 == 0 && SQUX % 2 == 0 &&
                     SQUU % 2 == 0 && SQX1 % 2 == 0 && SQU1 % 2 == 0 && (N * 8) % 16 == 0 && (M * 8) % 16 == 0,
                 "bulk copies need 16-byte alignment");
@@ -88,11 +98,13 @@ __device__ __forceinline__ void stage_issue(const plq_problem_t& p, int64_t st, 
     bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
   }
   bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
-  bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
-  bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
-  bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
-  bulk_g2s(sm + S::SQX1, p.qx1 + st * N, 8u * N, bar);
-  bulk_g2s(sm + S::SQU1, p.qu1 + st * M, 8u * M, bar);
+  if constexpr (!S::BIG) {
+    bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
+    bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
+    bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
+    bulk_g2s(sm + S::SQX1, p.qx1 + st * N, 8u * N, bar);
+    bulk_g2s(sm + S::SQU1, p.qu1 + st * M, 8u * M, bar);
+  }
 }
 
 // F(k, j) = [Fx | Fu | f1](k, j) from the staged fields
@@ -273,22 +285,20 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   const plq_problem_t& p = a.p;
   const int T = p.T, J = p.J;
   const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
+  constexpr int LDM = S::LDM;
+  double* gs = a.gscratch + (int64_t)blockIdx.x * S::GTOTAL;   // BIG: per-CTA L2 scratch
   double* Vxx = sm + S::V;
   double* Vzx = Vxx + N * LDN;
-  double* Vzz = Vzx + N * LDN;
+  double* Vzz = S::BIG ? gs + S::GVZZ : Vzx + N * LDN;
   double* vx1 = sm + S::VX1;
   double* vz1 = sm + S::VZ1;
-  const double* Qxx = sm + S::SQXX;
-  const double* Qux = sm + S::SQUX;
-  const double* Quu = sm + S::SQUU;
-  const double* qx1 = sm + S::SQX1;
-  const double* qu1 = sm + S::SQU1;
   double* VF = sm + S::VF;
   double* P = sm + S::P;
   double* G = sm + S::G;
-  double* Y = sm + S::Y;
+  double* Y = S::BIG ? gs + S::GY : sm + S::Y;
   double* Muu = sm + S::MUU;
-  double* H = sm + S::H;
+  double* H = S::BIG ? gs + S::GH : sm + S::H;
+  double* NTb = S::BIG ? gs + S::GNT : VF;   // tail-stage N = Hx F
   double* tau = sm + S::TAU;
   double* rdiag = sm + S::RD;
   double* red = sm + S::RED;
@@ -297,6 +307,8 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
 
   if (gt == 0) stage_issue<N, M>(p, b * T + lo + L - 1, sm, bar);
   for (int idx = gt; idx < S::VZ1 + N; idx += NT) sm[idx] = 0.0;
+  if constexpr (S::BIG)
+    for (int idx = gt; idx < N * LDN; idx += NT) Vzz[idx] = 0.0;
   gsync<NWG>(grp);
   if (SERIAL) {
     for (int idx = gt; idx < NN; idx += NT) Vxx[(idx / N) * LDN + idx % N] = p.QxxT[b * NN + idx];
@@ -314,6 +326,11 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
 #pragma unroll 1
   for (int s = L - 1; s >= 0; --s) {
     const int64_t st = b * T + lo + s;
+    const double* Qxx = S::BIG ? p.Qxx + st * NN : sm + S::SQXX;
+    const double* Qux = S::BIG ? p.Qux + st * (N * M) : sm + S::SQUX;
+    const double* Quu = S::BIG ? p.Quu + st * (M * M) : sm + S::SQUU;
+    const double* qx1 = S::BIG ? p.qx1 + st * N : sm + S::SQX1;
+    const double* qu1 = S::BIG ? p.qu1 + st * M : sm + S::SQU1;
     mbar_wait(bar, phase);
     phase ^= 1u;
 
@@ -356,7 +373,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           const int u = i - N;
           const bool xr = i < N, xc = c < N;
           const double* q = xr ? Qxx + i * N + (xc ? c : 0) : (xc ? Qux + u * N + c : Quu + u * M + (c - N));
-          double* d = xr ? (xc ? Vxx + i * LDN + c : dum) : (xc ? P + u * LDW + c : Muu + u * M + (c - N));
+          double* d = xr ? (xc ? Vxx + i * LDN + c : dum) : (xc ? P + u * LDW + c : Muu + u * LDM + (c - N));
           *d = *q + acc;
         });
     if (gt < N + M) {
@@ -378,13 +395,29 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     if (r == 0) {
       // ---- unconstrained stage: G = -Muu^{-1} P, Cholesky in every lane's registers
       if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);
+      if constexpr (S::BIG) {
+        // CTA Cholesky of Muu in place (not needed again in this stage) and
+        // a blocked DMMA solve of the m x W right-hand side
+        for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = P[(idx / W) * LDW + idx % W];
+        if (!cta_cholesky(Muu, M, LDM, nullptr)) {
+          status = 1 + s;
+          if (s > 0) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+          }
+          break;
+        }
+        cta_cho_solve_blocked(Muu, M, LDM, G, W, LDW);
+        for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = -G[(idx / W) * LDW + idx % W];
+        gsync<NWG>(grp);
+      } else {
       double Lr[M][M], id[M];
       int fail = 0;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
 #pragma unroll
         for (int i = k; i < M; ++i) {
-          double v = Muu[i * M + k];
+          double v = Muu[i * LDM + k];
 #pragma unroll
           for (int q = 0; q < k; ++q) v -= Lr[i][q] * Lr[k][q];
           if (i == k) {
@@ -426,6 +459,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
       }
       gsync<NWG>(grp);
+      }
     } else {
       // ---- constrained tail stage (r >= M since N % M == 0)
       double ph = 0.0, pu = 0.0;
@@ -444,19 +478,19 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       // N = Hx F -> VF rows 0..r-1
       ggemm_f<N, FW, N, NWG>(
           [&](int i, int k) { return H[i * LDW + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
-          [&](int i, int c, double acc) { VF[i * LDF + c] = acc; }, r);
+          [&](int i, int c, double acc) { NTb[i * LDF + c] = acc; }, r);
       gsync<NWG>(grp);
       if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
       for (int idx = gt; idx < r * N; idx += NT) {
         const int i = idx / N, c = idx % N;
-        H[i * LDW + c] = VF[i * LDF + c];
+        H[i * LDW + c] = NTb[i * LDF + c];
       }
-      for (int i = gt; i < r; i += NT) H[i * LDW + CC] += VF[i * LDF + N + M];
+      for (int i = gt; i < r; i += NT) H[i * LDW + CC] += NTb[i * LDF + N + M];
       gsync<NWG>(grp);
       if constexpr (NWG == 1) {
-        warp_qr_wy<M, W, LDF, LDW>(VF + N, r, H, tau, rdiag);   // tau slot holds T (M*M <= TAU+RD+RED)
+        warp_qr_wy<M, W, LDF, LDW>(NTb + N, r, H, tau, rdiag);   // tau slot holds T (M*M)
       } else {
-        gqr<M, W, LDF, LDW, NWG>(VF + N, r, H, tau, rdiag, red, grp, gw, gt);
+        gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
       double rmax = 0.0, rmin = 1e308;
 #pragma unroll
@@ -478,7 +512,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         for (int i = M - 1; i >= 0; --i) {
           double v = H[i * LDW + c];
 #pragma unroll
-          for (int k = i + 1; k < M; ++k) v -= VF[i * LDF + N + k] * x[k];
+          for (int k = i + 1; k < M; ++k) v -= NTb[i * LDF + N + k] * x[k];
           x[i] = v / rdiag[i];
         }
 #pragma unroll
@@ -515,10 +549,12 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       *d += acc;
     };
     if (constrained) {
-      ggemm<M, W, M, false, M, LDW, NWG>(Muu, G, gw,
-                                         [&](int i, int c, double acc) { Y[i * LDW + c] = P[i * LDW + c] + acc; });
+      ggemm<M, W, M, false, LDM, LDW, NWG>(Muu, G, gw,
+                                           [&](int i, int c, double acc) { Y[i * LDW + c] = P[i * LDW + c] + acc; });
       gsync<NWG>(grp);
-      ggemm<N + NZ, W - 1, 2 * M, true, LDW, LDW, NWG>(P, G, gw, vupd);
+      ggemm_f<N + NZ, W - 1, 2 * M, NWG>(
+          [&](int i, int k) { return k < M ? P[k * LDW + i] : G[(k - M) * LDW + i]; },
+          [&](int k, int c) { return k < M ? G[k * LDW + c] : Y[(k - M) * LDW + c]; }, gw, vupd);
     } else {
       ggemm<N + NZ, W - 1, M, true, LDW, LDW, NWG>(P, G, gw, vupd);
     }
@@ -558,7 +594,8 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
   for (int idx = gt; idx < 3 * NN; idx += NT) {
     const int blk = idx / NN, e = idx % NN;
-    dst[idx] = sm[S::V + blk * N * LDN + (e / N) * LDN + e % N];
+    const double* srcb = blk == 0 ? Vxx : (blk == 1 ? Vzx : Vzz);
+    dst[idx] = srcb[(e / N) * LDN + e % N];
   }
   for (int i = gt; i < 2 * N; i += NT) dst[3 * NN + i] = sm[S::VX1 + i];
   if (gt == 0) {
@@ -618,11 +655,19 @@ int launch_small(const SweepArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-bool sweep_small_supported(int n, int m) { return (n == 12 && m == 4) || (n == 32 && m == 8); }
+bool sweep_small_supported(int n, int m) {
+  return (n == 12 && m == 4) || (n == 32 && m == 8) || (n == 64 && m == 32);
+}
+
+size_t sweep_small_gscratch_doubles(int n, int m) {
+  if (n == 64 && m == 32) return (size_t)SL<64, 32>::GTOTAL;
+  return 0;
+}
 
 int launch_sweep_small(const SweepArgs& a, cudaStream_t s) {
   if (a.p.n == 12 && a.p.m == 4) return launch_small<12, 4, 1, 1>(a, s);
   if (a.p.n == 32 && a.p.m == 8) return launch_small<32, 8, 4, 1>(a, s);
+  if (a.p.n == 64 && a.p.m == 32) return launch_small<64, 32, 8, 1>(a, s);
   return -1;
 }
 
