@@ -69,9 +69,9 @@ struct SL {
   static constexpr int DUM = RED + 8;                   // 32 per-lane dummy slots (branch-free epilogues)
   static constexpr int BAR = (DUM + 32 + 1) & ~1;       // mbarrier (8 bytes)
   static constexpr int TOTAL = BAR + 2;
-  // global scratch per CTA (BIG): Vzz (N x LDN), H (N x LDW), Y (M x LDW), NT (N x LDF)
-  static constexpr int GVZZ = 0, GH = GVZZ + N * LDN, GY = GH + N * LDW, GNT = GY + M * LDW;
-  static constexpr int GTOTAL = BIG ? GNT + N * LDF : 0;
+  // global scratch per CTA (BIG): Vzz (N x LDN), H (N x LDW), Y (M x LDW)
+  static constexpr int GVZZ = 0, GH = GVZZ + N * LDN, GY = GH + N * LDW;
+  static constexpr int GTOTAL = BIG ? GY + M * LDW : 0;
   static constexpr uint32_t STAGE_BYTES = BIG ? 8u * (NN + NM + N) : 8u * (2 * NN + 2 * NM + MM + 2 * N + M);
   static_assert(SFX % 2 == 0 && SFU % 2 == 0 && SF1 % 2 == 0 && SQXX % 2 == 0 && SQUX % 2 == 0 &&
                     SQUU % 2 == 0 && SQX1 % 2 == 0 && SQU1 % 2 == 0 && (N * 8) % 16 == 0 && (M * 8) % 16 == 0,
@@ -298,7 +298,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   double* Y = S::BIG ? gs + S::GY : sm + S::Y;
   double* Muu = sm + S::MUU;
   double* H = S::BIG ? gs + S::GH : sm + S::H;
-  double* NTb = S::BIG ? gs + S::GNT : VF;   // tail-stage N = Hx F
+  double* NTb = VF;   // tail-stage N = Hx F (G, which overlays VF when BIG, is written after R is copied out)
   double* tau = sm + S::TAU;
   double* rdiag = sm + S::RD;
   double* red = sm + S::RED;
@@ -506,13 +506,22 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         }
         break;
       }
+      const double* Rm = NTb + N;   // R (upper) with stride LDF
+      int ldr = LDF;
+      if constexpr (S::BIG) {
+        // G overlays VF: move R out of the way first (TAU area, M x M)
+        for (int idx = gt; idx < M * M; idx += NT) tau[idx] = NTb[(idx / M) * LDF + N + idx % M];
+        gsync<NWG>(grp);
+        Rm = tau;
+        ldr = M;
+      }
       for (int c = gt; c < W; c += NT) {
         double x[M];
 #pragma unroll
         for (int i = M - 1; i >= 0; --i) {
           double v = H[i * LDW + c];
 #pragma unroll
-          for (int k = i + 1; k < M; ++k) v -= NTb[i * LDF + N + k] * x[k];
+          for (int k = i + 1; k < M; ++k) v -= Rm[i * ldr + k] * x[k];
           x[i] = v / rdiag[i];
         }
 #pragma unroll
@@ -574,17 +583,24 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     }
     gsync<NWG>(grp);
     // symmetrize Vxx (and Vzz) as 0.5 (V + V'): all N(N-1)/2 pairs in parallel
+    // (Vzz is never a GEMM operand; symmetrizing it once per segment is the
+    // same linear map as every stage: sym(sym(A) + X) = sym(A + X).)
     for (int pp = gt; pp < NP; pp += NT) {
       const int pr = pairs[pp];
       const int i = pr >> 8, c = pr & 255;
       const double v = 0.5 * (Vxx[i * LDN + c] + Vxx[c * LDN + i]);
       Vxx[i * LDN + c] = v;
       Vxx[c * LDN + i] = v;
-      if (!SERIAL) {
-        const double w = 0.5 * (Vzz[i * LDN + c] + Vzz[c * LDN + i]);
-        Vzz[i * LDN + c] = w;
-        Vzz[c * LDN + i] = w;
-      }
+    }
+    gsync<NWG>(grp);
+  }
+  if (!SERIAL) {
+    for (int pp = gt; pp < NP; pp += NT) {
+      const int pr = pairs[pp];
+      const int i = pr >> 8, c = pr & 255;
+      const double w = 0.5 * (Vzz[i * LDN + c] + Vzz[c * LDN + i]);
+      Vzz[i * LDN + c] = w;
+      Vzz[c * LDN + i] = w;
     }
     gsync<NWG>(grp);
   }
