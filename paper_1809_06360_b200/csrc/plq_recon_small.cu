@@ -543,6 +543,9 @@ __device__ __forceinline__ void ring_issue_bwd(const ReconArgs& A, double* slot,
 
 template <int N, int M, int NT, int RS>
 __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
+  // large n: the segment-start blocks (Vzx0, Vzz0, vz10) are read from global
+  // memory once per segment instead of being staged
+  constexpr bool VFG = N >= 64;
   using R = RingL<N, M>;
   constexpr int NN = N * N, NM = N * M, MM = M * M;
   static_assert(2 * N + 3 * M <= NT, "row-fused passes need one thread per row");
@@ -551,8 +554,8 @@ __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
   const int J = p.J, T = p.T, tid = threadIdx.x;
   const int LMAX = p.max_seg_len;
   double* ring = sm;                                  // RS x SLOT
-  double* vfb = ring + RS * R::SLOT;                  // Vzx0, Vzz0, vx10, vz10 (2NN + 2N)
-  double* gh = vfb + 2 * NN + 2 * N;                  // LMAX x (N+M)
+  double* vfb = ring + RS * R::SLOT;                  // Vzx0, Vzz0, vx10, vz10 (2NN + 2N) unless VFG
+  double* gh = vfb + (VFG ? 0 : 2 * NN + 2 * N);      // LMAX x (N+M)
   double* x = gh + (size_t)LMAX * (N + M);
   double* xn = x + N;
   double* uu = xn + N;
@@ -588,7 +591,7 @@ __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
     const double* vfg = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);
     if (tid == 0) {
       for (int k = 0; k < RS && k < L; ++k) ring_issue_fwd<N, M>(A, ring + k * R::SLOT, bars + k, s0 + k);
-      if (!last) {
+      if (!last && !VFG) {
         fence_proxy_async();
         mbar_arrive_tx(vbar, 8u * (2 * NN + 2 * N));
         bulk_g2s(vfb, vfg + NN, 8u * (2 * NN + 2 * N), vbar);
@@ -682,16 +685,19 @@ __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
         worst = fmax(worst, fabs(g + -g));
       }
     } else {
-      mbar_wait(vbar, ph[RS]);
-      ph[RS] ^= 1u;
+      const double* vsrc = VFG ? vfg + NN : vfb;
+      if (!VFG) {
+        mbar_wait(vbar, ph[RS]);
+        ph[RS] ^= 1u;
+      }
       if (tid < N) {
         A.xend[(b * J + j) * N + tid] = x[tid];
         double t0v = 0.0, t1v = 0.0;
         for (int c = 0; c < N; ++c) {
-          t0v += vfb[tid * N + c] * av[c];
-          t1v += vfb[NN + tid * N + c] * z[c];
+          t0v += vsrc[tid * N + c] * av[c];
+          t1v += vsrc[NN + tid * N + c] * z[c];
         }
-        const double mu = -((t0v + t1v) + vfb[2 * NN + N + tid]);
+        const double mu = -((t0v + t1v) + vsrc[2 * NN + N + tid]);
         A.mu_left[(b * (J - 1) + j) * N + tid] = mu;
         lam[tid] = -mu;
       }
@@ -971,7 +977,7 @@ int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, doub
 
 template <int N, int M, int NT, int RS>
 int launch_recon_ring(const ReconArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * ((size_t)RS * RingL<N, M>::SLOT + 2 * N * N + 2 * N +
+  const size_t smem = sizeof(double) * ((size_t)RS * RingL<N, M>::SLOT + (N >= 64 ? 0 : 2 * N * N + 2 * N) +
                                         (size_t)a.p.max_seg_len * (N + M) + 10 * N + 6 * M + NT / 32 + 16);
   auto kern = recon_ring_kernel<N, M, NT, RS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -985,9 +991,13 @@ int launch_recon_ring(const ReconArgs& a, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-bool recon_small_supported(int n, int m) { return (n == 12 && m == 4) || (n == 32 && m == 8); }
+bool recon_small_supported(int n, int m) { return (n == 12 && m == 4) || (n == 32 && m == 8) || (n == 64 && m == 32); }
 
 int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
+  if (a.p.n == 64 && a.p.m == 32) {
+    if (a.p.max_seg_len <= 128) return launch_recon_ring<64, 32, 256, 1>(a, s);
+    return -1;
+  }
   if (a.p.n == 32 && a.p.m == 8) {
     if (a.p.max_seg_len <= 512) return launch_recon_ring<32, 8, 128, 3>(a, s);
     return -1;
