@@ -93,6 +93,42 @@ __device__ __forceinline__ void ggemm_f(AL aload, BL bload, int gw, Epi epi, int
   }
 }
 
+// Same GEMM for single-warp groups with the epilogue also told the
+// compile-time fragment slot (tm * TN + tn) * 2 + e, so per-element operands
+// prefetched into a register array can be indexed statically.
+template <int M, int N, int K, class AL, class BL, class Epi>
+__device__ __forceinline__ void wgemm_slots(AL aload, BL bload, Epi epi) {
+  constexpr int TM = (M + 7) / 8, TN = (N + 7) / 8, KS = (K + 3) / 4;
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int tm = 0; tm < TM; ++tm) {
+    double acc[TN][2];
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn) acc[tn][0] = acc[tn][1] = 0.0;
+    const int i = tm * 8 + g;
+    const bool iok = i < M;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = ks * 4 + q;
+      const bool kok = (K % 4 == 0) || (k < K);
+      const double a = (iok && kok) ? aload(i, k) : 0.0;
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn) {
+        const int j = tn * 8 + g;
+        const double b = (((N % 8 == 0) || (j < N)) && kok) ? bload(k, j) : 0.0;
+        dmma884(acc[tn][0], acc[tn][1], a, b);
+      }
+    }
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tn * 8 + 2 * q + e;
+        if (iok && j < N) epi(i, j, acc[tn][e], (tm * TN + tn) * 2 + e);
+      }
+  }
+}
+
 // pointer-operand form: A row-major (or transposed, TA) with stride LDA, B row-major stride LDB
 template <int M, int N, int K, bool TA, int LDA, int LDB, int NWG, class Epi>
 __device__ __forceinline__ void ggemm(const double* __restrict__ A, const double* __restrict__ B, int gw, Epi epi,

@@ -32,6 +32,10 @@ struct SL {
   // tail temporaries live in a per-CTA slice of (L2-resident) global scratch,
   // and the Q blocks are read from global memory in the GEMM2 epilogue.
   static constexpr bool BIG = N >= 64;
+  // QREG (n <= 16, single-warp groups): the Q blocks are not staged; each lane
+  // prefetches the Q values of its own GEMM2 epilogue fragments into registers
+  static constexpr bool QREG = N <= 16;
+  static constexpr bool QSTAGED = !BIG && !QREG;
   static constexpr int NN = N * N, NM = N * M, MM = M * M;
   static constexpr int LDN = pad_ld(N);
   static constexpr int FW = N + M + 1;
@@ -53,11 +57,11 @@ struct SL {
   static constexpr int SFU = SFX + N * LFX;             // N x LFU
   static constexpr int SF1 = SFU + N * LFU;             // N
   static constexpr int SQXX = SF1 + N;                  // N x N  (not BIG)
-  static constexpr int SQUX = SQXX + (BIG ? 0 : NN);    // M x N
-  static constexpr int SQUU = SQUX + (BIG ? 0 : NM);    // M x M
-  static constexpr int SQX1 = SQUU + (BIG ? 0 : MM);    // N
-  static constexpr int SQU1 = SQX1 + (BIG ? 0 : N);     // M
-  static constexpr int VF = (SQU1 + (BIG ? 0 : M) + 1) & ~1;   // N x LDF (also N = Hx F when not BIG)
+  static constexpr int SQUX = SQXX + (QSTAGED ? NN : 0);    // M x N
+  static constexpr int SQUU = SQUX + (QSTAGED ? NM : 0);    // M x M
+  static constexpr int SQX1 = SQUU + (QSTAGED ? MM : 0);    // N
+  static constexpr int SQU1 = SQX1 + (QSTAGED ? N : 0);     // M
+  static constexpr int VF = (SQU1 + (QSTAGED ? M : 0) + 1) & ~1;   // N x LDF (also N = Hx F)
   static constexpr int P = VF + N * LDF;                // P (then G, Y when not BIG): M x LDW each
   static constexpr int G = BIG ? VF : P + M * LDW;      // BIG: G overlays VF (dead after GEMM2)
   static constexpr int Y = BIG ? -1 : G + M * LDW;
@@ -72,7 +76,7 @@ struct SL {
   // global scratch per CTA (BIG): Vzz (N x LDN), H (N x LDW), Y (M x LDW)
   static constexpr int GVZZ = 0, GH = GVZZ + N * LDN, GY = GH + N * LDW;
   static constexpr int GTOTAL = BIG ? GY + M * LDW : 0;
-  static constexpr uint32_t STAGE_BYTES = BIG ? 8u * (NN + NM + N) : 8u * (2 * NN + 2 * NM + MM + 2 * N + M);
+  static constexpr uint32_t STAGE_BYTES = QSTAGED ? 8u * (2 * NN + 2 * NM + MM + 2 * N + M) : 8u * (NN + NM + N);
   static_assert(SFX % 2 == 0 && SFU % 2 == 0 && SF1 % 2 == 0 && SQXX % 2 == 0 && SQUX % 2 == 0 &&
                     SQUU % 2 == 0 && SQX1 % 2 == 0 && SQU1 % 2 == 0 && (N * 8) % 16 == 0 && (M * 8) % 16 == 0,
                 "bulk copies need 16-byte alignment");
@@ -98,7 +102,7 @@ __device__ __forceinline__ void stage_issue(const plq_problem_t& p, int64_t st, 
     bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
   }
   bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
-  if constexpr (!S::BIG) {
+  if constexpr (S::QSTAGED) {
     bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
     bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
     bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
@@ -111,9 +115,9 @@ __device__ __forceinline__ void stage_issue(const plq_problem_t& p, int64_t st, 
 template <int N, int M>
 __device__ __forceinline__ double fload(const double* sm, int k, int j) {
   using S = SL<N, M>;
-  if (j < N) return sm[S::SFX + k * S::LFX + j];
-  if (j < N + M) return sm[S::SFU + k * S::LFU + (j - N)];
-  return sm[S::SF1 + k];
+  // one address select, one load
+  const int off = (j < N) ? S::SFX + k * S::LFX + j : ((j < N + M) ? S::SFU + k * S::LFU + (j - N) : S::SF1 + k);
+  return sm[off];
 }
 
 // Householder QR of the r x M panel A (stride LDA) applied to the r x W block
@@ -302,7 +306,8 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   double* tau = sm + S::TAU;
   double* rdiag = sm + S::RD;
   double* red = sm + S::RED;
-  double* dum = sm + S::DUM + lane;   // per-lane sink for skipped epilogue elements
+  // per-lane sink for skipped epilogue elements (QREG: unused VF padding columns)
+  double* dum = S::QREG ? sm + S::VF + (lane % N) * S::LDF + S::FW + lane / N : sm + S::DUM + lane;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
 
   if (gt == 0) stage_issue<N, M>(p, b * T + lo + L - 1, sm, bar);
@@ -321,16 +326,39 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   }
   int r = SERIAL ? 0 : N;
   int status = 0;
+  // QREG: Q values of this lane's GEMM2 epilogue slots (+ its qx1 / qu1 entry)
+  constexpr int QS = S::QREG ? ((N + M + 7) / 8) * ((N + M + 7) / 8) * 2 : 1;
+  double qv[QS], qw = 0.0;
+  auto q_prefetch = [&](int64_t stq) {
+    if constexpr (S::QREG) {
+      const int g = lane >> 2, q4 = lane & 3;
+      constexpr int TN2 = (N + M + 7) / 8;
+#pragma unroll
+      for (int sl = 0; sl < QS; ++sl) {
+        const int tm = sl / (2 * TN2), tn = (sl / 2) % TN2, e = sl & 1;
+        const int i = tm * 8 + g, c = tn * 8 + 2 * q4 + e;
+        double v = 0.0;
+        if (i < N + M && c < N + M) {
+          const int u = i - N;
+          v = (i < N) ? (c < N ? __ldg(p.Qxx + stq * NN + i * N + c) : 0.0)
+                      : (c < N ? __ldg(p.Qux + stq * (N * M) + u * N + c) : __ldg(p.Quu + stq * (M * M) + u * M + (c - N)));
+        }
+        qv[sl] = v;
+      }
+      qw = gt < N ? __ldg(p.qx1 + stq * N + gt) : (gt < N + M ? __ldg(p.qu1 + stq * M + gt - N) : 0.0);
+    }
+  };
+  q_prefetch(b * T + lo + L - 1);
   gsync<NWG>(grp);
 
 #pragma unroll 1
   for (int s = L - 1; s >= 0; --s) {
     const int64_t st = b * T + lo + s;
-    const double* Qxx = S::BIG ? p.Qxx + st * NN : sm + S::SQXX;
-    const double* Qux = S::BIG ? p.Qux + st * (N * M) : sm + S::SQUX;
-    const double* Quu = S::BIG ? p.Quu + st * (M * M) : sm + S::SQUU;
-    const double* qx1 = S::BIG ? p.qx1 + st * N : sm + S::SQX1;
-    const double* qu1 = S::BIG ? p.qu1 + st * M : sm + S::SQU1;
+    const double* Qxx = S::QSTAGED ? sm + S::SQXX : p.Qxx + st * NN;
+    const double* Qux = S::QSTAGED ? sm + S::SQUX : p.Qux + st * (N * M);
+    const double* Quu = S::QSTAGED ? sm + S::SQUU : p.Quu + st * (M * M);
+    const double* qx1 = S::QSTAGED ? sm + S::SQX1 : p.qx1 + st * N;
+    const double* qu1 = S::QSTAGED ? sm + S::SQU1 : p.qu1 + st * M;
     mbar_wait(bar, phase);
     phase ^= 1u;
 
@@ -367,15 +395,26 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     gsync<NWG>(grp);
     // GEMM2: [Mxx ; Mux Muu] = [Fx Fu]' [VFx VFu] + Q-blocks; the w column
     // (mx1 = qx1 + Fx' w, mu1 = qu1 + Fu' w) lane-parallel
-    ggemm_f<N + M, N + M, N, NWG>(
-        [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
-        [&](int i, int c, double acc) {
-          const int u = i - N;
-          const bool xr = i < N, xc = c < N;
-          const double* q = xr ? Qxx + i * N + (xc ? c : 0) : (xc ? Qux + u * N + c : Quu + u * M + (c - N));
-          double* d = xr ? (xc ? Vxx + i * LDN + c : dum) : (xc ? P + u * LDW + c : Muu + u * LDM + (c - N));
-          *d = *q + acc;
-        });
+    if constexpr (S::QREG) {
+      wgemm_slots<N + M, N + M, N>(
+          [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; },
+          [&](int i, int c, double acc, int slot) {
+            const int u = i - N;
+            const bool xr = i < N, xc = c < N;
+            double* d = xr ? (xc ? Vxx + i * LDN + c : dum) : (xc ? P + u * LDW + c : Muu + u * LDM + (c - N));
+            *d = qv[slot] + acc;
+          });
+    } else {
+      ggemm_f<N + M, N + M, N, NWG>(
+          [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
+          [&](int i, int c, double acc) {
+            const int u = i - N;
+            const bool xr = i < N, xc = c < N;
+            const double* q = xr ? Qxx + i * N + (xc ? c : 0) : (xc ? Qux + u * N + c : Quu + u * M + (c - N));
+            double* d = xr ? (xc ? Vxx + i * LDN + c : dum) : (xc ? P + u * LDW + c : Muu + u * LDM + (c - N));
+            *d = *q + acc;
+          });
+    }
     if (gt < N + M) {
       double t = 0.0, t2 = 0.0;
 #pragma unroll
@@ -384,11 +423,13 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         t2 += fload<N, M>(sm, k + 1, gt) * VF[(k + 1) * LDF + N + M];
       }
       t += t2;
+      const double qg = S::QREG ? qw : (gt < N ? qx1[gt] : qu1[gt - N]);
       if (gt < N)
-        vx1[gt] = qx1[gt] + t;
+        vx1[gt] = qg + t;
       else
-        P[(gt - N) * LDW + CC] = qu1[gt - N] + t;
+        P[(gt - N) * LDW + CC] = qg + t;
     }
+    if (s > 0) q_prefetch(st - 1);   // next stage's Q values, consumed one stage later
     gsync<NWG>(grp);
 
     const bool constrained = (r != 0);
@@ -622,7 +663,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
 }
 
 template <int N, int M, int NWG, int GROUPS>
-__global__ void __launch_bounds__(NWG * 32 * GROUPS) sweep_small_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(NWG * 32 * GROUPS, (NWG == 1 ? 16 : 1)) sweep_small_kernel(SweepArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int grp = threadIdx.x / (NWG * 32);
   const int gt = threadIdx.x % (NWG * 32);
