@@ -146,6 +146,31 @@ int plq_boundary_segments(const plq_problem_t* problem, const plq_outputs_t* out
 int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const double* partials, void* workspace,
                  size_t workspace_bytes, void* stream);
 
+/* Device outputs of the smoothing pass (parlqr.parallel.smooth,
+ * parallel.py:567-633): the smoothed LqrSolution's policies, trajectory and
+ * diagnostics.  Its lambdas are the parent's (unchanged). */
+typedef struct plq_smooth_outputs {
+  double* K;              /* (B,T,m,n) smoothed policies[t].Kx (parent's on the last segment) */
+  double* k;              /* (B,T,m)   smoothed policies[t].k1 */
+  double* x;              /* (B,T+1,n) states of the rollout of those policies from x_init */
+  double* u;              /* (B,T,m)   controls */
+  double* objective;      /* (B) evaluate_objective(states, controls) */
+  double* kkt_inf;        /* (B) kkt_residual with the parent's lambdas */
+  double* deviation;      /* (B) details.smooth_deviation = max |x - x_parent|, |u - u_parent| */
+  int32_t* status;        /* (B,J) 1+t: CholeskyFailure(t) in the sweep of segment j, else 0 */
+} plq_smooth_outputs_t;
+
+/* Smoothing pass over the completed parallel solve `parent` of the same
+ * problem batch (reads parent->K, k, x, u, lam, links, vf0): the sweeps of
+ * segments 0..J-2 with terminal cost TerminalCost(Vxx0_{j+1}, vx10_{j+1} +
+ * Vzx0_{j+1}' z_{j+1}) (serial.backward_pass, serial.py:37-79), then one
+ * rollout of all T policies (_rollout_policies, parallel.py:556-564) fused
+ * with the objective / KKT / deviation of the result.  The workspace is the
+ * plq_workspace_bytes() one.  J = 1 reproduces the parent (smooth() returns
+ * it unchanged, parallel.py:587-589). */
+int plq_smooth(const plq_problem_t* problem, const plq_outputs_t* parent, const plq_smooth_outputs_t* out,
+               void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of kernel launches the last plq_solve_parallel / phase call issued
  * on this thread (evidence for bench.py's gpu_launches). */
 int plq_last_launch_count(void);

@@ -449,6 +449,56 @@ def reconstruct_segment(prob, splits, j, seg, links):
     return out
 
 
+def smooth(prob, sol, workers=1):
+    """Second pass trading endpoint constraints for conditioned value costs
+    (parallel.py:567-633): for each segment ahead of the last, a plain
+    Riccati sweep whose terminal cost is the next segment's start value
+    conditioned on its link point, then a full rollout of all T policies.
+    ``sol`` is a dict returned by :func:`solve`."""
+    splits = sol["splits"]
+    J = len(splits) - 1
+    if J == 1:
+        return sol
+    links = sol["links"]
+    vf0 = sol["vf0"]
+    T, n = prob["qx1"].shape
+    m = prob["qu1"].shape[1]
+    tasks = []
+    for j in range(J - 1):
+        lo, hi = splits[j], splits[j + 1]
+        vf = vf0[j + 1]
+        if j + 1 == J - 1:
+            QT, qT = vf[0], vf[1]
+        else:
+            QT, qT = vf[0], vf[3] + vf[1].T @ links[j + 1]
+        QT = 0.5 * (QT + QT.T)          # TerminalCost symmetrizes (problem.py:135-139)
+        st = {f: np.array(prob[f][lo:hi]) for f in STAGE_FIELDS}
+        tasks.append(("serial", st, QT, qT, RANK_TOL))
+    if workers > 1 and len(tasks) > 1:
+        rep = list(_pool(workers).map(_segment_task, tasks))
+    else:
+        rep = [_segment_task(t) for t in tasks]
+    K = sol["K"].copy()
+    k = sol["k"].copy()
+    for j in range(J - 1):
+        lo, hi = splits[j], splits[j + 1]
+        K[lo:hi] = rep[j]["Kx"]
+        k[lo:hi] = rep[j]["k1"]
+    # _rollout_policies (parallel.py:556-564)
+    xs = np.empty((T + 1, n))
+    us = np.empty((T, m))
+    xs[0] = prob["x_init"]
+    for t in range(T):
+        us[t] = K[t] @ xs[t] + k[t]
+        xs[t + 1] = prob["Fx"][t] @ xs[t] + prob["Fu"][t] @ us[t] + prob["f1"][t]
+    dev = max(float(np.abs(xs - sol["states"]).max()), float(np.abs(us - sol["controls"]).max()))
+    out = dict(sol)
+    out.update({"K": K, "k": k, "states": xs, "controls": us, "smooth_deviation": dev,
+                "objective": objective(prob, xs, us),
+                "kkt": kkt_residual(prob, xs, us, sol["lambdas"])})
+    return out
+
+
 def _solve_one(args):
     prob, J, splits, rank_tol = args
     return solve(prob, J=J, splits=splits, rank_tol=rank_tol)

@@ -11,7 +11,7 @@ from .errors import (CholeskyFailure, FactorizationFailure, Infeasible, LinkSing
 from .problem import (DEFAULT_TOLERANCES, AffinePolicy, LqrProblem, LqrSolution, StageCost,
                       StageDynamics, TerminalCost, ToleranceSet)
 from .parallel import (BatchSolver, HostSolver, ParallelDetails, Partition, default_workers,
-                       make_partition, solve_parallel, solve_parallel_batch, solve_parallel_host,
+                       make_partition, smooth, solve_parallel, solve_parallel_batch, solve_parallel_host,
                        stack_problem)
 
 __version__ = "0.1.0"
@@ -21,5 +21,5 @@ __all__ = [
     "HostSolver", "Infeasible", "LinkSingular", "LqrProblem", "LqrSolution", "ParallelDetails",
     "Partition", "SingularKkt", "SolverError", "StageCost", "StageDynamics", "TerminalCost",
     "ToleranceSet", "UnsupportedPartition", "default_workers", "make_partition", "solve_parallel",
-    "solve_parallel_batch", "solve_parallel_host", "stack_problem",
+    "smooth", "solve_parallel_batch", "solve_parallel_host", "stack_problem",
 ]

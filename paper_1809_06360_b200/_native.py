@@ -21,7 +21,7 @@ EXPORTS = (
     "plq_abi_version", "plq_last_error", "plq_workspace_bytes", "plq_solve_parallel",
     "plq_host_arena_bytes", "plq_solve_parallel_host", "plq_sweep_segments",
     "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
-    "plq_finalize", "plq_last_launch_count",
+    "plq_finalize", "plq_last_launch_count", "plq_smooth",
 )
 
 _vp = ctypes.c_void_p
@@ -44,6 +44,13 @@ OUTPUT_FIELDS = ("K", "k", "x", "u", "lam", "links", "mu_left", "lambda_right", 
 
 class PlqOutputs(ctypes.Structure):
     _fields_ = [(f, _vp) for f in OUTPUT_FIELDS]
+
+
+SMOOTH_FIELDS = ("K", "k", "x", "u", "objective", "kkt_inf", "deviation", "status")
+
+
+class PlqSmoothOutputs(ctypes.Structure):
+    _fields_ = [(f, _vp) for f in SMOOTH_FIELDS]
 
 
 _LIB = None
@@ -77,9 +84,10 @@ def lib():
     L.plq_boundary_segments.argtypes = [P, O, ctypes.c_int32, ctypes.c_int32, _vp, _vp,
                                         ctypes.c_size_t, _vp]
     L.plq_finalize.argtypes = [P, O, _vp, _vp, ctypes.c_size_t, _vp]
+    L.plq_smooth.argtypes = [P, O, ctypes.POINTER(PlqSmoothOutputs), _vp, ctypes.c_size_t, _vp]
     for name in ("plq_solve_parallel", "plq_solve_parallel_host", "plq_sweep_segments",
                  "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
-                 "plq_finalize"):
+                 "plq_finalize", "plq_smooth"):
         getattr(L, name).restype = ctypes.c_int
     if L.plq_abi_version() != 1:
         raise RuntimeError("libparlqr_b200.so ABI version mismatch; rebuild it")

@@ -239,6 +239,60 @@ int plq_solve_parallel(const plq_problem_t* problem, const plq_outputs_t* out, v
   return PLQ_OK;
 }
 
+int plq_smooth(const plq_problem_t* problem, const plq_outputs_t* parent, const plq_smooth_outputs_t* out,
+               void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, parent, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  if (!out || !out->K || !out->k || !out->x || !out->u || !out->objective || !out->kkt_inf || !out->deviation ||
+      !out->status)
+    return fail(PLQ_ERR_ARG, "null smoothing output");
+  if (!parent->K || !parent->k || !parent->x || !parent->u || !parent->lam || !parent->links || !parent->vf0)
+    return fail(PLQ_ERR_ARG, "null parent solution field");
+  const int J = problem->J;
+  if (cudaMemsetAsync(out->status, 0, sizeof(int32_t) * problem->B * J, c.s) != cudaSuccess)
+    return cuda_fail("status reset");
+  if (J > 1) {
+    plq::SweepArgs a{};
+    a.p = *problem;
+    a.Kx = out->K;
+    a.Kz = c.ws + c.P.off_Kz;   // serial sweeps write Kz = 0: never into the parent's unfolded gains
+    a.k1 = out->k;
+    a.vf0 = nullptr;
+    a.status = out->status;
+    a.gscratch = c.ws + c.P.off_gs;
+    a.lay = c.P.lay;
+    a.seg_begin = 0;
+    a.seg_end = J - 1;
+    a.smooth_vf0 = parent->vf0;
+    a.smooth_links = parent->links;
+    const int64_t tasks = problem->B * (int64_t)(J - 1);
+    const int grid = (int)std::min<int64_t>(tasks, c.P.grid_max);
+    rc = use_small_sweep(problem) ? plq::launch_sweep_small(a, c.s)
+                                  : plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s);
+    if (rc) return cuda_fail("smoothing sweep launch");
+    ++g_launches;
+  }
+  plq::SmoothArgs s{};
+  s.p = *problem;
+  s.K0 = parent->K;
+  s.k0 = parent->k;
+  s.x0 = parent->x;
+  s.u0 = parent->u;
+  s.lam0 = parent->lam;
+  s.K = out->K;
+  s.k = out->k;
+  s.x = out->x;
+  s.u = out->u;
+  s.objective = out->objective;
+  s.kkt = out->kkt_inf;
+  s.deviation = out->deviation;
+  if (plq::launch_smooth_rollout(s, c.s)) return cuda_fail("smoothing rollout launch");
+  ++g_launches;
+  return PLQ_OK;
+}
+
 int plq_sweep_segments(const plq_problem_t* problem, const plq_outputs_t* out, int32_t seg_begin, int32_t seg_end,
                        void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;

@@ -44,7 +44,33 @@ struct SweepArgs {
   double* gscratch;
   SweepLayout lay;
   int seg_begin, seg_end;  // segment range [seg_begin, seg_end) of every problem
+  // Smoothing pass (parallel.py:567-633): when set, every swept segment is a
+  // plain (serial) sweep whose terminal cost is segment j+1's start value
+  // conditioned on its link point; vf0 may then be null (not written).
+  const double* smooth_vf0;    // (B,J,3n^2+2n) parent solve's start values
+  const double* smooth_links;  // (B,J-1,n) parent solve's link points
 };
+
+// Device-side terminal cost of a swept segment: the problem's terminal cost
+// for the last segment, or -- in the smoothing pass -- TerminalCost(Vxx,
+// vx1 + Vzx' z) of segment j+1 (TerminalCost symmetrizes, problem.py:129-133).
+struct SmoothArgs {
+  plq_problem_t p;
+  const double* K0;    // parent policies (B,T,m,n), (B,T,m)
+  const double* k0;
+  const double* x0;    // parent states / controls / multipliers
+  const double* u0;
+  const double* lam0;
+  double* K;           // smoothed policies: sweeps wrote stages < split[J-1]
+  double* k;
+  double* x;           // (B,T+1,n)
+  double* u;           // (B,T,m)
+  double* objective;   // (B,)
+  double* kkt;         // (B,)
+  double* deviation;   // (B,)
+};
+
+int launch_smooth_rollout(const SmoothArgs& a, cudaStream_t s);
 
 struct ReconArgs {
   plq_problem_t p;

@@ -136,7 +136,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   const int n = p.n, m = p.m, J = p.J, T = p.T;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
-  const bool serial = (j == J - 1);
+  const bool serial = (j == J - 1) || a.smooth_vf0;
   const int nz = serial ? 0 : n;
   const int cc = n + nz;            // constant column of G
   const int W = cc + 1;             // logical width of P/G/Y
@@ -174,7 +174,21 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   for (int idx = tid; idx < 3 * nn + 2 * n; idx += nt) bf.V[idx] = 0.0;
   if (tid == 0) *sflag = 0;
   __syncthreads();
-  if (serial) {
+  if (serial && a.smooth_vf0) {
+    // smoothing pass: TerminalCost(Vxx, vx1 + Vzx' z) of segment j+1 (parallel.py:598-606)
+    const double* v = a.smooth_vf0 + (b * J + j + 1) * (int64_t)(3 * nn + 2 * n);
+    const double* z = a.smooth_links + (b * (J - 1) + j + 1) * (int64_t)n;
+    for (int idx = tid; idx < nn; idx += nt) {
+      const int i = idx / n, c = idx % n;
+      Vxx[idx] = 0.5 * (v[i * n + c] + v[c * n + i]);
+    }
+    for (int i = tid; i < n; i += nt) {
+      double t = 0.0;
+      if (j + 1 < J - 1)
+        for (int k = 0; k < n; ++k) t += v[nn + k * n + i] * z[k];
+      vx1[i] = v[3 * nn + i] + t;
+    }
+  } else if (serial) {
     for (int idx = tid; idx < nn; idx += nt) Vxx[idx] = p.QxxT[b * nn + idx];
     for (int i = tid; i < n; i += nt) vx1[i] = p.qx1T[b * n + i];
   } else {
@@ -380,8 +394,10 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
 
   // ---- segment-start value blocks (parallel.py:230-237) and status
   const int vsz = 3 * nn + 2 * n;
-  double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
-  for (int idx = tid; idx < vsz; idx += nt) dst[idx] = bf.V[idx];
+  if (a.vf0) {
+    double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
+    for (int idx = tid; idx < vsz; idx += nt) dst[idx] = bf.V[idx];
+  }
   if (tid == 0) {
     int st = *sflag;
     if (st == 0 && !serial && r > 0) st = PLQ_STATUS_DEGENERATE;   // feasibility rows left

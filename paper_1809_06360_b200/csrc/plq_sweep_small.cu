@@ -315,7 +315,21 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   if constexpr (S::BIG)
     for (int idx = gt; idx < N * LDN; idx += NT) Vzz[idx] = 0.0;
   gsync<NWG>(grp);
-  if (SERIAL) {
+  if (SERIAL && a.smooth_vf0) {
+    // smoothing pass: TerminalCost(Vxx, vx1 + Vzx' z) of segment j+1 (parallel.py:598-606)
+    const double* v = a.smooth_vf0 + (b * J + j + 1) * (int64_t)(3 * NN + 2 * N);
+    const double* z = a.smooth_links + (b * (J - 1) + j + 1) * (int64_t)N;
+    for (int idx = gt; idx < NN; idx += NT) {
+      const int i = idx / N, c = idx % N;
+      Vxx[i * LDN + c] = 0.5 * (v[i * N + c] + v[c * N + i]);
+    }
+    for (int i = gt; i < N; i += NT) {
+      double t = 0.0;
+      if (j + 1 < J - 1)
+        for (int k = 0; k < N; ++k) t += v[NN + k * N + i] * z[k];
+      vx1[i] = v[3 * NN + i] + t;
+    }
+  } else if (SERIAL) {
     for (int idx = gt; idx < NN; idx += NT) Vxx[(idx / N) * LDN + idx % N] = p.QxxT[b * NN + idx];
     for (int i = gt; i < N; i += NT) vx1[i] = p.qx1T[b * N + i];
   } else {
@@ -648,13 +662,15 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   (void)lane;
 
   const int vsz = 3 * NN + 2 * N;
-  double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
-  for (int idx = gt; idx < 3 * NN; idx += NT) {
-    const int blk = idx / NN, e = idx % NN;
-    const double* srcb = blk == 0 ? Vxx : (blk == 1 ? Vzx : Vzz);
-    dst[idx] = srcb[(e / N) * LDN + e % N];
+  if (a.vf0) {
+    double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
+    for (int idx = gt; idx < 3 * NN; idx += NT) {
+      const int blk = idx / NN, e = idx % NN;
+      const double* srcb = blk == 0 ? Vxx : (blk == 1 ? Vzx : Vzz);
+      dst[idx] = srcb[(e / N) * LDN + e % N];
+    }
+    for (int i = gt; i < 2 * N; i += NT) dst[3 * NN + i] = sm[S::VX1 + i];
   }
-  for (int i = gt; i < 2 * N; i += NT) dst[3 * NN + i] = sm[S::VX1 + i];
   if (gt == 0) {
     if (status == 0 && !SERIAL && r > 0) status = PLQ_STATUS_DEGENERATE;
     a.status[b * J + j] = status;
@@ -683,7 +699,7 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS, (NWG == 1 ? 16 : 1)) sweep_
   for (int64_t task = (int64_t)blockIdx.x * GROUPS + grp; task < total; task += (int64_t)gridDim.x * GROUPS) {
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
-    if (j == a.p.J - 1)
+    if (j == a.p.J - 1 || a.smooth_vf0)
       small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j, phase, pairs);
     else
       small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j, phase, pairs);

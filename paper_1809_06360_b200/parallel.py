@@ -245,6 +245,32 @@ class BatchSolver:
         status = self.out["status"].cpu().numpy()
         raise_for_status(status)
 
+    def smooth(self, inputs, stream=None):
+        """Launch the smoothing pass (``plq_smooth``) over this solver's last
+        solve of the same ``inputs`` (no host sync).  Returns the device dict
+        of smoothed ``K, k, x, u, objective, kkt_inf, deviation, status``."""
+        torch = self.torch
+        if getattr(self, "smooth_out", None) is None:
+            B, T, n, m, J = self.B, self.T, self.n, self.m, self.J
+            dev = dict(device=self.device, dtype=torch.float64)
+            with torch.cuda.device(self.device):
+                self.smooth_out = {
+                    "K": torch.empty((B, T, m, n), **dev), "k": torch.empty((B, T, m), **dev),
+                    "x": torch.empty((B, T + 1, n), **dev), "u": torch.empty((B, T, m), **dev),
+                    "objective": torch.empty((B,), **dev), "kkt_inf": torch.empty((B,), **dev),
+                    "deviation": torch.empty((B,), **dev),
+                    "status": torch.zeros((B, J), dtype=torch.int32, device=self.device),
+                }
+            self._smooth_outs = _native.PlqSmoothOutputs(
+                **{f: _ptr(self.smooth_out[f]) for f in _native.SMOOTH_FIELDS})
+        prob = self._problem_struct(inputs)
+        stream = torch.cuda.current_stream(self.device) if stream is None else stream
+        rc = self.lib.plq_smooth(ctypes.byref(prob), ctypes.byref(self._outs), ctypes.byref(self._smooth_outs),
+                                 _ptr(self.workspace), self.ws_bytes, ctypes.c_void_p(stream.cuda_stream))
+        _native.check(rc, "plq_smooth")
+        self.launches = int(self.lib.plq_last_launch_count())
+        return self.smooth_out
+
 
 def raise_for_status(status):
     """Map per-(problem, segment) status codes to the reference exceptions,
@@ -350,6 +376,77 @@ def solve_parallel(problem, J, workers=None, tolerances=DEFAULT_TOLERANCES, coll
         policies=PolicySequence(o["K"], o["k"]),
         objective=float(o["objective"]), kkt_residual_inf=float(o["kkt_inf"]),
         details=details,
+    )
+
+
+def _policy_arrays(policies):
+    if isinstance(policies, PolicySequence):
+        return policies._K, policies._k
+    return (np.stack([np.asarray(p.Kx, dtype=np.float64) for p in policies]),
+            np.stack([np.asarray(p.k1, dtype=np.float64) for p in policies]))
+
+
+def _vf0_rows(values, n):
+    rows = np.zeros((len(values), 3 * n * n + 2 * n))
+    nn = n * n
+    for j, v in enumerate(values):
+        if len(v) == 2:
+            rows[j, :nn] = np.ravel(v[0])
+            rows[j, 3 * nn:3 * nn + n] = v[1]
+        else:
+            Vxx, Vzx, Vzz, vx1, vz1 = v
+            rows[j] = np.concatenate([np.ravel(Vxx), np.ravel(Vzx), np.ravel(Vzz), vx1, vz1])
+    return rows
+
+
+def smooth(problem, result, workers=None, tolerances=DEFAULT_TOLERANCES, *, device=None):
+    """Drop-in for ``parlqr.parallel.smooth`` (parallel.py:567-633).
+
+    The sweeps of segments ``0..J-2`` with conditioned terminal costs and the
+    rollout of the resulting policies run on the GPU (``plq_smooth``).
+    ``workers`` is accepted for signature parity and ignored.  A ``J = 1``
+    (or non-partitioned) result is returned unchanged, and a partition whose
+    conditioning segment cannot reach arbitrary endpoints raises
+    ``ValueError`` -- the reference's contract.
+    """
+    details = result.details
+    if details is None or not hasattr(details, "segment_values0"):
+        return result
+    partition = details.partition
+    J = partition.J
+    if J == 1:
+        return result
+    for j in range(1, J - 1):
+        feas = details.segment_feasibility[j]
+        if feas is not None and feas[0].shape[0]:
+            raise ValueError(
+                f"segment {j} cannot reach arbitrary endpoints "
+                f"({feas[0].shape[0]} feasibility rows); smoothing undefined "
+                "for this partition")
+    torch = _torch()
+    a = stack_problem(problem)
+    T, n = a["qx1"].shape
+    m = a["qu1"].shape[1]
+    batch = {f: a[f][None] for f in INPUT_FIELDS}
+    solver = BatchSolver(1, T, n, m, partition=_check_partition(partition, T), tolerances=tolerances,
+                         device=device)
+    inputs = _to_device(batch, solver.device, torch)
+    K, k = _policy_arrays(result.policies)
+    parent = {"K": K, "k": k, "x": result.states, "u": result.controls, "lam": result.lambdas,
+              "links": np.asarray(details.link_points).reshape(J - 1, n),
+              "vf0": _vf0_rows(details.segment_values0, n)}
+    for f, v in parent.items():
+        solver.out[f][0].copy_(torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)))
+    with torch.cuda.device(solver.device):
+        so = solver.smooth(inputs)
+    o = {f: v.cpu().numpy()[0] for f, v in so.items()}
+    raise_for_status(o["status"])
+    deviation = float(o["deviation"])
+    return LqrSolution(
+        states=o["x"], controls=o["u"], lambdas=result.lambdas,
+        policies=PolicySequence(o["K"], o["k"]),
+        objective=float(o["objective"]), kkt_residual_inf=float(o["kkt_inf"]),
+        details=dataclasses.replace(details, smooth_deviation=deviation),
     )
 
 

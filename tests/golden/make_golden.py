@@ -237,7 +237,31 @@ def main():
     rec.update({"J": np.int64(demo.DEMO_SPLITS), "csv_undisturbed": und,
                 "csv_disturbed": dis, "cost_p": np.float64(float(summ[1])),
                 "disturbance_smoothing": np.float64(demo.DISTURBANCE_SMOOTHING)})
+    # smoothed solution of the demo (parallel.py:567-633) and its stored rollouts
+    psol = parlqr.solve_parallel(prob, J=demo.DEMO_SPLITS, workers=1)
+    ssol = ref_parallel.smooth(prob, psol, workers=1)
+    rec.update({"smooth/K": np.stack([p.Kx for p in ssol.policies]),
+                "smooth/k": np.stack([p.k1 for p in ssol.policies]),
+                "smooth/states": ssol.states, "smooth/controls": ssol.controls,
+                "smooth/objective": np.float64(ssol.objective), "smooth/kkt": np.float64(ssol.kkt_residual_inf),
+                "smooth/deviation": np.float64(ssol.details.smooth_deviation),
+                "csv_smoothed_undisturbed": read_csv("smoothed_undisturbed.csv"),
+                "csv_smoothed_disturbed": read_csv("smoothed_disturbed.csv"),
+                "cost_smoothed": np.float64(float(summ[2]))})
     save("demo_double_integrator", **rec)
+    # smoothing on seeded config shapes
+    for name, cid, over in (("smooth_cfg0", 0, {}), ("smooth_cfg2_shape", 2, dict(T=256, J=4)),
+                            ("smooth_cfg4_shape", 4, dict(T=64, J=2))):
+        cfg = synth.CONFIGS[cid].scaled(**over) if over else synth.CONFIGS[cid]
+        a = {k: v[0] for k, v in synth.generate_batch(cfg, seed=1, count=1).items()}
+        pr = to_problem(a)
+        ps = parlqr.solve_parallel(pr, J=cfg.J, workers=1)
+        ss = ref_parallel.smooth(pr, ps, workers=1)
+        save(name, cfg_id=np.int64(cid), T=np.int64(cfg.T), J=np.int64(cfg.J), seed=np.int64(1),
+             input_sha256=np.array(digest({k: v[None] for k, v in a.items()})),
+             K=np.stack([p.Kx for p in ss.policies]), k=np.stack([p.k1 for p in ss.policies]),
+             states=ss.states, controls=ss.controls, objective=np.float64(ss.objective),
+             kkt=np.float64(ss.kkt_residual_inf), deviation=np.float64(ss.details.smooth_deviation))
 
 
 if __name__ == "__main__":

@@ -95,3 +95,32 @@ def test_demo_policies_reproduce_stored_rollouts():
     und = z["csv_undisturbed"]
     np.testing.assert_allclose(np.array(xs), und[:, :2], rtol=0, atol=1e-12)
     np.testing.assert_allclose(np.array(us)[:, 0], und[:-1, 2], rtol=0, atol=1e-9)
+
+
+SMOOTH_FIXTURES = ("smooth_cfg0", "smooth_cfg2_shape", "smooth_cfg4_shape")
+
+
+def test_oracle_smooth_matches_reference():
+    """oracle.smooth restates parallel.py:567-633; pinned against the
+    reference's own smoothed solutions (tests/golden/make_golden.py)."""
+    import os
+    from conftest import GOLDEN
+    from paper_1809_06360_b200 import synth
+    z = np.load(os.path.join(GOLDEN, "demo_double_integrator.npz"))
+    a = {k[3:]: z[k] for k in z.files if k.startswith("in/")}
+    sm = O.smooth(a, O.solve(a, J=int(z["J"])))
+    for k in ("K", "k", "states", "controls"):
+        assert rel_err(sm[k], z["smooth/" + k]) <= 1e-13, k
+    assert abs(sm["objective"] - float(z["smooth/objective"])) <= 1e-13 * abs(float(z["smooth/objective"]))
+    # the demo's stored smoothed rollouts (demo.py: smoothed_undisturbed.csv)
+    np.testing.assert_allclose(sm["states"], z["csv_smoothed_undisturbed"][:, :2], rtol=0, atol=1e-12)
+    for name in SMOOTH_FIXTURES:
+        zz = np.load(os.path.join(GOLDEN, name + ".npz"))
+        cfg = synth.CONFIGS[int(zz["cfg_id"])].scaled(T=int(zz["T"]), J=int(zz["J"]))
+        batch = synth.generate_batch(cfg, seed=int(zz["seed"]), count=1)
+        a = O.problem_slice(batch, 0)
+        sm = O.smooth(a, O.solve(a, J=cfg.J))
+        for k in ("K", "k", "states", "controls"):
+            assert rel_err(sm[k], zz[k]) <= 1e-12, (name, k)
+        assert abs(sm["objective"] - float(zz["objective"])) <= 1e-12 * abs(float(zz["objective"]))
+        assert sm["smooth_deviation"] <= 1e-8 and float(zz["deviation"]) <= 1e-8
