@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-smooth", action="store_true")
     return ap.parse_args()
 
 
@@ -143,6 +144,34 @@ def time_cpu(cfg, seed, steps, warmup):
         times.append(time.perf_counter() - t0)
     return {"value": knots / statistics.mean(times), "unit": "knots/s", "cores": used, "kind": "port",
             "sample": desc, "sample_seconds_mean": statistics.mean(times), "steps": steps}
+
+
+def time_cpu_smooth(cfg, seed, budget_s=4.0):
+    """Oracle smooth() (parallel.py:567-633) on a bounded sample, one core,
+    parent solves precomputed (only the smoothing pass is timed)."""
+    from oracle import parlqr_oracle as O
+    if cfg.B > 1:
+        batch = synth.generate_batch(cfg, seed=seed, count=min(cfg.B, 8))
+        probs = [O.problem_slice(batch, i) for i in range(batch["qx1"].shape[0])]
+        J, desc = cfg.J, "problems of the config"
+    else:
+        L = cfg.T // cfg.J
+        Js = min(cfg.J, 16)
+        sub = cfg.scaled(T=L * Js, J=Js)
+        probs = [O.problem_slice(synth.generate_batch(sub, seed=seed, count=1), 0)]
+        J, desc = Js, f"sub-horizon T={sub.T} (segment length {L}, J={Js})"
+    sols = [O.solve(p, J=J) for p in probs]
+    done, knots, t0 = 0, 0, time.perf_counter()
+    while True:
+        i = done % len(probs)
+        O.smooth(probs[i], sols[i])
+        done += 1
+        knots += probs[i]["qx1"].shape[0]
+        el = time.perf_counter() - t0
+        if el >= budget_s or done >= 4 * len(probs):
+            break
+    return {"value": knots / el, "unit": "knots/s", "cores": 1, "kind": "port",
+            "sample": f"{done} smoothing passes over {desc}, parent solves precomputed"}
 
 
 # ---------------------------------------------------------------------------
@@ -309,6 +338,31 @@ def run_ours(args):
                "api": "plq_solve_parallel_host (pinned host inputs -> host LqrSolution arrays)"}
         del hs, pinned
 
+    # ---- smoothing pass (parallel.smooth, §8f row 1) over this solve: device time
+    smooth = None
+    if not sharded and not args.no_smooth and cfg.J > 1:
+        solver.run(inputs)
+        solver.smooth(inputs)
+        torch.cuda.synchronize()
+        es = []
+        for _ in range(max(3, min(args.steps, 20))):
+            if flush is not None:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            solver.smooth(inputs)
+            b.record(stream)
+            es.append((a, b))
+        torch.cuda.synchronize()
+        sm_ms = statistics.mean(x.elapsed_time(y) for x, y in es)
+        smooth = {"metric": "smoothed_knots_per_s", "value": knots / (sm_ms / 1000.0), "unit": "knots/s",
+                  "ms_per_step": sm_ms, "gpu_launches": solver.launches,
+                  "what": "plq_smooth: J-1 conditioned serial sweeps + rollout/objective/KKT, "
+                          "parent solve resident"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            smooth["cpu_baseline"] = time_cpu_smooth(cfg, args.seed)
+        solver.raise_for_status()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = time_cpu(cfg, args.seed, steps=3, warmup=1)
@@ -338,6 +392,7 @@ def run_ours(args):
             "clocks": sampler.report(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "smooth": smooth,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -41,7 +41,7 @@ struct Plan {
   int threads = 0;
   size_t smem = 0;
   int grid_max = 0;
-  size_t off_Kz = 0, off_k1 = 0, off_gh = 0, off_xend = 0, off_part = 0, off_gs = 0, off_link = 0;
+  size_t off_Kz = 0, off_k1 = 0, off_gh = 0, off_xend = 0, off_part = 0, off_gs = 0, off_link = 0, off_smap = 0;
   size_t total_doubles = 0;
 };
 
@@ -87,6 +87,8 @@ Plan make_plan(const plq_problem_t* p) {
   P.off_link = off;
   off += up2(std::max(plq::link_workspace_doubles(B, p->J, p->n),
                       use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0)));
+  P.off_smap = off;
+  if (plq::smooth_segmented(B, p->J)) off += up2(plq::smooth_map_doubles(B, p->T, p->J, p->n, p->m));
   P.total_doubles = off;
   return P;
 }
@@ -288,8 +290,10 @@ int plq_smooth(const plq_problem_t* problem, const plq_outputs_t* parent, const 
   s.objective = out->objective;
   s.kkt = out->kkt_inf;
   s.deviation = out->deviation;
-  if (plq::launch_smooth_rollout(s, c.s)) return cuda_fail("smoothing rollout launch");
-  ++g_launches;
+  s.maps = c.ws + c.P.off_smap;
+  int nl = 0;
+  if (plq::launch_smooth_rollout(s, c.s, &nl)) return cuda_fail("smoothing rollout launch");
+  g_launches += nl;
   return PLQ_OK;
 }
 

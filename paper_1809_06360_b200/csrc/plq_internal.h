@@ -68,9 +68,17 @@ struct SmoothArgs {
   double* objective;   // (B,)
   double* kkt;         // (B,)
   double* deviation;   // (B,)
+  double* maps;        // segmented mode: (B,J-1,n,n+1) closed-loop segment maps [Phi | c],
+                       // then (B,J) join residuals and (B,ceil(T/CH),3) evaluation partials
 };
 
-int launch_smooth_rollout(const SmoothArgs& a, cudaStream_t s);
+constexpr int SMOOTH_EVAL_CH = 8;   // stages per evaluation CTA (segmented mode)
+size_t smooth_map_doubles(int64_t B, int T, int J, int n, int m);
+
+// Segment-parallel rollout (affine segment maps) when the batch alone cannot
+// fill the GPU; otherwise one CTA walks each problem's horizon.
+bool smooth_segmented(int64_t B, int J);
+int launch_smooth_rollout(const SmoothArgs& a, cudaStream_t s, int* launches);
 
 struct ReconArgs {
   plq_problem_t p;
