@@ -752,42 +752,64 @@ __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
 // sequential link solve, one warp per problem
 
 // One warp per problem: the reference's block Cholesky (endpoint.py:410-438).
-// The problem's segment-start value blocks (J x (3n^2+2n) doubles, contiguous)
-// arrive in shared memory by one bulk copy; pivot / right-hand-side blocks
-// ping-pong in smem, pivots are inverted once, only X_i goes to global.
+// The segment-start value blocks stream through a 3-slot ring of bulk copies
+// (block i+2 in flight while step i computes on blocks i, i+1), pivot /
+// right-hand-side blocks ping-pong in smem, the pivot block is factored
+// element-parallel across the warp (reciprocal pivots kept), only X_i goes to
+// global.  The residual pass streams the blocks again (L2-resident).
 template <int N>
 __global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const double* vf0, double* links,
                                                      double* link_residual, int32_t* status, double* Xs) {
-  constexpr int LD = N + 1, NN = N * N, VS = 3 * NN + 2 * N;
+  constexpr int LD = N + 1, NN = N * N, VS = 3 * NN + 2 * N, NS = 3;
+  constexpr int NTRI = N * (N + 1) / 2;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x;
   const int J = p.J, K = J - 1;
-  double* VF = sm;                       // J x VS
-  double* Pm = VF + J * VS;              // N x LD
+  double* RING = sm;                     // NS x VS
+  double* Pm = RING + NS * VS;           // N x LD
   double* R0 = Pm + N * LD;              // N x LD  ping
   double* R1 = R0 + N * LD;              // N x LD  pong
   double* dv = R1 + N * LD;              // K x N
   double* idg = dv + K * N;              // N
-  uint64_t* bar = reinterpret_cast<uint64_t*>(idg + N + 1);
-  if (lane == 0) mbar_init(bar, 1);
+  unsigned char* tri = reinterpret_cast<unsigned char*>(idg + N);   // NTRI (ri, ci) pairs
+  uint64_t* bar = reinterpret_cast<uint64_t*>(idg + N + (2 * NTRI + 7) / 8 + 1);
+  for (int e = lane; e < NTRI; e += 32) {
+    int ri = 0;
+    while ((ri + 1) * (ri + 2) / 2 <= e) ++ri;
+    tri[2 * e] = (unsigned char)ri;
+    tri[2 * e + 1] = (unsigned char)(e - ri * (ri + 1) / 2);
+  }
+  if (lane < NS) mbar_init(bar + lane, 1);
   __syncwarp();
-  uint32_t phase = 0;
-  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+  uint32_t phases = 0;   // bit s: parity of slot s's next completion
+  auto issue = [&](const double* src, int blk) {
     if (lane == 0) {
+      const int s = blk % NS;
       fence_proxy_async();
-      mbar_arrive_tx(bar, (uint32_t)(J * VS * 8));
-      bulk_g2s(VF, vf0 + b * (int64_t)J * VS, (uint32_t)(J * VS * 8), bar);
+      mbar_arrive_tx(bar + s, (uint32_t)(VS * 8));
+      bulk_g2s(RING + s * VS, src + (int64_t)blk * VS, (uint32_t)(VS * 8), bar + s);
     }
+  };
+  auto wait = [&](int blk) {
+    const int s = blk % NS;
+    mbar_wait(bar + s, (phases >> s) & 1u);
+    phases ^= 1u << s;
+  };
+  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+    const double* src = vf0 + b * (int64_t)J * VS;
+    issue(src, 0);
+    issue(src, 1);
     double* X = Xs + b * (int64_t)K * NN;
     const double* xi = p.x_init + b * N;
-    mbar_wait(bar, phase);
-    phase ^= 1u;
     int bad = 0;
     double* R = R0;
     double* RP = R1;
+    wait(0);
     for (int i = 0; i < K; ++i) {
-      const double* left = VF + i * VS;
-      const double* right = VF + (i + 1) * VS;
+      if (i + 2 < J) issue(src, i + 2);
+      wait(i + 1);
+      const double* left = RING + (i % NS) * VS;
+      const double* right = RING + ((i + 1) % NS) * VS;
       // P = Vzz0_i + Vxx0_{i+1};  R = [S_i' | b_i],  S_i = Vzx0_{i+1}
       for (int idx = lane; idx < NN; idx += 32) {
         const int r = idx / N, c = idx % N;
@@ -822,21 +844,23 @@ __global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const dou
         }
         __syncwarp();
       }
-      // Cholesky of P (lane = row), reciprocal pivots in idg
+      // Cholesky of P, element-parallel trailing updates; reciprocal pivots in idg
       for (int k = 0; k < N; ++k) {
         const double dkk = Pm[k * LD + k];
         bad |= !(dkk > 0.0);
         const double d = sqrt(dkk > 0.0 ? dkk : 1.0);
         const double inv = 1.0 / d;
+        __syncwarp();
         if (lane == k) {
           Pm[k * LD + k] = d;
           idg[k] = inv;
         }
         if (lane > k && lane < N) Pm[lane * LD + k] *= inv;
         __syncwarp();
-        if (lane > k && lane < N) {
-          const double lik = Pm[lane * LD + k];
-          for (int jj = k + 1; jj <= lane; ++jj) Pm[lane * LD + jj] -= lik * Pm[jj * LD + k];
+        const int s = N - 1 - k;   // trailing triangle (rows/cols k+1..N-1)
+        for (int e = lane; e < s * (s + 1) / 2; e += 32) {
+          const int r = k + 1 + tri[2 * e], c = k + 1 + tri[2 * e + 1];
+          Pm[r * LD + c] -= Pm[r * LD + k] * Pm[c * LD + k];
         }
         __syncwarp();
       }
@@ -880,12 +904,19 @@ __global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const dou
     }
     double* out = links + b * (int64_t)K * N;
     for (int idx = lane; idx < K * N; idx += 32) out[idx] = dv[idx];
-    // residual of the link equations at the solution (parallel.py:273-282)
+    // residual of the link equations at the solution (parallel.py:273-282),
+    // blocks streamed again through the ring
+    __syncwarp();
+    issue(src, 0);
+    issue(src, 1);
+    wait(0);
     double worst = 0.0;
-    if (lane < N) {
-      for (int i = 0; i < K; ++i) {
-        const double* left = VF + i * VS;
-        const double* right = VF + (i + 1) * VS;
+    for (int i = 0; i < K; ++i) {
+      if (i + 2 < J) issue(src, i + 2);
+      wait(i + 1);
+      const double* left = RING + (i % NS) * VS;
+      const double* right = RING + ((i + 1) % NS) * VS;
+      if (lane < N) {
         double s = 0.0;
 #pragma unroll
         for (int c = 0; c < N; ++c) s += (left[2 * NN + lane * N + c] + right[lane * N + c]) * dv[i * N + c];
@@ -906,6 +937,7 @@ __global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const dou
         }
         worst = fmax(worst, fabs(s - rhs));
       }
+      __syncwarp();
     }
     worst = warp_max(worst);
     if (lane == 0) {
@@ -960,14 +992,17 @@ template <int N>
 int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, double* link_residual, int32_t* status,
                   double* ws, cudaStream_t s) {
   const int J = p.J, K = J - 1;
-  const size_t smem = sizeof(double) * ((size_t)J * (3 * N * N + 2 * N) + 3 * N * (N + 1) + K * N + N + 4);
+  const size_t smem = sizeof(double) * (3 * (size_t)(3 * N * N + 2 * N) + 3 * N * (N + 1) + K * N + N +
+                                        (N * (N + 1) + 7) / 8 + 1 + 4);
   auto kern = link_seq_kernel<N>;
-  static size_t attr = 0;
-  if (smem > attr) {
+  static bool attr = false;
+  if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = 200 * 1024;
+    attr = true;
   }
-  const int64_t cap = (int64_t)sms_count() * 32;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem);
+  const int64_t cap = (int64_t)sms_count() * (per_sm > 0 ? per_sm : 1);
   const int grid = (int)(p.B < cap ? p.B : cap);
   kern<<<grid, 32, smem, s>>>(p, vf0, links, link_residual, status, ws);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -1010,8 +1045,7 @@ int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
   return -1;
 }
 
-// the sequential link solve is used while the chain is short
-// the whole problem's vf0 must fit in shared memory (J <= 64 at n = 12)
+// the sequential link solve is used while the chain is short (J <= 64 at n = 12)
 bool link_seq_supported(int n, int J) { return n == 12 && J <= 64; }
 
 size_t link_seq_workspace_doubles(int64_t B, int J, int n) { return (size_t)B * (J - 1) * n * n + 2; }
