@@ -249,6 +249,15 @@ def main():
                 "csv_smoothed_disturbed": read_csv("smoothed_disturbed.csv"),
                 "cost_smoothed": np.float64(float(summ[2]))})
     save("demo_double_integrator", **rec)
+    # JSON problem / solution files written by the reference itself
+    # (fileio.save_problem, cli solve --solver parallel --J 3, cli.py:26-59)
+    from parlqr import cli as ref_cli
+    from parlqr import fileio as ref_fileio
+    jp = os.path.join(HERE, "json_problem_n3_m2_T12.json")
+    js = os.path.join(HERE, "json_solution_parallel_J3.json")
+    ref_fileio.save_problem(ref_generate(3, 2, 12, seed=7), jp)
+    assert ref_cli.main(["solve", "--problem", jp, "--solver", "parallel", "--J", "3",
+                         "--workers", "1", "--out", js]) == 0
     # smoothing on seeded config shapes
     for name, cid, over in (("smooth_cfg0", 0, {}), ("smooth_cfg2_shape", 2, dict(T=256, J=4)),
                             ("smooth_cfg4_shape", 4, dict(T=64, J=2))):
