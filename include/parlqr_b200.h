@@ -171,6 +171,45 @@ typedef struct plq_smooth_outputs {
 int plq_smooth(const plq_problem_t* problem, const plq_outputs_t* parent, const plq_smooth_outputs_t* out,
                void* workspace, size_t workspace_bytes, void* stream);
 
+/* Two-point-boundary solve (parlqr.endpoint.solve_endpoint_affine /
+ * solve_endpoint, endpoint.py:603-653) of every problem in the batch:
+ * problem->J must be 1 (split_times = {0, T}).  W = 2n+1.
+ * Device outputs of plq_endpoint_affine: */
+typedef struct plq_endpoint_outputs {
+  double* Kx;             /* (B,T,m,n)  policies[t].Kx */
+  double* Kz;             /* (B,T,m,n)  policies[t].Kz */
+  double* k1;             /* (B,T,m)    policies[t].k1 */
+  double* value0;         /* (B,3n^2+2n) values[0]: Vxx, Vzx, Vzz, vx1, vz1 */
+  double* X;              /* (B,T+1,n,W) maps: x_t = [Ra|Rz|r1] [x_init; x_term; 1] */
+  double* S;              /* (B,T,m,W)   maps: u_t = [Sa|Sz|s1] [...] */
+  double* Lam;            /* (B,T+1,n,W) multipliers: lam_t = [La|Lz|l1] [...] */
+  double* E;              /* (B,n,W)     mu = [Ea|Ez|e1] [...] */
+  int32_t* status;        /* (B) backward pass: 0, 1+t CholeskyFailure(t), -1 unreachable endpoint
+                             directions (feasibility rows; not solved on the GPU) */
+  int32_t* gram_status;   /* (B) multiplier Gram system: 0, or 1+i FactorizationFailure(block i) */
+} plq_endpoint_outputs_t;
+
+/* Evaluation at concrete endpoints (EndpointAffineSolution.evaluate,
+ * endpoint.py:538-575): trajectories, objective and the full KKT stack. */
+typedef struct plq_endpoint_point {
+  const double* x_init;   /* (B,n) device; NULL = problem->x_init */
+  const double* x_term;   /* (B,n) device */
+  double* x;              /* (B,T+1,n) */
+  double* u;              /* (B,T,m) */
+  double* lam;            /* (B,T+1,n) */
+  double* mu;             /* (B,n) */
+  double* objective;      /* (B) */
+  double* kkt_inf;        /* (B) */
+} plq_endpoint_point_t;
+
+size_t plq_endpoint_workspace_bytes(const plq_problem_t* problem);
+/* backward_pass(stages, terminal) (endpoint.py:168-301), forward_pass
+ * (:326-349), multiplier_pass (:452-476). */
+int plq_endpoint_affine(const plq_problem_t* problem, const plq_endpoint_outputs_t* out, void* workspace,
+                        size_t workspace_bytes, void* stream);
+int plq_endpoint_evaluate(const plq_problem_t* problem, const plq_endpoint_outputs_t* affine,
+                          const plq_endpoint_point_t* point, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of kernel launches the last plq_solve_parallel / phase call issued
  * on this thread (evidence for bench.py's gpu_launches). */
 int plq_last_launch_count(void);

@@ -88,16 +88,19 @@ def _compress(Hx, Hz, h1, rank_tol, scale, cert_scale):
     return nHx, nHz, nh1
 
 
-def endpoint_sweep(st, rank_tol=RANK_TOL):
-    """Endpoint-explicit backward sweep of one segment with zero terminal
-    cost and terminal rows ``Hx=I, Hz=-I`` (endpoint.py:168-301 as called by
-    parallel.py:228-229).  Returns per-stage ``Kx, Kz, k1`` and the segment
-    start blocks ``vf0 = (Vxx, Vzx, Vzz, vx1, vz1)`` and feasibility rows.
+def endpoint_sweep(st, rank_tol=RANK_TOL, QxxT=None, qx1T=None):
+    """Endpoint-explicit backward sweep of one segment with terminal rows
+    ``Hx=I, Hz=-I`` and zero terminal cost (endpoint.py:168-301 as called by
+    parallel.py:228-229) -- or the terminal cost ``(QxxT, qx1T)`` when given
+    (backward_pass(stages, terminal), endpoint.py:178-184, as called by
+    solve_endpoint[_affine], :618-619, :640).  Returns per-stage ``Kx, Kz,
+    k1`` and the start blocks ``vf0 = (Vxx, Vzx, Vzz, vx1, vz1)`` and
+    feasibility rows.
     """
     L, n = st["qx1"].shape
     m = st["qu1"].shape[1]
-    Vxx = np.zeros((n, n))
-    vx1 = np.zeros(n)
+    Vxx = np.zeros((n, n)) if QxxT is None else 0.5 * (QxxT + QxxT.T)
+    vx1 = np.zeros(n) if qx1T is None else np.array(qx1T, dtype=float)
     Vzx = np.zeros((n, n))
     Vzz = np.zeros((n, n))
     vz1 = np.zeros(n)
@@ -238,6 +241,122 @@ def block_tridiagonal_solve(D, S, b):
     for i in range(K - 2, -1, -1):
         out[i] = d[i] - X[i] @ out[i + 1]
     return np.array(out)
+
+
+# ---------------------------------------------------------------------------
+# two-point-boundary solve (endpoint.py:303-653)
+
+class OracleFactorizationFailure(Exception):
+    """errors.py FactorizationFailure(block) from the multiplier Gram system."""
+
+    def __init__(self, block):
+        super().__init__(f"factorization failed at block {block}")
+        self.block = block
+
+
+def forward_maps(st, Kx, Kz, k1):
+    """forward_pass (endpoint.py:326-349): states / controls as affine maps
+    of (x_init, x_term), packed ``X[t] = [Ra | Rz | r1]`` (T+1, n, 2n+1) and
+    ``S[t] = [Sa | Sz | s1]`` (T, m, 2n+1)."""
+    T, n = st["qx1"].shape
+    m = st["qu1"].shape[1]
+    W = 2 * n + 1
+    X = np.empty((T + 1, n, W))
+    S = np.empty((T, m, W))
+    X[0] = 0.0
+    X[0, :, :n] = np.eye(n)
+    for t in range(T):
+        S[t, :, :n] = Kx[t] @ X[t, :, :n]
+        S[t, :, n:2 * n] = Kx[t] @ X[t, :, n:2 * n] + Kz[t]
+        S[t, :, 2 * n] = Kx[t] @ X[t, :, 2 * n] + k1[t]
+        Fx, Fu = st["Fx"][t], st["Fu"][t]
+        X[t + 1, :, :n] = Fx @ X[t, :, :n] + Fu @ S[t, :, :n]
+        X[t + 1, :, n:2 * n] = Fx @ X[t, :, n:2 * n] + Fu @ S[t, :, n:2 * n]
+        X[t + 1, :, 2 * n] = Fx @ X[t, :, 2 * n] + Fu @ S[t, :, 2 * n] + st["f1"][t]
+    return X, S
+
+
+def multiplier_maps(st, QxxT, qx1T, X, S):
+    """assemble_normal_equations + multiplier_pass (endpoint.py:370-476):
+    the (T+2)-block Gram system over ``lam_0..lam_T, mu`` with a (2n+1)-wide
+    affine right-hand side, solved by block Cholesky.  Returns ``Lam`` (T+1,
+    n, 2n+1) and ``E`` (n, 2n+1)."""
+    T, n = st["qx1"].shape
+    m = st["qu1"].shape[1]
+    W = 2 * n + 1
+    bx = np.empty((T + 1, n, W))
+    bu = np.empty((T, m, W))
+    for t in range(T):
+        bx[t] = -(st["Qxx"][t] @ X[t] + st["Qux"][t].T @ S[t])
+        bx[t, :, -1] -= st["qx1"][t]
+        bu[t] = -(st["Qux"][t] @ X[t] + st["Quu"][t] @ S[t])
+        bu[t, :, -1] -= st["qu1"][t]
+    QT = 0.5 * (QxxT + QxxT.T)
+    bx[T] = -(QT @ X[T])
+    bx[T, :, -1] -= qx1T
+    eye = np.eye(n)
+    D = np.empty((T + 2, n, n))
+    Sb = np.empty((T + 1, n, n))
+    rhs = np.empty((T + 2, n, W))
+    D[0] = eye
+    D[T + 1] = eye
+    rhs[0] = bx[0]
+    for t in range(T):
+        Fx, Fu = st["Fx"][t], st["Fu"][t]
+        D[t + 1] = eye + Fx @ Fx.T + Fu @ Fu.T
+        Sb[t] = -Fx
+        rhs[t + 1] = -Fx @ bx[t] - Fu @ bu[t] + bx[t + 1]
+    Sb[T] = eye
+    rhs[T + 1] = bx[T]
+    try:
+        sol = block_tridiagonal_solve(D, Sb, rhs)
+    except OracleLinkSingular as exc:
+        raise OracleFactorizationFailure(int(str(exc).split()[-1])) from None
+    return sol[:-1], sol[-1]
+
+
+def full_kkt_residual(prob, states, controls, lambdas, mu, x_term):
+    """kkt_residual with an endpoint constraint (problem.py:385-420): every
+    stationarity, dynamics, terminal (+mu), initial and endpoint row."""
+    worst = 0.0
+    for t in range(controls.shape[0]):
+        x, u = states[t], controls[t]
+        Fx, Fu = prob["Fx"][t], prob["Fu"][t]
+        r1 = prob["Qxx"][t] @ x + prob["Qux"][t].T @ u + prob["qx1"][t] + lambdas[t] - Fx.T @ lambdas[t + 1]
+        r2 = prob["Qux"][t] @ x + prob["Quu"][t] @ u + prob["qu1"][t] - Fu.T @ lambdas[t + 1]
+        r3 = states[t + 1] - (Fx @ x + Fu @ u + prob["f1"][t])
+        worst = max(worst, float(np.abs(r1).max()), float(np.abs(r2).max()), float(np.abs(r3).max()))
+    term = prob["QxxT"] @ states[-1] + prob["qx1T"] + lambdas[-1] + mu
+    return max(worst, float(np.abs(term).max()), float(np.abs(states[0] - prob["x_init"]).max()),
+               float(np.abs(states[-1] - x_term).max()))
+
+
+def solve_endpoint_affine(prob, rank_tol=RANK_TOL):
+    """solve_endpoint_affine (endpoint.py:603-636) for reachable problems
+    (empty feasibility triple; the GPU path raises otherwise)."""
+    st = {f: np.asarray(prob[f]) for f in STAGE_FIELDS}
+    sw = endpoint_sweep(st, rank_tol, prob["QxxT"], prob["qx1T"])
+    if sw["feas"][0].shape[0]:
+        raise OracleDegenerate(0)
+    X, S = forward_maps(st, sw["Kx"], sw["Kz"], sw["k1"])
+    Lam, E = multiplier_maps(st, prob["QxxT"], prob["qx1T"], X, S)
+    return {"Kx": sw["Kx"], "Kz": sw["Kz"], "k1": sw["k1"], "vf0": sw["vf0"], "X": X, "S": S,
+            "Lam": Lam, "E": E}
+
+
+def evaluate_endpoint(prob, aff, x_init, x_term):
+    """EndpointAffineSolution.evaluate (endpoint.py:538-575) with multiplier
+    maps: states, controls, lambdas, mu, objective, full KKT residual."""
+    v = np.concatenate([x_init, x_term, [1.0]])
+    states = aff["X"] @ v
+    controls = aff["S"] @ v
+    lambdas = aff["Lam"] @ v
+    mu = aff["E"] @ v
+    p = dict(prob)
+    p["x_init"] = np.asarray(x_init, dtype=float)
+    return {"states": states, "controls": controls, "lambdas": lambdas, "mu": mu,
+            "objective": objective(p, states, controls),
+            "kkt": full_kkt_residual(p, states, controls, lambdas, mu, x_term)}
 
 
 def link_system(vf0, x_init):

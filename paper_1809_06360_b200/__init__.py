@@ -14,6 +14,9 @@ from .parallel import (BatchSolver, HostSolver, ParallelDetails, Partition, defa
                        make_partition, smooth, solve_parallel, solve_parallel_batch, solve_parallel_host,
                        stack_problem)
 
+from .endpoint import (EndpointAffineSolution, EndpointBatch, solve_endpoint, solve_endpoint_affine,
+                       solve_endpoint_batch)
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -22,4 +25,5 @@ __all__ = [
     "Partition", "SingularKkt", "SolverError", "StageCost", "StageDynamics", "TerminalCost",
     "ToleranceSet", "UnsupportedPartition", "default_workers", "make_partition", "solve_parallel",
     "smooth", "solve_parallel_batch", "solve_parallel_host", "stack_problem",
+    "EndpointAffineSolution", "EndpointBatch", "solve_endpoint", "solve_endpoint_affine", "solve_endpoint_batch",
 ]

@@ -21,7 +21,8 @@ EXPORTS = (
     "plq_abi_version", "plq_last_error", "plq_workspace_bytes", "plq_solve_parallel",
     "plq_host_arena_bytes", "plq_solve_parallel_host", "plq_sweep_segments",
     "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
-    "plq_finalize", "plq_last_launch_count", "plq_smooth",
+    "plq_finalize", "plq_last_launch_count", "plq_smooth", "plq_endpoint_workspace_bytes",
+    "plq_endpoint_affine", "plq_endpoint_evaluate",
 )
 
 _vp = ctypes.c_void_p
@@ -51,6 +52,20 @@ SMOOTH_FIELDS = ("K", "k", "x", "u", "objective", "kkt_inf", "deviation", "statu
 
 class PlqSmoothOutputs(ctypes.Structure):
     _fields_ = [(f, _vp) for f in SMOOTH_FIELDS]
+
+
+ENDPOINT_FIELDS = ("Kx", "Kz", "k1", "value0", "X", "S", "Lam", "E", "status", "gram_status")
+
+
+class PlqEndpointOutputs(ctypes.Structure):
+    _fields_ = [(f, _vp) for f in ENDPOINT_FIELDS]
+
+
+POINT_FIELDS = ("x_init", "x_term", "x", "u", "lam", "mu", "objective", "kkt_inf")
+
+
+class PlqEndpointPoint(ctypes.Structure):
+    _fields_ = [(f, _vp) for f in POINT_FIELDS]
 
 
 _LIB = None
@@ -85,9 +100,14 @@ def lib():
                                         ctypes.c_size_t, _vp]
     L.plq_finalize.argtypes = [P, O, _vp, _vp, ctypes.c_size_t, _vp]
     L.plq_smooth.argtypes = [P, O, ctypes.POINTER(PlqSmoothOutputs), _vp, ctypes.c_size_t, _vp]
+    EO = ctypes.POINTER(PlqEndpointOutputs)
+    L.plq_endpoint_workspace_bytes.restype = ctypes.c_size_t
+    L.plq_endpoint_workspace_bytes.argtypes = [P]
+    L.plq_endpoint_affine.argtypes = [P, EO, _vp, ctypes.c_size_t, _vp]
+    L.plq_endpoint_evaluate.argtypes = [P, EO, ctypes.POINTER(PlqEndpointPoint), _vp, ctypes.c_size_t, _vp]
     for name in ("plq_solve_parallel", "plq_solve_parallel_host", "plq_sweep_segments",
                  "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
-                 "plq_finalize", "plq_smooth"):
+                 "plq_finalize", "plq_smooth", "plq_endpoint_affine", "plq_endpoint_evaluate"):
         getattr(L, name).restype = ctypes.c_int
     if L.plq_abi_version() != 1:
         raise RuntimeError("libparlqr_b200.so ABI version mismatch; rebuild it")

@@ -115,7 +115,7 @@ int setup(const plq_problem_t* p, const plq_outputs_t* o, void* ws, size_t bytes
   return PLQ_OK;
 }
 
-int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, int j1) {
+int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, int j1, int endpoint_terminal = 0) {
   if (!o->K || !o->vf0 || !o->status) return fail(PLQ_ERR_ARG, "null sweep output");
   if (j0 < 0 || j1 > p->J || j0 >= j1) return fail(PLQ_ERR_ARG, "bad segment range");
   plq::SweepArgs a{};
@@ -129,6 +129,7 @@ int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
   a.lay = c.P.lay;
   a.seg_begin = j0;
   a.seg_end = j1;
+  a.endpoint_terminal = endpoint_terminal;
   const int64_t tasks = p->B * (int64_t)(j1 - j0);
   const int grid = (int)std::min<int64_t>(tasks, c.P.grid_max);
   const int rc = use_small_sweep(p) ? plq::launch_sweep_small(a, c.s) : plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s);
@@ -294,6 +295,54 @@ int plq_smooth(const plq_problem_t* problem, const plq_outputs_t* parent, const 
   int nl = 0;
   if (plq::launch_smooth_rollout(s, c.s, &nl)) return cuda_fail("smoothing rollout launch");
   g_launches += nl;
+  return PLQ_OK;
+}
+
+size_t plq_endpoint_workspace_bytes(const plq_problem_t* problem) {
+  if (check_problem(problem) || problem->J != 1) return 0;
+  return (make_plan(problem).total_doubles + up2(plq::endpoint_scratch_doubles(*problem)) +
+          up2(plq::endpoint_eval_doubles(*problem))) * sizeof(double);
+}
+
+int plq_endpoint_affine(const plq_problem_t* problem, const plq_endpoint_outputs_t* out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  if (check_problem(problem)) return PLQ_ERR_ARG;
+  if (problem->J != 1) return fail(PLQ_ERR_ARG, "the two-point-boundary solve takes one segment (J = 1)");
+  if (!out || !out->Kx || !out->Kz || !out->k1 || !out->value0 || !out->X || !out->S || !out->Lam || !out->E ||
+      !out->status || !out->gram_status)
+    return fail(PLQ_ERR_ARG, "null endpoint output");
+  if (workspace_bytes < plq_endpoint_workspace_bytes(problem)) return fail(PLQ_ERR_WORKSPACE, "workspace too small");
+  plq_outputs_t o{};
+  o.K = out->Kx;
+  o.Kz = out->Kz;
+  o.k1 = out->k1;
+  o.vf0 = out->value0;
+  o.status = out->status;
+  Ctx c;
+  int rc = setup(problem, &o, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  if ((rc = phase_sweep(problem, &o, c, 0, 1, 1))) return rc;
+  if (plq::launch_endpoint_maps_mult(*problem, *out, c.ws + c.P.total_doubles, c.s, &g_launches))
+    return cuda_fail("endpoint maps / multiplier launch");
+  return PLQ_OK;
+}
+
+int plq_endpoint_evaluate(const plq_problem_t* problem, const plq_endpoint_outputs_t* affine,
+                          const plq_endpoint_point_t* point, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  if (check_problem(problem)) return PLQ_ERR_ARG;
+  if (problem->J != 1) return fail(PLQ_ERR_ARG, "the two-point-boundary solve takes one segment (J = 1)");
+  if (!affine || !affine->X || !affine->S || !affine->Lam || !affine->E) return fail(PLQ_ERR_ARG, "null maps");
+  if (!point || !point->x_term || !point->x || !point->u || !point->lam || !point->mu || !point->objective ||
+      !point->kkt_inf)
+    return fail(PLQ_ERR_ARG, "null evaluation argument");
+  if (!workspace || workspace_bytes < plq_endpoint_workspace_bytes(problem))
+    return fail(PLQ_ERR_WORKSPACE, "workspace too small");
+  const Plan P = make_plan(problem);
+  double* ws = static_cast<double*>(workspace) + P.total_doubles + up2(plq::endpoint_scratch_doubles(*problem));
+  if (plq::launch_endpoint_evaluate(*problem, *affine, *point, ws, static_cast<cudaStream_t>(stream), &g_launches))
+    return cuda_fail("endpoint evaluation launch");
   return PLQ_OK;
 }
 

@@ -49,6 +49,10 @@ struct SweepArgs {
   // conditioned on its link point; vf0 may then be null (not written).
   const double* smooth_vf0;    // (B,J,3n^2+2n) parent solve's start values
   const double* smooth_links;  // (B,J-1,n) parent solve's link points
+  // Two-point-boundary solve (endpoint.backward_pass(stages, terminal),
+  // endpoint.py:168-301 as called by solve_endpoint[_affine]): the last
+  // segment is an endpoint sweep seeded with the terminal cost.
+  int endpoint_terminal;
 };
 
 // Device-side terminal cost of a swept segment: the problem's terminal cost
@@ -79,6 +83,14 @@ size_t smooth_map_doubles(int64_t B, int T, int J, int n, int m);
 // fill the GPU; otherwise one CTA walks each problem's horizon.
 bool smooth_segmented(int64_t B, int J);
 int launch_smooth_rollout(const SmoothArgs& a, cudaStream_t s, int* launches);
+
+// Two-point-boundary solve (plq_endpoint.cu)
+size_t endpoint_scratch_doubles(const plq_problem_t& p);
+size_t endpoint_eval_doubles(const plq_problem_t& p);
+int launch_endpoint_maps_mult(const plq_problem_t& p, const plq_endpoint_outputs_t& o, double* ws, cudaStream_t s,
+                              int* launches);
+int launch_endpoint_evaluate(const plq_problem_t& p, const plq_endpoint_outputs_t& o, const plq_endpoint_point_t& pt,
+                             double* ws, cudaStream_t s, int* launches);
 
 struct ReconArgs {
   plq_problem_t p;

@@ -136,7 +136,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   const int n = p.n, m = p.m, J = p.J, T = p.T;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
-  const bool serial = (j == J - 1) || a.smooth_vf0;
+  const bool serial = (j == J - 1 && !a.endpoint_terminal) || a.smooth_vf0;
   const int nz = serial ? 0 : n;
   const int cc = n + nz;            // constant column of G
   const int W = cc + 1;             // logical width of P/G/Y
@@ -195,6 +195,13 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     for (int idx = tid; idx < n * ldw; idx += nt) {
       const int i = idx / ldw, c = idx % ldw;
       H[idx] = (c == i) ? 1.0 : ((c == n + i) ? -1.0 : 0.0);
+    }
+    if (a.endpoint_terminal && j == J - 1) {   // terminal cost + terminal rows (endpoint.py:178-191)
+      for (int idx = tid; idx < nn; idx += nt) {
+        const int i = idx / n, c = idx % n;
+        Vxx[idx] = 0.5 * (p.QxxT[b * nn + i * n + c] + p.QxxT[b * nn + c * n + i]);
+      }
+      for (int i = tid; i < n; i += nt) vx1[i] = p.qx1T[b * n + i];
     }
   }
   int r = serial ? 0 : n;

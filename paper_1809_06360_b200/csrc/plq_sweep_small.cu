@@ -337,6 +337,13 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       const int i = idx / LDW, c = idx % LDW;
       H[idx] = (c == i) ? 1.0 : ((c == N + i) ? -1.0 : 0.0);
     }
+    if (a.endpoint_terminal && j == J - 1) {   // terminal cost + terminal rows (endpoint.py:178-191)
+      for (int idx = gt; idx < NN; idx += NT) {
+        const int i = idx / N, c = idx % N;
+        Vxx[i * LDN + c] = 0.5 * (p.QxxT[b * NN + i * N + c] + p.QxxT[b * NN + c * N + i]);
+      }
+      for (int i = gt; i < N; i += NT) vx1[i] = p.qx1T[b * N + i];
+    }
   }
   int r = SERIAL ? 0 : N;
   int status = 0;
@@ -699,7 +706,7 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS, (NWG == 1 ? 16 : 1)) sweep_
   for (int64_t task = (int64_t)blockIdx.x * GROUPS + grp; task < total; task += (int64_t)gridDim.x * GROUPS) {
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
-    if (j == a.p.J - 1 || a.smooth_vf0)
+    if ((j == a.p.J - 1 && !a.endpoint_terminal) || a.smooth_vf0)
       small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j, phase, pairs);
     else
       small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j, phase, pairs);

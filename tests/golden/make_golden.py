@@ -174,6 +174,53 @@ def scalar_problem(T):
     return LqrProblem([(cost, dyn)] * T, TerminalCost([[1.0]], [0.0]), [1.0])
 
 
+def endpoint_case(a, seed):
+    """solve_endpoint_affine + solve_endpoint of the reference on ``a`` at a
+    reachable endpoint (a bounded random control sequence's end state)."""
+    from parlqr import endpoint as ref_endpoint
+    prob = to_problem(a)
+    aff = ref_endpoint.solve_endpoint_affine(prob)
+    mp, mm = aff.maps, aff.multipliers
+    rng = np.random.default_rng(seed)
+    x = prob.x_init.copy()
+    for _, dyn in prob.stages:
+        x = dyn.Fx @ x + dyn.Fu @ (0.3 * rng.standard_normal(prob.m)) + dyn.f1
+    z = x
+    sol = ref_endpoint.solve_endpoint(prob, prob.x_init, z)
+    v0 = aff.values[0]
+    return {
+        "Kx": np.stack([p.Kx for p in aff.policies]), "Kz": np.stack([p.Kz for p in aff.policies]),
+        "k1": np.stack([p.k1 for p in aff.policies]),
+        "Vxx0": v0.Vxx, "Vzx0": v0.Vzx, "Vzz0": v0.Vzz, "vx10": v0.vx1, "vz10": v0.vz1,
+        "X": np.concatenate([mp.Ra, mp.Rz, mp.r1[:, :, None]], axis=2),
+        "S": np.concatenate([mp.Sa, mp.Sz, mp.s1[:, :, None]], axis=2),
+        "Lam": np.concatenate([mm.La, mm.Lz, mm.l1[:, :, None]], axis=2),
+        "E": np.concatenate([mm.Ea, mm.Ez, mm.e1[:, None]], axis=1),
+        "x_term": z, "states": sol.states, "controls": sol.controls, "lambdas": sol.lambdas,
+        "mu": sol.mu, "objective": np.float64(sol.objective), "kkt": np.float64(sol.kkt_residual_inf),
+    }
+
+
+def endpoint_goldens():
+    rec = {}
+    cases = [(3, 2, 8, 11), (4, 1, 10, 12), (2, 1, 6, 13), (5, 3, 12, 14), (4, 2, 10, 15), (6, 2, 9, 16)]
+    for i, (n, m, T, seed) in enumerate(cases):
+        a = from_problem(ref_generate(n, m, T, seed=seed))
+        for k, v in a.items():
+            rec[f"{i}/in/{k}"] = v
+        for k, v in endpoint_case(a, 100 + i).items():
+            rec[f"{i}/out/{k}"] = v
+    rec["num"] = np.int64(len(cases))
+    save("endpoint_small", **rec)
+    for name, cid, T in (("endpoint_cfg0_shape", 0, 32), ("endpoint_cfg2_shape", 2, 32),
+                         ("endpoint_cfg4_shape", 4, 8), ("endpoint_cfg3_shape", 3, 4)):
+        cfg = synth.CONFIGS[cid].scaled(T=T, J=1)
+        batch = synth.generate_batch(cfg, seed=2, count=1)
+        a = {k: v[0] for k, v in batch.items()}
+        save(name, cfg_id=np.int64(cid), T=np.int64(T), seed=np.int64(2),
+             input_sha256=np.array(digest(batch)), **endpoint_case(a, 200 + cid))
+
+
 def main():
     # 1. hand example of test_parallel.py:48-54 (J=2 scalar problem)
     stored_case("hand_scalar", [from_problem(scalar_problem(2))], [2])
@@ -249,6 +296,8 @@ def main():
                 "csv_smoothed_disturbed": read_csv("smoothed_disturbed.csv"),
                 "cost_smoothed": np.float64(float(summ[2]))})
     save("demo_double_integrator", **rec)
+    # two-point-boundary solves (endpoint.py:603-653) by the reference itself
+    endpoint_goldens()
     # JSON problem / solution files written by the reference itself
     # (fileio.save_problem, cli solve --solver parallel --J 3, cli.py:26-59)
     from parlqr import cli as ref_cli
