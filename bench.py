@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-smooth", action="store_true")
+    ap.add_argument("--no-endpoint", action="store_true")
     return ap.parse_args()
 
 
@@ -172,6 +173,27 @@ def time_cpu_smooth(cfg, seed, budget_s=4.0):
             break
     return {"value": knots / el, "unit": "knots/s", "cores": 1, "kind": "port",
             "sample": f"{done} smoothing passes over {desc}, parent solves precomputed"}
+
+
+def time_cpu_endpoint(cfg, seed, budget_s=4.0):
+    """Oracle solve_endpoint_affine + evaluate (endpoint.py:603-653) on a
+    bounded sample of the config's problems, one core."""
+    from oracle import parlqr_oracle as O
+    batch = synth.generate_batch(cfg, seed=seed, count=min(cfg.B, 4))
+    probs = [O.problem_slice(batch, i) for i in range(batch["qx1"].shape[0])]
+    zs = np.random.default_rng(seed).standard_normal((len(probs), cfg.n))
+    done, knots, t0 = 0, 0, time.perf_counter()
+    while True:
+        i = done % len(probs)
+        aff = O.solve_endpoint_affine(probs[i])
+        O.evaluate_endpoint(probs[i], aff, probs[i]["x_init"], zs[i])
+        done += 1
+        knots += cfg.T
+        el = time.perf_counter() - t0
+        if el >= budget_s or done >= 4 * len(probs):
+            break
+    return {"value": knots / el, "unit": "knots/s", "cores": 1, "kind": "port",
+            "sample": f"{done} two-point-boundary solves of the config's problems"}
 
 
 # ---------------------------------------------------------------------------
@@ -369,6 +391,39 @@ def run_ours(args):
             smooth["cpu_baseline"] = time_cpu_smooth(cfg, args.seed)
         solver.raise_for_status()
 
+    # ---- two-point-boundary solve (§8f row 3) on the config's problems
+    endpoint = None
+    if not sharded and not args.no_endpoint and cfg.T <= 1024 and cfg.n <= 64:
+        from paper_1809_06360_b200 import EndpointBatch
+        eb = EndpointBatch(B_loc, cfg.T, cfg.n, cfg.m, device=dev)
+        zs = torch.from_numpy(np.random.default_rng(args.seed).standard_normal((B_loc, cfg.n))).to(dev)
+        def ep_step():
+            eb.affine(inputs)
+            n_aff = eb.launches
+            eb.evaluate(zs)
+            return n_aff + eb.launches
+        ep_step()
+        torch.cuda.synchronize()
+        eb.raise_for_status()
+        es = []
+        for _ in range(max(3, min(args.steps, 10))):
+            if flush is not None:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            nl = ep_step()
+            b.record(stream)
+            es.append((a, b))
+        torch.cuda.synchronize()
+        ep_ms = statistics.mean(x.elapsed_time(y) for x, y in es)
+        endpoint = {"metric": "endpoint_knots_per_s", "value": knots / (ep_ms / 1000.0), "unit": "knots/s",
+                    "ms_per_step": ep_ms, "gpu_launches": nl,
+                    "what": "plq_endpoint_affine + plq_endpoint_evaluate: terminal-seeded endpoint sweep, "
+                            "forward maps, multiplier normal equations, evaluation at x_term"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            endpoint["cpu_baseline"] = time_cpu_endpoint(cfg, args.seed)
+        del eb
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = time_cpu(cfg, args.seed, steps=3, warmup=1)
@@ -399,6 +454,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "smooth": smooth,
+            "endpoint": endpoint,
         }
         print(json.dumps(line), flush=True)
     if dist:

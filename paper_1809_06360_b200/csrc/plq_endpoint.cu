@@ -96,12 +96,13 @@ __host__ __device__ inline int64_t ep_scratch(int n, int m) {
 }
 
 // ---- forward_pass (endpoint.py:326-349)
-__global__ void __launch_bounds__(EP_NT) ep_maps_kernel(EpArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT) ep_maps_kernel(EpArgs a) {
   const plq_problem_t& p = a.p;
   const int n = p.n, m = p.m, T = p.T, W = 2 * n + 1, tid = threadIdx.x;
   const int64_t b = blockIdx.x, nn = (int64_t)n * n, nm = (int64_t)n * m;
   double* X0 = a.o.X + b * (T + 1) * n * W;
-  for (int idx = tid; idx < n * W; idx += EP_NT) X0[idx] = (idx / W == idx % W) ? 1.0 : 0.0;
+  for (int idx = tid; idx < n * W; idx += NT) X0[idx] = (idx / W == idx % W) ? 1.0 : 0.0;
   __syncthreads();
   for (int t = 0; t < T; ++t) {
     const int64_t bt = b * T + t;
@@ -163,6 +164,7 @@ __device__ void ep_bu(const EpArgs& a, int64_t b, int t, double* BU) {
 }
 
 // ---- assemble_normal_equations + multiplier_pass (endpoint.py:370-476)
+template <int EP_NT>
 __global__ void __launch_bounds__(EP_NT) ep_mult_kernel(EpArgs a) {
   __shared__ int flag;
   const plq_problem_t& p = a.p;
@@ -389,9 +391,16 @@ int launch_endpoint_maps_mult(const plq_problem_t& p, const plq_endpoint_outputs
   a.o = o;
   a.Xb = ws;
   a.scratch = ws + (size_t)p.B * (p.T + 1) * p.n * p.n;
-  ep_maps_kernel<<<(unsigned)p.B, EP_NT, 0, s>>>(a);
-  if (cudaGetLastError() != cudaSuccess) return -1;
-  ep_mult_kernel<<<(unsigned)p.B, EP_NT, 0, s>>>(a);
+  // small states: 4 warps cover every GEMM tile; more CTAs stay resident
+  if (p.n <= 32) {
+    ep_maps_kernel<128><<<(unsigned)p.B, 128, 0, s>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    ep_mult_kernel<128><<<(unsigned)p.B, 128, 0, s>>>(a);
+  } else {
+    ep_maps_kernel<EP_NT><<<(unsigned)p.B, EP_NT, 0, s>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    ep_mult_kernel<EP_NT><<<(unsigned)p.B, EP_NT, 0, s>>>(a);
+  }
   if (cudaGetLastError() != cudaSuccess) return -1;
   *launches += 2;
   return 0;
