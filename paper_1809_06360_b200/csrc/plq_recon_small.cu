@@ -275,7 +275,8 @@ __device__ __forceinline__ void seg_issue(const ReconArgs& A, double* buf, uint6
   fence_proxy_async();
   const uint32_t l8 = (uint32_t)L * 8u;
   const uint32_t vbytes = endpoint ? 8u * (2 * NN + 2 * N) : 0u;
-  mbar_arrive_tx(bar, l8 * (2 * NN + 4 * NM + MM + 2 * N + 2 * M) + vbytes);   // the fields below
+  (void)MM;
+  mbar_arrive_tx(bar, l8 * (NN + NM + N) + vbytes);   // the fields below
   double* d = buf;
   bulk_g2s(d, p.Fx + s0 * NN, l8 * NN, bar);
   d += L * NN;
@@ -283,33 +284,20 @@ __device__ __forceinline__ void seg_issue(const ReconArgs& A, double* buf, uint6
   d += L * NM;
   bulk_g2s(d, p.f1 + s0 * N, l8 * N, bar);
   d += L * N;
-  bulk_g2s(d, p.Qxx + s0 * NN, l8 * NN, bar);
-  d += L * NN;
-  bulk_g2s(d, p.Qux + s0 * NM, l8 * NM, bar);
-  d += L * NM;
-  bulk_g2s(d, p.Quu + s0 * MM, l8 * MM, bar);
-  d += L * MM;
-  bulk_g2s(d, p.qx1 + s0 * N, l8 * N, bar);
-  d += L * N;
-  bulk_g2s(d, p.qu1 + s0 * M, l8 * M, bar);
-  d += L * M;
-  bulk_g2s(d, A.Kx + s0 * NM, l8 * NM, bar);
-  d += L * NM;
-  bulk_g2s(d, A.Kz + s0 * NM, l8 * NM, bar);   // zeros for the last segment
-  d += L * NM;
-  bulk_g2s(d, A.k1 + s0 * M, l8 * M, bar);
-  d += L * M;
   if (endpoint) bulk_g2s(d, vf + NN, vbytes, bar);   // Vzx0, Vzz0, vx10, vz10
 }
 
 // Row-fused reconstruction for 2n + 2m = 32 (n = 12, m = 4): in each
 // dot-product pass every lane owns one row of a different matrix, e.g. pass 1
 // computes Fx x | Kx x | Qxx x | Qux x on lanes 0-11 | 12-15 | 16-27 | 28-31.
+// Only Fx, Fu, f1 (reused by the backward pass) are bulk-staged for the whole
+// segment; the policy / cost rows a lane owns are register-prefetched one
+// stage ahead from global, which keeps ~17 KB of smem per warp (occupancy).
 template <int N, int M, int LMAX>
 __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
   static_assert(2 * N + 2 * M == 32, "row-fused lane map");
   constexpr int NN = N * N, NM = N * M, MM = M * M;
-  constexpr int BUF = LMAX * (2 * NN + 4 * NM + MM + 2 * N + 2 * M) + 2 * NN + 2 * N;
+  constexpr int BUF = LMAX * (NN + NM + N) + 2 * NN + 2 * N;
   extern __shared__ __align__(16) double sm[];
   const plq_problem_t& p = A.p;
   const int J = p.J, T = p.T;
@@ -340,15 +328,9 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
     const double* FX = buf;
     const double* FU = FX + L * NN;
     const double* F1 = FU + L * NM;
-    const double* QXX = F1 + L * N;
-    const double* QUX = QXX + L * NN;
-    const double* QUU = QUX + L * NM;
-    const double* QX1 = QUU + L * MM;
-    const double* QU1 = QX1 + L * N;
-    const double* KX = QU1 + L * M;
-    const double* KZ = KX + L * NM;
-    const double* K1 = KZ + L * NM;
-    const double* VZX = K1 + L * M;      // endpoint segments only
+    const double* KZ = A.Kz + s0 * NM;   // global (fold)
+    const double* K1 = A.k1 + s0 * M;
+    const double* VZX = F1 + L * N;      // endpoint segments only
     const double* VZZ = VZX + NN;
     const double* VZ1 = VZZ + NN + N;
     if (lane < N) {
@@ -357,10 +339,9 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
       x[lane] = a0;
       z[lane] = last ? 0.0 : A.links[(b * (J - 1) + j) * N + lane];
     }
-    mbar_wait(bar, phase);
-    phase ^= 1u;
     __syncwarp();
-    // fold k = Kz z + k1 for every stage at once (parallel.py:495)
+    // fold k = Kz z + k1 for every stage at once (parallel.py:495), from
+    // global while the bulk copies land
     for (int r = lane; r < L * M; r += 32) {
       const double* kz = KZ + r * N;
       double t = 0.0;
@@ -368,23 +349,51 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
       for (int c = 0; c < N; ++c) t += kz[c] * z[c];
       kv[r] = t + K1[r];
     }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
     __syncwarp();
     double obj = 0.0, worst = 0.0;
     // lane roles of the two forward passes
     const int grp = lane < N ? 0 : (lane < N + M ? 1 : (lane < 2 * N + M ? 2 : 3));
     const int row = grp == 0 ? lane : (grp == 1 ? lane - N : (grp == 2 ? lane - N - M : lane - 2 * N - M));
+    // this lane's pass-1 row (Kx | Qxx | Qux), pass-2 vector (Qux col | Quu
+    // row) and scalar (qx1 | qu1) of a stage, straight from global
+    double pr[N], pq[M], ps = 0.0;
+    auto fetch = [&](int s, double* r, double* v, double& sc) {
+      const int64_t st = s0 + s;
+      if (grp == 1) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) r[c] = A.Kx[st * NM + row * N + c];
+      } else if (grp == 2) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) r[c] = p.Qxx[st * NN + row * N + c];
+#pragma unroll
+        for (int q = 0; q < M; ++q) v[q] = p.Qux[st * NM + q * N + row];
+        sc = p.qx1[st * N + row];
+      } else if (grp == 3) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) r[c] = p.Qux[st * NM + row * N + c];
+#pragma unroll
+        for (int q = 0; q < M; ++q) v[q] = p.Quu[st * MM + row * M + q];
+        sc = p.qu1[st * M + row];
+      }
+    };
+    fetch(0, pr, pq, ps);
 #pragma unroll 1
     for (int s = 0; s < L; ++s) {
       const int64_t st = s0 + s;
+      double nr[N], nq[M], ns = 0.0;
+      if (s + 1 < L) fetch(s + 1, nr, nq, ns);
+      if (grp == 0) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) pr[c] = FX[s * NN + row * N + c];
+      }
       // pass 1: Fx x | Kx x | Qxx x | Qux x
-      const double* r1 = grp == 0 ? FX + s * NN + row * N
-                                  : (grp == 1 ? KX + s * NM + row * N
-                                              : (grp == 2 ? QXX + s * NN + row * N : QUX + s * NM + row * N));
       double t = 0.0, t_ = 0.0;
 #pragma unroll
       for (int c = 0; c < N; c += 2) {
-        t += r1[c] * x[c];
-        t_ += r1[c + 1] * x[c + 1];
+        t += pr[c] * x[c];
+        t_ += pr[c + 1] * x[c + 1];
       }
       t += t_;
       if (grp == 1) {
@@ -403,21 +412,26 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
         xn[row] = (t + t2) + F1[s * N + row];
       } else if (grp == 2) {
 #pragma unroll
-        for (int q = 0; q < M; ++q) t2 += QUX[s * NM + q * N + row] * uu[q];
-        const double xi = x[row], qx = QX1[s * N + row];
+        for (int q = 0; q < M; ++q) t2 += pq[q] * uu[q];
+        const double xi = x[row], qx = ps;
         gh[s * (N + M) + row] = (t + t2) + qx;
         obj += 0.5 * xi * t + qx * xi;
         A.x[(b * (T + 1) + lo + s) * N + row] = xi;
       } else if (grp == 3) {
 #pragma unroll
-        for (int q = 0; q < M; ++q) t2 += QUU[s * MM + row * M + q] * uu[q];
-        const double ui = uu[row], qu = QU1[s * M + row];
+        for (int q = 0; q < M; ++q) t2 += pq[q] * uu[q];
+        const double ui = uu[row], qu = ps;
         gh[s * (N + M) + N + row] = (t + t2) + qu;
         obj += 0.5 * ui * t2 + ui * t + qu * ui;
       }
       __syncwarp();
       if (lane < N) x[lane] = xn[lane];
       __syncwarp();
+#pragma unroll
+      for (int c = 0; c < N; ++c) pr[c] = nr[c];
+#pragma unroll
+      for (int q = 0; q < M; ++q) pq[q] = nq[q];
+      ps = ns;
     }
     // g/h of the link stage feed the boundary kernel
     if (lane < N + M) A.gh[(s0 + L - 1) * (N + M) + lane] = gh[(L - 1) * (N + M) + lane];
@@ -758,7 +772,7 @@ __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
 // element-parallel across the warp (reciprocal pivots kept), only X_i goes to
 // global.  The residual pass streams the blocks again (L2-resident).
 template <int N>
-__global__ void __launch_bounds__(32) link_seq_kernel(plq_problem_t p, const double* vf0, double* links,
+__global__ void __launch_bounds__(32, 12) link_seq_kernel(plq_problem_t p, const double* vf0, double* links,
                                                      double* link_residual, int32_t* status, double* Xs) {
   constexpr int LD = N + 1, NN = N * N, VS = 3 * NN + 2 * N, NS = 3;
   constexpr int NTRI = N * (N + 1) / 2;
@@ -960,12 +974,13 @@ int sms_count() {
 
 template <int N, int M, int LMAX>
 int launch_recon_seg(const ReconArgs& a, cudaStream_t s) {
-  constexpr int BUF = LMAX * (2 * N * N + 4 * N * M + M * M + 2 * N + 2 * M) + 2 * N * N + 2 * N;
+  constexpr int BUF = LMAX * (N * N + N * M + N) + 2 * N * N + 2 * N;
   const size_t smem = sizeof(double) * (BUF + LMAX * (N + M) + LMAX * M + 5 * N + M + 4);
   auto kern = recon_seg_kernel<N, M, LMAX>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
@@ -998,6 +1013,7 @@ int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, doub
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   int per_sm = 0;
