@@ -81,9 +81,46 @@ __device__ __forceinline__ void ggemm_f(AL aload, BL bload, int gw, Epi epi, int
       }
   };
   if constexpr (NWG == 1) {
+    // single warp: every tile accumulated k-outer (one A fragment per band
+    // and one B fragment per column tile per k-step, instead of reloading B
+    // for every band), epilogue after all loads -- in-place safe
+    double acc[TM][TN][2];
 #pragma unroll
     for (int tm = 0; tm < TM; ++tm)
-      if (tm * 8 < rows) band(tm);
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn) acc[tm][tn][0] = acc[tm][tn][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = ks * 4 + q;
+      const bool kok = (K % 4 == 0) || (k < K);
+      double bv[TN];
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn) {
+        const int j = tn * 8 + g;
+        bv[tn] = (((N % 8 == 0) || (j < N)) && kok) ? bload(k, j) : 0.0;
+      }
+#pragma unroll
+      for (int tm = 0; tm < TM; ++tm) {
+        if (tm * 8 >= rows) continue;
+        const int i = tm * 8 + g;
+        const double a = ((i < M) && (i < rows) && kok) ? aload(i, k) : 0.0;
+#pragma unroll
+        for (int tn = 0; tn < TN; ++tn) dmma884(acc[tm][tn][0], acc[tm][tn][1], a, bv[tn]);
+      }
+    }
+#pragma unroll
+    for (int tm = 0; tm < TM; ++tm) {
+      const int i = tm * 8 + g;
+      if (tm * 8 >= rows || !(i < M && i < rows)) continue;
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = tn * 8 + 2 * q + e;
+          if (j < N) epi(i, j, acc[tm][tn][e]);
+        }
+    }
+    (void)band;
   } else {
 #pragma unroll 1
     for (int tm = gw; tm < TM; tm += NWG) {
@@ -100,31 +137,38 @@ template <int M, int N, int K, class AL, class BL, class Epi>
 __device__ __forceinline__ void wgemm_slots(AL aload, BL bload, Epi epi) {
   constexpr int TM = (M + 7) / 8, TN = (N + 7) / 8, KS = (K + 3) / 4;
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int tm = 0; tm < TM; ++tm)
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn) acc[tm][tn][0] = acc[tm][tn][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + q;
+    const bool kok = (K % 4 == 0) || (k < K);
+    double bv[TN];
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn) {
+      const int j = tn * 8 + g;
+      bv[tn] = (((N % 8 == 0) || (j < N)) && kok) ? bload(k, j) : 0.0;
+    }
+#pragma unroll
+    for (int tm = 0; tm < TM; ++tm) {
+      const int i = tm * 8 + g;
+      const double a = ((i < M) && kok) ? aload(i, k) : 0.0;
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn) dmma884(acc[tm][tn][0], acc[tm][tn][1], a, bv[tn]);
+    }
+  }
 #pragma unroll
   for (int tm = 0; tm < TM; ++tm) {
-    double acc[TN][2];
-#pragma unroll
-    for (int tn = 0; tn < TN; ++tn) acc[tn][0] = acc[tn][1] = 0.0;
     const int i = tm * 8 + g;
-    const bool iok = i < M;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int k = ks * 4 + q;
-      const bool kok = (K % 4 == 0) || (k < K);
-      const double a = (iok && kok) ? aload(i, k) : 0.0;
-#pragma unroll
-      for (int tn = 0; tn < TN; ++tn) {
-        const int j = tn * 8 + g;
-        const double b = (((N % 8 == 0) || (j < N)) && kok) ? bload(k, j) : 0.0;
-        dmma884(acc[tn][0], acc[tn][1], a, b);
-      }
-    }
 #pragma unroll
     for (int tn = 0; tn < TN; ++tn)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = tn * 8 + 2 * q + e;
-        if (iok && j < N) epi(i, j, acc[tn][e], (tm * TN + tn) * 2 + e);
+        if (i < M && j < N) epi(i, j, acc[tm][tn][e], (tm * TN + tn) * 2 + e);
       }
   }
 }
