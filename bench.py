@@ -359,11 +359,31 @@ def run_ours(args):
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
+        # the copy roofline of this leg: pinned H2D / D2H bandwidth measured here
+        probe = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+        dprobe = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        bw = {}
+        for name, dst, src in (("h2d", dprobe, probe), ("d2h", probe, dprobe)):
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record()
+            for _ in range(4):
+                dst.copy_(src, non_blocking=True)
+            b_.record()
+            torch.cuda.synchronize()
+            bw[name] = 4 * probe.numel() / (a_.elapsed_time(b_) / 1000.0) / 1e9
+        del probe, dprobe
+        copy_floor = max(hs.h2d_bytes / (bw["h2d"] * 1e9), hs.d2h_bytes / (bw["d2h"] * 1e9))
         e2e = {"value": knots / el, "unit": "knots/s", "h2d_bytes_per_step": int(hs.h2d_bytes) * world,
                "d2h_bytes_per_step": int(hs.d2h_bytes) * world, "ms_per_step": el * 1000.0,
                "ms_per_step_min_mean_max": [1000 * min(per), 1000 * statistics.mean(per), 1000 * max(per)],
                "steps": e_steps, "statistic": "median of per-step host wall clock",
-               "api": "plq_solve_parallel_host (pinned host inputs -> host LqrSolution arrays)"}
+               "api": "plq_solve_parallel_host (pinned host inputs -> host LqrSolution arrays)",
+               "copy_roofline": {"h2d_gbs": bw["h2d"], "d2h_gbs": bw["d2h"],
+                                 "floor_ms": 1000.0 * copy_floor, "frac": copy_floor / el,
+                                 "note": "pinned-copy bandwidth measured in this run; floor = max(H2D, D2H) "
+                                         "time of the step's bytes (the directions overlap)"}}
         del hs, pinned
 
     # ---- smoothing pass (parallel.smooth, §8f row 1) over this solve: device time

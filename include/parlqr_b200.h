@@ -45,6 +45,7 @@ extern "C" {
 #define PLQ_STATUS_OK 0
 #define PLQ_STATUS_DEGENERATE (-1)
 #define PLQ_STATUS_LINK_SINGULAR (-2)
+#define PLQ_STATUS_INFEASIBLE (-3)  /* segment's feasibility rows violated at the solved links */
 
 /* One batch of B independent problems sharing (T, n, m) and one partition.
  * Replaces the (problem, partition, tolerances) arguments of
@@ -89,6 +90,14 @@ typedef struct plq_outputs {
   double* link_mismatch;  /* (B) details.link_mismatch */
   double* link_residual;  /* (B) details.link_residual */
   int32_t* status;        /* (B,J) see PLQ_STATUS_* */
+  /* Degenerate partitions (segments that cannot reach arbitrary endpoints,
+   * parallel.py:320-384, 452-475).  All three NULL: such segments report
+   * PLQ_STATUS_DEGENERATE.  Given: the rows are returned and the links come
+   * from the feasibility-constrained dense KKT solve. */
+  double* feas;           /* (B,J,n,2n+1) details.segment_feasibility rows [Hx | Hz | h1] (an orthonormal
+                             rotation of the reference's rows; row counts in feas_rows) */
+  int32_t* feas_rows;     /* (B,J) */
+  double* feas_residual;  /* (B,J) details.feasibility_residuals */
 } plq_outputs_t;
 
 /* Library identification. */

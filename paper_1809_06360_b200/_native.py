@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libparlqr_b
 PLQ_OK = 0
 PLQ_STATUS_DEGENERATE = -1
 PLQ_STATUS_LINK_SINGULAR = -2
+PLQ_STATUS_INFEASIBLE = -3
 
 # every entry point declared in include/parlqr_b200.h
 EXPORTS = (
@@ -40,7 +41,7 @@ class PlqProblem(ctypes.Structure):
 
 OUTPUT_FIELDS = ("K", "k", "x", "u", "lam", "links", "mu_left", "lambda_right", "vf0",
                  "Kz", "k1", "objective", "kkt_inf", "link_mismatch", "link_residual",
-                 "status")
+                 "status", "feas", "feas_rows", "feas_residual")
 
 
 class PlqOutputs(ctypes.Structure):

@@ -42,6 +42,7 @@ struct Plan {
   size_t smem = 0;
   int grid_max = 0;
   size_t off_Kz = 0, off_k1 = 0, off_gh = 0, off_xend = 0, off_part = 0, off_gs = 0, off_link = 0, off_smap = 0;
+  size_t off_mucorr = 0, off_lfpool = 0;
   size_t total_doubles = 0;
 };
 
@@ -87,6 +88,10 @@ Plan make_plan(const plq_problem_t* p) {
   P.off_link = off;
   off += up2(std::max(plq::link_workspace_doubles(B, p->J, p->n),
                       use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0)));
+  P.off_mucorr = off;
+  off += up2(B * J * n);
+  P.off_lfpool = off;
+  if (J > 1) off += up2(plq::link_feas_pool_doubles(B, p->J, p->n));
   P.off_smap = off;
   if (plq::smooth_segmented(B, p->J)) off += up2(plq::smooth_map_doubles(B, p->T, p->J, p->n, p->m));
   P.total_doubles = off;
@@ -130,6 +135,8 @@ int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
   a.seg_begin = j0;
   a.seg_end = j1;
   a.endpoint_terminal = endpoint_terminal;
+  a.feas = o->feas;
+  a.feas_rows = o->feas_rows;
   const int64_t tasks = p->B * (int64_t)(j1 - j0);
   const int grid = (int)std::min<int64_t>(tasks, c.P.grid_max);
   const int rc = use_small_sweep(p) ? plq::launch_sweep_small(a, c.s) : plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s);
@@ -149,6 +156,22 @@ int phase_link(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c) {
   } else if (plq::launch_link_solve(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s,
                                     &nl)) {
     return cuda_fail("link launch");
+  }
+  if (o->feas && o->feas_rows && o->feas_residual) {
+    // problems with feasibility rows: the constrained dense link solve replaces the links
+    plq::LinkFeasArgs lf{};
+    lf.p = *p;
+    lf.vf0 = o->vf0;
+    lf.feas = o->feas;
+    lf.feas_rows = o->feas_rows;
+    lf.links = o->links;
+    lf.link_residual = o->link_residual;
+    lf.mu_corr = c.ws + c.P.off_mucorr;
+    lf.feas_residual = o->feas_residual;
+    lf.status = o->status;
+    lf.pool = c.ws + c.P.off_lfpool;
+    if (plq::launch_link_feas(lf, c.s)) return cuda_fail("constrained link launch");
+    ++nl;
   }
   g_launches += nl;
   return PLQ_OK;
@@ -173,6 +196,8 @@ plq::ReconArgs recon_args(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c
   a.part = part ? part : c.ws + c.P.off_part;
   a.seg_begin = j0;
   a.seg_end = j1;
+  a.mu_corr = (o->feas && o->feas_rows && o->feas_residual) ? c.ws + c.P.off_mucorr : nullptr;
+  a.feas_rows = o->feas_rows;
   return a;
 }
 
@@ -528,7 +553,7 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
     const double** fields[11] = {&dp.Qxx, &dp.Qux, &dp.Quu, &dp.qx1, &dp.qu1, &dp.Fx,
                                  &dp.Fu, &dp.f1, &dp.QxxT, &dp.qx1T, &dp.x_init};
     for (int i = 1; i < 12; ++i) *fields[i - 1] = reinterpret_cast<const double*>(din[i] + b0 * (in_sz[i] / hp->B));
-    plq_outputs_t o;
+    plq_outputs_t o{};   // feas* null: degenerate partitions report PLQ_STATUS_DEGENERATE here
     double** ofields[15] = {&o.K, &o.k, &o.x, &o.u, &o.lam, &o.links, &o.mu_left, &o.lambda_right,
                             &o.vf0, &o.Kz, &o.k1, &o.objective, &o.kkt_inf, &o.link_mismatch, &o.link_residual};
     for (int i = 0; i < 15; ++i) *ofields[i] = reinterpret_cast<double*>(dout[i] + b0 * (out_sz[i] / hp->B));

@@ -53,7 +53,28 @@ struct SweepArgs {
   // endpoint.py:168-301 as called by solve_endpoint[_affine]): the last
   // segment is an endpoint sweep seeded with the terminal cost.
   int endpoint_terminal;
+  // degenerate partitions: rows left at a segment start are written here
+  // (else the segment reports PLQ_STATUS_DEGENERATE)
+  double* feas;          // (B,J,n,2n+1)
+  int32_t* feas_rows;    // (B,J)
 };
+
+struct LinkFeasArgs {
+  plq_problem_t p;
+  const double* vf0;
+  const double* feas;
+  const int32_t* feas_rows;
+  double* links;
+  double* link_residual;
+  double* mu_corr;       // (B,J,n) Hz' nu per segment
+  double* feas_residual; // (B,J)
+  int32_t* status;
+  double* pool;          // dense KKT scratch when it exceeds shared memory
+  int dmax;
+};
+int link_feas_dmax(int J, int n);
+size_t link_feas_pool_doubles(int64_t B, int J, int n);
+int launch_link_feas(const LinkFeasArgs& a, cudaStream_t s);
 
 // Device-side terminal cost of a swept segment: the problem's terminal cost
 // for the last segment, or -- in the smoothing pass -- TerminalCost(Vxx,
@@ -109,6 +130,8 @@ struct ReconArgs {
   double* xend;          // (B,J,n) rollout end state of each segment
   double* part;          // (B,J,3) objective partial, interior KKT, link-stage KKT
   int seg_begin, seg_end;
+  const double* mu_corr; // (B,J,n) Hz' nu of degenerate segments (parallel.py:511-513), or null
+  const int32_t* feas_rows;  // (B,J): mu_corr is valid where > 0
 };
 
 int launch_sweep(const SweepArgs& a, int grid, int threads, size_t smem, cudaStream_t s);

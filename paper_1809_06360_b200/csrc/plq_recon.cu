@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(NT) recon_kernel(ReconArgs A) {
       gemv_rows(n, n, vf + 2 * nn, s.z, s.t1, nullptr);
       __syncthreads();
       for (int i = tid; i < n; i += nt) {
-        const double mu = -((s.t0[i] + s.t1[i]) + vf[3 * nn + n + i]);
+        const double mu = -((s.t0[i] + s.t1[i]) + vf[3 * nn + n + i]) - (A.mu_corr && A.feas_rows[b * J + j] > 0 ? A.mu_corr[(b * J + j) * n + i] : 0.0);
         A.mu_left[(b * (J - 1) + j) * n + i] = mu;
         s.lam[i] = -mu;
       }

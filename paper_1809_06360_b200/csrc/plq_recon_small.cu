@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(32) recon_small_kernel(ReconArgs A) {
           t0 += vf[NN + lane * N + c] * av[c];
           t1 += vf[2 * NN + lane * N + c] * z[c];
         }
-        const double mu = -((t0 + t1) + vf[3 * NN + N + lane]);
+        const double mu = -((t0 + t1) + vf[3 * NN + N + lane]) - (A.mu_corr && A.feas_rows[b * J + j] > 0 ? A.mu_corr[(b * J + j) * N + lane] : 0.0);
         A.mu_left[(b * (J - 1) + j) * N + lane] = mu;
         lam[lane] = -mu;
       }
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
       const double tz = __shfl_down_sync(0xffffffffu, tv, 16);
       if (lane < N) {
         A.xend[(b * J + j) * N + lane] = x[lane];
-        const double mu = -((tv + tz) + VZ1[lane]);
+        const double mu = -((tv + tz) + VZ1[lane]) - (A.mu_corr && A.feas_rows[b * J + j] > 0 ? A.mu_corr[(b * J + j) * N + lane] : 0.0);
         A.mu_left[(b * (J - 1) + j) * N + lane] = mu;
         lam[lane] = -mu;
       }
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
           t0v += vsrc[tid * N + c] * av[c];
           t1v += vsrc[NN + tid * N + c] * z[c];
         }
-        const double mu = -((t0v + t1v) + vsrc[2 * NN + N + tid]);
+        const double mu = -((t0v + t1v) + vsrc[2 * NN + N + tid]) - (A.mu_corr && A.feas_rows[b * J + j] > 0 ? A.mu_corr[(b * J + j) * N + tid] : 0.0);
         A.mu_left[(b * (J - 1) + j) * N + tid] = mu;
         lam[tid] = -mu;
       }

@@ -405,9 +405,18 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     double* dst = a.vf0 + (b * J + j) * (int64_t)vsz;
     for (int idx = tid; idx < vsz; idx += nt) dst[idx] = bf.V[idx];
   }
+  if (!serial && r > 0 && *sflag == 0 && a.feas) {
+    // feasibility rows [Hx | Hz | h1] left at the segment start (parallel.py:452-456)
+    double* dst = a.feas + (b * J + j) * (int64_t)n * (2 * n + 1);
+    for (int idx = tid; idx < r * (2 * n + 1); idx += nt) {
+      const int i = idx / (2 * n + 1), c = idx % (2 * n + 1);
+      dst[idx] = H[i * ldw + c];
+    }
+  }
   if (tid == 0) {
     int st = *sflag;
-    if (st == 0 && !serial && r > 0) st = PLQ_STATUS_DEGENERATE;   // feasibility rows left
+    if (a.feas_rows) a.feas_rows[b * J + j] = (!serial && st == 0) ? r : 0;
+    if (st == 0 && !serial && r > 0 && !a.feas) st = PLQ_STATUS_DEGENERATE;   // feasibility rows left
     a.status[b * J + j] = st;
   }
   __syncthreads();

@@ -678,8 +678,17 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     }
     for (int i = gt; i < 2 * N; i += NT) dst[3 * NN + i] = sm[S::VX1 + i];
   }
+  if (!SERIAL && r > 0 && status == 0 && a.feas) {
+    // feasibility rows [Hx | Hz | h1] left at the segment start (parallel.py:452-456)
+    double* dst = a.feas + (b * J + j) * (int64_t)N * (2 * N + 1);
+    for (int idx = gt; idx < r * (2 * N + 1); idx += NT) {
+      const int i = idx / (2 * N + 1), c = idx % (2 * N + 1);
+      dst[idx] = H[i * LDW + c];
+    }
+  }
   if (gt == 0) {
-    if (status == 0 && !SERIAL && r > 0) status = PLQ_STATUS_DEGENERATE;
+    if (a.feas_rows) a.feas_rows[b * J + j] = (!SERIAL && status == 0) ? r : 0;
+    if (status == 0 && !SERIAL && r > 0 && !a.feas) status = PLQ_STATUS_DEGENERATE;
     a.status[b * J + j] = status;
   }
   gsync<NWG>(grp);

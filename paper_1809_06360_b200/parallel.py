@@ -22,7 +22,7 @@ import os
 import numpy as np
 
 from . import _native
-from .errors import CholeskyFailure, LinkSingular, UnsupportedPartition
+from .errors import CholeskyFailure, Infeasible, LinkSingular, UnsupportedPartition
 from .problem import DEFAULT_TOLERANCES, AffinePolicy, LqrSolution
 
 __all__ = [
@@ -159,7 +159,7 @@ class BatchSolver:
     the per-segment status to the reference's exceptions."""
 
     def __init__(self, B, T, n, m, J=None, partition=None, tolerances=DEFAULT_TOLERANCES,
-                 device=None, keep_unfolded=False):
+                 device=None, keep_unfolded=False, degenerate=True):
         torch = _torch()
         self.torch = torch
         self.lib = _native.lib()
@@ -194,6 +194,10 @@ class BatchSolver:
                 "link_mismatch": torch.zeros((B,), **dev),
                 "link_residual": torch.zeros((B,), **dev),
                 "status": torch.zeros((B, J), dtype=torch.int32, device=self.device),
+                # degenerate partitions (parallel.py:320-384): rows, counts, residuals
+                "feas": torch.empty((B, J, n, 2 * n + 1), **dev) if degenerate else None,
+                "feas_rows": torch.zeros((B, J), dtype=torch.int32, device=self.device) if degenerate else None,
+                "feas_residual": torch.zeros((B, J), **dev) if degenerate else None,
             }
         self._outs = _native.PlqOutputs(**{f: _ptr(self.out[f]) for f in _native.OUTPUT_FIELDS})
         self._prob = self._problem_struct(None)
@@ -243,7 +247,8 @@ class BatchSolver:
 
     def raise_for_status(self):
         status = self.out["status"].cpu().numpy()
-        raise_for_status(status)
+        fr = self.out.get("feas_residual")
+        raise_for_status(status, None if fr is None else fr.cpu().numpy())
 
     def smooth(self, inputs, stream=None):
         """Launch the smoothing pass (``plq_smooth``) over this solver's last
@@ -272,10 +277,11 @@ class BatchSolver:
         return self.smooth_out
 
 
-def raise_for_status(status):
+def raise_for_status(status, feas_residual=None):
     """Map per-(problem, segment) status codes to the reference exceptions,
     in the order the reference raises them: segment sweeps first, in segment
-    order (pool.map, parallel.py:207), then the link solve."""
+    order (pool.map, parallel.py:207), then the link solve, then the
+    feasibility check at the solved links (parallel.py:462-475)."""
     status = np.atleast_2d(status)
     bad = np.argwhere((status > 0) | (status == _native.PLQ_STATUS_DEGENERATE))
     if bad.size:
@@ -286,6 +292,11 @@ def raise_for_status(status):
         raise UnsupportedPartition(j)
     if np.any(status == _native.PLQ_STATUS_LINK_SINGULAR):
         raise LinkSingular("singular pivot block in the link system")
+    inf = np.argwhere(status == _native.PLQ_STATUS_INFEASIBLE)
+    if inf.size:
+        b, j = (int(v) for v in inf[np.lexsort((inf[:, 1], inf[:, 0]))][0])
+        res = float(np.atleast_2d(feas_residual)[b, j]) if feas_residual is not None else float("nan")
+        raise Infeasible(res, segment=j)
 
 
 def _to_device(arrays, device, torch):
@@ -356,8 +367,19 @@ def solve_parallel(problem, J, workers=None, tolerances=DEFAULT_TOLERANCES, coll
         else:
             values.append((Vxx, row[nn:2 * nn].reshape(n, n), row[2 * nn:3 * nn].reshape(n, n),
                            vx1, row[3 * nn + n:3 * nn + 2 * n]))
-    empty = (np.zeros((0, n)), np.zeros((0, n)), np.zeros(0))
     links = o["links"][:Jp - 1]
+    # feasibility triples of the endpoint segments (rows in the GPU's
+    # orthonormal basis; parallel.py:398-401) and their residuals (:462-475)
+    rows = o["feas_rows"] if o.get("feas_rows") is not None else np.zeros(Jp, dtype=np.int32)
+    feas = []
+    for j in range(Jp):
+        if j == Jp - 1:
+            feas.append(None)
+            continue
+        r = int(rows[j])
+        F = o["feas"][j][:r] if r else np.zeros((0, 2 * n + 1))
+        feas.append((F[:, :n].copy(), F[:, n:2 * n].copy(), F[:, 2 * n].copy()))
+    fres = o.get("feas_residual")
     details = ParallelDetails(
         partition=partition,
         link_points=links,
@@ -366,9 +388,10 @@ def solve_parallel(problem, J, workers=None, tolerances=DEFAULT_TOLERANCES, coll
         lambda_right=o["lambda_right"][:Jp - 1],
         link_mismatch=float(o["link_mismatch"]) if Jp > 1 else 0.0,
         segment_values0=tuple(values),
-        segment_feasibility=tuple(empty if j < Jp - 1 else None for j in range(Jp)),
-        feasibility_residuals=tuple(0.0 for _ in range(Jp)),
-        degenerate=False,
+        segment_feasibility=tuple(feas),
+        feasibility_residuals=tuple(float(fres[j]) if fres is not None and int(rows[j]) else 0.0
+                                    for j in range(Jp)),
+        degenerate=bool(np.any(rows[:Jp - 1] > 0)),
         segment_diagnostics=tuple(None for _ in range(Jp)),
     )
     return LqrSolution(

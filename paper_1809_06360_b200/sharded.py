@@ -182,7 +182,7 @@ def sharded_solve_device(inputs, J=None, partition=None, dist=None, group=None, 
     B, T, n = (int(s) for s in inputs["qx1"].shape)
     m = int(inputs["qu1"].shape[2])
     solver = BatchSolver(B, T, n, m, J=J, partition=partition, device=device,
-                         tolerances=tolerances or DEFAULT_TOLERANCES)
+                         tolerances=tolerances or DEFAULT_TOLERANCES, degenerate=False)
     backend = DeviceBackend(solver, inputs)
     res = solve_sharded(backend, dist, group)
     return solver, res

@@ -77,6 +77,11 @@ def ref_solve(a, J, splits=None):
         "splits": np.array(d.partition.split_times),
     }
     if d.degenerate:
+        # feasibility-constrained link solve (parallel.py:320-384): links and
+        # multipliers; the rows themselves are basis-dependent (not stored)
+        out.update({"links": d.link_points, "mu_left": d.mu_left, "lambda_right": d.lambda_right,
+                    "link_mismatch": np.float64(d.link_mismatch),
+                    "feas_rows": np.array([0 if f is None else f[0].shape[0] for f in d.segment_feasibility])})
         return out
     out.update({
         "links": d.link_points, "mu_left": d.mu_left, "lambda_right": d.lambda_right,

@@ -40,7 +40,7 @@ def test_abi_version_and_struct_layout():
     assert lib.plq_abi_version() == 1
     # plq_problem_t: int64 + 5 int32 + 4 pad + 12 pointers + 2 doubles
     assert ctypes.sizeof(_native.PlqProblem) == 8 + 20 + 4 + 12 * 8 + 16
-    assert ctypes.sizeof(_native.PlqOutputs) == 16 * 8
+    assert ctypes.sizeof(_native.PlqOutputs) == 19 * 8
 
 
 def test_argument_errors_without_gpu():

@@ -60,20 +60,28 @@ def _check(g, i, ref, floors, K_gate=K_TOL):
 
 @pytest.mark.parametrize("name", ["hand_scalar", "small_random", "random_splits"])
 def test_reference_goldens_small(name):
-    from paper_1809_06360_b200 import UnsupportedPartition
-    checked = 0
+    checked = degenerate = 0
     for a, o, J in load_stored(name):
         splits = tuple(int(s) for s in o["splits"])
         batch = {k: v[None] for k, v in a.items()}
         if bool(o["degenerate"]):
-            with pytest.raises(UnsupportedPartition):
-                _gpu_batch(batch, splits=splits)
+            # feasibility-constrained link solve (parallel.py:320-384)
+            g, _ = _gpu_batch(batch, splits=splits)
+            assert np.array_equal(g["feas_rows"][0][:len(splits) - 2], o["feas_rows"][:-1])
+            sc = 1.0 + max(float(np.abs(v).max()) for v in a.values())
+            for key, rk in (("x", "states"), ("u", "controls"), ("lam", "lambdas"), ("K", "K"), ("k", "k")):
+                assert rel_err(g[key][0], o[rk]) <= 1e-8 * sc, (key, rel_err(g[key][0], o[rk]))
+            assert rel_err(g["links"][0][:len(splits) - 2], o["links"]) <= 1e-8 * sc
+            assert abs(g["objective"][0] - o["objective"]) <= 1e-9 * sc * (1 + abs(o["objective"]))
+            degenerate += 1
             continue
         g, _ = _gpu_batch(batch, splits=splits)
         floors = _floor(a, None, O.solve(a, splits=splits), splits=splits)
         _check(g, 0, o, floors)
         checked += 1
     assert checked >= 1
+    if name != "hand_scalar":
+        assert degenerate >= 1
 
 
 @pytest.fixture(params=["specialized", "generic"])
