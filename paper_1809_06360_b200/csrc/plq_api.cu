@@ -21,7 +21,14 @@ bool force_generic() {
 }
 bool use_small_sweep(const plq_problem_t* p) { return !force_generic() && plq::sweep_small_supported(p->n, p->m); }
 bool use_small_recon(const plq_problem_t* p) { return !force_generic() && plq::recon_small_supported(p->n, p->m); }
-bool use_seq_link(const plq_problem_t* p) { return !force_generic() && plq::link_seq_supported(p->n, p->J); }
+// PLQ_LINK=bcr forces block cyclic reduction for the link solve (measurement)
+bool force_bcr() {
+  const char* e = getenv("PLQ_LINK");
+  return e && e[0] == 'b';
+}
+bool use_seq_link(const plq_problem_t* p) {
+  return !force_generic() && !force_bcr() && plq::link_seq_supported(p->n, p->J);
+}
 
 int fail(int code, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);

@@ -1,0 +1,12 @@
+# Round-end evidence refresh (run on the GPU box via gpurun).
+set -u
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/refresh
+for c in 1 0 2 3 4; do
+  timeout 900 python bench.py --config $c > gpurun_out/refresh/bench_cfg$c.json 2> gpurun_out/refresh/bench_cfg$c.err
+done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/refresh/reference_arm_default.json 2> gpurun_out/refresh/reference_arm_default.err
+timeout 300 python bench.py > gpurun_out/refresh/bench_default.json 2> gpurun_out/refresh/bench_default.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/refresh/launches_default.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_launch.log 2>&1
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:sweep_small_kernel -c 1 --csv --log-file gpurun_out/refresh/sweep_traffic_cfg1.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_traffic.log 2>&1
+ls gpurun_out/refresh
