@@ -10,3 +10,7 @@ timeout 300 python bench.py > gpurun_out/refresh/bench_default.json 2> gpurun_ou
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/refresh/launches_default.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_launch.log 2>&1
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:sweep_small_kernel -c 1 --csv --log-file gpurun_out/refresh/sweep_traffic_cfg1.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_traffic.log 2>&1
 ls gpurun_out/refresh
+# full ncu captures of the three cfg1 kernels (one launch each)
+for k in sweep_small_kernel link_seq_kernel recon_seg_kernel; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o gpurun_out/refresh/cfg1_$k -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_full_$k.log 2>&1 || true
+done
