@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-smooth", action="store_true")
     ap.add_argument("--no-endpoint", action="store_true")
+    ap.add_argument("--graph", type=int, default=1, help="replay the solve as one CUDA graph (1) or launch eagerly (0)")
     return ap.parse_args()
 
 
@@ -249,6 +250,14 @@ def run_ours(args):
 
         def one_step():
             solve_sharded(backend, dist)
+    elif args.graph:
+        # the whole solve captured once into a CUDA graph, replayed per step
+        graph = solver.capture(inputs)
+        launches_per_graph = solver.launches
+
+        def one_step():
+            graph.replay()
+            solver.launches = launches_per_graph
     else:
         def one_step():
             solver.run(inputs)
@@ -458,7 +467,8 @@ def run_ours(args):
             "config": {"workload": cfg.name, "B": cfg.B, "n": cfg.n, "m": cfg.m, "T": cfg.T, "J": cfg.J,
                        "global_batch": cfg.B,
                        "parallelism": (f"batch-shard x{world}" if cfg.B > 1 else f"segment-shard x{world}"),
-                       "l2": "inputs exceed L2" if flush is None else "L2 flushed between steps"},
+                       "l2": "inputs exceed L2" if flush is None else "L2 flushed between steps",
+                       "launch": "CUDA graph replay" if (args.graph and not sharded) else "eager"},
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "sweep_kernel (K1, DMMA.8x8x4 fp64)",
                          "achieved": achieved, "peak": peak_f64, "unit": "TFLOP/s",

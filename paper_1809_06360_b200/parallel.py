@@ -245,6 +245,22 @@ class BatchSolver:
         _native.check(rc, "plq_solve_parallel")
         self.launches = int(self.lib.plq_last_launch_count())
 
+    def capture(self, inputs, stream=None):
+        """Capture ``run(inputs)`` into a CUDA graph (the launches are
+        stream-ordered and allocation-free, so the whole solve replays as one
+        graph launch).  Returns the ``torch.cuda.CUDAGraph``; ``replay()``
+        re-solves whatever the captured input tensors hold."""
+        torch = self.torch
+        with torch.cuda.device(self.device):
+            self.run(inputs)                     # warm: one-time kernel attributes
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(self.device) if stream is None else stream
+            with torch.cuda.graph(g, stream=s):
+                self.run(inputs, stream=s)
+            self._graph_inputs = inputs          # keep the captured buffers alive
+        return g
+
     def raise_for_status(self):
         status = self.out["status"].cpu().numpy()
         fr = self.out.get("feas_residual")
