@@ -858,23 +858,34 @@ __global__ void __launch_bounds__(32, 12) link_seq_kernel(plq_problem_t p, const
         }
         __syncwarp();
       }
-      // Cholesky of P, element-parallel trailing updates; reciprocal pivots in idg
+      // Cholesky of P with unscaled pivot columns (one reciprocal and one
+      // barrier per column, P_rc -= P_rk P_ck / P_kk), element-parallel
+      // trailing updates; the columns are scaled by 1/sqrt(pivot) in one
+      // pass at the end.  Reciprocal pivots in idg.
       for (int k = 0; k < N; ++k) {
         const double dkk = Pm[k * LD + k];
         bad |= !(dkk > 0.0);
-        const double d = sqrt(dkk > 0.0 ? dkk : 1.0);
-        const double inv = 1.0 / d;
-        __syncwarp();
-        if (lane == k) {
-          Pm[k * LD + k] = d;
-          idg[k] = inv;
-        }
-        if (lane > k && lane < N) Pm[lane * LD + k] *= inv;
-        __syncwarp();
+        const double rk = 1.0 / (dkk > 0.0 ? dkk : 1.0);
         const int s = N - 1 - k;   // trailing triangle (rows/cols k+1..N-1)
         for (int e = lane; e < s * (s + 1) / 2; e += 32) {
           const int r = k + 1 + tri[2 * e], c = k + 1 + tri[2 * e + 1];
-          Pm[r * LD + c] -= Pm[r * LD + k] * Pm[c * LD + k];
+          Pm[r * LD + c] -= (Pm[r * LD + k] * rk) * Pm[c * LD + k];
+        }
+        __syncwarp();
+      }
+      {
+        // off-diagonal entries first (they read the unscaled pivots), then the diagonal
+        for (int e = lane; e < N * (N - 1) / 2; e += 32) {
+          const int r = 1 + tri[2 * e], c = tri[2 * e + 1];   // strict lower triangle
+          const double pk = Pm[c * LD + c];
+          Pm[r * LD + c] *= rsqrt(pk > 0.0 ? pk : 1.0);
+        }
+        __syncwarp();
+        if (lane < N) {
+          const double pk = Pm[lane * LD + lane];
+          const double ir = rsqrt(pk > 0.0 ? pk : 1.0);
+          Pm[lane * LD + lane] = pk * ir;
+          idg[lane] = ir;
         }
         __syncwarp();
       }
