@@ -179,10 +179,21 @@ __device__ __forceinline__ void gqr(double* A, int r, double* X, double* tau, do
 // dot products instead of M sequential reflector sweeps.  R (upper) and V
 // (strictly lower, unit diagonal implicit) are written back LAPACK-style to
 // A; rdiag gets diag(R).
-template <int M, int W, int LDA, int LDX>
+template <int M, int W, int LDA, int LDX, int RMAX>
 __device__ __forceinline__ void warp_qr_wy(double* A, int r, double* X, double* Tm, double* rdiag) {
   const int lane = threadIdx.x & 31;
   const bool row = lane < r;
+  // rows live in lanes < r <= RMAX: for RMAX <= 16 a half-warp butterfly is
+  // the full sum for lanes 0-15 (lanes 16-31 hold zeros, never use it)
+  auto warp_sum = [&](double x) {
+    if constexpr (RMAX <= 16) {
+#pragma unroll
+      for (int o = 8; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      return x;
+    } else {
+      return plq::warp_sum(x);
+    }
+  };
   double a[M], v[M], tau[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) a[k] = row ? A[lane * LDA + k] : 0.0;
@@ -550,7 +561,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       for (int i = gt; i < r; i += NT) H[i * LDW + CC] += NTb[i * LDF + N + M];
       gsync<NWG>(grp);
       if constexpr (NWG == 1) {
-        warp_qr_wy<M, W, LDF, LDW>(NTb + N, r, H, tau, rdiag);   // tau slot holds T (M*M)
+        warp_qr_wy<M, W, LDF, LDW, N>(NTb + N, r, H, tau, rdiag);   // tau slot holds T (M*M)
       } else {
         gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
