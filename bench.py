@@ -397,7 +397,9 @@ def run_ours(args):
 
     # ---- smoothing pass (parallel.smooth, §8f row 1) over this solve: device time
     smooth = None
-    if not sharded and not args.no_smooth and cfg.J > 1:
+    # (single-GPU runs only: the whole-job throughput of N ranks would need a
+    # max-over-ranks time for these legs as well)
+    if world == 1 and not args.no_smooth and cfg.J > 1:
         solver.run(inputs)
         solver.smooth(inputs)
         torch.cuda.synchronize()
@@ -422,7 +424,7 @@ def run_ours(args):
 
     # ---- two-point-boundary solve (§8f row 3) on the config's problems
     endpoint = None
-    if not sharded and not args.no_endpoint and cfg.T <= 1024 and cfg.n <= 64:
+    if world == 1 and not args.no_endpoint and cfg.T <= 1024 and cfg.n <= 64:
         from paper_1809_06360_b200 import EndpointBatch
         eb = EndpointBatch(B_loc, cfg.T, cfg.n, cfg.m, device=dev)
         zs = torch.from_numpy(np.random.default_rng(args.seed).standard_normal((B_loc, cfg.n))).to(dev)
