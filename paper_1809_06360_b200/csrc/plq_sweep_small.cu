@@ -548,18 +548,21 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       gsync<NWG>(grp);
       const double fu2 = gsum<NWG>(pu, red, grp, gw);
       const double nu_scale = sqrt(hx2) * sqrt(fu2);
-      // N = Hx F -> VF rows 0..r-1
+      // N = Hx F, stacked in place: [Nx | Hz | Hx f1 + h1] into H, Nu into
+      // NTb (every band's loads precede its stores; bands own their rows)
       ggemm_f<N, FW, N, NWG>(
           [&](int i, int k) { return H[i * LDW + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
-          [&](int i, int c, double acc) { NTb[i * LDF + c] = acc; }, r);
+          [&](int i, int c, double acc) {
+            if (c < N)
+              H[i * LDW + c] = acc;
+            else if (c < N + M)
+              NTb[i * LDF + c] = acc;
+            else
+              H[i * LDW + CC] += acc;
+          },
+          r);
       gsync<NWG>(grp);
       if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
-      for (int idx = gt; idx < r * N; idx += NT) {
-        const int i = idx / N, c = idx % N;
-        H[i * LDW + c] = NTb[i * LDF + c];
-      }
-      for (int i = gt; i < r; i += NT) H[i * LDW + CC] += NTb[i * LDF + N + M];
-      gsync<NWG>(grp);
       if constexpr (NWG == 1) {
         warp_qr_wy<M, W, LDF, LDW, N>(NTb + N, r, H, tau, rdiag);   // tau slot holds T (M*M)
       } else {
