@@ -1061,7 +1061,7 @@ int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
     return -1;
   }
   if (a.p.n == 32 && a.p.m == 8) {
-    if (a.p.max_seg_len <= 512) return launch_recon_ring<32, 8, 128, 3>(a, s);
+    if (a.p.max_seg_len <= 512) return launch_recon_ring<32, 8, 128, 2>(a, s);  // 2 slots: 2 CTAs per SM
     return -1;
   }
   if (a.p.n == 12 && a.p.m == 4) {
