@@ -468,7 +468,9 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
                                                      3 * (size_t)p.n * p.n + p.n)
                                  : (threads == 256 ? sizeof(double) * TileCfg<8>::DOUBLES : 0);
     if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-    link_eliminate<<<B * P.lv[l].E, threads, tsm, s>>>(p, P.lv[l], status);
+    // the elimination is the level's critical path: 8 warps from n = 17 up
+    const int ethreads = p.n <= 16 ? threads : 256;
+    link_eliminate<<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], status);
     ++nl;
     if (!P.lv[l].top) {
       link_assemble_next<<<B * P.lv[l + 1].K, threads, 0, s>>>(p, P.lv[l], P.lv[l + 1]);
