@@ -192,14 +192,15 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
   const int64_t b = blockIdx.x / E;
   const int o = blockIdx.x % E;
   const int i = L.top ? 0 : 2 * o + 1;
-  const bool sm = n <= 64;
-  const int ldl = sm ? n + 1 : n;
+  const bool sm = n <= 64;     // factor and right-hand sides on chip
+  const bool lsm = n <= 128;   // the factor on chip (n <= 128: 132 KB), W in L2
+  const int ldl = lsm ? n + 1 : n;
   const int ldw = sm ? ((w + 3) / 8) * 8 + 4 : w;
   double* gLc = L.Lc + (b * E + o) * nn;
   double* gWm = L.Wm + (b * E + o) * n * w;
-  double* Lc = sm ? dsm : gLc;
+  double* Lc = lsm ? dsm : gLc;
   double* Wm = sm ? dsm + n * ldl : gWm;
-  double* tiles = sm ? nullptr : dsm;
+  double* tiles = sm ? nullptr : dsm + (lsm ? ((n * ldl + 1) & ~1) : 0);
   const double* D = L.D + (b * K + i) * nn;
   const bool has_l = i >= 1, has_r = i + 1 < K;
   const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;   // A(i,i-1)
@@ -255,10 +256,10 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
     cta_trsm_lower_blocked(Lc, n, ldl, Wm, w, ldw);
   else
     cta_trsm_lower(Lc, n, ldl, Wm, w, ldw);
-  if (sm) {
+  if (lsm)
     for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) gLc[idx] = Lc[(idx / n) * ldl + idx % n];
+  if (sm)
     for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) gWm[idx] = Wm[(idx / w) * ldw + idx % w];
-  }
   if (L.top) return;
   double* CL = L.CL + (b * E + o) * nn;
   double* CR = L.CR + (b * E + o) * nn;
@@ -466,7 +467,8 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
     const int w = 2 * p.n + 1, ldw = ((w + 3) / 8) * 8 + 4;
     const size_t tsm = p.n <= 64 ? sizeof(double) * ((size_t)p.n * (p.n + 1) + (size_t)p.n * ldw + 2 +
                                                      3 * (size_t)p.n * p.n + p.n)
-                                 : (threads == 256 ? sizeof(double) * TileCfg<8>::DOUBLES : 0);
+                                 : sizeof(double) * ((p.n <= 128 ? (((size_t)p.n * (p.n + 1) + 1) & ~size_t(1)) : 0) +
+                                                     (threads == 256 ? TileCfg<8>::DOUBLES : 0));
     if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     // the elimination is the level's critical path: 8 warps from n = 17 up
     const int ethreads = p.n <= 16 ? threads : 256;
