@@ -49,7 +49,7 @@ struct Plan {
   size_t smem = 0;
   int grid_max = 0;
   size_t off_Kz = 0, off_k1 = 0, off_gh = 0, off_xend = 0, off_part = 0, off_gs = 0, off_link = 0, off_smap = 0;
-  size_t off_mucorr = 0, off_lfpool = 0;
+  size_t off_mucorr = 0, off_lfpool = 0, off_ctr = 0;
   size_t total_doubles = 0;
 };
 
@@ -95,6 +95,8 @@ Plan make_plan(const plq_problem_t* p) {
   P.off_link = off;
   off += up2(std::max(plq::link_workspace_doubles(B, p->J, p->n),
                       use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0)));
+  P.off_ctr = off;
+  off += 2;
   P.off_mucorr = off;
   off += up2(B * J * n);
   P.off_lfpool = off;
@@ -138,6 +140,7 @@ int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
   a.vf0 = o->vf0;
   a.status = o->status;
   a.gscratch = c.ws + c.P.off_gs;
+  a.task_ctr = reinterpret_cast<unsigned long long*>(c.ws + c.P.off_ctr);
   a.lay = c.P.lay;
   a.seg_begin = j0;
   a.seg_end = j1;
@@ -297,6 +300,7 @@ int plq_smooth(const plq_problem_t* problem, const plq_outputs_t* parent, const 
     a.vf0 = nullptr;
     a.status = out->status;
     a.gscratch = c.ws + c.P.off_gs;
+    a.task_ctr = reinterpret_cast<unsigned long long*>(c.ws + c.P.off_ctr);
     a.lay = c.P.lay;
     a.seg_begin = 0;
     a.seg_end = J - 1;

@@ -9,6 +9,18 @@
 
 namespace plq {
 
+// One-time per-device setup guard: kernel attributes (dynamic shared memory
+// opt-in, carveout) are per device, so a process driving several GPUs must
+// set them on each.  `mask` is a function-local static bitmask.
+inline bool first_on_device(unsigned* mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = 1u << (dev & 31);
+  if (*mask & bit) return false;
+  *mask |= bit;
+  return true;
+}
+
 // Per-CTA scratch buffers of the segment sweep.  Each one is placed in
 // shared memory or in a per-CTA slice of global scratch by plan_sweep().
 enum SweepBuf {
@@ -57,6 +69,9 @@ struct SweepArgs {
   // (else the segment reports PLQ_STATUS_DEGENERATE)
   double* feas;          // (B,J,n,2n+1)
   int32_t* feas_rows;    // (B,J)
+  // dynamic task queue of the specialized sweep (reset by the launcher);
+  // null: static round-robin
+  unsigned long long* task_ctr;
 };
 
 struct LinkFeasArgs {

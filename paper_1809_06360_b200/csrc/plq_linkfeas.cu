@@ -263,11 +263,9 @@ size_t link_feas_pool_doubles(int64_t B, int J, int n) {
 int launch_link_feas(const LinkFeasArgs& args, cudaStream_t s) {
   LinkFeasArgs a = args;
   a.dmax = link_feas_dmax(a.p.J, a.p.n);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned attr = 0;
+  if (first_on_device(&attr))
     cudaFuncSetAttribute(link_feas_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LF_SMEM);
-    attr = true;
-  }
   const int64_t chunks = (a.p.B + LF_NT - 1) / LF_NT;
   const int grid = (int)(chunks < 32 ? chunks : 32);
   link_feas_kernel<<<grid, LF_NT, LF_SMEM, s>>>(a);

@@ -988,11 +988,10 @@ int launch_recon_seg(const ReconArgs& a, cudaStream_t s) {
   constexpr int BUF = LMAX * (N * N + N * M + N) + 2 * N * N + 2 * N;
   const size_t smem = sizeof(double) * (BUF + LMAX * (N + M) + LMAX * M + 5 * N + M + 4);
   auto kern = recon_seg_kernel<N, M, LMAX>;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned attr = 0;
+  if (first_on_device(&attr)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr = true;
   }
   const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
   const int per_sm = (int)((227 * 1024) / (smem + 1024));
@@ -1021,11 +1020,10 @@ int launch_link_t(const plq_problem_t& p, const double* vf0, double* links, doub
   const size_t smem = sizeof(double) * (3 * (size_t)(3 * N * N + 2 * N) + 3 * N * (N + 1) + K * N + N +
                                         (N * (N + 1) + 7) / 8 + 1 + 4);
   auto kern = link_seq_kernel<N>;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned attr = 0;
+  if (first_on_device(&attr)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr = true;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem);

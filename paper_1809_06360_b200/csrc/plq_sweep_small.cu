@@ -721,18 +721,29 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS, (NWG == 1 ? 16 : 1)) sweep_
     const int i = p / N, c = p % N;
     if (i < c) pairs[i * (2 * N - i - 1) / 2 + (c - i - 1)] = (unsigned short)((i << 8) | c);
   }
+  __shared__ long long next_task[GROUPS];
   if (gt == 0) mbar_init(bar, 1);
   __syncthreads();
   uint32_t phase = 0;
   const int nloc = a.seg_end - a.seg_begin;
   const int64_t total = a.p.B * nloc;
-  for (int64_t task = (int64_t)blockIdx.x * GROUPS + grp; task < total; task += (int64_t)gridDim.x * GROUPS) {
+  const int64_t first_free = (int64_t)gridDim.x * GROUPS;
+  // first task static, the rest from a dynamic queue: segments differ in
+  // cost (tail stages, serial last segment), so the tail of the launch
+  // balances instead of following a fixed stride
+  int64_t task = (int64_t)blockIdx.x * GROUPS + grp;
+  while (task < total) {
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
     if ((j == a.p.J - 1 && !a.endpoint_terminal) || a.smooth_vf0)
       small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j, phase, pairs);
     else
       small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j, phase, pairs);
+    if (gt == 0)
+      next_task[grp] = a.task_ctr ? first_free + (long long)atomicAdd(a.task_ctr, 1ULL) : task + first_free;
+    gsync<NWG>(grp);
+    task = next_task[grp];
+    gsync<NWG>(grp);
   }
 }
 
@@ -741,7 +752,8 @@ int launch_small(const SweepArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(double) * SL<N, M>::TOTAL * GROUPS;
   auto kern = sweep_small_kernel<N, M, NWG, GROUPS>;
   static int per_sm = -1, sms = 148;
-  if (per_sm < 0) {
+  static unsigned attr = 0;
+  if (first_on_device(&attr)) {
     int dev = 0;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWG * 32 * GROUPS, smem);
@@ -749,10 +761,15 @@ int launch_small(const SweepArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
+  SweepArgs args = a;
+  // dynamic queue for the multi-warp groups (long tasks); the single-warp
+  // n = 12 tasks are short enough that the queue round trip costs more
+  if (NWG == 1) args.task_ctr = nullptr;
+  if (args.task_ctr && cudaMemsetAsync(args.task_ctr, 0, sizeof(unsigned long long), s) != cudaSuccess) return -1;
   const int64_t blocks_needed = (tasks + GROUPS - 1) / GROUPS;
   const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   const int grid = (int)(blocks_needed < cap ? blocks_needed : cap);
-  kern<<<grid, NWG * 32 * GROUPS, smem, s>>>(a);
+  kern<<<grid, NWG * 32 * GROUPS, smem, s>>>(args);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
