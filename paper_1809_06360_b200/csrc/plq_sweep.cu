@@ -262,28 +262,8 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     __syncthreads();
 
     // ---- gains
-    if (r == 0) {
-      // unconstrained stage: G = -Muu^{-1} P (endpoint.py:239-250 with p = 0;
-      // serial.py:63-70)
-      for (int idx = tid; idx < m * m; idx += nt) Lm[idx] = Muu[idx];
-      for (int idx = tid; idx < m * W; idx += nt) {
-        const int u = idx / W, c = idx % W;
-        G[u * ldw + c] = P[u * ldw + c];
-      }
-      if (tid == 0) *iflag = 0;
-      __syncthreads();
-      if (!cta_cholesky(Lm, m, m, iflag)) {
-        if (tid == 0) *sflag = 1 + s;
-        __syncthreads();
-        break;
-      }
-      cho_solve_x(Lm, m, m, G, W, ldw);
-      for (int idx = tid; idx < m * W; idx += nt) {
-        const int u = idx / W, c = idx % W;
-        G[u * ldw + c] = -G[u * ldw + c];
-      }
-      __syncthreads();
-    } else {
+    bool chol = (r == 0);
+    if (r != 0) {
       // constrained tail stage (endpoint.py:219-238, 251-252, 267-281)
       double part_h = 0.0, part_u = 0.0;
       for (int idx = tid; idx < r * n; idx += nt) {
@@ -314,41 +294,72 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           rmax = fmax(rmax, fabs(rdiag[i]));
           rmin = fmin(rmin, fabs(rdiag[i]));
         }
-        if (!(rmin > p.rank_tol * fmax(nu_scale, rmax))) {
+        const double thr = p.rank_tol * fmax(nu_scale, rmax);
+        if (rmax <= thr) {
+          // p = 0 (Nu numerically zero, e.g. a segment without control
+          // authority): the reflectors are the identity, all r rows stay
+          // and the gains are the null-space solve with Zw = I
+          // (endpoint.py:239-250)
+          chol = true;
+        } else if (!(rmin > thr)) {
+          // 0 < p < m: rank-revealing branch not built
           if (tid == 0) *sflag = PLQ_STATUS_DEGENERATE;
           __syncthreads();
           break;
-        }
-        // G = -R^{-1} (Q1' stack): back substitution, thread per column
-        for (int c = tid; c < W; c += nt) {
-          for (int i = m - 1; i >= 0; --i) {
-            double v = H[i * ldw + c];
-            for (int k = i + 1; k < m; ++k) v -= VF[i * Fw + n + k] * G[k * ldw + c];
-            G[i * ldw + c] = v / rdiag[i];
-          }
-        }
-        __syncthreads();
-        for (int idx = tid; idx < m * W; idx += nt) {
-          const int u = idx / W, c = idx % W;
-          G[u * ldw + c] = -G[u * ldw + c];
-        }
-        // surviving rows Q2' stack: shift rows m..r-1 up by m, one block of
-        // m rows at a time so sources and destinations never overlap
-        for (int blk = 0; blk < r - m; blk += m) {
-          const int rows = min(m, r - m - blk);
-          for (int idx = tid; idx < rows * W; idx += nt) {
-            const int i = blk + idx / W, c = idx % W;
-            H[i * ldw + c] = H[(i + m) * ldw + c];
+        } else {
+          // G = -R^{-1} (Q1' stack): back substitution, thread per column
+          for (int c = tid; c < W; c += nt) {
+            for (int i = m - 1; i >= 0; --i) {
+              double v = H[i * ldw + c];
+              for (int k = i + 1; k < m; ++k) v -= VF[i * Fw + n + k] * G[k * ldw + c];
+              G[i * ldw + c] = v / rdiag[i];
+            }
           }
           __syncthreads();
+          for (int idx = tid; idx < m * W; idx += nt) {
+            const int u = idx / W, c = idx % W;
+            G[u * ldw + c] = -G[u * ldw + c];
+          }
+          // surviving rows Q2' stack: shift rows m..r-1 up by m, one block of
+          // m rows at a time so sources and destinations never overlap
+          for (int blk = 0; blk < r - m; blk += m) {
+            const int rows = min(m, r - m - blk);
+            for (int idx = tid; idx < rows * W; idx += nt) {
+              const int i = blk + idx / W, c = idx % W;
+              H[i * ldw + c] = H[(i + m) * ldw + c];
+            }
+            __syncthreads();
+          }
+          r -= m;
+          __syncthreads();
         }
-        r -= m;
-        __syncthreads();
       } else {
         wide_branch(p, n, m, r, W, ldw, Fw, VF, H, P, G, Muu, bf.WIDE, tau, rdiag, red, iflag, nu_scale, sflag, s);
         if (*sflag) break;
         r = 0;
       }
+    }
+    if (chol) {
+      // G = -Muu^{-1} P: unconstrained stage, or p = 0 in a constrained one
+      // (endpoint.py:239-250 with Zw = I; serial.py:63-70)
+      for (int idx = tid; idx < m * m; idx += nt) Lm[idx] = Muu[idx];
+      for (int idx = tid; idx < m * W; idx += nt) {
+        const int u = idx / W, c = idx % W;
+        G[u * ldw + c] = P[u * ldw + c];
+      }
+      if (tid == 0) *iflag = 0;
+      __syncthreads();
+      if (!cta_cholesky(Lm, m, m, iflag)) {
+        if (tid == 0) *sflag = 1 + s;
+        __syncthreads();
+        break;
+      }
+      cho_solve_x(Lm, m, m, G, W, ldw);
+      for (int idx = tid; idx < m * W; idx += nt) {
+        const int u = idx / W, c = idx % W;
+        G[u * ldw + c] = -G[u * ldw + c];
+      }
+      __syncthreads();
     }
 
     // ---- policy outputs (parallel.py:224-236 stacking)

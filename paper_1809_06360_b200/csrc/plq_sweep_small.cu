@@ -465,9 +465,98 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     gsync<NWG>(grp);
 
     const bool constrained = (r != 0);
-    if (r == 0) {
-      // ---- unconstrained stage: G = -Muu^{-1} P, Cholesky in every lane's registers
-      if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);
+    bool chol = !constrained;
+    if (constrained) {
+      // ---- constrained tail stage (r >= M since N % M == 0)
+      double ph = 0.0, pu = 0.0;
+      for (int idx = gt; idx < r * N; idx += NT) {
+        const double v = H[(idx / N) * LDW + idx % N];
+        ph += v * v;
+      }
+      for (int idx = gt; idx < N * M; idx += NT) {
+        const double v = sm[S::SFU + (idx / M) * S::LFU + idx % M];
+        pu += v * v;
+      }
+      const double hx2 = gsum<NWG>(ph, red, grp, gw);
+      gsync<NWG>(grp);
+      const double fu2 = gsum<NWG>(pu, red, grp, gw);
+      const double nu_scale = sqrt(hx2) * sqrt(fu2);
+      // N = Hx F, stacked in place: [Nx | Hz | Hx f1 + h1] into H, Nu into
+      // NTb (every band's loads precede its stores; bands own their rows)
+      ggemm_f<N, FW, N, NWG>(
+          [&](int i, int k) { return H[i * LDW + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
+          [&](int i, int c, double acc) {
+            if (c < N)
+              H[i * LDW + c] = acc;
+            else if (c < N + M)
+              NTb[i * LDF + c] = acc;
+            else
+              H[i * LDW + CC] += acc;
+          },
+          r);
+      gsync<NWG>(grp);
+      if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
+      if constexpr (NWG == 1) {
+        warp_qr_wy<M, W, LDF, LDW, N>(NTb + N, r, H, tau, rdiag);   // tau slot holds T (M*M)
+      } else {
+        gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
+      }
+      double rmax = 0.0, rmin = 1e308;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        rmax = fmax(rmax, fabs(rdiag[i]));
+        rmin = fmin(rmin, fabs(rdiag[i]));
+      }
+      const double thr = p.rank_tol * fmax(nu_scale, rmax);
+      if (rmax <= thr) {
+        // p = 0 (Nu numerically zero): identity reflectors, all r rows stay,
+        // gains by the null-space solve with Zw = I (endpoint.py:239-250)
+        chol = true;
+      } else if (!(rmin > thr)) {
+        // 0 < p < m: rank-revealing branch not built
+        status = PLQ_STATUS_DEGENERATE;
+        if (s > 0) {
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
+        break;
+      } else {
+        const double* Rm = NTb + N;   // R (upper) with stride LDF
+        int ldr = LDF;
+        if constexpr (S::BIG) {
+          // G overlays VF: move R out of the way first (TAU area, M x M)
+          for (int idx = gt; idx < M * M; idx += NT) tau[idx] = NTb[(idx / M) * LDF + N + idx % M];
+          gsync<NWG>(grp);
+          Rm = tau;
+          ldr = M;
+        }
+        for (int c = gt; c < W; c += NT) {
+          double x[M];
+  #pragma unroll
+          for (int i = M - 1; i >= 0; --i) {
+            double v = H[i * LDW + c];
+  #pragma unroll
+            for (int k = i + 1; k < M; ++k) v -= Rm[i * ldr + k] * x[k];
+            x[i] = v / rdiag[i];
+          }
+  #pragma unroll
+          for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
+        }
+        gsync<NWG>(grp);
+        for (int blk = 0; blk < r - M; blk += M) {
+          const int rows = min(M, r - M - blk);
+          for (int idx = gt; idx < rows * W; idx += NT) {
+            const int i = blk + idx / W, c = idx % W;
+            H[i * LDW + c] = H[(i + M) * LDW + c];
+          }
+          gsync<NWG>(grp);
+        }
+        r -= M;
+      }
+    }
+    if (chol) {
+      // ---- G = -Muu^{-1} P (unconstrained stage, or p = 0), Cholesky in every lane's registers
+      if (gt == 0 && s > 0 && !constrained) stage_issue<N, M>(p, st - 1, sm, bar);
       if constexpr (S::BIG) {
         // CTA Cholesky of Muu in place (not needed again in this stage) and
         // a blocked DMMA solve of the m x W right-hand side
@@ -533,86 +622,6 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       }
       gsync<NWG>(grp);
       }
-    } else {
-      // ---- constrained tail stage (r >= M since N % M == 0)
-      double ph = 0.0, pu = 0.0;
-      for (int idx = gt; idx < r * N; idx += NT) {
-        const double v = H[(idx / N) * LDW + idx % N];
-        ph += v * v;
-      }
-      for (int idx = gt; idx < N * M; idx += NT) {
-        const double v = sm[S::SFU + (idx / M) * S::LFU + idx % M];
-        pu += v * v;
-      }
-      const double hx2 = gsum<NWG>(ph, red, grp, gw);
-      gsync<NWG>(grp);
-      const double fu2 = gsum<NWG>(pu, red, grp, gw);
-      const double nu_scale = sqrt(hx2) * sqrt(fu2);
-      // N = Hx F, stacked in place: [Nx | Hz | Hx f1 + h1] into H, Nu into
-      // NTb (every band's loads precede its stores; bands own their rows)
-      ggemm_f<N, FW, N, NWG>(
-          [&](int i, int k) { return H[i * LDW + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
-          [&](int i, int c, double acc) {
-            if (c < N)
-              H[i * LDW + c] = acc;
-            else if (c < N + M)
-              NTb[i * LDF + c] = acc;
-            else
-              H[i * LDW + CC] += acc;
-          },
-          r);
-      gsync<NWG>(grp);
-      if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
-      if constexpr (NWG == 1) {
-        warp_qr_wy<M, W, LDF, LDW, N>(NTb + N, r, H, tau, rdiag);   // tau slot holds T (M*M)
-      } else {
-        gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
-      }
-      double rmax = 0.0, rmin = 1e308;
-#pragma unroll
-      for (int i = 0; i < M; ++i) {
-        rmax = fmax(rmax, fabs(rdiag[i]));
-        rmin = fmin(rmin, fabs(rdiag[i]));
-      }
-      if (!(rmin > p.rank_tol * fmax(nu_scale, rmax))) {
-        status = PLQ_STATUS_DEGENERATE;
-        if (s > 0) {
-          mbar_wait(bar, phase);
-          phase ^= 1u;
-        }
-        break;
-      }
-      const double* Rm = NTb + N;   // R (upper) with stride LDF
-      int ldr = LDF;
-      if constexpr (S::BIG) {
-        // G overlays VF: move R out of the way first (TAU area, M x M)
-        for (int idx = gt; idx < M * M; idx += NT) tau[idx] = NTb[(idx / M) * LDF + N + idx % M];
-        gsync<NWG>(grp);
-        Rm = tau;
-        ldr = M;
-      }
-      for (int c = gt; c < W; c += NT) {
-        double x[M];
-#pragma unroll
-        for (int i = M - 1; i >= 0; --i) {
-          double v = H[i * LDW + c];
-#pragma unroll
-          for (int k = i + 1; k < M; ++k) v -= Rm[i * ldr + k] * x[k];
-          x[i] = v / rdiag[i];
-        }
-#pragma unroll
-        for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
-      }
-      gsync<NWG>(grp);
-      for (int blk = 0; blk < r - M; blk += M) {
-        const int rows = min(M, r - M - blk);
-        for (int idx = gt; idx < rows * W; idx += NT) {
-          const int i = blk + idx / W, c = idx % W;
-          H[i * LDW + c] = H[(i + M) * LDW + c];
-        }
-        gsync<NWG>(grp);
-      }
-      r -= M;
     }
 
     // ---- policy outputs

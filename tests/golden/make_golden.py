@@ -301,6 +301,19 @@ def main():
                 "csv_smoothed_disturbed": read_csv("smoothed_disturbed.csv"),
                 "cost_smoothed": np.float64(float(summ[2]))})
     save("demo_double_integrator", **rec)
+    # segments without control authority (test_parallel.py:114-129): rank
+    # p = 0 in every stage of the segment, feasibility-constrained link solve
+    probs, Js = [], []
+    a = from_problem(ref_generate(3, 2, 9, seed=123))
+    a["Fu"][3:6] = 0.0
+    probs.append(a)
+    Js.append(3)
+    cfg = synth.CONFIGS[1]
+    b = {k: v[0] for k, v in synth.generate_batch(cfg, seed=5, count=1).items()}
+    b["Fu"][24:32] = 0.0
+    probs.append(b)
+    Js.append(8)
+    stored_case("uncontrollable", probs, Js)
     # two-point-boundary solves (endpoint.py:603-653) by the reference itself
     endpoint_goldens()
     # JSON problem / solution files written by the reference itself
