@@ -994,7 +994,10 @@ int launch_recon_seg(const ReconArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
   const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
-  const int per_sm = (int)((227 * 1024) / (smem + 1024));
+  // persistent grid: exactly the resident CTAs (registers and shared memory
+  // both counted), so no CTA's task stride starts after the others finish
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem);
   const int64_t cap = (int64_t)sms_count() * (per_sm > 0 ? per_sm : 1);
   const int grid = (int)(tasks < cap ? tasks : cap);
   if (grid <= 0) return 0;
@@ -1006,7 +1009,9 @@ template <int N, int M>
 int launch_recon_t(const ReconArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(double) * RL<N, M>::TOTAL;
   const int64_t tasks = a.p.B * (int64_t)(a.seg_end - a.seg_begin);
-  const int64_t cap = (int64_t)sms_count() * 32;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, recon_small_kernel<N, M>, 32, smem);
+  const int64_t cap = (int64_t)sms_count() * (per_sm > 0 ? per_sm : 1);
   const int grid = (int)(tasks < cap ? tasks : cap);
   if (grid <= 0) return 0;
   recon_small_kernel<N, M><<<grid, 32, smem, s>>>(a);
