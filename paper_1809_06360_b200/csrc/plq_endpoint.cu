@@ -96,19 +96,30 @@ __host__ __device__ inline int64_t ep_scratch(int n, int m) {
 }
 
 // ---- forward_pass (endpoint.py:326-349)
-template <int NT>
+template <int NT, bool ONCHIP>
 __global__ void __launch_bounds__(NT) ep_maps_kernel(EpArgs a) {
+  extern __shared__ __align__(16) double esm[];
   const plq_problem_t& p = a.p;
   const int n = p.n, m = p.m, T = p.T, W = 2 * n + 1, tid = threadIdx.x;
   const int64_t b = blockIdx.x, nn = (int64_t)n * n, nm = (int64_t)n * m;
   double* X0 = a.o.X + b * (T + 1) * n * W;
-  for (int idx = tid; idx < n * W; idx += NT) X0[idx] = (idx / W == idx % W) ? 1.0 : 0.0;
+  // ONCHIP: X_t ping-pongs and S_t lives in shared memory (the GEMM operands),
+  // each is streamed out to the output maps once
+  double* XS[2] = {esm, esm + n * W};
+  double* SS = esm + 2 * n * W;
+  for (int idx = tid; idx < n * W; idx += NT) {
+    const double v = (idx / W == idx % W) ? 1.0 : 0.0;
+    X0[idx] = v;
+    if (ONCHIP) XS[0][idx] = v;
+  }
   __syncthreads();
   for (int t = 0; t < T; ++t) {
     const int64_t bt = b * T + t;
-    double* X = X0 + (int64_t)t * n * W;
-    double* Xn = X + n * W;
-    double* S = a.o.S + bt * m * W;
+    double* Xg = X0 + (int64_t)t * n * W;
+    double* Sg = a.o.S + bt * m * W;
+    double* X = ONCHIP ? XS[t & 1] : Xg;
+    double* Xn = ONCHIP ? XS[(t + 1) & 1] : Xg + n * W;
+    double* S = ONCHIP ? SS : Sg;
     const double* Kz = a.o.Kz + bt * nm;
     const double* k1 = a.o.k1 + bt * m;
     gemm_c<false, false, 1, 2>(m, W, n, a.o.Kx + bt * nm, n, X, W, [&](int i, int c, double v) {
@@ -122,6 +133,10 @@ __global__ void __launch_bounds__(NT) ep_maps_kernel(EpArgs a) {
     __syncthreads();
     gemm_c<false, false, 1, 2>(n, W, m, p.Fu + bt * nm, m, S, W, [&](int i, int c, double v) { Xn[i * W + c] += v; });
     __syncthreads();
+    if (ONCHIP) {
+      for (int idx = tid; idx < m * W; idx += NT) Sg[idx] = S[idx];
+      for (int idx = tid; idx < n * W; idx += NT) Xg[n * W + idx] = Xn[idx];
+    }
   }
 }
 
@@ -164,24 +179,30 @@ __device__ void ep_bu(const EpArgs& a, int64_t b, int t, double* BU) {
 }
 
 // ---- assemble_normal_equations + multiplier_pass (endpoint.py:370-476)
-template <int EP_NT>
+template <int EP_NT, bool ONCHIP>
 __global__ void __launch_bounds__(EP_NT) ep_mult_kernel(EpArgs a) {
   __shared__ int flag;
+  extern __shared__ __align__(16) double esm[];
   const plq_problem_t& p = a.p;
   const int n = p.n, m = p.m, T = p.T, W = 2 * n + 1, tid = threadIdx.x;
   const int64_t b = blockIdx.x, nn = (int64_t)n * n, nm = (int64_t)n * m;
-  double* sc = a.scratch + b * ep_scratch(n, m);
+  // ONCHIP: the work blocks, d_i and X_i (ping-pong) in shared memory; d_i
+  // and X_i are streamed out once for the back substitution
+  double* sc = ONCHIP ? esm : a.scratch + b * ep_scratch(n, m);
   double* BX = sc;             // bx[t]       n x W
   double* BXn = BX + n * W;    // bx[t+1]     n x W
   double* BU = BXn + n * W;    // bu[t]       m x W
   double* P = BU + m * W;      // pivot block n x n (Cholesky in place)
   double* Y = P + nn;          // Fx' + X_{i-1}  n x n
+  double* DB[2] = {Y + nn, Y + nn + n * W};
+  double* XB[2] = {DB[1] + n * W, DB[1] + n * W + nn};
   double* Xb = a.Xb + b * (T + 1) * nn;
   double* Lam = a.o.Lam + b * (T + 1) * n * W;
   double* E = a.o.E + b * n * W;
   int fail = 0;
   for (int i = 0; i <= T + 1 && !fail; ++i) {
-    double* d = (i <= T) ? Lam + (int64_t)i * n * W : E;   // d_i written in place
+    double* dg = (i <= T) ? Lam + (int64_t)i * n * W : E;   // d_i's home
+    double* d = ONCHIP ? DB[i & 1] : dg;
     if (i == 0) {
       ep_bx(a, b, 0, BX);
       for (int idx = tid; idx < n * W; idx += EP_NT) d[idx] = BX[idx];
@@ -191,13 +212,13 @@ __global__ void __launch_bounds__(EP_NT) ep_mult_kernel(EpArgs a) {
       const int64_t bt = b * T + t;
       const double* Fx = p.Fx + bt * nn;
       const double* Fu = p.Fu + bt * nm;
-      const double* dprev = Lam + (int64_t)(i - 1) * n * W;
+      const double* dprev = ONCHIP ? DB[(i - 1) & 1] : Lam + (int64_t)(i - 1) * n * W;
       ep_bu(a, b, t, BU);
       ep_bx(a, b, t + 1, BXn);
       // g = bx[t+1] - Fx (bx[t] - d_{i-1}) - Fu bu[t]
       for (int idx = tid; idx < n * W; idx += EP_NT) BX[idx] -= dprev[idx];
       // P = I + Fx (Fx' + X_{i-1}) + Fu Fu'
-      const double* Xprev = Xb + (int64_t)(i - 1) * nn;
+      const double* Xprev = ONCHIP ? XB[(i - 1) & 1] : Xb + (int64_t)(i - 1) * nn;
       for (int idx = tid; idx < n * n; idx += EP_NT) {
         const int r = idx / n, c = idx % n;
         Y[idx] = Fx[c * n + r] + Xprev[idx];
@@ -216,8 +237,8 @@ __global__ void __launch_bounds__(EP_NT) ep_mult_kernel(EpArgs a) {
       BXn = tmp;
     } else {
       // mu block: P = I - X_T, g = bx[T] - d_T
-      const double* dprev = Lam + (int64_t)T * n * W;
-      const double* Xprev = Xb + (int64_t)T * nn;
+      const double* dprev = ONCHIP ? DB[T & 1] : Lam + (int64_t)T * n * W;
+      const double* Xprev = ONCHIP ? XB[T & 1] : Xb + (int64_t)T * nn;
       for (int idx = tid; idx < n * W; idx += EP_NT) d[idx] = BX[idx] - dprev[idx];
       for (int idx = tid; idx < n * n; idx += EP_NT) P[idx] = (idx / n == idx % n ? 1.0 : 0.0) - Xprev[idx];
     }
@@ -227,9 +248,11 @@ __global__ void __launch_bounds__(EP_NT) ep_mult_kernel(EpArgs a) {
       break;
     }
     cta_cho_solve(P, n, n, d, W, W);
+    if (ONCHIP)
+      for (int idx = tid; idx < n * W; idx += EP_NT) dg[idx] = d[idx];
     if (i <= T) {
       // X_i = P^{-1} sub_i',  sub_i = -Fx_i (i < T), I (i = T)
-      double* Xi = Xb + (int64_t)i * nn;
+      double* Xi = ONCHIP ? XB[i & 1] : Xb + (int64_t)i * nn;
       const double* Fxi = p.Fx + (b * T + i) * nn;
       for (int idx = tid; idx < n * n; idx += EP_NT) {
         const int r = idx / n, c = idx % n;
@@ -237,6 +260,8 @@ __global__ void __launch_bounds__(EP_NT) ep_mult_kernel(EpArgs a) {
       }
       __syncthreads();
       cta_cho_solve(P, n, n, Xi, n, n);
+      if (ONCHIP)
+        for (int idx = tid; idx < n * n; idx += EP_NT) Xb[(int64_t)i * nn + idx] = Xi[idx];
     }
     __syncthreads();
   }
@@ -391,15 +416,24 @@ int launch_endpoint_maps_mult(const plq_problem_t& p, const plq_endpoint_outputs
   a.o = o;
   a.Xb = ws;
   a.scratch = ws + (size_t)p.B * (p.T + 1) * p.n * p.n;
-  // small states: 4 warps cover every GEMM tile; more CTAs stay resident
-  if (p.n <= 32) {
-    ep_maps_kernel<128><<<(unsigned)p.B, 128, 0, s>>>(a);
+  // small states: 4 warps cover every GEMM tile, more CTAs stay resident,
+  // and the sequential working sets fit in shared memory
+  const int n = p.n, m = p.m, W = 2 * n + 1;
+  if (n <= 32) {
+    const size_t maps_sm = sizeof(double) * (2 * (size_t)n * W + (size_t)m * W);
+    const size_t mult_sm = sizeof(double) * (4 * (size_t)n * W + (size_t)m * W + 4 * (size_t)n * n);
+    static unsigned attr = 0;
+    if (first_on_device(&attr)) {
+      cudaFuncSetAttribute(ep_maps_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(ep_mult_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    }
+    ep_maps_kernel<128, true><<<(unsigned)p.B, 128, maps_sm, s>>>(a);
     if (cudaGetLastError() != cudaSuccess) return -1;
-    ep_mult_kernel<128><<<(unsigned)p.B, 128, 0, s>>>(a);
+    ep_mult_kernel<128, true><<<(unsigned)p.B, 128, mult_sm, s>>>(a);
   } else {
-    ep_maps_kernel<EP_NT><<<(unsigned)p.B, EP_NT, 0, s>>>(a);
+    ep_maps_kernel<EP_NT, false><<<(unsigned)p.B, EP_NT, 0, s>>>(a);
     if (cudaGetLastError() != cudaSuccess) return -1;
-    ep_mult_kernel<EP_NT><<<(unsigned)p.B, EP_NT, 0, s>>>(a);
+    ep_mult_kernel<EP_NT, false><<<(unsigned)p.B, EP_NT, 0, s>>>(a);
   }
   if (cudaGetLastError() != cudaSuccess) return -1;
   *launches += 2;
