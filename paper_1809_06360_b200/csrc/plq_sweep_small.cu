@@ -180,7 +180,8 @@ __device__ __forceinline__ void gqr(double* A, int r, double* X, double* tau, do
 // (strictly lower, unit diagonal implicit) are written back LAPACK-style to
 // A; rdiag gets diag(R).
 template <int M, int W, int LDA, int LDX, int RMAX>
-__device__ __forceinline__ void warp_qr_wy(double* A, int r, double* X, double* Tm, double* rdiag) {
+__device__ __forceinline__ void warp_qr_wy(double* A, int r, double* X, double* Tm, double* rdiag, double* VTs,
+                                           double* Ys) {
   const int lane = threadIdx.x & 31;
   const bool row = lane < r;
   // rows live in lanes < r <= RMAX: for RMAX <= 16 a half-warp butterfly is
@@ -251,37 +252,25 @@ __device__ __forceinline__ void warp_qr_wy(double* A, int r, double* X, double* 
       for (int j = 0; j < M; ++j) Tm[i * M + j] = T[i][j];
   }
   __syncwarp();
-  // X <- (I - V T' V') X, lane per column; V read back from A (unit diagonal)
-  for (int c = lane; c < W; c += 32) {
-    double y[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) y[j] = 0.0;
-    for (int i = 0; i < r; ++i) {
-      const double xi = X[i * LDX + c];
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        const double vij = (i == j) ? 1.0 : (i > j ? A[i * LDA + j] : 0.0);
-        y[j] += vij * xi;
-      }
-    }
-    double z[M];
+  // X <- X - (V T') (V' X) on the FP64 tensor pipe: Y = V'X (M x W, K = r),
+  // VT = V T' (r x M, each row-lane from its own v), X -= VT Y (r x W, K = M).
+  // V' rows are read back from A (unit diagonal, zeros above); rows >= r are 0.
+  ggemm_f<M, W, RMAX, 1>(
+      [&](int i, int k) { return (k == i) ? 1.0 : ((k > i && k < r) ? A[k * LDA + i] : 0.0); },
+      [&](int k, int c) { return k < r ? X[k * LDX + c] : 0.0; }, 0,
+      [&](int i, int c, double acc) { Ys[i * LDX + c] = acc; });
+  if (row) {
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       double t = 0.0;
 #pragma unroll
-      for (int i = 0; i <= j; ++i) t += Tm[i * M + j] * y[i];   // (T' y)_j
-      z[j] = t;
-    }
-    for (int i = 0; i < r; ++i) {
-      double t = 0.0;
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        const double vij = (i == j) ? 1.0 : (i > j ? A[i * LDA + j] : 0.0);
-        t += vij * z[j];
-      }
-      X[i * LDX + c] -= t;
+      for (int l = j; l < M; ++l) t += v[l] * Tm[j * M + l];   // (V T')_{lane, j}, T upper
+      VTs[lane * LDA + j] = t;
     }
   }
+  __syncwarp();
+  ggemm_f<RMAX, W, M, 1>([&](int i, int k) { return VTs[i * LDA + k]; }, [&](int k, int c) { return Ys[k * LDX + c]; },
+                         0, [&](int i, int c, double acc) { X[i * LDX + c] -= acc; }, r);
   __syncwarp();
 }
 
@@ -497,7 +486,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       gsync<NWG>(grp);
       if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
       if constexpr (NWG == 1) {
-        warp_qr_wy<M, W, LDF, LDW, N>(NTb + N, r, H, tau, rdiag);   // tau slot holds T (M*M)
+        // tau slot holds T (M*M); NTb columns 0..M-1 (free: Nx went to H) take V T',
+        // the Y slot (dead until the value update) takes V'X
+        warp_qr_wy<M, W, LDF, LDW, N>(NTb + N, r, H, tau, rdiag, NTb, Y);
       } else {
         gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
