@@ -534,14 +534,10 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
         }
         gsync<NWG>(grp);
-        for (int blk = 0; blk < r - M; blk += M) {
-          const int rows = min(M, r - M - blk);
-          for (int idx = gt; idx < rows * W; idx += NT) {
-            const int i = blk + idx / W, c = idx % W;
-            H[i * LDW + c] = H[(i + M) * LDW + c];
-          }
-          gsync<NWG>(grp);
-        }
+        // the surviving rows Q2' stack are rows M..r-1: advance the row base
+        // instead of moving them (H is re-based at every segment start and
+        // r + offset never exceeds the N-row buffer)
+        H += M * LDW;
         r -= M;
       }
     }
