@@ -233,6 +233,50 @@ __global__ void __launch_bounds__(NT) boundary_kernel(ReconArgs A) {
   }
 }
 
+// Small states (n, m <= 16): one thread per link stage, so every link stage
+// of the batch is in flight at once (the per-stage work is two tiny
+// transposed mat-vecs; the CTA-per-stage form is launch/latency bound).
+template <int N, int M>
+__global__ void __launch_bounds__(128) boundary_small_kernel(ReconArgs A) {
+  const plq_problem_t& p = A.p;
+  const int J = p.J, T = p.T;
+  const int nloc = A.seg_end - A.seg_begin;
+  const int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (task >= p.B * nloc) return;
+  const int64_t b = task / nloc;
+  const int j = A.seg_begin + (int)(task % nloc);
+  if (j == J - 1) {
+    A.part[(b * J + j) * 3 + 2] = 0.0;
+    return;
+  }
+  const int hi = p.split_times[j + 1];
+  const int64_t st = b * T + (hi - 1);
+  double ln[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) ln[k] = A.lambda_right[(b * (J - 1) + j) * N + k];
+  const double* Fx = p.Fx + st * N * N;
+  const double* Fu = p.Fu + st * N * M;
+  const double* gh = A.gh + st * (N + M);
+  double worst = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double t0 = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) t0 += Fx[k * N + i] * ln[k];
+    const double lt = A.lam[(b * (T + 1) + hi - 1) * N + i];
+    worst = fmax(worst, fabs((gh[i] + lt) - t0));
+    worst = fmax(worst, fabs(A.links[(b * (J - 1) + j) * N + i] - A.xend[(b * J + j) * N + i]));
+  }
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    double t2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) t2 += Fu[k * M + i] * ln[k];
+    worst = fmax(worst, fabs(gh[N + i] - t2));
+  }
+  A.part[(b * J + j) * 3 + 2] = worst;
+}
+
 // objective = fixed-order sum of segment partials; kkt = max of all rows;
 // link_mismatch = max |mu_left + lambda_right| (parallel.py:527).  The sum is
 // deterministic: thread t adds a fixed contiguous run of segments, then a
@@ -272,7 +316,7 @@ int grid_for(int64_t tasks, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t per_sm = 2048 / threads;
+  const int64_t per_sm = (2048 / threads) < 32 ? (2048 / threads) : 32;   // resident-CTA limit
   const int64_t cap = (int64_t)sms * per_sm;
   return (int)(tasks < cap ? tasks : cap);
 }
@@ -304,6 +348,10 @@ int launch_boundary(const ReconArgs& a, double* /*unused*/, cudaStream_t s) {
   const size_t smem = sizeof(double) * (2 * a.p.n + a.p.m + 40);
   const int64_t tasks = a.p.B * (a.seg_end - a.seg_begin);
   if (tasks <= 0) return 0;
+  if (a.p.n == 12 && a.p.m == 4) {
+    boundary_small_kernel<12, 4><<<(unsigned)((tasks + 127) / 128), 128, 0, s>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   const int grid = grid_for(tasks, threads);
   switch (threads) {
     case 32:
