@@ -15,6 +15,7 @@
 // A pivot block that is not positive-definite raises LinkSingular, as the
 // reference does (parallel.py:267-271).
 #include "plq_device.cuh"
+#include "plq_blocked.cuh"
 #include "plq_gemm.cuh"
 #include "plq_internal.h"
 #include "plq_tma.cuh"
@@ -181,6 +182,15 @@ __device__ __forceinline__ bool warp_cholesky_smem(double* A, int n, int ld) {
   return ok;
 }
 
+// offset (doubles) of the blocked-factorization scratch in link_eliminate's
+// dynamic shared memory: after the factor / right-hand sides / staging (n <=
+// 64) or the factor / GEMM tiles (n > 64); 2 * ceil(n/8) * 64 + 8 * 64 doubles
+__host__ __device__ inline size_t link_elim_blocked_off(int n, bool sm, bool lsm, int ldl, int ldw, int threads) {
+  if (sm) return ((((size_t)n * ldl + (size_t)n * ldw + 1) & ~size_t(1)) + 3 * (size_t)n * n + n + 1) & ~size_t(1);
+  return (lsm ? (((size_t)n * ldl + 1) & ~size_t(1)) : 0) + (threads == 256 ? (size_t)TileCfg<8>::DOUBLES : 0);
+}
+__host__ __device__ inline size_t link_elim_blocked_doubles(int n) { return 2 * (size_t)((n + 7) / 8) * 64 + 8 * 64; }
+
 // eliminate the odd blocks of one level (or the single top block).  For
 // n <= 64 the pivot block and W live in shared memory; the factor and W are
 // written back to global once for the back-substitution.
@@ -247,12 +257,21 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
   }
   if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  const bool ok = cta_cholesky(Lc, n, ldl, &flag);
+  // blocked Cholesky / forward solve (plq_blocked.cuh) for 8-warp CTAs; the
+  // scratch (block inverses, diagonal staging, warp tiles) follows the layout
+  const bool blocked = n >= 16 && blockDim.x == 256;
+  double* bsc = dsm + link_elim_blocked_off(n, sm, lsm, ldl, ldw, blockDim.x);
+  auto csync = [] { __syncthreads(); };
+  const int nbk = (n + 7) / 8;
+  const bool ok = blocked ? gchol8<8>(Lc, n, ldl, bsc, &flag, threadIdx.x, csync, bsc + nbk * 64)
+                          : cta_cholesky(Lc, n, ldl, &flag);
   if (!ok) {
     flag_singular(p, status, b);
     return;
   }
-  if (n >= 16)
+  if (blocked)
+    gtrsm8<0, 8>(Lc, n, ldl, bsc, Wm, w, ldw, bsc + 2 * nbk * 64, threadIdx.x, csync);
+  else if (n >= 16)
     cta_trsm_lower_blocked(Lc, n, ldl, Wm, w, ldw);
   else
     cta_trsm_lower(Lc, n, ldl, Wm, w, ldw);
@@ -465,13 +484,13 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
     const int w = 2 * p.n + 1, ldw = ((w + 3) / 8) * 8 + 4;
-    const size_t tsm = p.n <= 64 ? sizeof(double) * ((size_t)p.n * (p.n + 1) + (size_t)p.n * ldw + 2 +
-                                                     3 * (size_t)p.n * p.n + p.n)
-                                 : sizeof(double) * ((p.n <= 128 ? (((size_t)p.n * (p.n + 1) + 1) & ~size_t(1)) : 0) +
-                                                     (threads == 256 ? TileCfg<8>::DOUBLES : 0));
-    if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     // the elimination is the level's critical path: 8 warps from n = 17 up
     const int ethreads = p.n <= 16 ? threads : 256;
+    const bool esm = p.n <= 64, elsm = p.n <= 128;
+    const int eldl = elsm ? p.n + 1 : p.n, eldw = esm ? ldw : w;
+    const size_t tsm = sizeof(double) * (link_elim_blocked_off(p.n, esm, elsm, eldl, eldw, ethreads) +
+                                         link_elim_blocked_doubles(p.n));
+    if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     link_eliminate<<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], status);
     ++nl;
     if (!P.lv[l].top) {

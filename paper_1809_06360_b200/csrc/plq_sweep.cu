@@ -18,6 +18,7 @@
 //          basis); 0 < r < m: mixed range/null branch.
 //   value  Y = P + Muu G;  [Vxx Vzx' vx1; Vzx Vzz vz1] = M + P'G + G'Y
 //          which is term-for-term endpoint.py:285-294.
+#include "plq_blocked.cuh"
 #include "plq_device.cuh"
 #include "plq_gemm.cuh"
 #include "plq_internal.h"
@@ -165,6 +166,13 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   double* red = rdiag + m;
   int* iflag = reinterpret_cast<int*>(red + 32);
   int* sflag = iflag + 1;
+  // blocked-factorization scratch (plq_blocked.cuh): block inverses, per-warp
+  // tiles, V T' of the QR panel
+  double* binv = red + 34;
+  double* wsc = binv + ((m + 7) / 8) * 64;
+  double* vts = wsc + (NT / 32) * 64;
+  auto csync = [] { __syncthreads(); };
+  const bool blocked = m >= 16;
   double* VF = bf.VF;
   double* Z = bf.Z;
   double* MX = bf.MX;
@@ -288,7 +296,10 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       for (int i = tid; i < r; i += nt) H[i * ldw + cc] += VF[i * Fw + n + m];
       __syncthreads();
       if (r >= m) {
-        cta_householder_qr(VF + n, r, m, Fw, H, W, ldw, tau, rdiag, red);
+        if (blocked)
+          gqr8<NT / 32>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync);
+        else
+          cta_householder_qr(VF + n, r, m, Fw, H, W, ldw, tau, rdiag, red);
         double rmax = 0.0, rmin = 1e308;
         for (int i = 0; i < m; ++i) {
           rmax = fmax(rmax, fabs(rdiag[i]));
@@ -308,7 +319,12 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           break;
         } else {
           // G = -R^{-1} (Q1' stack): back substitution, thread per column
-          for (int c = tid; c < W; c += nt) {
+          // (blocked: in place on H's first m rows, DMMA tiles)
+          if (blocked) {
+            gtri_inv_upper8<NT / 32>(VF + n, m, Fw, rdiag, binv, tid, csync);
+            gtrsm8<2, NT / 32>(VF + n, m, Fw, binv, H, W, ldw, wsc, tid, csync);
+          }
+          for (int c = tid; c < W && !blocked; c += nt) {
             for (int i = m - 1; i >= 0; --i) {
               double v = H[i * ldw + c];
               for (int k = i + 1; k < m; ++k) v -= VF[i * Fw + n + k] * G[k * ldw + c];
@@ -318,8 +334,9 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           __syncthreads();
           for (int idx = tid; idx < m * W; idx += nt) {
             const int u = idx / W, c = idx % W;
-            G[u * ldw + c] = -G[u * ldw + c];
+            G[u * ldw + c] = -(blocked ? H[u * ldw + c] : G[u * ldw + c]);
           }
+          __syncthreads();
           // surviving rows Q2' stack: shift rows m..r-1 up by m, one block of
           // m rows at a time so sources and destinations never overlap
           for (int blk = 0; blk < r - m; blk += m) {
@@ -349,12 +366,17 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       if (tid == 0) *iflag = 0;
       __syncthreads();
-      if (!cta_cholesky(Lm, m, m, iflag)) {
+      if (!(blocked ? gchol8<NT / 32>(Lm, m, m, binv, iflag, tid, csync) : cta_cholesky(Lm, m, m, iflag))) {
         if (tid == 0) *sflag = 1 + s;
         __syncthreads();
         break;
       }
-      cho_solve_x(Lm, m, m, G, W, ldw);
+      if (blocked) {
+        gtrsm8<0, NT / 32>(Lm, m, m, binv, G, W, ldw, wsc, tid, csync);
+        gtrsm8<1, NT / 32>(Lm, m, m, binv, G, W, ldw, wsc, tid, csync);
+      } else {
+        cho_solve_x(Lm, m, m, G, W, ldw);
+      }
       for (int idx = tid; idx < m * W; idx += nt) {
         const int u = idx / W, c = idx % W;
         G[u * ldw + c] = -G[u * ldw + c];
@@ -477,7 +499,9 @@ SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
   sz[SB_IN] = n * Fw + (int64_t)n * n + (int64_t)m * n + (int64_t)m * m + n + m;
   sz[SB_PGY] = 3 * m * W;
   sz[SB_MUU] = 2LL * m * m;
-  sz[SB_MISC] = 2LL * m + 32 + 2;
+  // tau, rdiag, reduction (32), flags (2), blocked scratch: block inverses,
+  // per-warp tiles, V T' (plq_blocked.cuh)
+  sz[SB_MISC] = 2LL * m + 32 + 2 + ((m + 7) / 8) * 64LL + (threads / 32) * 64LL + 8LL * n;
   sz[SB_VF] = n * Fw;
   sz[SB_Z] = n * Fw;
   sz[SB_MX] = (int64_t)n * (n + 1);

@@ -16,6 +16,7 @@
 //     Mxx/mx1 into Vxx/vx1, and the value update accumulates into V;
 //   * the m x m Cholesky of Muu is computed redundantly in every lane's
 //     registers (m <= 8), so the gain solve needs no barrier.
+#include "plq_blocked.cuh"
 #include "plq_gemm.cuh"
 #include "plq_internal.h"
 #include "plq_small.cuh"
@@ -72,7 +73,8 @@ struct SL {
   static constexpr int RED = RD + M;                    // 8
   static constexpr int DUM = RED + 8;                   // 32 per-lane dummy slots (branch-free epilogues)
   static constexpr int BAR = (DUM + 32 + 1) & ~1;       // mbarrier (8 bytes)
-  static constexpr int TOTAL = BAR + 2;
+  static constexpr int FLAG = BAR + 2;                  // int flag of the blocked Cholesky (BIG)
+  static constexpr int TOTAL = FLAG + 2;
   // global scratch per CTA (BIG): Vzz (N x LDN), H (N x LDW), Y (M x LDW)
   static constexpr int GVZZ = 0, GH = GVZZ + N * LDN, GY = GH + N * LDW;
   static constexpr int GTOTAL = BIG ? GY + M * LDW : 0;
@@ -489,6 +491,11 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         // tau slot holds T (M*M); NTb columns 0..M-1 (free: Nx went to H) take V T',
         // the Y slot (dead until the value update) takes V'X
         warp_qr_wy<M, W, LDF, LDW, N>(NTb + N, r, H, tau, rdiag, NTb, Y);
+      } else if constexpr (S::BIG) {
+        // blocked compact-WY QR: the TAU slot (M*M >= 8N + 8*64 doubles) holds
+        // V T' and the per-warp tiles
+        static_assert(M * M >= N * 8 + NWG * 64, "TAU slot too small for the blocked QR");
+        gqr8<NWG>(NTb + N, r, M, LDF, H, W, LDW, rdiag, tau, tau + N * 8, gt, [&] { gsync<NWG>(grp); });
       } else {
         gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
@@ -515,12 +522,14 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         const double* Rm = NTb + N;   // R (upper) with stride LDF
         int ldr = LDF;
         if constexpr (S::BIG) {
-          // G overlays VF: move R out of the way first (TAU area, M x M)
-          for (int idx = gt; idx < M * M; idx += NT) tau[idx] = NTb[(idx / M) * LDF + N + idx % M];
+          // G = -R^{-1} (Q1' stack): blocked back substitution in place on
+          // H's first M rows (R stays in NTb, which G overlays), then G = -H
+          auto sy = [&] { gsync<NWG>(grp); };
+          gtri_inv_upper8<NWG>(Rm, M, ldr, rdiag, tau, gt, sy);
+          gtrsm8<2, NWG>(Rm, M, ldr, tau, H, W, LDW, tau + 256, gt, sy);
+          for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = -H[(idx / W) * LDW + idx % W];
           gsync<NWG>(grp);
-          Rm = tau;
-          ldr = M;
-        }
+        } else {
         for (int c = gt; c < W; c += NT) {
           double x[M];
   #pragma unroll
@@ -534,6 +543,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
         }
         gsync<NWG>(grp);
+        }
         // the surviving rows Q2' stack are rows M..r-1: advance the row base
         // instead of moving them (H is re-based at every segment start and
         // r + offset never exceeds the N-row buffer)
@@ -548,7 +558,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         // CTA Cholesky of Muu in place (not needed again in this stage) and
         // a blocked DMMA solve of the m x W right-hand side
         for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = P[(idx / W) * LDW + idx % W];
-        if (!cta_cholesky(Muu, M, LDM, nullptr)) {
+        auto sy = [&] { gsync<NWG>(grp); };
+        static_assert(M * M >= 256 + NWG * 64, "TAU slot too small for the blocked solve");
+        if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy)) {
           status = 1 + s;
           if (s > 0) {
             mbar_wait(bar, phase);
@@ -556,7 +568,8 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           }
           break;
         }
-        cta_cho_solve_blocked(Muu, M, LDM, G, W, LDW);
+        gtrsm8<0, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);
+        gtrsm8<1, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);
         for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = -G[(idx / W) * LDW + idx % W];
         gsync<NWG>(grp);
       } else {
