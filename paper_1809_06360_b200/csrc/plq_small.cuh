@@ -173,6 +173,62 @@ __device__ __forceinline__ void wgemm_slots(AL aload, BL bload, Epi epi) {
   }
 }
 
+// Tile-selective group GEMM: warp gw processes the row bands bandof(gw, slot)
+// (slot < NSLOT; a negative band is skipped) and, in band tm, only the 8 x 8
+// column tiles with on(tm, tn) -- e.g. the lower triangle of a symmetric
+// block, or no wasted blocks.  pre(i, j) is an addend (e.g. a Q-block entry
+// read from global memory) loaded BEFORE the k-loop so its latency hides
+// behind the DMMAs; epi(i, j, pre + acc) receives each selected element once.
+template <int M, int N, int K, int NSLOT, class BandOf, class On, class AL, class BL, class Pre, class Epi>
+__device__ __forceinline__ void ggemm_sel(AL aload, BL bload, int gw, BandOf bandof, On on, Pre pre, Epi epi) {
+  constexpr int TN = (N + 7) / 8, KS = (K + 3) / 4;
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+#pragma unroll 1
+  for (int slot = 0; slot < NSLOT; ++slot) {
+    const int tm = bandof(gw, slot);
+    if (tm < 0) continue;
+    const int i = tm * 8 + g;
+    const bool iok = i < M;
+    double acc[TN][2], add[TN][2];
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn) {
+      acc[tn][0] = acc[tn][1] = 0.0;
+      add[tn][0] = add[tn][1] = 0.0;
+      if (on(tm, tn)) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = tn * 8 + 2 * q + e;
+          if (iok && j < N) add[tn][e] = pre(i, j);
+        }
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = ks * 4 + q;
+      const bool kok = (K % 4 == 0) || (k < K);
+      const double a = (iok && kok) ? aload(i, k) : 0.0;
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn) {
+        if (on(tm, tn)) {
+          const int j = tn * 8 + g;
+          const double b = (((N % 8 == 0) || (j < N)) && kok) ? bload(k, j) : 0.0;
+          dmma884(acc[tn][0], acc[tn][1], a, b);
+        }
+      }
+    }
+#pragma unroll
+    for (int tn = 0; tn < TN; ++tn) {
+      if (on(tm, tn)) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = tn * 8 + 2 * q + e;
+          if (iok && j < N) epi(i, j, add[tn][e] + acc[tn][e]);
+        }
+      }
+    }
+  }
+}
+
 // pointer-operand form: A row-major (or transposed, TA) with stride LDA, B row-major stride LDB
 template <int M, int N, int K, bool TA, int LDA, int LDB, int NWG, class Epi>
 __device__ __forceinline__ void ggemm(const double* __restrict__ A, const double* __restrict__ B, int gw, Epi epi,

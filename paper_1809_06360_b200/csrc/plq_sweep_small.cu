@@ -292,6 +292,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   const int T = p.T, J = p.J;
   const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
   constexpr int LDM = S::LDM;
+  // tile-selective GEMM2 / value update (symmetric blocks computed once)
+  constexpr bool SEL = S::BIG && N == 64 && M == 32 && NWG == 8;
+  constexpr int XB = N / 8;
   double* gs = a.gscratch + (int64_t)blockIdx.x * S::GTOTAL;   // BIG: per-CTA L2 scratch
   double* Vxx = sm + S::V;
   double* Vzx = Vxx + N * LDN;
@@ -426,6 +429,29 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
             const bool xr = i < N, xc = c < N;
             double* d = xr ? (xc ? Vxx + i * LDN + c : dum) : (xc ? P + u * LDW + c : Muu + u * LDM + (c - N));
             *d = qv[slot] + acc;
+          });
+    } else if constexpr (SEL) {
+      // x bands: the lower triangle of Mxx only (the value update mirrors
+      // V), no Mxu block; u bands: Mux | Muu in full.  Warps 0-3 take a u
+      // band (12 tiles), warps 4-7 a pair of x bands (9 tiles).  The Q-block
+      // addends are loaded from global memory before each band's k-loop.
+      ggemm_sel<N + M, N + M, N, 2>(
+          [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
+          [](int w, int slot) { return w < 4 ? (slot == 0 ? XB + w : -1) : (slot == 0 ? w - 4 : XB + 3 - w); },
+          [](int tm, int tn) { return tm >= XB || tn <= tm; },
+          [&](int i, int c) {
+            const int u = i - N;
+            return i < N ? __ldg(Qxx + i * N + c) : (c < N ? __ldg(Qux + u * N + c) : __ldg(Quu + u * M + (c - N)));
+          },
+          [&](int i, int c, double v) {
+            const int u = i - N;
+            if (i < N) {
+              if (c <= i) Vxx[i * LDN + c] = v;
+            } else if (c < N) {
+              P[u * LDW + c] = v;
+            } else {
+              Muu[u * LDM + (c - N)] = v;
+            }
           });
     } else {
       ggemm_f<N + M, N + M, N, NWG>(
@@ -642,13 +668,41 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
                           : ((c < N) ? Vzx + zi * LDN + c : Vzz + zi * LDN + (c - N));
       *d += acc;
     };
+    // SEL: the lower triangles of Vxx (mirrored: V is exactly symmetric, no
+    // symmetrization pass) and Vzz (mirrored at the segment end), Vzx in
+    // full, no wasted Vxz block; warp gw takes bands gw and TM-1-gw.
+    constexpr int VTM = (N + NZ) / 8;
+    auto vband = [](int w, int slot) { return slot == 0 ? w : (VTM > NWG ? VTM - 1 - w : -1); };
+    auto von = [](int tm, int tn) { return tm < XB ? tn <= tm : (tn < XB || tn - XB <= tm - XB); };
+    auto vzero = [](int, int) { return 0.0; };
+    auto vsel = [&](int i, int c, double acc) {
+      if (i < N) {
+        if (c <= i) {
+          const double v = Vxx[i * LDN + c] + acc;
+          Vxx[i * LDN + c] = v;
+          Vxx[c * LDN + i] = v;
+        }
+      } else {
+        const int zi = i - N;
+        if (c < N)
+          Vzx[zi * LDN + c] += acc;
+        else if (c - N <= zi)
+          Vzz[zi * LDN + (c - N)] += acc;
+      }
+    };
     if (constrained) {
       ggemm<M, W, M, false, LDM, LDW, NWG>(Muu, G, gw,
                                            [&](int i, int c, double acc) { Y[i * LDW + c] = P[i * LDW + c] + acc; });
       gsync<NWG>(grp);
-      ggemm_f<N + NZ, W - 1, 2 * M, NWG>(
-          [&](int i, int k) { return k < M ? P[k * LDW + i] : G[(k - M) * LDW + i]; },
-          [&](int k, int c) { return k < M ? G[k * LDW + c] : Y[(k - M) * LDW + c]; }, gw, vupd);
+      auto aP = [&](int i, int k) { return k < M ? P[k * LDW + i] : G[(k - M) * LDW + i]; };
+      auto bG = [&](int k, int c) { return k < M ? G[k * LDW + c] : Y[(k - M) * LDW + c]; };
+      if constexpr (SEL)
+        ggemm_sel<N + NZ, W - 1, 2 * M, 2>(aP, bG, gw, vband, von, vzero, vsel);
+      else
+        ggemm_f<N + NZ, W - 1, 2 * M, NWG>(aP, bG, gw, vupd);
+    } else if constexpr (SEL) {
+      ggemm_sel<N + NZ, W - 1, M, 2>([&](int i, int k) { return P[k * LDW + i]; },
+                                     [&](int k, int c) { return G[k * LDW + c]; }, gw, vband, von, vzero, vsel);
     } else {
       ggemm<N + NZ, W - 1, M, true, LDW, LDW, NWG>(P, G, gw, vupd);
     }
@@ -667,23 +721,26 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         vz1[gt - N] += t;
     }
     gsync<NWG>(grp);
-    // symmetrize Vxx (and Vzz) as 0.5 (V + V'): all N(N-1)/2 pairs in parallel
-    // (Vzz is never a GEMM operand; symmetrizing it once per segment is the
-    // same linear map as every stage: sym(sym(A) + X) = sym(A + X).)
-    for (int pp = gt; pp < NP; pp += NT) {
-      const int pr = pairs[pp];
-      const int i = pr >> 8, c = pr & 255;
-      const double v = 0.5 * (Vxx[i * LDN + c] + Vxx[c * LDN + i]);
-      Vxx[i * LDN + c] = v;
-      Vxx[c * LDN + i] = v;
+    if constexpr (!SEL) {
+      // symmetrize Vxx (and Vzz) as 0.5 (V + V'): all N(N-1)/2 pairs in parallel
+      // (Vzz is never a GEMM operand; symmetrizing it once per segment is the
+      // same linear map as every stage: sym(sym(A) + X) = sym(A + X).)
+      for (int pp = gt; pp < NP; pp += NT) {
+        const int pr = pairs[pp];
+        const int i = pr >> 8, c = pr & 255;
+        const double v = 0.5 * (Vxx[i * LDN + c] + Vxx[c * LDN + i]);
+        Vxx[i * LDN + c] = v;
+        Vxx[c * LDN + i] = v;
+      }
+      gsync<NWG>(grp);
     }
-    gsync<NWG>(grp);
   }
   if (!SERIAL) {
     for (int pp = gt; pp < NP; pp += NT) {
       const int pr = pairs[pp];
       const int i = pr >> 8, c = pr & 255;
-      const double w = 0.5 * (Vzz[i * LDN + c] + Vzz[c * LDN + i]);
+      // SEL: only the lower triangle (c < i) was updated -- mirror it
+      const double w = SEL ? Vzz[c * LDN + i] : 0.5 * (Vzz[i * LDN + c] + Vzz[c * LDN + i]);
       Vzz[i * LDN + c] = w;
       Vzz[c * LDN + i] = w;
     }
