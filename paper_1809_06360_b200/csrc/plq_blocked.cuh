@@ -222,7 +222,127 @@ __device__ __forceinline__ void gtrsm8(const double* T, int m, int ldt, const do
 // Y = V' C (DMMA, K = r - p0) and C -= VT Y (DMMA, K = 8).
 // On exit A holds R (upper) and V (strictly lower), rdiag = diag(R).
 // Scratch: Tm 64 doubles, VT r * 8 doubles, wsc NWG * 64.
-template <int NWG, class Sync>
+// RS > 0: warp 0 holds the panel in registers (row li = lane + 32 s, s < RS;
+// needs r <= 32 RS) and batches the independent warp reductions of each
+// column step; RS = 0: the panel stays in memory (any r, fewer registers).
+template <int N8>
+__device__ __forceinline__ void warp_sum_batch(double (&v)[N8]) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < N8; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+}
+
+template <int RS>
+__device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb, int rows, double* rdiag,
+                                              double* VT, int lane) {
+  double a[RS][8];
+#pragma unroll
+  for (int s = 0; s < RS; ++s)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int li = lane + 32 * s;
+      a[s][c] = (li < rows && c < pb) ? A[(p0 + li) * lda + p0 + c] : 0.0;
+    }
+  double tau[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    tau[j] = 0.0;
+    if (j < pb) {
+      double part = 0.0;
+#pragma unroll
+      for (int s = 0; s < RS; ++s) part += (lane + 32 * s > j) ? a[s][j] * a[s][j] : 0.0;
+      const double sig = warp_sum(part);
+      const double alpha = __shfl_sync(0xffffffffu, a[0][j], j);
+      double t = 0.0, beta = alpha, scale = 0.0;
+      if (sig > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + sig), alpha);
+        t = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      tau[j] = t;
+      double v[RS];
+#pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        const int li = lane + 32 * s;
+        v[s] = (li == j) ? 1.0 : (li > j ? a[s][j] * scale : 0.0);
+      }
+      // H_j applied to the columns k > j: a_k -= t v (v' a_k), all sums at once
+      double pk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        pk[k] = 0.0;
+        if (k > j) {
+#pragma unroll
+          for (int s = 0; s < RS; ++s) pk[k] += v[s] * a[s][k];
+        }
+      }
+      warp_sum_batch(pk);
+#pragma unroll
+      for (int k = j + 1; k < 8; ++k)
+#pragma unroll
+        for (int s = 0; s < RS; ++s) a[s][k] -= t * pk[k] * v[s];
+#pragma unroll
+      for (int s = 0; s < RS; ++s) {
+        const int li = lane + 32 * s;
+        if (li > j) a[s][j] = v[s];
+        if (li == j) a[s][j] = beta;
+      }
+      if (lane == 0) rdiag[p0 + j] = beta;
+    }
+  }
+  // T (upper): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] (V' v_j)[0:j]
+  double Tr[8][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w[i] = 0.0;
+      if (i < j) {
+#pragma unroll
+        for (int s = 0; s < RS; ++s) {
+          const int li = lane + 32 * s;
+          const double vi = (li == i) ? 1.0 : (li > i ? a[s][i] : 0.0);
+          const double vj = (li == j) ? 1.0 : (li > j ? a[s][j] : 0.0);
+          w[i] += vi * vj;
+        }
+      }
+    }
+    warp_sum_batch(w);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Tr[i][j] = 0.0;
+    Tr[j][j] = tau[j];
+#pragma unroll
+    for (int i = 0; i < j; ++i) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = i; k < j; ++k) sacc += Tr[i][k] * w[k];
+      Tr[i][j] = -tau[j] * sacc;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < RS; ++s) {
+    const int li = lane + 32 * s;
+    if (li < rows) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < pb) A[(p0 + li) * lda + p0 + c] = a[s][c];
+      double v[8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) v[l] = (l >= pb || li < l) ? 0.0 : (li == l ? 1.0 : a[s][l]);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int l = c; l < 8; ++l) sacc += v[l] * Tr[c][l];
+        VT[li * 8 + c] = sacc;
+      }
+    }
+  }
+}
+
+template <int NWG, class Sync, int RS = 0>
 __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X, int W, int ldx, double* rdiag,
                                      double* VT, double* wsc, int gt, Sync sync) {
   const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, q = lane & 3;
@@ -230,7 +350,9 @@ __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X
   for (int p0 = 0; p0 < M; p0 += 8) {
     const int pb = min(8, M - p0);
     const int rows = r - p0;   // panel rows p0 .. r-1 (local index li)
-    if (gw == 0) {
+    if constexpr (RS > 0) {
+      if (gw == 0) qr_panel_regs<RS>(A, lda, p0, pb, rows, rdiag, VT, lane);
+    } else if (gw == 0) {
       double tau[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {

@@ -521,7 +521,8 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         // blocked compact-WY QR: the TAU slot (M*M >= 8N + 8*64 doubles) holds
         // V T' and the per-warp tiles
         static_assert(M * M >= N * 8 + NWG * 64, "TAU slot too small for the blocked QR");
-        gqr8<NWG>(NTb + N, r, M, LDF, H, W, LDW, rdiag, tau, tau + N * 8, gt, [&] { gsync<NWG>(grp); });
+        auto sy = [&] { gsync<NWG>(grp); };
+        gqr8<NWG, decltype(sy), (N + 31) / 32>(NTb + N, r, M, LDF, H, W, LDW, rdiag, tau, tau + N * 8, gt, sy);
       } else {
         gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
