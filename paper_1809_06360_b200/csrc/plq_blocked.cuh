@@ -233,9 +233,11 @@ __device__ __forceinline__ void warp_sum_batch(double (&v)[N8]) {
     for (int k = 0; k < N8; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
 }
 
+// TS != nullptr keeps T (8 x 8) in shared memory instead of registers (for
+// register-capped 16-warp CTAs).
 template <int RS>
 __device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb, int rows, double* rdiag,
-                                              double* VT, int lane) {
+                                              double* VT, int lane, double* TS = nullptr) {
   double a[RS][8];
 #pragma unroll
   for (int s = 0; s < RS; ++s)
@@ -310,15 +312,34 @@ __device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb
       }
     }
     warp_sum_batch(w);
+    if (TS != nullptr) {
+      double col[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) Tr[i][j] = 0.0;
-    Tr[j][j] = tau[j];
+      for (int i = 0; i < 8; ++i) {
+        double sacc = 0.0;
+        if (i < j) {
 #pragma unroll
-    for (int i = 0; i < j; ++i) {
-      double sacc = 0.0;
+          for (int k = i; k < j; ++k) sacc += TS[i * 8 + k] * w[k];
+        }
+        col[i] = (i < j) ? -tau[j] * sacc : (i == j ? tau[j] : 0.0);
+      }
+      __syncwarp();
+      if (lane == 0) {
 #pragma unroll
-      for (int k = i; k < j; ++k) sacc += Tr[i][k] * w[k];
-      Tr[i][j] = -tau[j] * sacc;
+        for (int i = 0; i < 8; ++i) TS[i * 8 + j] = col[i];
+      }
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) Tr[i][j] = 0.0;
+      Tr[j][j] = tau[j];
+#pragma unroll
+      for (int i = 0; i < j; ++i) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int k = i; k < j; ++k) sacc += Tr[i][k] * w[k];
+        Tr[i][j] = -tau[j] * sacc;
+      }
     }
   }
 #pragma unroll
@@ -335,7 +356,7 @@ __device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb
       for (int c = 0; c < 8; ++c) {
         double sacc = 0.0;
 #pragma unroll
-        for (int l = c; l < 8; ++l) sacc += v[l] * Tr[c][l];
+        for (int l = c; l < 8; ++l) sacc += v[l] * (TS != nullptr ? TS[c * 8 + l] : Tr[c][l]);
         VT[li * 8 + c] = sacc;
       }
     }
@@ -344,14 +365,14 @@ __device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb
 
 template <int NWG, class Sync, int RS = 0>
 __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X, int W, int ldx, double* rdiag,
-                                     double* VT, double* wsc, int gt, Sync sync) {
+                                     double* VT, double* wsc, int gt, Sync sync, double* TS = nullptr) {
   const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, q = lane & 3;
   double* ws = wsc + gw * 64;
   for (int p0 = 0; p0 < M; p0 += 8) {
     const int pb = min(8, M - p0);
     const int rows = r - p0;   // panel rows p0 .. r-1 (local index li)
     if constexpr (RS > 0) {
-      if (gw == 0) qr_panel_regs<RS>(A, lda, p0, pb, rows, rdiag, VT, lane);
+      if (gw == 0) qr_panel_regs<RS>(A, lda, p0, pb, rows, rdiag, VT, lane, TS);
     } else if (gw == 0) {
       double tau[8];
 #pragma unroll

@@ -38,6 +38,7 @@ struct LinkLevel {
   double* X;     // (B,E,n,n)
   double* cL;    // (B,E,n)
   double* cR;    // (B,E,n)
+  double* Linv;  // (B,E,ceil(n/8)*64) diagonal-block inverses (split path)
   int K, E, top;
 };
 
@@ -76,6 +77,7 @@ LinkPlan plan_link(int64_t B, int J, int n, double* base) {
     L.X = take(B * L.E * nn);
     L.cL = take(B * L.E * n);
     L.cR = take(B * L.E * n);
+    L.Linv = take(B * L.E * ((n + 7) / 8) * 64);
     P.lv.push_back(L);
     if (L.top) break;
     K = (K + 1) / 2;
@@ -307,6 +309,131 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
     cta_gemm<true, false, 1, 1>(2 * n, w, n, Wm, ldw, Wm, ldw, gram);
 }
 
+// ---- large blocks (n > 64): one elimination split over many CTAs ---------
+// The elimination of a level is its critical path, and the deep levels have
+// only a few blocks (cfg3: 127, 64, ..., 1 of n = 128), so for n > 64 each
+// block's elimination runs as three kernels: the blocked Cholesky (one CTA
+// per block), the forward solve W = L^{-1}[A(i,i-1) | A(i,i+1) | b_i] in
+// column slabs (LINK_SLABS CTAs per block), and the Gram products in 64 x 64
+// tiles (LINK_GRAM_TILES CTAs per block).  Same arithmetic as link_eliminate.
+constexpr int LINK_SLABS = 4;        // column slabs of W (w = 2n+1 columns)
+constexpr int LINK_SLAB_LD = 76;     // widest slab: ceil(w/32)*8 <= 72 for n <= 128, stride = 4 (mod 8)
+
+__host__ __device__ inline int link_ldl_big(int n) { return n + ((12 - n % 8) % 8); }   // = 4 (mod 8)
+
+__host__ __device__ inline void link_slab(int w, int sidx, int* c0, int* c1) {
+  const int base = ((w + 31) / 32) * 8;   // multiple of 8 (72, 72, 72, 41 at n = 128)
+  *c0 = sidx * base;
+  *c1 = (sidx == LINK_SLABS - 1) ? w : (sidx + 1) * base;
+}
+
+__global__ void __launch_bounds__(256) link_factor_big(plq_problem_t p, LinkLevel L, int32_t* status) {
+  __shared__ int flag;
+  extern __shared__ __align__(16) double dsm[];
+  const int n = p.n, K = L.K, E = L.E, ldl = n + 1, nbk = (n + 7) / 8;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t b = blockIdx.x / E;
+  const int o = blockIdx.x % E;
+  const int i = L.top ? 0 : 2 * o + 1;
+  const double* D = L.D + (b * K + i) * nn;
+  double* Lc = dsm;
+  double* Ld = dsm + (((size_t)n * ldl + 1) & ~size_t(1));
+  double* Linv = L.Linv + (b * E + o) * nbk * 64;
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[(idx / n) * ldl + idx % n] = D[idx];
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  if (!gchol8<8>(Lc, n, ldl, Linv, &flag, threadIdx.x, [] { __syncthreads(); }, Ld)) {
+    flag_singular(p, status, b);
+    return;
+  }
+  double* gLc = L.Lc + (b * E + o) * nn;
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+    const int r = idx / n, c = idx % n;
+    gLc[idx] = c <= r ? Lc[r * ldl + c] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) link_trsm_big(plq_problem_t p, LinkLevel L, const int32_t* status) {
+  extern __shared__ __align__(16) double dsm[];
+  const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1, nbk = (n + 7) / 8;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t b = blockIdx.x / (E * LINK_SLABS);
+  const int o = (blockIdx.x / LINK_SLABS) % E;
+  const int sidx = blockIdx.x % LINK_SLABS;
+  if (status[b * p.J] == PLQ_STATUS_LINK_SINGULAR) return;
+  const int i = L.top ? 0 : 2 * o + 1;
+  int c0, c1;
+  link_slab(w, sidx, &c0, &c1);
+  const int sw = c1 - c0;
+  const bool has_l = !L.top && i >= 1, has_r = !L.top && i + 1 < K;
+  const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;
+  const double* Sr = has_r ? L.S + (b * (K - 1) + i) * nn : nullptr;
+  const double* rh = L.rhs + (b * K + i) * n;
+  const double* gLc = L.Lc + (b * E + o) * nn;
+  const int lls = link_ldl_big(n);
+  double* Ls = dsm;                                   // n x lls (factor)
+  double* Li = Ls + (size_t)n * lls;                  // nbk * 64
+  double* X = Li + nbk * 64;                          // n x LINK_SLAB_LD
+  double* wsc = X + (size_t)n * LINK_SLAB_LD;          // 8 * 64
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Ls[(idx / n) * lls + idx % n] = gLc[idx];
+  for (int idx = threadIdx.x; idx < nbk * 64; idx += blockDim.x) Li[idx] = L.Linv[(b * E + o) * nbk * 64 + idx];
+  for (int idx = threadIdx.x; idx < n * sw; idx += blockDim.x) {
+    const int r = idx / sw, c = c0 + idx % sw;
+    double v;
+    if (c < n)
+      v = has_l ? Sl[r * n + c] : 0.0;
+    else if (c < 2 * n)
+      v = has_r ? Sr[(c - n) * n + r] : 0.0;
+    else
+      v = rh[r];
+    X[r * LINK_SLAB_LD + (c - c0)] = v;
+  }
+  __syncthreads();
+  gtrsm8<0, 8>(Ls, n, lls, Li, X, sw, LINK_SLAB_LD, wsc, threadIdx.x, [] { __syncthreads(); });
+  double* gWm = L.Wm + (b * E + o) * n * w;
+  for (int idx = threadIdx.x; idx < n * sw; idx += blockDim.x) {
+    const int r = idx / sw, c = idx % sw;
+    gWm[r * w + c0 + c] = X[r * LINK_SLAB_LD + c];
+  }
+}
+
+// Gram tiles of W'W: CL = W_L'W_L, X = W_R'W_L, CR = W_R'W_R (n x n each, in
+// 64 x 64 tiles), cL = W_L'W_b, cR = W_R'W_b (one 2n x 1 column, tile 0 of
+// the extra row).  grid = B * E * (3 * (n/64)^2 + 1)
+__global__ void __launch_bounds__(256) link_gram_big(plq_problem_t p, LinkLevel L, const int32_t* status) {
+  extern __shared__ __align__(16) double tiles[];
+  const int n = p.n, E = L.E, w = 2 * n + 1, nt = (n + 63) / 64, per = 3 * nt * nt + 1;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t b = blockIdx.x / (E * per);
+  const int o = (blockIdx.x / per) % E;
+  const int t = blockIdx.x % per;
+  if (status[b * p.J] == PLQ_STATUS_LINK_SINGULAR) return;
+  const double* Wm = L.Wm + (b * E + o) * n * w;
+  double* CL = L.CL + (b * E + o) * nn;
+  double* CR = L.CR + (b * E + o) * nn;
+  double* Xo = L.X + (b * E + o) * nn;
+  if (t == per - 1) {
+    // [cL; cR] = [W_L W_R]' W_b : 2n outputs, thread per output
+    for (int r = threadIdx.x; r < 2 * n; r += blockDim.x) {
+      double acc = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < n; ++k) acc += Wm[k * w + r] * Wm[k * w + 2 * n];
+      if (r < n)
+        L.cL[(b * E + o) * n + r] = acc;
+      else
+        L.cR[(b * E + o) * n + r - n] = acc;
+    }
+    return;
+  }
+  const int blk = t / (nt * nt), tt = t % (nt * nt), ti = tt / nt, tj = tt % nt;
+  // blk 0: CL (rows W_L, cols W_L); 1: X (rows W_R, cols W_L); 2: CR (rows W_R, cols W_R)
+  const int ra = (blk == 0 ? 0 : n) + ti * 64, cb = (blk == 2 ? n : 0) + tj * 64;
+  double* dst = blk == 0 ? CL : (blk == 1 ? Xo : CR);
+  const int M = min(64, n - ti * 64), N = min(64, n - tj * 64);
+  cta_gemm_tiled<true, 8>(M, N, n, Wm + ra, w, Wm + cb, w, tiles,
+                          [&](int r, int c, double acc) { dst[(ti * 64 + r) * n + tj * 64 + c] = acc; });
+}
+
 // next level's system on the even blocks
 __global__ void link_assemble_next(plq_problem_t p, LinkLevel L, LinkLevel N) {
   const int n = p.n, K = L.K, E = L.E, K2 = N.K;
@@ -412,6 +539,33 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
     }
     return;
   }
+  if (n > 64) {
+    // blocked x = L^{-T} v with the diagonal-block inverses of the split
+    // elimination: per 8-row block, warp j reduces row k0 + j over the solved
+    // rows, then x_k = Linv_k' r
+    const int nbk = (n + 7) / 8, lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const double* Li = L.Linv + (b * E + o) * nbk * 64;
+    double* rr = v + n;   // 8 doubles (v has n + 2 + ...)
+    for (int kb = nbk - 1; kb >= 0; --kb) {
+      const int k0 = kb * 8, rb = min(8, n - k0);
+      for (int jj = wp; jj < rb; jj += blockDim.x >> 5) {
+        const int j = k0 + jj;
+        double t = 0.0;
+        for (int c = k0 + rb + lane; c < n; c += 32) t += Lc[c * n + j] * v[c];
+        t = warp_sum(t);
+        if (lane == 0) rr[jj] = v[j] - t;
+      }
+      __syncthreads();
+      if (threadIdx.x < rb) {
+        double xt = 0.0;
+        for (int j = 0; j < rb; ++j) xt += Li[kb * 64 + j * 8 + threadIdx.x] * rr[j];
+        v[k0 + threadIdx.x] = xt;
+      }
+      __syncthreads();
+    }
+    for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = v[r];
+    return;
+  }
   const double* Lp = sm ? Ls : Lc;
   const int lp = sm ? ldl : n;
   for (int r = n - 1; r >= 0; --r) {
@@ -490,9 +644,28 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
     const int eldl = elsm ? p.n + 1 : p.n, eldw = esm ? ldw : w;
     const size_t tsm = sizeof(double) * (link_elim_blocked_off(p.n, esm, elsm, eldl, eldw, ethreads) +
                                          link_elim_blocked_doubles(p.n));
-    if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-    link_eliminate<<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], status);
-    ++nl;
+    if (p.n > 64) {
+      const LinkLevel& Lv = P.lv[l];
+      const int nbk = (p.n + 7) / 8, nt = (p.n + 63) / 64;
+      const size_t fsm = sizeof(double) * (((size_t)p.n * (p.n + 1) + 1) / 2 * 2 + nbk * 64);
+      const size_t rsm =
+          sizeof(double) * ((size_t)p.n * link_ldl_big(p.n) + nbk * 64 + (size_t)p.n * LINK_SLAB_LD + 8 * 64);
+      const size_t gsm = sizeof(double) * TileCfg<8>::DOUBLES;
+      cudaFuncSetAttribute(link_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+      cudaFuncSetAttribute(link_trsm_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+      if (gsm > 48 * 1024) cudaFuncSetAttribute(link_gram_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
+      link_factor_big<<<B * Lv.E, 256, fsm, s>>>(p, Lv, status);
+      link_trsm_big<<<B * Lv.E * LINK_SLABS, 256, rsm, s>>>(p, Lv, status);
+      nl += 2;
+      if (!Lv.top) {
+        link_gram_big<<<B * Lv.E * (3 * nt * nt + 1), 256, gsm, s>>>(p, Lv, status);
+        ++nl;
+      }
+    } else {
+      if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      link_eliminate<<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], status);
+      ++nl;
+    }
     if (!P.lv[l].top) {
       link_assemble_next<<<B * P.lv[l + 1].K, threads, 0, s>>>(p, P.lv[l], P.lv[l + 1]);
       ++nl;
@@ -500,7 +673,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   }
   for (int l = (int)P.lv.size() - 1; l >= 0; --l) {
     const LinkLevel& C = P.lv[l + 1 < (int)P.lv.size() ? l + 1 : l];
-    const size_t bsm = sizeof(double) * (p.n + 2 + (p.n <= 64 ? (size_t)p.n * (p.n + 1) + 4 + (size_t)p.n * p.n +
+    const size_t bsm = sizeof(double) * (p.n + 10 + (p.n <= 64 ? (size_t)p.n * (p.n + 1) + 4 + (size_t)p.n * p.n +
                                                               (size_t)p.n * (2 * p.n + 1) + 2 * p.n + 2 : 0));
     if (bsm > 48 * 1024) cudaFuncSetAttribute(link_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     link_backsub<<<B * P.lv[l].K, threads, bsm, s>>>(p, P.lv[l], C, l + 1 < (int)P.lv.size());

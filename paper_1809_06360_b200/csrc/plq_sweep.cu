@@ -296,7 +296,9 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       for (int i = tid; i < r; i += nt) H[i * ldw + cc] += VF[i * Fw + n + m];
       __syncthreads();
       if (r >= m) {
-        if (blocked)
+        if (blocked && NT == 512 && r <= 128)
+          gqr8<NT / 32, decltype(csync), 4>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync, vts + 8 * n);
+        else if (blocked)
           gqr8<NT / 32>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync);
         else
           cta_householder_qr(VF + n, r, m, Fw, H, W, ldw, tau, rdiag, red);
@@ -501,7 +503,7 @@ SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
   sz[SB_MUU] = 2LL * m * m;
   // tau, rdiag, reduction (32), flags (2), blocked scratch: block inverses,
   // per-warp tiles, V T' (plq_blocked.cuh)
-  sz[SB_MISC] = 2LL * m + 32 + 2 + ((m + 7) / 8) * 64LL + (threads / 32) * 64LL + 8LL * n;
+  sz[SB_MISC] = 2LL * m + 32 + 2 + ((m + 7) / 8) * 64LL + (threads / 32) * 64LL + 8LL * n + 64;
   sz[SB_VF] = n * Fw;
   sz[SB_Z] = n * Fw;
   sz[SB_MX] = (int64_t)n * (n + 1);

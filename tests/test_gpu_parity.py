@@ -296,3 +296,18 @@ def test_cuda_graph_replay_is_bitwise_identical(cfg_id, T, J, B):
     torch.cuda.synchronize()
     for k in ("K", "k", "x", "u", "lam", "objective", "kkt_inf"):
         assert torch.equal(s.out[k], ref.out[k]), k
+
+
+@pytest.mark.parametrize("n,m,T,J", [(72, 24, 96, 12), (100, 20, 128, 16), (127, 5, 160, 6)])
+def test_large_n_split_link_vs_oracle(n, m, T, J, kernel_path):
+    """n > 64: the link elimination runs split over CTAs (blocked Cholesky,
+    column-slab forward solve, Gram tiles) and the blocked back-substitution;
+    ragged 8-blocks (n % 8 != 0) and a BCR depth of several levels."""
+    from paper_1809_06360_b200 import synth
+    cfg = synth.CONFIGS[3].scaled(n=n, m=m, T=T, J=J, B=1)
+    batch = synth.generate_batch(cfg, seed=777, count=1)
+    g, _ = _gpu_batch(batch, J=J)
+    prob = O.problem_slice(batch, 0)
+    ref = O.solve(prob, J=J)
+    floors = _floor(prob, J, ref)
+    _check(g, 0, ref, floors)
