@@ -218,33 +218,64 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   for (int s = L - 1; s >= 0; --s) {
     const int64_t st = b * T + (lo + s);
     // ---- stage inputs -> shared/scratch (coalesced global reads)
+    // (streaming loads: read once, so they do not evict the L2-resident scratch)
     for (int idx = tid; idx < nn; idx += nt) {
-      F[(idx / n) * Fw + idx % n] = p.Fx[st * nn + idx];
-      Qxx[idx] = p.Qxx[st * nn + idx];
+      F[(idx / n) * Fw + idx % n] = __ldcs(p.Fx + st * nn + idx);
+      Qxx[idx] = __ldcs(p.Qxx + st * nn + idx);
     }
     for (int idx = tid; idx < n * m; idx += nt) {
-      F[(idx / m) * Fw + n + idx % m] = p.Fu[st * n * m + idx];
-      Qux[idx] = p.Qux[st * m * n + idx];
+      F[(idx / m) * Fw + n + idx % m] = __ldcs(p.Fu + st * n * m + idx);
+      Qux[idx] = __ldcs(p.Qux + st * m * n + idx);
     }
     for (int i = tid; i < n; i += nt) {
-      F[i * Fw + n + m] = p.f1[st * n + i];
-      qx1[i] = p.qx1[st * n + i];
+      F[i * Fw + n + m] = __ldcs(p.f1 + st * n + i);
+      qx1[i] = __ldcs(p.qx1 + st * n + i);
     }
-    for (int idx = tid; idx < m * m; idx += nt) Quu[idx] = p.Quu[st * m * m + idx];
-    for (int i = tid; i < m; i += nt) qu1[i] = p.qu1[st * m + i];
+    for (int idx = tid; idx < m * m; idx += nt) Quu[idx] = __ldcs(p.Quu + st * m * m + idx);
+    for (int i = tid; i < m; i += nt) qu1[i] = __ldcs(p.qu1 + st * m + i);
     __syncthreads();
 
-    // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217)
-    gemm_x<false, NT>(n + nz, Fw, n, bf.V, n, F, Fw, bf.tiles, [&](int i, int c, double acc) {
+    // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217).
+    // The f1 column ([w; mz1] = [Vxx; Vzx] f1 + [vx1; vz1]) is a thread-per-row
+    // matvec, so the GEMM's N is n + m (a whole 64-wide tile less in large mode)
+    gemm_x<false, NT>(n + nz, Fw - 1, n, bf.V, n, F, Fw, bf.tiles, [&](int i, int c, double acc) {
       if (i < n) {
-        VF[i * Fw + c] = (c == n + m) ? vx1[i] + acc : acc;
+        VF[i * Fw + c] = acc;
       } else {
-        Z[(i - n) * Fw + c] = (c == n + m) ? vz1[i - n] + acc : acc;
+        Z[(i - n) * Fw + c] = acc;
       }
     });
+    for (int i = tid; i < n + nz; i += nt) {
+      const double* vr = bf.V + (size_t)i * n;
+      double t0 = 0.0, t1 = 0.0;
+      int k = 0;
+      for (; k + 1 < n; k += 2) {
+        t0 += vr[k] * F[k * Fw + n + m];
+        t1 += vr[k + 1] * F[(k + 1) * Fw + n + m];
+      }
+      if (k < n) t0 += vr[k] * F[k * Fw + n + m];
+      if (i < n)
+        VF[i * Fw + n + m] = vx1[i] + (t0 + t1);
+      else
+        Z[(i - n) * Fw + n + m] = vz1[i - n] + (t0 + t1);
+    }
     __syncthreads();
-    // ---- GEMM2: M-terms (endpoint.py:209-211, 215-216)
-    gemm_x<true, NT>(n + m, Fw, n, F, Fw, VF, Fw, bf.tiles, [&](int i, int c, double acc) {
+    // ---- GEMM2: M-terms (endpoint.py:209-211, 215-216); the w column
+    // (mx1 = qx1 + Fx' w, mu1 = qu1 + Fu' w) again as a matvec
+    for (int i = tid; i < n + m; i += nt) {
+      double t0 = 0.0, t1 = 0.0;
+      int k = 0;
+      for (; k + 1 < n; k += 2) {
+        t0 += F[k * Fw + i] * VF[k * Fw + n + m];
+        t1 += F[(k + 1) * Fw + i] * VF[(k + 1) * Fw + n + m];
+      }
+      if (k < n) t0 += F[k * Fw + i] * VF[k * Fw + n + m];
+      if (i < n)
+        MX[i * (n + 1) + n] = qx1[i] + (t0 + t1);
+      else
+        P[(i - n) * ldw + cc] = qu1[i - n] + (t0 + t1);
+    }
+    gemm_x<true, NT>(n + m, Fw - 1, n, F, Fw, VF, Fw, bf.tiles, [&](int i, int c, double acc) {
       if (i < n) {
         if (c < n) {
           MX[i * (n + 1) + c] = Qxx[i * n + c] + acc;
@@ -398,24 +429,28 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     gemm_x<false, NT>(m, W, m, Muu, m, G, ldw, bf.tiles,
                   [&](int i, int c, double acc) { Y[i * ldw + c] = P[i * ldw + c] + acc; });
     __syncthreads();
-    gemm_x<true, NT>(n + nz, W, 2 * m, P, ldw, G, ldw, bf.tiles, [&](int i, int c, double acc) {
-      if (i < n) {
-        if (c < n) {
-          Vxx[i * n + c] = MX[i * (n + 1) + c] + acc;
-        } else if (c == cc) {
-          vx1[i] = MX[i * (n + 1) + n] + acc;
-        }
-      } else {
-        const int zi = i - n;
-        if (c < n) {
+    // V += [P; G]'[G; Y]: x rows over the x columns only (no discarded Vxz
+    // block), z rows over [x | z] columns, the constant column as a matvec
+    gemm_x<true, NT>(n, n, 2 * m, P, ldw, G, ldw, bf.tiles,
+                     [&](int i, int c, double acc) { Vxx[i * n + c] = MX[i * (n + 1) + c] + acc; });
+    if (nz)
+      gemm_x<true, NT>(nz, 2 * n, 2 * m, P + n, ldw, G, ldw, bf.tiles, [&](int zi, int c, double acc) {
+        if (c < n)
           Vzx[zi * n + c] = Z[zi * Fw + c] + acc;
-        } else if (c < cc) {
+        else
           Vzz[zi * n + (c - n)] += acc;
-        } else {
-          vz1[zi] = Z[zi * Fw + n + m] + acc;
-        }
+      });
+    for (int i = tid; i < n + nz; i += nt) {
+      double t0 = 0.0, t1 = 0.0;
+      for (int k = 0; k < 2 * m; k += 2) {
+        t0 += P[k * ldw + i] * G[k * ldw + cc];
+        t1 += P[(k + 1) * ldw + i] * G[(k + 1) * ldw + cc];
       }
-    });
+      if (i < n)
+        vx1[i] = MX[i * (n + 1) + n] + (t0 + t1);
+      else
+        vz1[i - n] = Z[(i - n) * Fw + n + m] + (t0 + t1);
+    }
     __syncthreads();
     // symmetrize Vxx (and Vzz): 0.5 * (V + V')
     for (int idx = tid; idx < nn; idx += nt) {
