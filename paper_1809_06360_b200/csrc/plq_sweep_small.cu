@@ -524,6 +524,8 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         auto sy = [&] { gsync<NWG>(grp); };
         gqr8<NWG, decltype(sy), (N + 31) / 32>(NTb + N, r, M, LDF, H, W, LDW, rdiag, tau, tau + N * 8, gt, sy);
       } else {
+        // n = 32 (M = 8, one panel, H on chip): the column-wise group QR
+        // (measured faster here than gqr8: 2.46 vs 2.51 ms cfg2 sweep)
         gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
       double rmax = 0.0, rmin = 1e308;
@@ -675,7 +677,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     constexpr int VTM = (N + NZ) / 8;
     auto vband = [](int w, int slot) { return slot == 0 ? w : (VTM > NWG ? VTM - 1 - w : -1); };
     auto von = [](int tm, int tn) { return tm < XB ? tn <= tm : (tn < XB || tn - XB <= tm - XB); };
-    auto vzero = [](int, int) { return 0.0; };
+    // Vzz (global scratch when BIG) is read before the k-loop (its latency
+    // hides behind the DMMAs) and written back as pre + acc
+    auto vzero = [&](int i, int c) { return (i >= N && c >= N && c - N <= i - N) ? Vzz[(i - N) * LDN + (c - N)] : 0.0; };
     auto vsel = [&](int i, int c, double acc) {
       if (i < N) {
         if (c <= i) {
@@ -688,7 +692,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         if (c < N)
           Vzx[zi * LDN + c] += acc;
         else if (c - N <= zi)
-          Vzz[zi * LDN + (c - N)] += acc;
+          Vzz[zi * LDN + (c - N)] = acc;   // acc = Vzz (pre) + update
       }
     };
     if (constrained) {
