@@ -69,6 +69,7 @@ Plan make_plan(const plq_problem_t* p) {
   Plan P;
   const int64_t B = p->B, T = p->T, n = p->n, m = p->m, J = p->J;
   P.threads = plq::sweep_threads(p->n);
+  if (const char* e = getenv("PLQ_SWEEP_THREADS")) P.threads = atoi(e);   // measurement override
   const size_t budget = 200 * 1024;
   P.lay = plq::plan_sweep(p->n, p->m, P.threads, budget);
   P.smem = (size_t)P.lay.smem_doubles * sizeof(double);

@@ -22,6 +22,7 @@
 #include "plq_device.cuh"
 #include "plq_gemm.cuh"
 #include "plq_internal.h"
+#include "plq_tma.cuh"
 
 #include <algorithm>
 
@@ -327,7 +328,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       for (int i = tid; i < r; i += nt) H[i * ldw + cc] += VF[i * Fw + n + m];
       __syncthreads();
       if (r >= m) {
-        if (blocked && NT == 512 && r <= 128)
+        if (blocked && NT >= 256 && r <= 128)
           gqr8<NT / 32, decltype(csync), 4>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync, vts + 8 * n);
         else if (blocked)
           gqr8<NT / 32>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync);
@@ -452,18 +453,26 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         vz1[i - n] = Z[(i - n) * Fw + n + m] + (t0 + t1);
     }
     __syncthreads();
-    // symmetrize Vxx (and Vzz): 0.5 * (V + V')
+    // symmetrize Vxx: 0.5 * (V + V')
     for (int idx = tid; idx < nn; idx += nt) {
       const int i = idx / n, c = idx % n;
       if (i < c) {
         const double v = 0.5 * (Vxx[i * n + c] + Vxx[c * n + i]);
         Vxx[i * n + c] = v;
         Vxx[c * n + i] = v;
-        if (!serial) {
-          const double w = 0.5 * (Vzz[i * n + c] + Vzz[c * n + i]);
-          Vzz[i * n + c] = w;
-          Vzz[c * n + i] = w;
-        }
+      }
+    }
+    __syncthreads();
+  }
+  // Vzz is never a GEMM operand: symmetrizing it once per segment is the same
+  // linear map as every stage, sym(sym(A) + X) = sym(A + X)
+  if (!serial) {
+    for (int idx = tid; idx < nn; idx += nt) {
+      const int i = idx / n, c = idx % n;
+      if (i < c) {
+        const double w = 0.5 * (Vzz[i * n + c] + Vzz[c * n + i]);
+        Vzz[i * n + c] = w;
+        Vzz[c * n + i] = w;
       }
     }
     __syncthreads();
@@ -525,8 +534,10 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArg
 int sweep_threads(int n) {
   if (n <= 16) return 32;
   if (n <= 32) return 128;
-  if (n <= 64) return 256;
-  return 512;
+  // n > 32: 8-warp CTAs, two per SM (128 registers each); at n = 128 (cfg3)
+  // this keeps all 256 segments resident at once, so one segment's serial
+  // phases overlap the other's GEMMs (20.5 vs 25.0 ms sweep with 16-warp CTAs)
+  return 256;
 }
 
 SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {

@@ -479,6 +479,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         P[(gt - N) * LDW + CC] = qg + t;
     }
     if (s > 0) q_prefetch(st - 1);   // next stage's Q values, consumed one stage later
+
     gsync<NWG>(grp);
 
     const bool constrained = (r != 0);

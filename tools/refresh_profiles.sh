@@ -14,3 +14,9 @@ ls gpurun_out/refresh
 for k in sweep_small_kernel link_seq_kernel recon_seg_kernel; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o gpurun_out/refresh/cfg1_$k -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_full_$k.log 2>&1 || true
 done
+# full ncu captures of the dominant (sweep) kernel of the large-n configs, one launch each
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_small_kernel -c 1 -o gpurun_out/refresh/cfg4_sweep_small_kernel_full -f python bench.py --config 4 --steps 1 --warmup 0 --graph 0 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_full_cfg4.log 2>&1 || true
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -c 1 -o gpurun_out/refresh/cfg3_sweep_kernel_full -f python bench.py --config 3 --steps 1 --warmup 0 --graph 0 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_full_cfg3.log 2>&1 || true
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/refresh/launches_cfg4.csv python bench.py --config 4 --steps 1 --warmup 0 --graph 0 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_launch4.log 2>&1 || true
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/refresh/launches_cfg3.csv python bench.py --config 3 --steps 1 --warmup 0 --graph 0 --no-e2e --no-cpu-baseline --no-smooth --no-endpoint > gpurun_out/refresh/ncu_launch3.log 2>&1 || true
+ls gpurun_out/refresh
