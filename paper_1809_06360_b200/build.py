@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparlqr_b200.so")
-SOURCES = ("plq_sweep.cu", "plq_sweep_small.cu", "plq_link.cu", "plq_recon.cu", "plq_recon_small.cu",
+SOURCES = ("plq_sweep.cu", "plq_sweep_small.cu", "plq_link.cu", "plq_recon.cu", "plq_recon_small.cu", "plq_recon_ring.cu",
            "plq_smooth.cu", "plq_endpoint.cu", "plq_linkfeas.cu",
            "plq_api.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -30,9 +30,16 @@ struct TileCfg {
   static constexpr int DOUBLES = 2 * (BM * LDA + BK * LDB);
 };
 
-template <bool TA, int NW, class Epi>
+struct NoPre {
+  __device__ __forceinline__ double operator()(int, int) const { return 0.0; }
+};
+
+// PRE: pre(i, j) (e.g. a Q-block entry in HBM) is loaded before each tile's
+// k-loop and the epilogue receives pre(i, j) + acc
+template <bool TA, int NW, class Epi, bool PRE = false, class Pre = NoPre>
 __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double* __restrict__ A, int lda,
-                                               const double* __restrict__ B, int ldb, double* tiles, Epi epi) {
+                                               const double* __restrict__ B, int ldb, double* tiles, Epi epi,
+                                               Pre pre = Pre()) {
   using C = TileCfg<NW>;
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, LDA = C::LDA, LDB = C::LDB, NT = NW * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -45,11 +52,18 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
   const int tmc = (M + BM - 1) / BM, tnc = (N + BN - 1) / BN, kc = (K + BK - 1) / BK;
   for (int tile = 0; tile < tmc * tnc; ++tile) {
     const int m0 = (tile / tnc) * BM, n0 = (tile % tnc) * BN;
-    double acc[2][4][2];
+    double acc[2][4][2], pv[2][4][2];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) acc[r][t][0] = acc[r][t][1] = 0.0;
+      for (int t = 0; t < 4; ++t) {
+        acc[r][t][0] = acc[r][t][1] = 0.0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = m0 + wr * 16 + r * 8 + g, j = n0 + wc * 32 + t * 8 + 2 * q + e;
+          pv[r][t][e] = (PRE && i < M && j < N) ? pre(i, j) : 0.0;
+        }
+      }
     auto load = [&](int c, int buf) {
       const int k0 = c * BK;
       double* as = buf ? As1 : As0;
@@ -108,7 +122,7 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int i = m0 + wr * 16 + r * 8 + g, j = n0 + wc * 32 + t * 8 + 2 * q + e;
-          if (i < M && j < N) epi(i, j, acc[r][t][e]);
+          if (i < M && j < N) epi(i, j, PRE ? pv[r][t][e] + acc[r][t][e] : acc[r][t][e]);
         }
   }
 }

@@ -165,6 +165,8 @@ bool sweep_small_supported(int n, int m);
 size_t sweep_small_gscratch_doubles(int n, int m);   // per CTA (n >= 64 variants)
 int launch_sweep_small(const SweepArgs& a, cudaStream_t s);
 bool recon_small_supported(int n, int m);
+bool recon_split_supported(int n, int m);
+int launch_recon_split(const ReconArgs& a, cudaStream_t s);
 int launch_recon_small(const ReconArgs& a, cudaStream_t s);
 bool link_seq_supported(int n, int J);
 size_t link_seq_workspace_doubles(int64_t B, int J, int n);

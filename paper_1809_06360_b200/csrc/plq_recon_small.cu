@@ -9,6 +9,8 @@
 //     lane = state row, stage matrices staged in shared memory (odd strides:
 //     row-per-lane reads are bank-conflict free) with the next stage
 //     prefetched into registers.
+#include <stdlib.h>
+
 #include "plq_internal.h"
 #include "plq_small.cuh"
 #include "plq_tma.cuh"
@@ -1059,6 +1061,11 @@ int launch_recon_ring(const ReconArgs& a, cudaStream_t s) {
 bool recon_small_supported(int n, int m) { return (n == 12 && m == 4) || (n == 32 && m == 8) || (n == 64 && m == 32); }
 
 int launch_recon_small(const ReconArgs& a, cudaStream_t s) {
+  // n = 32 / 64: forward rollout, stage-parallel evaluation and backward
+  // multipliers as three streaming kernels (plq_recon_ring.cu); the fused
+  // single-kernel ring (PLQ_RECON_FUSED=1) is kept for measurement
+  const char* fused = getenv("PLQ_RECON_FUSED");
+  if (recon_split_supported(a.p.n, a.p.m) && !(fused && fused[0] == '1')) return launch_recon_split(a, s);
   if (a.p.n == 64 && a.p.m == 32) {
     if (a.p.max_seg_len <= 128) return launch_recon_ring<64, 32, 256, 1>(a, s);
     return -1;

@@ -49,6 +49,19 @@ __device__ __forceinline__ void gemm_x(int M, int N, int K, const double* A, int
   cta_gemm<TA, false, 1, 1>(M, N, K, A, lda, B, ldb, epi);
 }
 
+// gemm_x with an addend pre(i, j) loaded before the k-loop (epi gets pre + acc)
+template <bool TA, int NT, class Pre, class Epi>
+__device__ __forceinline__ void gemm_x_pre(int M, int N, int K, const double* A, int lda, const double* B, int ldb,
+                                           double* tiles, Pre pre, Epi epi) {
+  if constexpr (NT >= 256) {
+    if (tiles != nullptr && (long long)M * N * K >= 16384) {
+      cta_gemm_tiled<TA, NT / 32, Epi, true, Pre>(M, N, K, A, lda, B, ldb, tiles, epi, pre);
+      return;
+    }
+  }
+  cta_gemm<TA, false, 1, 1>(M, N, K, A, lda, B, ldb, [&](int i, int j, double acc) { epi(i, j, pre(i, j) + acc); });
+}
+
 __device__ __forceinline__ void cho_solve_x(const double* L, int m, int ldl, double* X, int W, int ldx) {
   if (m >= 16)
     cta_cho_solve_blocked(L, m, ldl, X, W, ldx);
@@ -220,20 +233,30 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     const int64_t st = b * T + (lo + s);
     // ---- stage inputs -> shared/scratch (coalesced global reads)
     // (streaming loads: read once, so they do not evict the L2-resident scratch)
+    // Large mode: the Q blocks are not copied -- GEMM2 reads them from the
+    // input arrays as addends loaded before its k-loop (less L2 scratch).
+    const bool qdirect = bf.tiles != nullptr;
+    const double* Qxx_s = qdirect ? p.Qxx + st * nn : Qxx;
+    const double* Qux_s = qdirect ? p.Qux + st * m * n : Qux;
+    const double* Quu_s = qdirect ? p.Quu + st * m * m : Quu;
+    const double* qx1_s = qdirect ? p.qx1 + st * n : qx1;
+    const double* qu1_s = qdirect ? p.qu1 + st * m : qu1;
     for (int idx = tid; idx < nn; idx += nt) {
       F[(idx / n) * Fw + idx % n] = __ldcs(p.Fx + st * nn + idx);
-      Qxx[idx] = __ldcs(p.Qxx + st * nn + idx);
+      if (!qdirect) Qxx[idx] = __ldcs(p.Qxx + st * nn + idx);
     }
     for (int idx = tid; idx < n * m; idx += nt) {
       F[(idx / m) * Fw + n + idx % m] = __ldcs(p.Fu + st * n * m + idx);
-      Qux[idx] = __ldcs(p.Qux + st * m * n + idx);
+      if (!qdirect) Qux[idx] = __ldcs(p.Qux + st * m * n + idx);
     }
     for (int i = tid; i < n; i += nt) {
       F[i * Fw + n + m] = __ldcs(p.f1 + st * n + i);
-      qx1[i] = __ldcs(p.qx1 + st * n + i);
+      if (!qdirect) qx1[i] = __ldcs(p.qx1 + st * n + i);
     }
-    for (int idx = tid; idx < m * m; idx += nt) Quu[idx] = __ldcs(p.Quu + st * m * m + idx);
-    for (int i = tid; i < m; i += nt) qu1[i] = __ldcs(p.qu1 + st * m + i);
+    if (!qdirect) {
+      for (int idx = tid; idx < m * m; idx += nt) Quu[idx] = __ldcs(p.Quu + st * m * m + idx);
+      for (int i = tid; i < m; i += nt) qu1[i] = __ldcs(p.qu1 + st * m + i);
+    }
     __syncthreads();
 
     // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217).
@@ -272,28 +295,27 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       if (k < n) t0 += F[k * Fw + i] * VF[k * Fw + n + m];
       if (i < n)
-        MX[i * (n + 1) + n] = qx1[i] + (t0 + t1);
+        MX[i * (n + 1) + n] = qx1_s[i] + (t0 + t1);
       else
-        P[(i - n) * ldw + cc] = qu1[i - n] + (t0 + t1);
+        P[(i - n) * ldw + cc] = qu1_s[i - n] + (t0 + t1);
     }
-    gemm_x<true, NT>(n + m, Fw - 1, n, F, Fw, VF, Fw, bf.tiles, [&](int i, int c, double acc) {
-      if (i < n) {
-        if (c < n) {
-          MX[i * (n + 1) + c] = Qxx[i * n + c] + acc;
-        } else if (c == n + m) {
-          MX[i * (n + 1) + n] = qx1[i] + acc;
-        }
-      } else {
-        const int u = i - n;
-        if (c < n) {
-          P[u * ldw + c] = Qux[u * n + c] + acc;
-        } else if (c < n + m) {
-          Muu[u * m + (c - n)] = Quu[u * m + (c - n)] + acc;
-        } else {
-          P[u * ldw + cc] = qu1[u] + acc;
-        }
-      }
-    });
+    gemm_x_pre<true, NT>(
+        n + m, n + m, n, F, Fw, VF, Fw, bf.tiles,
+        [&](int i, int c) {
+          return i < n ? (c < n ? Qxx_s[i * n + c] : 0.0)
+                       : (c < n ? Qux_s[(i - n) * n + c] : Quu_s[(i - n) * m + (c - n)]);
+        },
+        [&](int i, int c, double v) {
+          if (i < n) {
+            if (c < n) MX[i * (n + 1) + c] = v;
+          } else {
+            const int u = i - n;
+            if (c < n)
+              P[u * ldw + c] = v;
+            else
+              Muu[u * m + (c - n)] = v;
+          }
+        });
     // P z-block = Mzu' (Mzu = Vzx Fu lives in Z's middle columns)
     for (int idx = tid; idx < m * nz; idx += nt) {
       const int u = idx / nz, c = idx % nz;
