@@ -513,6 +513,21 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
         for (int c = 0; c < n; ++c) t += Ws[r * w + n + c] * xrs[c];
       v[r] = Ws[r * w + 2 * n] - t;
     }
+  } else if (n > 64) {
+    // stage the factor (coalesced) for the blocked solve below; v by one
+    // warp per row with the lanes over the (coalesced) columns of W
+    double* Lsb = v + ((n + 16) & ~1);
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lsb[(idx / n) * (n + 1) + idx % n] = Lc[idx];
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int r = threadIdx.x >> 5; r < n; r += nw) {
+      double t = 0.0;
+      for (int c = lane; c < n; c += 32) {
+        if (has_l) t += Wm[r * w + c] * xl[c];
+        if (has_r) t += Wm[r * w + n + c] * xr[c];
+      }
+      t = warp_sum(t);
+      if (lane == 0) v[r] = Wm[r * w + 2 * n] - t;
+    }
   } else {
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
       double s = Wm[r * w + 2 * n];
@@ -545,13 +560,14 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
     // rows, then x_k = Linv_k' r
     const int nbk = (n + 7) / 8, lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const double* Li = L.Linv + (b * E + o) * nbk * 64;
+    const double* Lsb = v + ((n + 16) & ~1);   // staged factor, stride n + 1
     double* rr = v + n;   // 8 doubles (v has n + 2 + ...)
     for (int kb = nbk - 1; kb >= 0; --kb) {
       const int k0 = kb * 8, rb = min(8, n - k0);
       for (int jj = wp; jj < rb; jj += blockDim.x >> 5) {
         const int j = k0 + jj;
         double t = 0.0;
-        for (int c = k0 + rb + lane; c < n; c += 32) t += Lc[c * n + j] * v[c];
+        for (int c = k0 + rb + lane; c < n; c += 32) t += Lsb[c * (n + 1) + j] * v[c];
         t = warp_sum(t);
         if (lane == 0) rr[jj] = v[j] - t;
       }
@@ -674,7 +690,8 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   for (int l = (int)P.lv.size() - 1; l >= 0; --l) {
     const LinkLevel& C = P.lv[l + 1 < (int)P.lv.size() ? l + 1 : l];
     const size_t bsm = sizeof(double) * (p.n + 10 + (p.n <= 64 ? (size_t)p.n * (p.n + 1) + 4 + (size_t)p.n * p.n +
-                                                              (size_t)p.n * (2 * p.n + 1) + 2 * p.n + 2 : 0));
+                                                              (size_t)p.n * (2 * p.n + 1) + 2 * p.n + 2
+                                                          : (size_t)p.n * (p.n + 1) + 8));
     if (bsm > 48 * 1024) cudaFuncSetAttribute(link_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     link_backsub<<<B * P.lv[l].K, threads, bsm, s>>>(p, P.lv[l], C, l + 1 < (int)P.lv.size());
     ++nl;

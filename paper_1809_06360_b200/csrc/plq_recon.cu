@@ -309,7 +309,11 @@ __global__ void finalize_kernel(plq_problem_t p, const double* part, const doubl
 int recon_threads(int n) {
   if (n <= 16) return 32;
   if (n <= 32) return 64;
-  return 128;
+  if (n <= 64) return 128;
+  // n > 64 (cfg3: 256 segments, fewer than two per SM): the per-stage
+  // matrix-vector products are latency bound, so spread their rows over
+  // 16 warps
+  return 512;
 }
 
 int grid_for(int64_t tasks, int threads) {
@@ -336,8 +340,11 @@ int launch_recon(const ReconArgs& a, cudaStream_t s) {
     case 64:
       recon_kernel<64><<<grid, 64, smem, s>>>(a);
       break;
-    default:
+    case 128:
       recon_kernel<128><<<grid, 128, smem, s>>>(a);
+      break;
+    default:
+      recon_kernel<512><<<grid, 512, smem, s>>>(a);
       break;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -1;

@@ -449,15 +449,23 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     for (int u = tid; u < m; u += nt) a.k1[st * m + u] = G[u * ldw + cc];
 
     // ---- value update (endpoint.py:285-294; serial.py:75-77)
-    gemm_x<false, NT>(m, W, m, Muu, m, G, ldw, bf.tiles,
-                  [&](int i, int c, double acc) { Y[i * ldw + c] = P[i * ldw + c] + acc; });
-    __syncthreads();
-    // V += [P; G]'[G; Y]: x rows over the x columns only (no discarded Vxz
-    // block), z rows over [x | z] columns, the constant column as a matvec
-    gemm_x<true, NT>(n, n, 2 * m, P, ldw, G, ldw, bf.tiles,
+    // Constrained stages: Y = P + Muu G and V += [P; G]'[G; Y] (the
+    // reference's terms).  Stages whose gains came from the Cholesky branch
+    // have G = -Muu^{-1} P, so Y = 0 in exact arithmetic and the update is the
+    // standard Riccati form V += P'G (K = m: half the update, no Y GEMM), as
+    // in the specialized kernels.
+    const int KV = chol ? m : 2 * m;
+    if (!chol) {
+      gemm_x<false, NT>(m, W, m, Muu, m, G, ldw, bf.tiles,
+                        [&](int i, int c, double acc) { Y[i * ldw + c] = P[i * ldw + c] + acc; });
+      __syncthreads();
+    }
+    // x rows over the x columns only (no discarded Vxz block), z rows over
+    // [x | z] columns, the constant column as a matvec
+    gemm_x<true, NT>(n, n, KV, P, ldw, G, ldw, bf.tiles,
                      [&](int i, int c, double acc) { Vxx[i * n + c] = MX[i * (n + 1) + c] + acc; });
     if (nz)
-      gemm_x<true, NT>(nz, 2 * n, 2 * m, P + n, ldw, G, ldw, bf.tiles, [&](int zi, int c, double acc) {
+      gemm_x<true, NT>(nz, 2 * n, KV, P + n, ldw, G, ldw, bf.tiles, [&](int zi, int c, double acc) {
         if (c < n)
           Vzx[zi * n + c] = Z[zi * Fw + c] + acc;
         else
@@ -465,10 +473,12 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       });
     for (int i = tid; i < n + nz; i += nt) {
       double t0 = 0.0, t1 = 0.0;
-      for (int k = 0; k < 2 * m; k += 2) {
+      int k = 0;
+      for (; k + 1 < KV; k += 2) {
         t0 += P[k * ldw + i] * G[k * ldw + cc];
         t1 += P[(k + 1) * ldw + i] * G[(k + 1) * ldw + cc];
       }
+      if (k < KV) t0 += P[k * ldw + i] * G[k * ldw + cc];
       if (i < n)
         vx1[i] = MX[i * (n + 1) + n] + (t0 + t1);
       else
