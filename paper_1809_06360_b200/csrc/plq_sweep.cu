@@ -189,7 +189,6 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   const bool blocked = m >= 16;
   double* VF = bf.VF;
   double* Z = bf.Z;
-  double* MX = bf.MX;
   double* H = bf.H;
 
   // ---- initial value function and constraint rows (endpoint.py:182-199, serial.py:46-48)
@@ -295,26 +294,23 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       if (k < n) t0 += F[k * Fw + i] * VF[k * Fw + n + m];
       if (i < n)
-        MX[i * (n + 1) + n] = qx1_s[i] + (t0 + t1);
+        vx1[i] = qx1_s[i] + (t0 + t1);   // mx1 in place (vx1 was consumed by GEMM1's f1 column)
       else
         P[(i - n) * ldw + cc] = qu1_s[i - n] + (t0 + t1);
     }
+    // x rows over the x columns only (the Mxu block is never used), u rows
+    // over all columns
     gemm_x_pre<true, NT>(
-        n + m, n + m, n, F, Fw, VF, Fw, bf.tiles,
-        [&](int i, int c) {
-          return i < n ? (c < n ? Qxx_s[i * n + c] : 0.0)
-                       : (c < n ? Qux_s[(i - n) * n + c] : Quu_s[(i - n) * m + (c - n)]);
-        },
-        [&](int i, int c, double v) {
-          if (i < n) {
-            if (c < n) MX[i * (n + 1) + c] = v;
-          } else {
-            const int u = i - n;
-            if (c < n)
-              P[u * ldw + c] = v;
-            else
-              Muu[u * m + (c - n)] = v;
-          }
+        n, n, n, F, Fw, VF, Fw, bf.tiles, [&](int i, int c) { return Qxx_s[i * n + c]; },
+        [&](int i, int c, double v) { Vxx[i * n + c] = v; });   // Mxx in place (Vxx was consumed by GEMM1)
+    gemm_x_pre<true, NT>(
+        m, n + m, n, F + n, Fw, VF, Fw, bf.tiles,
+        [&](int u, int c) { return c < n ? Qux_s[u * n + c] : Quu_s[u * m + (c - n)]; },
+        [&](int u, int c, double v) {
+          if (c < n)
+            P[u * ldw + c] = v;
+          else
+            Muu[u * m + (c - n)] = v;
         });
     // P z-block = Mzu' (Mzu = Vzx Fu lives in Z's middle columns)
     for (int idx = tid; idx < m * nz; idx += nt) {
@@ -463,7 +459,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     // x rows over the x columns only (no discarded Vxz block), z rows over
     // [x | z] columns, the constant column as a matvec
     gemm_x<true, NT>(n, n, KV, P, ldw, G, ldw, bf.tiles,
-                     [&](int i, int c, double acc) { Vxx[i * n + c] = MX[i * (n + 1) + c] + acc; });
+                     [&](int i, int c, double acc) { Vxx[i * n + c] += acc; });
     if (nz)
       gemm_x<true, NT>(nz, 2 * n, KV, P + n, ldw, G, ldw, bf.tiles, [&](int zi, int c, double acc) {
         if (c < n)
@@ -480,7 +476,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       if (k < KV) t0 += P[k * ldw + i] * G[k * ldw + cc];
       if (i < n)
-        vx1[i] = MX[i * (n + 1) + n] + (t0 + t1);
+        vx1[i] += (t0 + t1);
       else
         vz1[i - n] = Z[(i - n) * Fw + n + m] + (t0 + t1);
     }
@@ -584,7 +580,7 @@ SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
   sz[SB_MISC] = 2LL * m + 32 + 2 + ((m + 7) / 8) * 64LL + (threads / 32) * 64LL + 8LL * n + 64;
   sz[SB_VF] = n * Fw;
   sz[SB_Z] = n * Fw;
-  sz[SB_MX] = (int64_t)n * (n + 1);
+  sz[SB_MX] = 0;   // Mxx / mx1 are written into Vxx / vx1 in place
   sz[SB_H] = n * W;
   const bool wide = (n % m) != 0;
   sz[SB_WIDE] = wide ? ((int64_t)m * std::min(n, m) + (int64_t)m * m + 2 * m * W) : 0;
