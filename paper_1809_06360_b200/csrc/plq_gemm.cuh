@@ -17,6 +17,10 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -27,6 +31,8 @@ template <int NW>
 struct TileCfg {
   static constexpr int BM = 8 * NW, BN = 64, BK = 16;
   static constexpr int LDA = 20, LDB = 68;   // = 4 (mod 8): conflict-free fragment loads
+  static constexpr int LDAT = BM + 4;        // transposed A tile (BK x BM), also = 4 (mod 8)
+  static_assert(BK * LDAT <= BM * LDA, "transposed A tile fits the A buffer");
   static constexpr int DOUBLES = 2 * (BM * LDA + BK * LDB);
 };
 
@@ -50,6 +56,10 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
   double* Bs0 = tiles + 2 * BM * LDA;
   double* Bs1 = Bs0 + BK * LDB;
   const int tmc = (M + BM - 1) / BM, tnc = (N + BN - 1) / BN, kc = (K + BK - 1) / BK;
+  // 16-byte copies when both operands have even leading dimensions and
+  // 16-byte-aligned bases (large-mode scratch); the A tile of a transposed
+  // operand is then kept k-major (BK x LDAT) so its pairs stay contiguous
+  const bool vec = ((lda | ldb) & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
   for (int tile = 0; tile < tmc * tnc; ++tile) {
     const int m0 = (tile / tnc) * BM, n0 = (tile % tnc) * BN;
     double acc[2][4][2], pv[2][4][2];
@@ -64,7 +74,58 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
           pv[r][t][e] = (PRE && i < M && j < N) ? pre(i, j) : 0.0;
         }
       }
+    auto load_vec = [&](int c, int buf) {
+      const int k0 = c * BK;
+      double* as = buf ? As1 : As0;
+      double* bs = buf ? Bs1 : Bs0;
+      for (int e = tid; e < BM * BK / 2; e += NT) {
+        int i, k;
+        if (TA) {
+          i = 2 * (e % (BM / 2));
+          k = e / (BM / 2);
+        } else {
+          k = 2 * (e % (BK / 2));
+          i = e / (BK / 2);
+        }
+        const int gi = m0 + i, gk = k0 + k;
+        double* dst = TA ? as + k * C::LDAT + i : as + i * LDA + k;
+        if (TA) {
+          const double* src = A + (size_t)gk * lda + gi;
+          if (gk < K && gi + 1 < M) {
+            cp_async16(dst, src);
+          } else {
+            cp_async8(dst, gk < K && gi < M ? src : A, gk < K && gi < M);
+            cp_async8(dst + 1, gk < K && gi + 1 < M ? src + 1 : A, gk < K && gi + 1 < M);
+          }
+        } else {
+          const double* src = A + (size_t)gi * lda + gk;
+          if (gi < M && gk + 1 < K) {
+            cp_async16(dst, src);
+          } else {
+            cp_async8(dst, gi < M && gk < K ? src : A, gi < M && gk < K);
+            cp_async8(dst + 1, gi < M && gk + 1 < K ? src + 1 : A, gi < M && gk + 1 < K);
+          }
+        }
+      }
+      for (int e = tid; e < BK * BN / 2; e += NT) {
+        const int k = e / (BN / 2), j = 2 * (e % (BN / 2));
+        const int gk = k0 + k, gj = n0 + j;
+        const double* src = B + (size_t)gk * ldb + gj;
+        double* dst = bs + k * LDB + j;
+        if (gk < K && gj + 1 < N) {
+          cp_async16(dst, src);
+        } else {
+          cp_async8(dst, gk < K && gj < N ? src : B, gk < K && gj < N);
+          cp_async8(dst + 1, gk < K && gj + 1 < N ? src + 1 : B, gk < K && gj + 1 < N);
+        }
+      }
+      cp_async_commit();
+    };
     auto load = [&](int c, int buf) {
+      if (vec) {
+        load_vec(c, buf);
+        return;
+      }
       const int k0 = c * BK;
       double* as = buf ? As1 : As0;
       double* bs = buf ? Bs1 : Bs0;
@@ -105,7 +166,8 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
       for (int kk = 0; kk < BK; kk += 4) {
         double af[2], bf[4];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) af[r] = as[(wr * 16 + r * 8 + g) * LDA + kk + q];
+        for (int r = 0; r < 2; ++r)
+          af[r] = (TA && vec) ? as[(kk + q) * C::LDAT + wr * 16 + r * 8 + g] : as[(wr * 16 + r * 8 + g) * LDA + kk + q];
 #pragma unroll
         for (int t = 0; t < 4; ++t) bf[t] = bs[(kk + q) * LDB + wc * 32 + t * 8 + g];
 #pragma unroll

@@ -155,8 +155,10 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   const int nz = serial ? 0 : n;
   const int cc = n + nz;            // constant column of G
   const int W = cc + 1;             // logical width of P/G/Y
-  const int ldw = 2 * n + 1;        // storage stride of P/G/Y/H
-  const int Fw = n + m + 1;
+  // storage strides of P/G/Y/H and of F/VF/Z (logical width n+m+1): even in
+  // large mode, so the tiled GEMM streams its operands with 16-byte copies
+  const int ldw = a.lay.large ? 2 * n + 2 : 2 * n + 1;
+  const int Fw = a.lay.large ? ((n + m + 2) & ~1) : n + m + 1;
   const int nn = n * n;
 
   double* Vxx = bf.V;
@@ -336,7 +338,8 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       const double fu2 = block_sum(part_u, red);
       const double nu_scale = sqrt(hx2) * sqrt(fu2);
       // N = Hx F -> VF (r x Fw): [Nx | Nu | Hx f1]
-      gemm_x<false, NT>(r, Fw, n, H, ldw, F, Fw, bf.tiles, [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
+      gemm_x<false, NT>(r, n + m + 1, n, H, ldw, F, Fw, bf.tiles,
+                        [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
       __syncthreads();
       // stack [Nx | Nz=Hz | n1 = Hx f1 + h1] in place in H
       for (int idx = tid; idx < r * n; idx += nt) {
@@ -569,7 +572,9 @@ int sweep_threads(int n) {
 }
 
 SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
-  const int64_t Fw = n + m + 1, W = 2 * n + 1;
+  // storage strides (even in large mode, see sweep_segment)
+  const bool large = n >= 48;
+  const int64_t Fw = large ? ((n + m + 2) & ~1) : n + m + 1, W = large ? 2 * n + 2 : 2 * n + 1;
   int64_t sz[SB_COUNT];
   sz[SB_V] = 3LL * n * n + 2 * n;
   sz[SB_IN] = n * Fw + (int64_t)n * n + (int64_t)m * n + (int64_t)m * m + n + m;
