@@ -161,29 +161,6 @@ __device__ __forceinline__ void flag_singular(plq_problem_t& p, int32_t* status,
   if (threadIdx.x == 0 && status[b * p.J] == 0) status[b * p.J] = PLQ_STATUS_LINK_SINGULAR;
 }
 
-// lane-per-row Cholesky of an n x n block (n <= 32) by one warp, in place in
-// shared memory (stride ld); returns false on a non-positive pivot
-__device__ __forceinline__ bool warp_cholesky_smem(double* A, int n, int ld) {
-  const int lane = threadIdx.x & 31;
-  bool ok = true;
-  for (int k = 0; k < n; ++k) {
-    const double dkk = A[k * ld + k];
-    ok = ok && (dkk > 0.0);
-    const double d = sqrt(dkk > 0.0 ? dkk : 1.0);
-    const double inv = 1.0 / d;
-    __syncwarp();
-    if (lane == k) A[k * ld + k] = d;
-    if (lane > k && lane < n) A[lane * ld + k] *= inv;
-    __syncwarp();
-    if (lane > k && lane < n) {
-      const double lik = A[lane * ld + k];
-      for (int jj = k + 1; jj <= lane; ++jj) A[lane * ld + jj] -= lik * A[jj * ld + k];
-    }
-    __syncwarp();
-  }
-  return ok;
-}
-
 // offset (doubles) of the blocked-factorization scratch in link_eliminate's
 // dynamic shared memory: after the factor / right-hand sides / staging (n <=
 // 64) or the factor / GEMM tiles (n > 64); 2 * ceil(n/8) * 64 + 8 * 64 doubles
@@ -327,10 +304,33 @@ __host__ __device__ inline void link_slab(int w, int sidx, int* c0, int* c1) {
   *c1 = (sidx == LINK_SLABS - 1) ? w : (sidx + 1) * base;
 }
 
+// Stage an n x n row-major global block into shared memory with row stride
+// ld (= 4 mod 8, rows 16-byte aligned) by one bulk copy per row (TMA 1-D),
+// plus an optional contiguous extra range; falls back to a cooperative copy
+// when a row is not a multiple of 16 bytes.
+__device__ __forceinline__ void stage_rows(double* dst, int ld, const double* src, int n, double* xdst,
+                                           const double* xsrc, int xcount, uint64_t* bar, uint32_t& phase) {
+  if ((n % 2) == 0 && (ld % 2) == 0 && (xcount % 2) == 0) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      mbar_arrive_tx(bar, 8u * (uint32_t)(n * n + xcount));
+      for (int r = 0; r < n; ++r) bulk_g2s(dst + (size_t)r * ld, src + (size_t)r * n, 8u * n, bar);
+      if (xcount) bulk_g2s(xdst, xsrc, 8u * xcount, bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+  } else {
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) dst[(idx / n) * ld + idx % n] = src[idx];
+    for (int idx = threadIdx.x; idx < xcount; idx += blockDim.x) xdst[idx] = xsrc[idx];
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) link_factor_big(plq_problem_t p, LinkLevel L, int32_t* status) {
   __shared__ int flag;
   extern __shared__ __align__(16) double dsm[];
-  const int n = p.n, K = L.K, E = L.E, ldl = n + 1, nbk = (n + 7) / 8;
+  __shared__ __align__(8) uint64_t bar;
+  const int n = p.n, K = L.K, E = L.E, ldl = link_ldl_big(n), nbk = (n + 7) / 8;
   const int64_t nn = (int64_t)n * n;
   const int64_t b = blockIdx.x / E;
   const int o = blockIdx.x % E;
@@ -339,9 +339,13 @@ __global__ void __launch_bounds__(256) link_factor_big(plq_problem_t p, LinkLeve
   double* Lc = dsm;
   double* Ld = dsm + (((size_t)n * ldl + 1) & ~size_t(1));
   double* Linv = L.Linv + (b * E + o) * nbk * 64;
-  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[(idx / n) * ldl + idx % n] = D[idx];
-  if (threadIdx.x == 0) flag = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    flag = 0;
+  }
   __syncthreads();
+  uint32_t phase = 0;
+  stage_rows(Lc, ldl, D, n, nullptr, nullptr, 0, &bar, phase);
   if (!gchol8<8>(Lc, n, ldl, Linv, &flag, threadIdx.x, [] { __syncthreads(); }, Ld)) {
     flag_singular(p, status, b);
     return;
@@ -375,8 +379,21 @@ __global__ void __launch_bounds__(256) link_trsm_big(plq_problem_t p, LinkLevel 
   double* Li = Ls + (size_t)n * lls;                  // nbk * 64
   double* X = Li + nbk * 64;                          // n x LINK_SLAB_LD
   double* wsc = X + (size_t)n * LINK_SLAB_LD;          // 8 * 64
-  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Ls[(idx / n) * lls + idx % n] = gLc[idx];
-  for (int idx = threadIdx.x; idx < nbk * 64; idx += blockDim.x) Li[idx] = L.Linv[(b * E + o) * nbk * 64 + idx];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  // factor rows and the block inverses by bulk copies, overlapping the slab assembly
+  if ((n % 2) == 0 && threadIdx.x == 0) {
+    fence_proxy_async();
+    mbar_arrive_tx(&bar, 8u * (uint32_t)(nn + nbk * 64));
+    for (int r = 0; r < n; ++r) bulk_g2s(Ls + (size_t)r * lls, gLc + (size_t)r * n, 8u * n, &bar);
+    bulk_g2s(Li, L.Linv + (b * E + o) * nbk * 64, 8u * nbk * 64, &bar);
+  }
+  if ((n % 2) != 0) {
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Ls[(idx / n) * lls + idx % n] = gLc[idx];
+    for (int idx = threadIdx.x; idx < nbk * 64; idx += blockDim.x) Li[idx] = L.Linv[(b * E + o) * nbk * 64 + idx];
+  }
   for (int idx = threadIdx.x; idx < n * sw; idx += blockDim.x) {
     const int r = idx / sw, c = c0 + idx % sw;
     double v;
@@ -388,6 +405,7 @@ __global__ void __launch_bounds__(256) link_trsm_big(plq_problem_t p, LinkLevel 
       v = rh[r];
     X[r * LINK_SLAB_LD + (c - c0)] = v;
   }
+  if ((n % 2) == 0) mbar_wait(&bar, phase);
   __syncthreads();
   gtrsm8<0, 8>(Ls, n, lls, Li, X, sw, LINK_SLAB_LD, wsc, threadIdx.x, [] { __syncthreads(); });
   double* gWm = L.Wm + (b * E + o) * n * w;
@@ -663,7 +681,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
     if (p.n > 64) {
       const LinkLevel& Lv = P.lv[l];
       const int nbk = (p.n + 7) / 8, nt = (p.n + 63) / 64;
-      const size_t fsm = sizeof(double) * (((size_t)p.n * (p.n + 1) + 1) / 2 * 2 + nbk * 64);
+      const size_t fsm = sizeof(double) * (((size_t)p.n * link_ldl_big(p.n) + 1) / 2 * 2 + nbk * 64);
       const size_t rsm =
           sizeof(double) * ((size_t)p.n * link_ldl_big(p.n) + nbk * 64 + (size_t)p.n * LINK_SLAB_LD + 8 * 64);
       const size_t gsm = sizeof(double) * TileCfg<8>::DOUBLES;
@@ -683,7 +701,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
       ++nl;
     }
     if (!P.lv[l].top) {
-      link_assemble_next<<<B * P.lv[l + 1].K, threads, 0, s>>>(p, P.lv[l], P.lv[l + 1]);
+      link_assemble_next<<<B * P.lv[l + 1].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, P.lv[l], P.lv[l + 1]);
       ++nl;
     }
   }
