@@ -33,9 +33,13 @@ namespace plq {
 // ARE NOT OVERWRITTEN unless `Ld` (another nb * 64 doubles of staging) is
 // given -- consumers use Linv for them.  Returns false (all threads) on a
 // non-positive / NaN pivot (dpotrf failure).  `flag`: one int.
+// With X (m x W, ldx) given, the forward solve X <- L^{-1} X is fused in:
+// block row k of X is solved in step k's trailing phase, next to the Schur
+// tiles (`wsc`: NWG * 64 doubles), which saves gtrsm8<0>'s m/8 barriers.
 template <int NWG, class Sync>
 __device__ __forceinline__ bool gchol8(double* A, int m, int lda, double* Linv, int* flag, int gt, Sync sync,
-                                       double* Ld = nullptr) {
+                                       double* Ld = nullptr, double* X = nullptr, int W = 0, int ldx = 0,
+                                       double* wsc = nullptr) {
   constexpr int NT = NWG * 32;
   const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, q = lane & 3;
   for (int k0 = 0; k0 < m; k0 += 8) {
@@ -100,10 +104,42 @@ __device__ __forceinline__ bool gchol8(double* A, int m, int lda, double* Linv, 
       sync();
       return false;
     }
-    // trailing update of the lower tiles: A[i][j] -= sum_c l_ic l_jc
+    // trailing update of the lower tiles: A[i][j] -= sum_c l_ic l_jc, and
+    // (fused solve) block row k of X
     const int r0 = k0 + rb;
     const int tt = (below + 7) >> 3;
-    for (int tile = gw; tile < tt * (tt + 1) / 2; tile += NWG) {
+    const int nschur = tt * (tt + 1) / 2, nrhs = X != nullptr ? (W + 7) >> 3 : 0;
+    for (int t = gw; t < nschur + nrhs; t += NWG) {
+      if (t < nschur) continue;
+      // X_k = Linv_kk (X_k - sum_{c < k0} L[k][c] X_c)
+      double* ws = wsc + gw * 64;
+      const double* D = Linv + (k0 >> 3) * 64;
+      const int j0 = (t - nschur) * 8;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < k0; kk += 4) {
+        const int k = kk + q;
+        const double av = (g < rb) ? A[(k0 + g) * lda + k] : 0.0;
+        const double bv = (j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
+        dmma884(c0, c1, av, bv);
+      }
+      const int j = j0 + 2 * q;
+      ws[g * 8 + 2 * q] = (g < rb && j < W) ? X[(k0 + g) * ldx + j] - c0 : 0.0;
+      ws[g * 8 + 2 * q + 1] = (g < rb && j + 1 < W) ? X[(k0 + g) * ldx + j + 1] - c1 : 0.0;
+      __syncwarp();
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 4) {
+        const int k = kk + q;
+        dmma884(d0, d1, D[g * 8 + k], ws[k * 8 + g]);
+      }
+      if (g < rb) {
+        if (j < W) X[(k0 + g) * ldx + j] = d0;
+        if (j + 1 < W) X[(k0 + g) * ldx + j + 1] = d1;
+      }
+      __syncwarp();
+    }
+    for (int tile = gw; tile < nschur; tile += NWG) {
       int ti = 0;
       while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
       const int tj = tile - ti * (ti + 1) / 2;
@@ -183,6 +219,7 @@ __device__ __forceinline__ void gtrsm8(const double* T, int m, int ldt, const do
     for (int tj = gw; tj < tn; tj += NWG) {
       const int j0 = tj * 8;
       double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
       for (int kk = c_lo; kk < c_hi; kk += 4) {
         const int k = kk + q;
         const bool kv = k < c_hi;
@@ -479,6 +516,7 @@ __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X
       }
       // Y = V' C (8 x 8, K = rows): V'(i, l) = v_i(l)
       double y0 = 0.0, y1 = 0.0;
+#pragma unroll 4
       for (int kk = 0; kk < rows; kk += 4) {
         const int l = kk + q;
         double av = 0.0;
@@ -490,6 +528,7 @@ __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X
       ws[g * 8 + 2 * q + 1] = y1;
       __syncwarp();
       // C -= VT Y, 8-row bands
+#pragma unroll 2
       for (int b0 = 0; b0 < rows; b0 += 8) {
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
