@@ -590,7 +590,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = P[(idx / W) * LDW + idx % W];
         auto sy = [&] { gsync<NWG>(grp); };
         static_assert(M * M >= 256 + NWG * 64, "TAU slot too small for the blocked solve");
-        if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy)) {
+        // Cholesky with the forward solve of G fused in (block row k of G in step k)
+        if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy, nullptr, G, W, LDW,
+                         tau + 256)) {
           status = 1 + s;
           if (s > 0) {
             mbar_wait(bar, phase);
@@ -598,7 +600,6 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           }
           break;
         }
-        gtrsm8<0, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);
         gtrsm8<1, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);
         for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = -G[(idx / W) * LDW + idx % W];
         gsync<NWG>(grp);
