@@ -421,13 +421,14 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       if (tid == 0) *iflag = 0;
       __syncthreads();
-      if (!(blocked ? gchol8<NT / 32>(Lm, m, m, binv, iflag, tid, csync) : cta_cholesky(Lm, m, m, iflag))) {
+      // blocked: Cholesky with the forward solve of G fused in
+      if (!(blocked ? gchol8<NT / 32>(Lm, m, m, binv, iflag, tid, csync, nullptr, G, W, ldw, wsc)
+                    : cta_cholesky(Lm, m, m, iflag))) {
         if (tid == 0) *sflag = 1 + s;
         __syncthreads();
         break;
       }
       if (blocked) {
-        gtrsm8<0, NT / 32>(Lm, m, m, binv, G, W, ldw, wsc, tid, csync);
         gtrsm8<1, NT / 32>(Lm, m, m, binv, G, W, ldw, wsc, tid, csync);
       } else {
         cho_solve_x(Lm, m, m, G, W, ldw);
