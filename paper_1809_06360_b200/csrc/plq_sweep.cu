@@ -242,19 +242,27 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     const double* Quu_s = qdirect ? p.Quu + st * m * m : Quu;
     const double* qx1_s = qdirect ? p.qx1 + st * n : qx1;
     const double* qu1_s = qdirect ? p.qu1 + st * m : qu1;
-    for (int idx = tid; idx < nn; idx += nt) {
-      F[(idx / n) * Fw + idx % n] = __ldcs(p.Fx + st * nn + idx);
-      if (!qdirect) Qxx[idx] = __ldcs(p.Qxx + st * nn + idx);
-    }
-    for (int idx = tid; idx < n * m; idx += nt) {
-      F[(idx / m) * Fw + n + idx % m] = __ldcs(p.Fu + st * n * m + idx);
-      if (!qdirect) Qux[idx] = __ldcs(p.Qux + st * m * n + idx);
-    }
-    for (int i = tid; i < n; i += nt) {
-      F[i * Fw + n + m] = __ldcs(p.f1 + st * n + i);
-      if (!qdirect) qx1[i] = __ldcs(p.qx1 + st * n + i);
-    }
+    // Large mode: F = [Fx | Fu | f1] is not copied either -- the GEMMs take
+    // Fx and Fu straight from the inputs (two operands instead of one)
+    const double* fxp = qdirect ? p.Fx + st * nn : F;
+    const double* fup = qdirect ? p.Fu + st * n * m : F + n;
+    const double* f1p = qdirect ? p.f1 + st * n : nullptr;
+    const int ldfx = qdirect ? n : Fw, ldfu = qdirect ? m : Fw;
+    auto f1at = [&](int k) { return qdirect ? f1p[k] : F[k * Fw + n + m]; };
+    auto fat = [&](int k, int c) { return c < n ? fxp[k * ldfx + c] : fup[k * ldfu + (c - n)]; };
     if (!qdirect) {
+      for (int idx = tid; idx < nn; idx += nt) {
+        F[(idx / n) * Fw + idx % n] = __ldcs(p.Fx + st * nn + idx);
+        Qxx[idx] = __ldcs(p.Qxx + st * nn + idx);
+      }
+      for (int idx = tid; idx < n * m; idx += nt) {
+        F[(idx / m) * Fw + n + idx % m] = __ldcs(p.Fu + st * n * m + idx);
+        Qux[idx] = __ldcs(p.Qux + st * m * n + idx);
+      }
+      for (int i = tid; i < n; i += nt) {
+        F[i * Fw + n + m] = __ldcs(p.f1 + st * n + i);
+        qx1[i] = __ldcs(p.qx1 + st * n + i);
+      }
       for (int idx = tid; idx < m * m; idx += nt) Quu[idx] = __ldcs(p.Quu + st * m * m + idx);
       for (int i = tid; i < m; i += nt) qu1[i] = __ldcs(p.qu1 + st * m + i);
     }
@@ -263,11 +271,18 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217).
     // The f1 column ([w; mz1] = [Vxx; Vzx] f1 + [vx1; vz1]) is a thread-per-row
     // matvec, so the GEMM's N is n + m (a whole 64-wide tile less in large mode)
-    gemm_x<false, NT>(n + nz, Fw - 1, n, bf.V, n, F, Fw, bf.tiles, [&](int i, int c, double acc) {
+    gemm_x<false, NT>(n + nz, n, n, bf.V, n, fxp, ldfx, bf.tiles, [&](int i, int c, double acc) {
       if (i < n) {
         VF[i * Fw + c] = acc;
       } else {
         Z[(i - n) * Fw + c] = acc;
+      }
+    });
+    gemm_x<false, NT>(n + nz, m, n, bf.V, n, fup, ldfu, bf.tiles, [&](int i, int c, double acc) {
+      if (i < n) {
+        VF[i * Fw + n + c] = acc;
+      } else {
+        Z[(i - n) * Fw + n + c] = acc;
       }
     });
     for (int i = tid; i < n + nz; i += nt) {
@@ -275,10 +290,10 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       double t0 = 0.0, t1 = 0.0;
       int k = 0;
       for (; k + 1 < n; k += 2) {
-        t0 += vr[k] * F[k * Fw + n + m];
-        t1 += vr[k + 1] * F[(k + 1) * Fw + n + m];
+        t0 += vr[k] * f1at(k);
+        t1 += vr[k + 1] * f1at(k + 1);
       }
-      if (k < n) t0 += vr[k] * F[k * Fw + n + m];
+      if (k < n) t0 += vr[k] * f1at(k);
       if (i < n)
         VF[i * Fw + n + m] = vx1[i] + (t0 + t1);
       else
@@ -291,10 +306,10 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       double t0 = 0.0, t1 = 0.0;
       int k = 0;
       for (; k + 1 < n; k += 2) {
-        t0 += F[k * Fw + i] * VF[k * Fw + n + m];
-        t1 += F[(k + 1) * Fw + i] * VF[(k + 1) * Fw + n + m];
+        t0 += fat(k, i) * VF[k * Fw + n + m];
+        t1 += fat(k + 1, i) * VF[(k + 1) * Fw + n + m];
       }
-      if (k < n) t0 += F[k * Fw + i] * VF[k * Fw + n + m];
+      if (k < n) t0 += fat(k, i) * VF[k * Fw + n + m];
       if (i < n)
         vx1[i] = qx1_s[i] + (t0 + t1);   // mx1 in place (vx1 was consumed by GEMM1's f1 column)
       else
@@ -303,10 +318,10 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     // x rows over the x columns only (the Mxu block is never used), u rows
     // over all columns
     gemm_x_pre<true, NT>(
-        n, n, n, F, Fw, VF, Fw, bf.tiles, [&](int i, int c) { return Qxx_s[i * n + c]; },
+        n, n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return Qxx_s[i * n + c]; },
         [&](int i, int c, double v) { Vxx[i * n + c] = v; });   // Mxx in place (Vxx was consumed by GEMM1)
     gemm_x_pre<true, NT>(
-        m, n + m, n, F + n, Fw, VF, Fw, bf.tiles,
+        m, n + m, n, fup, ldfu, VF, Fw, bf.tiles,
         [&](int u, int c) { return c < n ? Qux_s[u * n + c] : Quu_s[u * m + (c - n)]; },
         [&](int u, int c, double v) {
           if (c < n)
@@ -331,15 +346,21 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         part_h += v * v;
       }
       for (int idx = tid; idx < n * m; idx += nt) {
-        const double v = F[(idx / m) * Fw + n + idx % m];
+        const double v = fup[(idx / m) * ldfu + idx % m];
         part_u += v * v;
       }
       const double hx2 = block_sum(part_h, red);
       const double fu2 = block_sum(part_u, red);
       const double nu_scale = sqrt(hx2) * sqrt(fu2);
       // N = Hx F -> VF (r x Fw): [Nx | Nu | Hx f1]
-      gemm_x<false, NT>(r, n + m + 1, n, H, ldw, F, Fw, bf.tiles,
-                        [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
+      gemm_x<false, NT>(r, n, n, H, ldw, fxp, ldfx, bf.tiles, [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
+      gemm_x<false, NT>(r, m, n, H, ldw, fup, ldfu, bf.tiles,
+                        [&](int i, int c, double acc) { VF[i * Fw + n + c] = acc; });
+      for (int i = tid; i < r; i += nt) {
+        double t = 0.0;
+        for (int k = 0; k < n; ++k) t += H[i * ldw + k] * f1at(k);
+        VF[i * Fw + n + m] = t;
+      }
       __syncthreads();
       // stack [Nx | Nz=Hz | n1 = Hx f1 + h1] in place in H
       for (int idx = tid; idx < r * n; idx += nt) {
