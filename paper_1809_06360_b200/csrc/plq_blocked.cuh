@@ -36,10 +36,13 @@ namespace plq {
 // With X (m x W, ldx) given, the forward solve X <- L^{-1} X is fused in:
 // block row k of X is solved in step k's trailing phase, next to the Schur
 // tiles (`wsc`: NWG * 64 doubles), which saves gtrsm8<0>'s m/8 barriers.
+// Xsrc (optional, same stride) supplies the right-hand side instead of X's
+// own contents, scaled by xscale: X <- L^{-1} (xscale * Xsrc) with no copy
+// pass (block row k of Xsrc is read once, in step k).
 template <int NWG, class Sync>
 __device__ __forceinline__ bool gchol8(double* A, int m, int lda, double* Linv, int* flag, int gt, Sync sync,
                                        double* Ld = nullptr, double* X = nullptr, int W = 0, int ldx = 0,
-                                       double* wsc = nullptr) {
+                                       double* wsc = nullptr, const double* Xsrc = nullptr, double xscale = 1.0) {
   constexpr int NT = NWG * 32;
   const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, q = lane & 3;
   for (int k0 = 0; k0 < m; k0 += 8) {
@@ -124,8 +127,9 @@ __device__ __forceinline__ bool gchol8(double* A, int m, int lda, double* Linv, 
         dmma884(c0, c1, av, bv);
       }
       const int j = j0 + 2 * q;
-      ws[g * 8 + 2 * q] = (g < rb && j < W) ? X[(k0 + g) * ldx + j] - c0 : 0.0;
-      ws[g * 8 + 2 * q + 1] = (g < rb && j + 1 < W) ? X[(k0 + g) * ldx + j + 1] - c1 : 0.0;
+      const double* Xs = Xsrc != nullptr ? Xsrc : X;
+      ws[g * 8 + 2 * q] = (g < rb && j < W) ? xscale * Xs[(k0 + g) * ldx + j] - c0 : 0.0;
+      ws[g * 8 + 2 * q + 1] = (g < rb && j + 1 < W) ? xscale * Xs[(k0 + g) * ldx + j + 1] - c1 : 0.0;
       __syncwarp();
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll

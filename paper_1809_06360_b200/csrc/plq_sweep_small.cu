@@ -587,12 +587,12 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       if constexpr (S::BIG) {
         // CTA Cholesky of Muu in place (not needed again in this stage) and
         // a blocked DMMA solve of the m x W right-hand side
-        for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = P[(idx / W) * LDW + idx % W];
         auto sy = [&] { gsync<NWG>(grp); };
         static_assert(M * M >= 256 + NWG * 64, "TAU slot too small for the blocked solve");
-        // Cholesky with the forward solve of G fused in (block row k of G in step k)
+        // Cholesky with the forward solve fused in: G <- L^{-1} (-P), block
+        // row k in step k (no copy / negation passes)
         if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy, nullptr, G, W, LDW,
-                         tau + 256)) {
+                         tau + 256, P, -1.0)) {
           status = 1 + s;
           if (s > 0) {
             mbar_wait(bar, phase);
@@ -600,9 +600,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           }
           break;
         }
-        gtrsm8<1, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);
-        for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = -G[(idx / W) * LDW + idx % W];
-        gsync<NWG>(grp);
+        gtrsm8<1, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);   // G = -Muu^{-1} P
       } else {
       double Lr[M][M], id[M];
       int fail = 0;
@@ -681,20 +679,25 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     auto von = [](int tm, int tn) { return tm < XB ? tn <= tm : (tn < XB || tn - XB <= tm - XB); };
     // Vzz (global scratch when BIG) is read before the k-loop (its latency
     // hides behind the DMMAs) and written back as pre + acc
-    auto vzero = [&](int i, int c) { return (i >= N && c >= N && c - N <= i - N) ? Vzz[(i - N) * LDN + (c - N)] : 0.0; };
-    auto vsel = [&](int i, int c, double acc) {
+    // (so are the on-chip Vxx / Vzx entries: no read-modify-write in the
+    // epilogue); epi gets V + update
+    auto vzero = [&](int i, int c) {
+      if (i < N) return c <= i ? Vxx[i * LDN + c] : 0.0;
+      const int zi = i - N;
+      return c < N ? Vzx[zi * LDN + c] : (c - N <= zi ? Vzz[zi * LDN + (c - N)] : 0.0);
+    };
+    auto vsel = [&](int i, int c, double v) {
       if (i < N) {
         if (c <= i) {
-          const double v = Vxx[i * LDN + c] + acc;
           Vxx[i * LDN + c] = v;
           Vxx[c * LDN + i] = v;
         }
       } else {
         const int zi = i - N;
         if (c < N)
-          Vzx[zi * LDN + c] += acc;
+          Vzx[zi * LDN + c] = v;
         else if (c - N <= zi)
-          Vzz[zi * LDN + (c - N)] = acc;   // acc = Vzz (pre) + update
+          Vzz[zi * LDN + (c - N)] = v;
       }
     };
     if (constrained) {
