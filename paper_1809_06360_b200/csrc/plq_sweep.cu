@@ -435,30 +435,34 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     if (chol) {
       // G = -Muu^{-1} P: unconstrained stage, or p = 0 in a constrained one
       // (endpoint.py:239-250 with Zw = I; serial.py:63-70)
-      for (int idx = tid; idx < m * m; idx += nt) Lm[idx] = Muu[idx];
-      for (int idx = tid; idx < m * W; idx += nt) {
-        const int u = idx / W, c = idx % W;
-        G[u * ldw + c] = P[u * ldw + c];
+      // blocked: Cholesky of Muu in place (dead after this in Cholesky-gain
+      // stages, which take the short value update) with the forward solve
+      // fused in, G <- L^{-1}(-P); then the backward solve gives G directly
+      if (!blocked) {
+        for (int idx = tid; idx < m * m; idx += nt) Lm[idx] = Muu[idx];
+        for (int idx = tid; idx < m * W; idx += nt) {
+          const int u = idx / W, c = idx % W;
+          G[u * ldw + c] = P[u * ldw + c];
+        }
       }
       if (tid == 0) *iflag = 0;
       __syncthreads();
-      // blocked: Cholesky with the forward solve of G fused in
-      if (!(blocked ? gchol8<NT / 32>(Lm, m, m, binv, iflag, tid, csync, nullptr, G, W, ldw, wsc)
+      if (!(blocked ? gchol8<NT / 32>(Muu, m, m, binv, iflag, tid, csync, nullptr, G, W, ldw, wsc, P, -1.0)
                     : cta_cholesky(Lm, m, m, iflag))) {
         if (tid == 0) *sflag = 1 + s;
         __syncthreads();
         break;
       }
       if (blocked) {
-        gtrsm8<1, NT / 32>(Lm, m, m, binv, G, W, ldw, wsc, tid, csync);
+        gtrsm8<1, NT / 32>(Muu, m, m, binv, G, W, ldw, wsc, tid, csync);
       } else {
         cho_solve_x(Lm, m, m, G, W, ldw);
+        for (int idx = tid; idx < m * W; idx += nt) {
+          const int u = idx / W, c = idx % W;
+          G[u * ldw + c] = -G[u * ldw + c];
+        }
+        __syncthreads();
       }
-      for (int idx = tid; idx < m * W; idx += nt) {
-        const int u = idx / W, c = idx % W;
-        G[u * ldw + c] = -G[u * ldw + c];
-      }
-      __syncthreads();
     }
 
     // ---- policy outputs (parallel.py:224-236 stacking)
