@@ -37,8 +37,41 @@ __device__ __forceinline__ void gemv_cols(int R, int C, const double* __restrict
   }
 }
 
+// Same product with the rows split over the CTA when it has more threads
+// than columns: blockDim / C chunks of rows, per-chunk partial sums in `part`
+// (blockDim doubles), summed in chunk order (deterministic).  Ends with a
+// barrier; all threads must call it.
+__device__ __forceinline__ void gemv_cols_par(int R, int C, const double* __restrict__ A, const double* x,
+                                              double* y, double* part) {
+  const int S = blockDim.x / C;
+  if (S < 2) {
+    gemv_cols(R, C, A, x, y);
+    __syncthreads();
+    return;
+  }
+  const int tid = threadIdx.x, chunk = tid / C, i = tid % C;
+  if (chunk < S) {
+    const int r0 = (int)((int64_t)R * chunk / S), r1 = (int)((int64_t)R * (chunk + 1) / S);
+    double t0 = 0.0, t1 = 0.0;
+    int k = r0;
+    for (; k + 1 < r1; k += 2) {
+      t0 += A[(int64_t)k * C + i] * x[k];
+      t1 += A[(int64_t)(k + 1) * C + i] * x[k + 1];
+    }
+    if (k < r1) t0 += A[(int64_t)k * C + i] * x[k];
+    part[chunk * C + i] = t0 + t1;
+  }
+  __syncthreads();
+  for (int c = tid; c < C; c += blockDim.x) {
+    double t = 0.0;
+    for (int h = 0; h < S; ++h) t += part[h * C + c];
+    y[c] = t;
+  }
+  __syncthreads();
+}
+
 struct ReconSmem {
-  double *x, *xn, *u, *k, *lam, *t0, *t1, *t2, *t3, *z, *a, *red;
+  double *x, *xn, *u, *k, *lam, *t0, *t1, *t2, *t3, *z, *a, *red, *part;
 };
 
 template <int NT>
@@ -60,6 +93,7 @@ __global__ void __launch_bounds__(NT) recon_kernel(ReconArgs A) {
   s.t2 = s.k + m;
   s.t3 = s.t2 + m;
   s.red = s.t3 + m;
+  s.part = s.red + 32;   // blockDim doubles (gemv_cols_par)
   const int nloc = A.seg_end - A.seg_begin;
   const int64_t total = p.B * nloc;
   for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
@@ -162,9 +196,8 @@ __global__ void __launch_bounds__(NT) recon_kernel(ReconArgs A) {
       const double* Fx = p.Fx + st * nn;
       const double* Fu = p.Fu + st * n * m;
       const double* gh = A.gh + st * (n + m);
-      gemv_cols(n, n, Fx, s.lam, s.t0);     // Fx' lam_next
-      gemv_cols(n, m, Fu, s.lam, s.t2);     // Fu' lam_next
-      __syncthreads();
+      gemv_cols_par(n, n, Fx, s.lam, s.t0, s.part);     // Fx' lam_next
+      gemv_cols_par(n, m, Fu, s.lam, s.t2, s.part);     // Fu' lam_next
       const bool interior = last || (sidx < L - 1);
       for (int i = tid; i < n; i += nt) {
         const double g = gh[i];
@@ -329,7 +362,7 @@ int grid_for(int64_t tasks, int threads) {
 
 int launch_recon(const ReconArgs& a, cudaStream_t s) {
   const int threads = recon_threads(a.p.n);
-  const size_t smem = sizeof(double) * (7 * a.p.n + 4 * a.p.m + 40);
+  const size_t smem = sizeof(double) * (7 * a.p.n + 4 * a.p.m + 40 + threads);
   const int64_t tasks = a.p.B * (a.seg_end - a.seg_begin);
   if (tasks <= 0) return 0;
   const int grid = grid_for(tasks, threads);
