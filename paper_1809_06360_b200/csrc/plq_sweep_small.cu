@@ -1,5 +1,7 @@
-// K1 specialized: segment sweeps for the small-state configs (compile-time
-// n, m; BASELINE configs 0-2: n=12/m=4 and n=32/m=8).
+// K1 specialized: segment sweeps with compile-time n, m (BASELINE configs
+// 0-2 and 4: n=12/m=4, n=32/m=8, n=64/m=32).  n = 64 ("BIG") keeps the GEMM
+// operands on chip and the rest in L2 scratch, uses the blocked
+// factorizations of plq_blocked.cuh and tile-selective GEMMs.
 //
 // Same recurrences as the generic sweep (plq_sweep.cu; endpoint.py:168-301,
 // serial.py:37-79), restructured for latency:
@@ -560,6 +562,10 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = -H[(idx / W) * LDW + idx % W];
           gsync<NWG>(grp);
         } else {
+        // reciprocal pivots off the dependent chain (independent divisions)
+        double rr[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) rr[i] = 1.0 / rdiag[i];
         for (int c = gt; c < W; c += NT) {
           double x[M];
   #pragma unroll
@@ -567,7 +573,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
             double v = H[i * LDW + c];
   #pragma unroll
             for (int k = i + 1; k < M; ++k) v -= Rm[i * ldr + k] * x[k];
-            x[i] = v / rdiag[i];
+            x[i] = v * rr[i];
           }
   #pragma unroll
           for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
