@@ -15,6 +15,8 @@
 // per stage at n = 64) through one slot, so every stage waited for its own
 // copy; here the recurrent passes stream 83 / 50 KB per stage through 2- /
 // 3-slot rings and the Q-block work runs at streaming bandwidth.
+#include <stdlib.h>
+
 #include "plq_device.cuh"
 #include "plq_internal.h"
 #include "plq_tma.cuh"
@@ -392,8 +394,21 @@ int launch_split(const ReconArgs& a, cudaStream_t s) {
 bool recon_split_supported(int n, int m) { return (n == 64 && m == 32) || (n == 32 && m == 8); }
 
 int launch_recon_split(const ReconArgs& a, cudaStream_t s) {
-  if (a.p.n == 64 && a.p.m == 32) return launch_split<64, 32, 128, 2, 3, 3>(a, s);
-  if (a.p.n == 32 && a.p.m == 8) return launch_split<32, 8, 64, 4, 4, 4>(a, s);
+  // ring depths (fwd, eval, bwd).  n = 64: one slot per CTA and 2-4 CTAs per
+  // SM beat deep rings in one CTA (cfg4 recon 15.3 -> 12.7 ms with (1,1,1)
+  // vs (2,3,3)); PLQ_RECON_RS selects measurement variants.
+  const char* e = getenv("PLQ_RECON_RS");
+  const int v = (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 0;
+  if (a.p.n == 64 && a.p.m == 32) {
+    if (v == 2) return launch_split<64, 32, 128, 1, 2, 2>(a, s);
+    if (v == 3) return launch_split<64, 32, 128, 2, 3, 3>(a, s);
+    return launch_split<64, 32, 128, 1, 1, 1>(a, s);
+  }
+  if (a.p.n == 32 && a.p.m == 8) {   // cfg2 recon 0.79 -> 0.57 ms with (2,2,2) vs (4,4,4)
+    if (v == 1) return launch_split<32, 8, 64, 1, 1, 1>(a, s);
+    if (v == 4) return launch_split<32, 8, 64, 4, 4, 4>(a, s);
+    return launch_split<32, 8, 64, 2, 2, 2>(a, s);
+  }
   return -1;
 }
 
