@@ -283,7 +283,7 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
   if (!sm && blockDim.x == 256)
     cta_gemm_tiled<true, 8>(2 * n, w, n, Wm, w, Wm, w, tiles, gram);
   else
-    cta_gemm<true, false, 1, 1>(2 * n, w, n, Wm, ldw, Wm, ldw, gram);
+    cta_gemm<true, false, 2, 2>(2 * n, w, n, Wm, ldw, Wm, ldw, gram);   // 16 x 16 per warp: half the fragment loads per DMMA
 }
 
 // ---- large blocks (n > 64): one elimination split over many CTAs ---------
