@@ -6,11 +6,16 @@ solved knot-points/s, fp64, including the K_t, k_t policies).
 
 One step = one full ``solve_parallel`` of the configured batch (sweeps, link
 solve, reconstruction, objective and KKT diagnostics) with inputs resident in
-HBM.  Default workload: BASELINE config 1 (4096 independent problems, n=12,
-m=4, T=64, J=8), the config the metric is quoted on; the batch is sharded
-across ranks (``torchrun``), no collective on the data path.  Rank 0 prints
-one JSON line.  ``--impl reference`` times the CPU oracle port of the
-reference's path on the host cores instead (rank 0 only).
+HBM.  Default workload: BASELINE config 4 (256 independent problems, n=64,
+m=32, T=1024, J=32) -- BASELINE.json's metric names no config, so the line
+is quoted on the largest configuration that fits one GPU (28.3 GB of
+inputs); ``--config 0..3`` select the others.  Batches are sharded across
+ranks with no collective on the data path; single horizons (cfg 2, 3) are
+segment-sharded with one all-gather of the segment value blocks
+(``sharded.py``).  ``--gpus N`` without a torchrun environment re-launches
+itself under ``torch.distributed.run`` with N ranks.  Rank 0 prints one JSON
+line.  ``--impl reference`` times the CPU oracle port of the reference's path
+on the host cores instead (rank 0 only).
 """
 
 import os
@@ -45,13 +50,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=1, choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", type=int, default=4, choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-smooth", action="store_true")
     ap.add_argument("--no-endpoint", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--graph", type=int, default=1, help="replay the solve as one CUDA graph (1) or launch eagerly (0)")
     return ap.parse_args()
 
@@ -197,6 +203,38 @@ def time_cpu_endpoint(cfg, seed, budget_s=4.0):
             "sample": f"{done} two-point-boundary solves of the config's problems"}
 
 
+def parity_sample(cfg, host, out, B_loc):
+    """A sample of the solved problems against the CPU oracle, computed
+    outside the timed region (the oracle is the checker here, never the
+    thing measured).  ``K`` and the objective are gated at 1e-9 (SURVEY.md
+    8(c)); ``x, u, lam, k`` are reported -- their gate is 10x the oracle's
+    own perturbation floor, which the parity tests measure."""
+    from oracle import parlqr_oracle as O
+    picks = [0] if B_loc == 1 else sorted({0, B_loc // 2, B_loc - 1})
+    probs = [{k: v[i].numpy() for k, v in host.items()} for i in picks]
+    w = O.host_cores()
+    t0 = time.perf_counter()
+    if B_loc == 1:
+        refs = [O.solve(probs[0], J=cfg.J, workers=min(w, cfg.J))]
+    else:
+        refs = O.solve_batch({k: np.stack([p[k] for p in probs]) for k in probs[0]}, J=cfg.J, workers=w)
+
+    def rel(a, b):
+        d = float(np.abs(b).max())
+        return float(np.abs(a - b).max()) / d if d else float(np.abs(a - b).max())
+
+    errs = {}
+    for i, ref in zip(picks, refs):
+        for key, rk in (("K", "K"), ("k", "k"), ("x", "states"), ("u", "controls"), ("lam", "lambdas")):
+            errs[key] = max(errs.get(key, 0.0), rel(out[key][i].cpu().numpy(), ref[rk]))
+        errs["objective"] = max(errs.get("objective", 0.0),
+                                rel(out["objective"][i:i + 1].cpu().numpy(), np.array([ref["objective"]])))
+    ok = errs["K"] <= 1e-9 and errs["objective"] <= 1e-9
+    return {"problems": picks, "max_rel_err": errs, "pass_K_objective_1e-9": ok,
+            "oracle": "oracle/parlqr_oracle.py (the reference's call sequence restated)",
+            "oracle_seconds": time.perf_counter() - t0}
+
+
 # ---------------------------------------------------------------------------
 
 def run_reference(args):
@@ -240,8 +278,12 @@ def run_ours(args):
     else:
         B_loc, first = 1, 0          # single horizon: segments sharded across ranks
     scaling = "strong"
-    host = synth.generate_batch(cfg, seed=args.seed, count=B_loc, first=first)
-    inputs = {k: torch.from_numpy(v).to(dev) for k, v in host.items()}
+    # seeded host inputs (fork-pool generator), pinned once: the e2e leg reads
+    # them as its host buffers, the device-resident leg copies them to HBM
+    gen = synth.generate_batch_parallel(cfg, seed=args.seed, count=B_loc, first=first)
+    host = {k: torch.from_numpy(v).pin_memory() for k, v in gen.items()}
+    del gen
+    inputs = {k: v.to(dev) for k, v in host.items()}
     solver = BatchSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev)
     stream = torch.cuda.current_stream(dev)
     if sharded:
@@ -331,11 +373,23 @@ def run_ours(args):
     achieved = B_loc * sweep_fl / (phase_ms["sweep"] / 1000.0) / 1e12
     hbm_peak, hbm_src = perfmodel.hbm_peak_gbs(ROOT)
     sweep_b = B_loc * perfmodel.sweep_bytes(cfg.n, cfg.m, cfg.T, cfg.J)
-    traffic = None
+    kernel = perfmodel.sweep_kernel_name(cfg.n, cfg.m)
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get(cfg.name)
+            tj = json.load(fh).get(cfg.name)
+        if isinstance(tj, dict) and tj.get("kernel") == kernel:
+            # ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch
+            # of the whole-config sweep (B_loc = the batch the capture ran)
+            traffic = tj["bytes"] * B_loc / tj.get("B", B_loc)
+            traffic_src = tj.get("source")
+
+    # ---- parity of a sample of this rank's problems against the CPU oracle
+    # (outside the timed region; the tests gate every output at the floor)
+    parity = None
+    if not args.no_parity and rank == 0:
+        parity = parity_sample(cfg, host, solver.out, B_loc)
     total_fl, _ = perfmodel.problem_flops(cfg.n, cfg.m, cfg.T, cfg.J)
     bin_, bout = perfmodel.knot_bytes(cfg.n, cfg.m)
     whole = {
@@ -349,7 +403,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         hs = HostSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev, pin=True)
-        pinned = {k: torch.from_numpy(v).pin_memory() for k, v in host.items()}
+        pinned = host
         for _ in range(max(1, min(args.warmup, 3))):
             hs.run(pinned)
         if dist:
@@ -394,6 +448,7 @@ def run_ours(args):
                                  "note": "pinned-copy bandwidth measured in this run; floor = max(H2D, D2H) "
                                          "time of the step's bytes (the directions overlap)"}}
         del hs, pinned
+        torch.cuda.empty_cache()
 
     # ---- smoothing pass (parallel.smooth, §8f row 1) over this solve: device time
     smooth = None
@@ -472,10 +527,12 @@ def run_ours(args):
                        "l2": "inputs exceed L2" if flush is None else "L2 flushed between steps",
                        "launch": "CUDA graph replay" if (args.graph and not sharded) else "eager"},
             "gpu_launches": launches,
-            "roofline": {"bound": "tensor", "kernel": "sweep_kernel (K1, DMMA.8x8x4 fp64)",
+            "roofline": {"bound": "tensor", "kernel": kernel + " (K1 segment sweep, DMMA.8x8x4 fp64)",
                          "achieved": achieved, "peak": peak_f64, "unit": "TFLOP/s",
-                         "frac": achieved / peak_f64, "traffic": traffic,
-                         "peak_source": "measured fp64 (tools/fp64_peak.cu, profiles/fp64_peak.json)",
+                         "frac": achieved / peak_f64, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": "FP64 (DFMA / DMMA) peak measured on this pool's B200 by "
+                                        "tools/fp64_peak.cu (profiles/fp64_peak.json); MEASURED_PEAKS.json "
+                                        "has no FP64 entry",
                          "algorithmic_flops_per_launch": B_loc * sweep_fl,
                          "algorithmic_bytes_per_launch": sweep_b,
                          "hbm_frac": sweep_b / (phase_ms["sweep"] / 1000.0) / 1e9 / hbm_peak,
@@ -483,6 +540,7 @@ def run_ours(args):
             "whole_solve": whole,
             "phases_ms": phase_ms,
             "clocks": sampler.report(),
+            "parity_checked": parity,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "smooth": smooth,
@@ -493,8 +551,31 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """``--gpus N`` outside torchrun: re-launch this script with N ranks
+    (one process per GPU, rendezvous on 127.0.0.1); returns the exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                raise SystemExit(f"--gpus {args.gpus}: only {have} CUDA device(s) visible (one rank per GPU)")
+        raise SystemExit(spawn_ranks(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

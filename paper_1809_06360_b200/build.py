@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparlqr_b200.so")
-SOURCES = ("plq_sweep.cu", "plq_sweep_small.cu", "plq_link.cu", "plq_recon.cu", "plq_recon_small.cu", "plq_recon_ring.cu",
+SOURCES = ("plq_sweep.cu", "plq_sweep_t32.cu", "plq_sweep_t128.cu", "plq_sweep_t256.cu", "plq_sweep_t512.cu", "plq_sweep_small.cu", "plq_link.cu", "plq_recon.cu", "plq_recon_small.cu", "plq_recon_ring.cu",
            "plq_smooth.cu", "plq_endpoint.cu", "plq_linkfeas.cu",
            "plq_api.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -45,16 +45,20 @@ def build(force=False, verbose=False):
         return LIB
     objdir = os.path.join(HERE, "_build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    objs = [os.path.join(objdir, src.replace(".cu", ".o")) for src in SOURCES]
+    # translation units are independent: compile them concurrently
+    procs = [subprocess.Popen([nvcc(), *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for src, obj in zip(SOURCES, objs)]
     log = []
-    for src in SOURCES:
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
-        if r.returncode:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
-        objs.append(obj)
+    failed = []
+    for src, p in zip(SOURCES, procs):
+        out, _ = p.communicate()
+        log.append(out)
+        if p.returncode:
+            failed.append(f"nvcc failed for {src}:\n{out}")
+    if failed:
+        raise RuntimeError("\n".join(failed))
     tmp = LIB + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

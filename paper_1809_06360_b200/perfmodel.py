@@ -40,6 +40,17 @@ def hbm_peak_gbs(repo_root=None):
         return 6650.0, "fallback"
 
 
+def sweep_kernel_name(n, m, force_generic=False):
+    """The K1 kernel the C-ABI layer picks for (n, m) (plq_api.cu
+    use_small_sweep / sweep_threads), named as ncu lists it."""
+    small = {(12, 4): "sweep_small_kernel<12,4,1,1>", (32, 8): "sweep_small_kernel<32,8,4,1>",
+             (64, 32): "sweep_small_kernel<64,32,8,1>"}
+    if not force_generic and (n, m) in small:
+        return small[(n, m)]
+    nt = 32 if n <= 16 else (128 if n <= 32 else 256)
+    return f"sweep_kernel<{nt}>"
+
+
 def stage_flops(n, m):
     Fe = 6 * n**3 + 20 * n**2 * m + 12 * n * m**2 + m**3 / 3 + 20 * n**2 + 16 * n * m + 7 * m**2
     Fs = 4 * n**3 + 8 * n**2 * m + 8 * n * m**2 + m**3 / 3 + 11 * n**2 + 9 * n * m + 5 * m**2

@@ -10,6 +10,14 @@ Appendix B:
 * ``qx1, qu1 ~ N(0, 1)``; terminal ``Qxx_T`` from the ``Qxx`` recipe and
   ``qx1_T ~ N(0, 1)``; ``x_init ~ N(0, 1)``.
 
+``cross > 0`` (not a BASELINE config: test data for the ``Qux`` paths of
+the kernels) adds ``Qux = cross * N(0, 1)``, drawn after everything else and
+halved until the control-eliminated state cost ``Qxx - Qux' Quu^-1 Qux`` is
+PSD -- the shrink rule of the reference's generator (generate.py:27-32).
+
+:func:`generate_reference_recipe` restates the reference's own generator
+(``parlqr.generate``, generate.py:14-47) for the fuzz / cross-term tests.
+
 One ``numpy.random.default_rng(seed + i)`` per problem ``i``.  Draw order
 (fixed, documented in DESIGN.md): ``G (T,n,n), Bu (T,n,m), c (T,n),
 W (T,n,n), V (T,m,m), q (T,n), r (T,m), W_T (n,n), qT (n), x0 (n)``.
@@ -38,6 +46,7 @@ class Config:
     a_scale: float = 0.1
     q_eps: float = 1e-2
     r_eps: float = 1e-1
+    cross: float = 0.0
 
     @property
     def knots(self):
@@ -62,7 +71,16 @@ def _sym(a):
     return 0.5 * (a + np.swapaxes(a, -1, -2))
 
 
-def generate_one(n, m, T, seed, a_scale=0.1, q_eps=1e-2, r_eps=1e-1):
+def _shrink_cross(Qxx, Quu, Qux):
+    """Halve each stage's ``Qux`` until ``Qxx - Qux' Quu^-1 Qux`` is PSD
+    (the acceptance loop of generate.py:29-32, applied stage-wise)."""
+    for t in range(Qux.shape[0]):
+        while np.linalg.eigvalsh(Qxx[t] - Qux[t].T @ np.linalg.solve(Quu[t], Qux[t])).min() < 0.0:
+            Qux[t] *= 0.5
+    return Qux
+
+
+def generate_one(n, m, T, seed, a_scale=0.1, q_eps=1e-2, r_eps=1e-1, cross=0.0):
     """One problem as a dict of stacked arrays (``(T, ...)`` per field)."""
     rng = np.random.default_rng(seed)
     G = rng.standard_normal((T, n, n))
@@ -90,6 +108,50 @@ def generate_one(n, m, T, seed, a_scale=0.1, q_eps=1e-2, r_eps=1e-1):
         "qx1T": qT,
         "x_init": x0,
     }
+    if cross:
+        Qux = cross * rng.standard_normal((T, m, n))
+        out["Qux"] = _shrink_cross(out["Qxx"], out["Quu"], Qux)
+    return {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in out.items()}
+
+
+def generate_reference_recipe(n, m, T, seed):
+    """The reference's random problem (``parlqr.generate``, generate.py:14-47)
+    restated on stacked arrays: per stage ``Quu = B B' + I``, ``Qxx = C C'``,
+    ``Qux = 0.3 N(0,1)`` halved until ``Qxx - Qux' Quu^-1 Qux`` is PSD,
+    ``qx1, qu1 ~ N(0,1)``, ``Fx ~ N(0,1)`` rescaled to spectral radius
+    <= 1.05, ``Fu, f1 ~ N(0,1)``; then terminal ``D D'``, ``qx1_T`` and
+    ``x_init``.  Same draw order as the reference, so a given seed yields the
+    reference's problem (up to the symmetrization of its constructors, which
+    is applied here as well)."""
+    if min(n, m, T) < 1:
+        raise ValueError("n, m and T must all be at least 1")
+    rng = np.random.default_rng(seed)
+    f = {k: [] for k in STAGE_FIELDS}
+    for _ in range(T):
+        Bm = rng.standard_normal((m, m))
+        Quu = Bm @ Bm.T + np.eye(m)
+        C = rng.standard_normal((n, n))
+        Qxx = C @ C.T
+        Qux = 0.3 * rng.standard_normal((m, n))
+        while np.linalg.eigvalsh(Qxx - Qux.T @ np.linalg.solve(Quu, Qux)).min() < 0.0:
+            Qux = Qux * 0.5
+        f["qx1"].append(rng.standard_normal(n))
+        f["qu1"].append(rng.standard_normal(m))
+        Fx = rng.standard_normal((n, n))
+        rho = float(np.abs(np.linalg.eigvals(Fx)).max())
+        if rho > 1.05:
+            Fx = Fx * (1.05 / rho)
+        f["Fx"].append(Fx)
+        f["Fu"].append(rng.standard_normal((n, m)))
+        f["f1"].append(rng.standard_normal(n))
+        f["Qxx"].append(_sym(Qxx))
+        f["Quu"].append(_sym(Quu))
+        f["Qux"].append(Qux)
+    D = rng.standard_normal((n, n))
+    out = {k: np.stack(v) for k, v in f.items()}
+    out["QxxT"] = _sym(D @ D.T)
+    out["qx1T"] = rng.standard_normal(n)
+    out["x_init"] = rng.standard_normal(n)
     return {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in out.items()}
 
 
@@ -97,9 +159,55 @@ def generate_batch(cfg, seed=0, count=None, first=0):
     """Problems ``first .. first+count-1`` of ``cfg`` stacked as ``(B, T, ...)``."""
     count = cfg.B if count is None else count
     probs = [generate_one(cfg.n, cfg.m, cfg.T, seed + first + i, cfg.a_scale,
-                          cfg.q_eps, cfg.r_eps) for i in range(count)]
+                          cfg.q_eps, cfg.r_eps, cfg.cross) for i in range(count)]
     return {k: np.ascontiguousarray(np.stack([p[k] for p in probs]))
             for k in probs[0]}
+
+
+def _fill_rows(args):
+    cfg, seed, first, lo, hi = args
+    for i in range(lo, hi):
+        one = generate_one(cfg.n, cfg.m, cfg.T, seed + first + i, cfg.a_scale, cfg.q_eps, cfg.r_eps, cfg.cross)
+        for k, v in one.items():
+            _SHARED[k][i] = v
+    return hi - lo
+
+
+_SHARED = {}
+
+
+def generate_batch_parallel(cfg, seed=0, count=None, first=0, workers=None):
+    """:func:`generate_batch` with the problems drawn by a fork pool into one
+    shared anonymous mapping (same bytes; cfg4's 28 GB batch takes seconds
+    instead of minutes).  Returns numpy arrays backed by that mapping."""
+    import mmap
+    import multiprocessing
+    import os
+    count = cfg.B if count is None else count
+    workers = workers or min(count, os.cpu_count() or 1)
+    if workers <= 1 or count < 4:
+        return generate_batch(cfg, seed, count, first)
+    one = generate_one(cfg.n, cfg.m, 1, 0)
+    shapes = {k: (count, cfg.T, *v.shape[1:]) if k in STAGE_FIELDS else (count, *v.shape)
+              for k, v in one.items()}
+    sizes = {k: 8 * int(np.prod(s)) for k, s in shapes.items()}
+    buf = mmap.mmap(-1, sum(sizes.values()))
+    off = 0
+    out = {}
+    for k, shp in shapes.items():
+        out[k] = np.frombuffer(buf, dtype=np.float64, count=sizes[k] // 8, offset=off).reshape(shp)
+        off += sizes[k]
+    _SHARED.clear()
+    _SHARED.update(out)
+    step = -(-count // (4 * workers))
+    chunks = [(cfg, seed, first, lo, min(count, lo + step)) for lo in range(0, count, step)]
+    try:
+        with multiprocessing.get_context("fork").Pool(workers) as pool:
+            done = sum(pool.map(_fill_rows, chunks))
+    finally:
+        _SHARED.clear()
+    assert done == count
+    return out
 
 
 def batch_nbytes(cfg, B=None):

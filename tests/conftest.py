@@ -45,3 +45,13 @@ def load_synth(name):
 
 SYNTH_FIXTURES = ("cfg0_seed0", "cfg1_first4", "cfg2_shape_T256_J4", "cfg3_shape_T16_J2",
                   "cfg4_shape_T64_J2")
+
+
+@pytest.fixture(params=["specialized", "generic"])
+def kernel_path(request, monkeypatch):
+    # PLQ_FORCE_GENERIC=1 routes the config shapes through the generic kernels
+    if request.param == "generic":
+        monkeypatch.setenv("PLQ_FORCE_GENERIC", "1")
+    else:
+        monkeypatch.delenv("PLQ_FORCE_GENERIC", raising=False)
+    return request.param

@@ -1,7 +1,9 @@
 """Randomised GPU parity over odd shapes: n = 1..9, m = 1..5 (m > n, n % m != 0
 mixed branch), J up to T (one-stage segments), random unbalanced partitions,
-generated by the reference's generator recipe restated (synth.generate_one)
-and by the BASELINE recipe.  Non-degenerate partitions are compared with the
+generated alternately by the reference's own generator restated
+(``synth.generate_reference_recipe``, generate.py:14-47: cross term
+``Qux = 0.3 N(0,1)``, spectral radius 1.05) and by the BASELINE recipe with a
+cross term (``synth.generate_one(..., cross=0.3)``).  Non-degenerate partitions are compared with the
 oracle (max(1e-9, 10 * floor) on x/u/lambda, 1e-9 on K and the objective);
 degenerate ones (feasibility-constrained link path) must reach the method's
 own KKT accuracy and link mismatch (test_parallel.py:131-135, 105-119)."""
@@ -36,8 +38,11 @@ def _cases(count, seed):
 def test_random_shapes_and_partitions(block):
     from paper_1809_06360_b200 import Partition, UnsupportedPartition, solve_parallel_batch, synth
     checked = degenerate = unsupported = 0
-    for n, m, T, J, splits, seed in _cases(40, 1000 + block):
-        a = synth.generate_one(n, m, T, seed=seed)
+    for c, (n, m, T, J, splits, seed) in enumerate(_cases(40, 1000 + block)):
+        if c % 2 == 0:
+            a = synth.generate_reference_recipe(n, m, T, seed=seed)
+        else:
+            a = synth.generate_one(n, m, T, seed=seed, cross=0.3)
         sp = splits if splits is not None else tuple(O.make_partition(T, J))
         part = Partition(len(sp) - 1, tuple(sp))
         try:

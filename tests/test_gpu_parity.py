@@ -89,16 +89,6 @@ def test_reference_goldens_small(name):
         assert degenerate >= 1
 
 
-@pytest.fixture(params=["specialized", "generic"])
-def kernel_path(request, monkeypatch):
-    # PLQ_FORCE_GENERIC=1 routes the config shapes through the generic kernels
-    if request.param == "generic":
-        monkeypatch.setenv("PLQ_FORCE_GENERIC", "1")
-    else:
-        monkeypatch.delenv("PLQ_FORCE_GENERIC", raising=False)
-    return request.param
-
-
 @pytest.mark.parametrize("name", SYNTH_FIXTURES)
 def test_reference_goldens_configs(name, kernel_path):
     cfg, batch, z = load_synth(name)

@@ -155,6 +155,41 @@ class TestGenerator:
         assert np.all(np.linalg.eigvalsh(a["Quu"]) > 0.1 - 1e-12)
         assert not np.any(a["Qux"])
 
+    def test_cross_term_option(self):
+        base = synth.generate_one(12, 4, 16, seed=3)
+        a = synth.generate_one(12, 4, 16, seed=3, cross=0.3)
+        for k in base:                       # drawn last: the other fields are unchanged
+            if k != "Qux":
+                np.testing.assert_array_equal(a[k], base[k])
+        assert np.all(np.abs(a["Qux"]).max(axis=(1, 2)) > 0)
+        for t in range(16):
+            S = a["Qxx"][t] - a["Qux"][t].T @ np.linalg.solve(a["Quu"][t], a["Qux"][t])
+            assert np.linalg.eigvalsh(S).min() >= 0.0
+
+    def test_reference_recipe_matches_reference_generator(self):
+        """synth.generate_reference_recipe restates parlqr.generate
+        (generate.py:14-47): same seed, same problem, byte for byte."""
+        import os
+        import sys
+        src = "/root/reference/pkg/src"
+        if not os.path.isdir(src):
+            pytest.skip("reference not mounted (GPU box)")
+        sys.path.insert(0, src)
+        try:
+            from parlqr.generate import generate
+        finally:
+            sys.path.remove(src)
+        for n, m, T, seed in ((3, 2, 5, 0), (12, 4, 6, 7), (5, 7, 4, 11)):
+            ref = generate(n, m, T, seed)
+            a = synth.generate_reference_recipe(n, m, T, seed)
+            for f in synth.STAGE_FIELDS:
+                want = np.stack([getattr(c if f[0] in "Qq" else d, f) for c, d in ref.stages])
+                np.testing.assert_array_equal(a[f], want, err_msg=f)
+            np.testing.assert_array_equal(a["QxxT"], ref.terminal.Qxx)
+            np.testing.assert_array_equal(a["qx1T"], ref.terminal.qx1)
+            np.testing.assert_array_equal(a["x_init"], ref.x_init)
+            assert np.any(a["Qux"])
+
     def test_batch_rows_are_per_problem_seeds(self):
         cfg = synth.CONFIGS[1].scaled(B=3)
         batch = synth.generate_batch(cfg, seed=5, count=3)
