@@ -38,14 +38,19 @@ extern "C" {
  *   0          ok
  *   1 + t      CholeskyFailure(t), t = segment-local stage (endpoint.py:243-245,
  *              serial.py:63-66)
- *   -1         rank-deficient constraint-to-go / leftover feasibility rows:
- *              the degenerate-partition path (parallel.py:322-384, 452-456) is
- *              not built on the GPU -> UnsupportedPartition
- *   -2         LinkSingular (parallel.py:267-271); stored in segment 0's slot */
+ *   -1         segment ends with feasibility rows (a degenerate partition,
+ *              parallel.py:322-384, 452-456) but plq_outputs_t.feas is NULL, so
+ *              the constrained link solve cannot run -> UnsupportedPartition
+ *   -2         LinkSingular (parallel.py:267-271); stored in segment 0's slot
+ *   -3         Infeasible(residual, segment) (parallel.py:462-475)
+ *   -4         malformed partition (ValueError, parallel.py:88-89, 434-440) */
 #define PLQ_STATUS_OK 0
 #define PLQ_STATUS_DEGENERATE (-1)
 #define PLQ_STATUS_LINK_SINGULAR (-2)
 #define PLQ_STATUS_INFEASIBLE (-3)  /* segment's feasibility rows violated at the solved links */
+#define PLQ_STATUS_BAD_PARTITION (-4) /* split_times not increasing from 0 to T, or a segment longer
+                                         than max_seg_len (checked on the device; the segment is
+                                         skipped, the Python layer raises ValueError) */
 
 /* One batch of B independent problems sharing (T, n, m) and one partition.
  * Replaces the (problem, partition, tolerances) arguments of

@@ -16,6 +16,7 @@ PLQ_OK = 0
 PLQ_STATUS_DEGENERATE = -1
 PLQ_STATUS_LINK_SINGULAR = -2
 PLQ_STATUS_INFEASIBLE = -3
+PLQ_STATUS_BAD_PARTITION = -4
 
 # every entry point declared in include/parlqr_b200.h
 EXPORTS = (

@@ -46,6 +46,16 @@ struct SweepLayout {
   int64_t tiles_off;         // smem offset of the tiled-GEMM staging area
 };
 
+// Segment j of the partition is well formed: 1 <= L <= max_seg_len, the
+// first segment starts at 0 and the last ends at T.  The kernels whose
+// shared-memory buffers are sized from max_seg_len skip (and the sweeps
+// flag, PLQ_STATUS_BAD_PARTITION) a segment that is not -- the C ABI cannot
+// read device-resident split_times without a host synchronization.
+__host__ __device__ inline bool segment_bounds_ok(const plq_problem_t& p, int j) {
+  const int lo = p.split_times[j], hi = p.split_times[j + 1];
+  return hi - lo >= 1 && hi - lo <= p.max_seg_len && (j > 0 || lo == 0) && (j < p.J - 1 || hi == p.T);
+}
+
 struct SweepArgs {
   plq_problem_t p;
   double* Kx;      // (B,T,m,n)

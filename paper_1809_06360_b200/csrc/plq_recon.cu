@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(NT) recon_kernel(ReconArgs A) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
     const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
+    if (!segment_bounds_ok(p, j)) continue;   // malformed partition (flagged by the sweep)
     const bool last = (j == J - 1);
     const int vsz = 3 * nn + 2 * n;
     const double* vf = A.vf0 + (b * J + j) * (int64_t)vsz;
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(NT) boundary_kernel(ReconArgs A) {
       if (tid == 0) A.part[(b * J + j) * 3 + 2] = 0.0;
       continue;
     }
+    if (!segment_bounds_ok(p, j)) continue;
     const int hi = p.split_times[j + 1];
     const int64_t st = b * T + (hi - 1);
     for (int i = tid; i < n; i += blockDim.x) lamn[i] = A.lambda_right[(b * (J - 1) + j) * n + i];
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(128) boundary_small_kernel(ReconArgs A) {
     A.part[(b * J + j) * 3 + 2] = 0.0;
     return;
   }
+  if (!segment_bounds_ok(p, j)) return;
   const int hi = p.split_times[j + 1];
   const int64_t st = b * T + (hi - 1);
   double ln[N];

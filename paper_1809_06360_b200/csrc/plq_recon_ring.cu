@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(NT) recon_fwd_kernel(ReconArgs A) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
     const int lo = p.split_times[j], L = p.split_times[j + 1] - lo;
+    if (!segment_bounds_ok(p, j)) continue;   // malformed partition (flagged by the sweep)
     const bool last = (j == J - 1);
     const int64_t s0 = b * T + lo;
     if (tid == 0)
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(NT) recon_eval_kernel(ReconArgs A) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
     const int lo = p.split_times[j], L = p.split_times[j + 1] - lo;
+    if (!segment_bounds_ok(p, j)) continue;   // malformed partition (flagged by the sweep)
     const int64_t s0 = b * T + lo, x0 = b * (T + 1) + lo;
     if (tid == 0)
       for (int k = 0; k < RS && k < L; ++k) eval_issue<N, M>(A, ring + k * R::SLOT, bars + k, s0 + k, x0 + k);
@@ -270,6 +272,7 @@ __global__ void __launch_bounds__(NT) recon_bwd_kernel(ReconArgs A) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
     const int lo = p.split_times[j], L = p.split_times[j + 1] - lo;
+    if (!segment_bounds_ok(p, j)) continue;   // malformed partition (flagged by the sweep)
     const bool last = (j == J - 1);
     const int64_t s0 = b * T + lo;
     if (tid == 0)

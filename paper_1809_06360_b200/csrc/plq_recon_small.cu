@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(32) recon_small_kernel(ReconArgs A) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
     const int lo = p.split_times[j], hi = p.split_times[j + 1], L = hi - lo;
+    if (!segment_bounds_ok(p, j)) continue;   // malformed partition (flagged by the sweep)
     const bool last = (j == J - 1);
     if (lane < N) {
       const double a0 = (j == 0) ? p.x_init[b * N + lane] : A.links[(b * (J - 1) + (j - 1)) * N + lane];
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(32) recon_seg_kernel(ReconArgs A) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
     const int lo = p.split_times[j], L = p.split_times[j + 1] - lo;
+    if (L < 1 || L > LMAX) continue;     // malformed partition: flagged by the sweep, buffers sized for LMAX
     const bool last = (j == J - 1);
     const int64_t s0 = b * T + lo;
     const double* vfg = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);
@@ -602,6 +604,7 @@ __global__ void __launch_bounds__(NT) recon_ring_kernel(ReconArgs A) {
     const int64_t b = task / nloc;
     const int j = A.seg_begin + (int)(task % nloc);
     const int lo = p.split_times[j], L = p.split_times[j + 1] - lo;
+    if (L < 1 || L > LMAX) continue;     // malformed partition: flagged by the sweep; gh holds LMAX stages
     const bool last = (j == J - 1);
     const int64_t s0 = b * T + lo;
     const double* vfg = A.vf0 + (b * J + j) * (int64_t)(3 * NN + 2 * N);

@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(NT) smooth_map_kernel(SmoothArgs a, MapLayout 
   const int64_t b = blockIdx.x / (J - 1);
   const int j = (int)(blockIdx.x % (J - 1));
   const int lo = p.split_times[j], hi = p.split_times[j + 1];
+  if (!segment_bounds_ok(p, j)) return;
   const int64_t nn = (int64_t)n * n, nm = (int64_t)n * m;
   double* X = L.onchip ? sm : scratch + (int64_t)blockIdx.x * (2 * n + m) * ld;
   double* X2 = X + n * ld;
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(NT) smooth_roll_kernel(SmoothArgs a, RollLayou
   const int64_t b = blockIdx.x / J;
   const int j = (int)(blockIdx.x % J);
   const int lo = p.split_times[j], hi = p.split_times[j + 1];
+  if (!segment_bounds_ok(p, j)) return;
   const int tlast = p.split_times[J - 1];
   const int64_t nn = (int64_t)n * n, nm = (int64_t)n * m;
   double* x = sm;

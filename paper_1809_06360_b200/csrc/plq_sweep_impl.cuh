@@ -583,6 +583,10 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArg
   for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
+    if (!segment_bounds_ok(a.p, j)) {
+      if (threadIdx.x == 0) a.status[b * a.p.J + j] = PLQ_STATUS_BAD_PARTITION;
+      continue;
+    }
     sweep_segment<NT>(a, bf, b, j);
   }
 }

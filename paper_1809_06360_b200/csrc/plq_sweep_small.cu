@@ -817,10 +817,13 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS, (NWG == 1 ? 16 : 1)) sweep_
   while (task < total) {
     const int64_t b = task / nloc;
     const int j = a.seg_begin + (int)(task % nloc);
-    if ((j == a.p.J - 1 && !a.endpoint_terminal) || a.smooth_vf0)
+    if (!segment_bounds_ok(a.p, j)) {
+      if (gt == 0) a.status[b * a.p.J + j] = PLQ_STATUS_BAD_PARTITION;
+    } else if ((j == a.p.J - 1 && !a.endpoint_terminal) || a.smooth_vf0) {
       small_segment<N, M, NWG, true>(a, sm, grp, gt, b, j, phase, pairs);
-    else
+    } else {
       small_segment<N, M, NWG, false>(a, sm, grp, gt, b, j, phase, pairs);
+    }
     if (gt == 0)
       next_task[grp] = a.task_ctr ? first_free + (long long)atomicAdd(a.task_ctr, 1ULL) : task + first_free;
     gsync<NWG>(grp);

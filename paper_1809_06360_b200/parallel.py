@@ -21,7 +21,7 @@ import os
 
 import numpy as np
 
-from . import _native
+from . import _native, compat
 from .errors import CholeskyFailure, Infeasible, LinkSingular, UnsupportedPartition
 from .problem import DEFAULT_TOLERANCES, AffinePolicy, LqrSolution
 
@@ -37,7 +37,7 @@ WORKERS_ENV_VAR = "PAR_RICCATI_WORKERS"
 
 
 @dataclasses.dataclass(frozen=True)
-class Partition:
+class _Partition:
     """Split of the horizon into ``J`` contiguous segments (parallel.py:67-79)."""
 
     J: int
@@ -49,6 +49,11 @@ class Partition:
     @property
     def interior(self):
         return self.split_times[1:-1]
+
+
+_ref_parallel = compat.reference_module("parallel")
+# the reference's own Partition when parlqr is importable (see compat.py)
+Partition = _ref_parallel.Partition if _ref_parallel is not None else _Partition
 
 
 def make_partition(T, J):
@@ -71,7 +76,7 @@ def default_workers(J):
 
 
 @dataclasses.dataclass(eq=False, repr=False)
-class ParallelDetails:
+class _ParallelDetails:
     """Diagnostics of a partitioned solve (parallel.py:390-405)."""
 
     partition: Partition
@@ -86,6 +91,9 @@ class ParallelDetails:
     degenerate: bool
     segment_diagnostics: tuple = None
     smooth_deviation: float = None
+
+
+ParallelDetails = _ref_parallel.ParallelDetails if _ref_parallel is not None else _ParallelDetails
 
 
 class PolicySequence(collections.abc.Sequence):
@@ -299,6 +307,10 @@ def raise_for_status(status, feas_residual=None):
     order (pool.map, parallel.py:207), then the link solve, then the
     feasibility check at the solved links (parallel.py:462-475)."""
     status = np.atleast_2d(status)
+    if np.any(status == _native.PLQ_STATUS_BAD_PARTITION):
+        j = int(np.argwhere(status == _native.PLQ_STATUS_BAD_PARTITION)[0][1])
+        raise ValueError(f"malformed partition at segment {j}: split times must increase from 0 to T "
+                         "with no segment longer than max_seg_len")
     bad = np.argwhere((status > 0) | (status == _native.PLQ_STATUS_DEGENERATE))
     if bad.size:
         b, j = (int(v) for v in bad[np.lexsort((bad[:, 1], bad[:, 0]))][0])
@@ -369,7 +381,14 @@ def solve_parallel(problem, J, workers=None, tolerances=DEFAULT_TOLERANCES, coll
     batch = {f: a[f][None] for f in INPUT_FIELDS}
     solver = solve_parallel_batch(batch, partition=partition, tolerances=tolerances, device=device)
     o = {k: (v.cpu().numpy()[0] if v is not None else None) for k, v in solver.out.items()}
-    n = a["x_init"].shape[0]
+    return solution_from_outputs(o, partition)
+
+
+def solution_from_outputs(o, partition):
+    """``LqrSolution`` + ``ParallelDetails`` (the reference's classes when
+    ``parlqr`` is importable) from one problem's host outputs ``o`` (the
+    ``BatchSolver.out`` fields of one batch row, parallel.py:529-553)."""
+    n = o["x"].shape[1]
     Jp = partition.J
     nn = n * n
     vf = o["vf0"]
@@ -397,7 +416,7 @@ def solve_parallel(problem, J, workers=None, tolerances=DEFAULT_TOLERANCES, coll
         feas.append((F[:, :n].copy(), F[:, n:2 * n].copy(), F[:, 2 * n].copy()))
     fres = o.get("feas_residual")
     details = ParallelDetails(
-        partition=partition,
+        partition=Partition(partition.J, tuple(partition.split_times)),
         link_points=links,
         link_residual=float(o["link_residual"]),
         mu_left=o["mu_left"][:Jp - 1],

@@ -1,8 +1,13 @@
-"""Problem / solution containers with the reference's field names and
-conventions (parlqr/problem.py:44-280), so code written against ``parlqr``
-runs unchanged.  Objects of the reference package itself are accepted too:
-the solver only reads ``stages[t] = (cost, dynamics)``, ``terminal`` and
-``x_init`` attributes.
+"""Problem / solution containers of the drop-in.
+
+When the reference package ``parlqr`` is importable, this module re-exports
+ITS classes (``parlqr.problem``: ``StageCost``, ``StageDynamics``,
+``TerminalCost``, ``LqrProblem``, ``AffinePolicy``, ``LqrSolution``,
+``ToleranceSet``), so a caller of the drop-in receives exactly the reference's
+types (``isinstance(sol, parlqr.LqrSolution)`` holds).  Without ``parlqr``
+(e.g. on a GPU box that only has this package) small stand-ins with the same
+field names and conventions are used (problem.py:44-280): the solver itself
+only reads ``stages[t] = (cost, dynamics)``, ``terminal`` and ``x_init``.
 
 Stage cost ``1/2 x'Qxx x + 1/2 u'Quu u + u'Qux x + qx1'x + qu1'u``, dynamics
 ``x' = Fx x + Fu u + f1``, terminal ``1/2 x'Qxx_T x + qx1_T'x``; multipliers
@@ -15,14 +20,41 @@ import dataclasses
 
 import numpy as np
 
+from . import compat
+
 __all__ = [
     "ToleranceSet", "DEFAULT_TOLERANCES", "StageCost", "TerminalCost",
-    "StageDynamics", "LqrProblem", "AffinePolicy", "LqrSolution",
+    "StageDynamics", "LqrProblem", "AffinePolicy", "LqrSolution", "problem_from_arrays",
+    "USING_REFERENCE_TYPES",
 ]
 
 
+def _frozen(value, shape=None, what="array"):
+    """float64 copy, shape-checked, read-only (the reference's arrays are)."""
+    out = np.array(value, dtype=np.float64)
+    if shape is not None and out.shape != tuple(shape):
+        raise ValueError(f"{what} must have shape {tuple(shape)}, got {out.shape}")
+    out.setflags(write=False)
+    return out
+
+
+def _symmetric_part(value, what):
+    """(0.5 (A + A'), relative asymmetry of A) -- problem.py:81-88."""
+    a = np.array(value, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError(f"{what} must be square, got shape {a.shape}")
+    scale = float(np.abs(a).max()) if a.size else 0.0
+    asym = float(np.abs(a - a.T).max()) / scale if scale else 0.0
+    return _frozen(0.5 * (a + a.T)), asym
+
+
+def _set(obj, **fields):
+    for k, v in fields.items():
+        object.__setattr__(obj, k, v)
+
+
 @dataclasses.dataclass(frozen=True)
-class ToleranceSet:
+class _ToleranceSet:
     """Numerical thresholds (problem.py:44-58)."""
 
     rank_tol: float = 1e-10
@@ -30,30 +62,8 @@ class ToleranceSet:
     kkt_tol: float = 1e-8
 
 
-DEFAULT_TOLERANCES = ToleranceSet()
-
-
-def _ro(a, shape=None, name="array"):
-    arr = np.array(a, dtype=np.float64)
-    if shape is not None and arr.shape != shape:
-        raise ValueError(f"{name} must have shape {shape}, got {arr.shape}")
-    arr.setflags(write=False)
-    return arr
-
-
-def _sym(a, name):
-    arr = np.array(a, dtype=np.float64)
-    if arr.ndim != 2 or arr.shape[0] != arr.shape[1]:
-        raise ValueError(f"{name} must be square, got shape {arr.shape}")
-    amax = float(np.abs(arr).max()) if arr.size else 0.0
-    defect = float(np.abs(arr - arr.T).max()) / amax if amax else 0.0
-    out = 0.5 * (arr + arr.T)
-    out.setflags(write=False)
-    return out, defect
-
-
-@dataclasses.dataclass(frozen=True, eq=False, repr=False)
-class StageCost:
+@dataclasses.dataclass(frozen=True, eq=False, repr=False, init=False)
+class _StageCost:
     """Quadratic stage cost; ``Qxx``/``Quu`` symmetrized on construction."""
 
     Qxx: np.ndarray
@@ -61,82 +71,58 @@ class StageCost:
     Quu: np.ndarray
     qx1: np.ndarray
     qu1: np.ndarray
-    asymmetry: float = 0.0
+    asymmetry: float
 
     def __init__(self, Qxx, Qux, Quu, qx1, qu1):
-        Qxx, dx = _sym(Qxx, "Qxx")
-        Quu, du = _sym(Quu, "Quu")
-        n, m = Qxx.shape[0], Quu.shape[0]
-        object.__setattr__(self, "Qxx", Qxx)
-        object.__setattr__(self, "Quu", Quu)
-        object.__setattr__(self, "Qux", _ro(Qux, (m, n), "Qux"))
-        object.__setattr__(self, "qx1", _ro(qx1, (n,), "qx1"))
-        object.__setattr__(self, "qu1", _ro(qu1, (m,), "qu1"))
-        object.__setattr__(self, "asymmetry", max(dx, du))
+        sxx, ax = _symmetric_part(Qxx, "Qxx")
+        suu, au = _symmetric_part(Quu, "Quu")
+        n, m = len(sxx), len(suu)
+        _set(self, Qxx=sxx, Quu=suu, Qux=_frozen(Qux, (m, n), "Qux"), qx1=_frozen(qx1, (n,), "qx1"),
+             qu1=_frozen(qu1, (m,), "qu1"), asymmetry=max(ax, au))
 
-    @property
-    def n(self):
-        return self.Qxx.shape[0]
-
-    @property
-    def m(self):
-        return self.Quu.shape[0]
+    n = property(lambda self: self.Qxx.shape[0])
+    m = property(lambda self: self.Quu.shape[0])
 
 
-@dataclasses.dataclass(frozen=True, eq=False, repr=False)
-class TerminalCost:
+@dataclasses.dataclass(frozen=True, eq=False, repr=False, init=False)
+class _TerminalCost:
     Qxx: np.ndarray
     qx1: np.ndarray
-    asymmetry: float = 0.0
+    asymmetry: float
 
     def __init__(self, Qxx, qx1):
-        Qxx, d = _sym(Qxx, "terminal Qxx")
-        object.__setattr__(self, "Qxx", Qxx)
-        object.__setattr__(self, "qx1", _ro(qx1, (Qxx.shape[0],), "terminal qx1"))
-        object.__setattr__(self, "asymmetry", d)
+        sxx, ax = _symmetric_part(Qxx, "terminal Qxx")
+        _set(self, Qxx=sxx, qx1=_frozen(qx1, (len(sxx),), "terminal qx1"), asymmetry=ax)
 
-    @property
-    def n(self):
-        return self.Qxx.shape[0]
+    n = property(lambda self: self.Qxx.shape[0])
 
     @classmethod
     def zero(cls, n):
         return cls(np.zeros((n, n)), np.zeros(n))
 
 
-@dataclasses.dataclass(frozen=True, eq=False, repr=False)
-class StageDynamics:
+@dataclasses.dataclass(frozen=True, eq=False, repr=False, init=False)
+class _StageDynamics:
     Fx: np.ndarray
     Fu: np.ndarray
     f1: np.ndarray
 
     def __init__(self, Fx, Fu, f1):
-        Fx = np.array(Fx, dtype=np.float64)
-        if Fx.ndim != 2 or Fx.shape[0] != Fx.shape[1]:
-            raise ValueError(f"Fx must be square, got shape {Fx.shape}")
-        n = Fx.shape[0]
-        Fu = np.array(Fu, dtype=np.float64)
-        if Fu.ndim != 2 or Fu.shape[0] != n:
-            raise ValueError(f"Fu must have {n} rows, got shape {Fu.shape}")
-        Fx.setflags(write=False)
-        Fu.setflags(write=False)
-        object.__setattr__(self, "Fx", Fx)
-        object.__setattr__(self, "Fu", Fu)
-        object.__setattr__(self, "f1", _ro(f1, (n,), "f1"))
+        fx, fu = _frozen(Fx), _frozen(Fu)
+        if fx.ndim != 2 or fx.shape[0] != fx.shape[1]:
+            raise ValueError(f"Fx must be square, got shape {fx.shape}")
+        if fu.ndim != 2 or fu.shape[0] != fx.shape[0]:
+            raise ValueError(f"Fu must have {fx.shape[0]} rows, got shape {fu.shape}")
+        _set(self, Fx=fx, Fu=fu, f1=_frozen(f1, (fx.shape[0],), "f1"))
 
-    @property
-    def n(self):
-        return self.Fx.shape[0]
-
-    @property
-    def m(self):
-        return self.Fu.shape[1]
+    n = property(lambda self: self.Fx.shape[0])
+    m = property(lambda self: self.Fu.shape[1])
 
 
-@dataclasses.dataclass(frozen=True, eq=False, repr=False)
-class LqrProblem:
+@dataclasses.dataclass(frozen=True, eq=False, repr=False, init=False)
+class _LqrProblem:
     stages: tuple
-    terminal: TerminalCost
+    terminal: object
     x_init: np.ndarray
 
     def __init__(self, stages, terminal, x_init):
@@ -144,41 +130,23 @@ class LqrProblem:
         if not stages:
             raise ValueError("horizon must contain at least one stage")
         n, m = stages[0][0].n, stages[0][0].m
-        for t, (c, d) in enumerate(stages):
-            if c.n != n or c.m != m or d.n != n or d.m != m:
-                raise ValueError(f"inconsistent dimensions at stage {t}")
+        bad = [t for t, (c, d) in enumerate(stages) if (c.n, c.m, d.n, d.m) != (n, m, n, m)]
+        if bad:
+            raise ValueError(f"inconsistent dimensions at stage {bad[0]}")
         if terminal.n != n:
             raise ValueError("terminal cost dimension mismatch")
-        object.__setattr__(self, "stages", stages)
-        object.__setattr__(self, "terminal", terminal)
-        object.__setattr__(self, "x_init", _ro(x_init, (n,), "x_init"))
+        _set(self, stages=stages, terminal=terminal, x_init=_frozen(x_init, (n,), "x_init"))
 
-    @classmethod
-    def from_arrays(cls, a):
-        """Build from one problem's stacked arrays (``synth`` layout)."""
-        T = a["qx1"].shape[0]
-        stages = [(StageCost(a["Qxx"][t], a["Qux"][t], a["Quu"][t], a["qx1"][t], a["qu1"][t]),
-                   StageDynamics(a["Fx"][t], a["Fu"][t], a["f1"][t])) for t in range(T)]
-        return cls(stages, TerminalCost(a["QxxT"], a["qx1T"]), a["x_init"])
-
-    @property
-    def n(self):
-        return self.stages[0][0].n
-
-    @property
-    def m(self):
-        return self.stages[0][0].m
-
-    @property
-    def T(self):
-        return len(self.stages)
+    n = property(lambda self: self.stages[0][0].n)
+    m = property(lambda self: self.stages[0][0].m)
+    T = property(lambda self: len(self.stages))
 
     def __repr__(self):
         return f"LqrProblem(n={self.n}, m={self.m}, T={self.T})"
 
 
-@dataclasses.dataclass(frozen=True, eq=False, repr=False)
-class AffinePolicy:
+@dataclasses.dataclass(frozen=True, eq=False, repr=False, init=False)
+class _AffinePolicy:
     """``u = Kx x + Kz x_term + k1`` (problem.py:224-259)."""
 
     Kx: np.ndarray
@@ -186,32 +154,27 @@ class AffinePolicy:
     k1: np.ndarray
 
     def __init__(self, Kx, Kz, k1):
-        Kx = np.array(Kx, dtype=np.float64)
-        if Kx.ndim != 2:
+        kx = _frozen(Kx)
+        if kx.ndim != 2:
             raise ValueError("Kx must be a matrix")
-        m, n = Kx.shape
-        Kx.setflags(write=False)
-        object.__setattr__(self, "Kx", Kx)
-        object.__setattr__(self, "Kz", _ro(Kz, (m, n), "Kz"))
-        object.__setattr__(self, "k1", _ro(k1, (m,), "k1"))
-        object.__setattr__(self, "_uses_terminal", bool(np.any(self.Kz)))
+        kz = _frozen(Kz, kx.shape, "Kz")
+        _set(self, Kx=kx, Kz=kz, k1=_frozen(k1, kx.shape[:1], "k1"), _uses_terminal=bool(kz.any()))
 
     @classmethod
     def state_feedback(cls, Kx, k1):
-        Kx = np.asarray(Kx, dtype=np.float64)
-        return cls(Kx, np.zeros_like(Kx), k1)
+        return cls(Kx, np.zeros(np.shape(Kx)), k1)
 
     def __call__(self, x, x_term=None):
         u = self.Kx @ x + self.k1
-        if self._uses_terminal:
-            if x_term is None:
-                raise ValueError("policy depends on x_term but none was given")
-            u = u + self.Kz @ x_term
-        return u
+        if not self._uses_terminal:
+            return u
+        if x_term is None:
+            raise ValueError("policy depends on x_term but none was given")
+        return u + self.Kz @ x_term
 
 
 @dataclasses.dataclass(frozen=True, eq=False, repr=False)
-class LqrSolution:
+class _LqrSolution:
     """Numeric solution (problem.py:262-280)."""
 
     states: np.ndarray
@@ -223,3 +186,35 @@ class LqrSolution:
     mu: np.ndarray = None
     x_term: np.ndarray = None
     details: object = None
+
+
+_ref = compat.reference_module("problem")
+USING_REFERENCE_TYPES = _ref is not None
+if _ref is not None:
+    ToleranceSet = _ref.ToleranceSet
+    DEFAULT_TOLERANCES = _ref.DEFAULT_TOLERANCES
+    StageCost = _ref.StageCost
+    TerminalCost = _ref.TerminalCost
+    StageDynamics = _ref.StageDynamics
+    LqrProblem = _ref.LqrProblem
+    AffinePolicy = _ref.AffinePolicy
+    LqrSolution = _ref.LqrSolution
+else:
+    ToleranceSet = _ToleranceSet
+    DEFAULT_TOLERANCES = _ToleranceSet()
+    StageCost = _StageCost
+    TerminalCost = _TerminalCost
+    StageDynamics = _StageDynamics
+    LqrProblem = _LqrProblem
+    AffinePolicy = _AffinePolicy
+    LqrSolution = _LqrSolution
+
+
+def problem_from_arrays(a):
+    """An ``LqrProblem`` (the active class) from one problem's stacked arrays
+    (``synth`` layout: ``Qxx (T,n,n) ... f1 (T,n)``, ``QxxT``, ``qx1T``,
+    ``x_init``)."""
+    T = a["qx1"].shape[0]
+    stages = [(StageCost(a["Qxx"][t], a["Qux"][t], a["Quu"][t], a["qx1"][t], a["qu1"][t]),
+               StageDynamics(a["Fx"][t], a["Fu"][t], a["f1"][t])) for t in range(T)]
+    return LqrProblem(stages, TerminalCost(a["QxxT"], a["qx1T"]), a["x_init"])

@@ -141,7 +141,7 @@ def test_dependent_constraints():
     # test_endpoint.py:171-175: one step cannot pin three states with one control
     import paper_1809_06360_b200 as plq
     from paper_1809_06360_b200 import synth
-    prob = plq.LqrProblem.from_arrays(synth.generate_one(3, 1, 1, seed=61))
+    prob = plq.problem_from_arrays(synth.generate_one(3, 1, 1, seed=61))
     with pytest.raises(plq.FactorizationFailure):
         plq.solve_endpoint_affine(prob, require_multipliers=True)
     with pytest.raises(plq.SolverError):
@@ -153,7 +153,7 @@ def test_map_boundary_blocks_equal_value_gradients():
     import paper_1809_06360_b200 as plq
     from conftest import load_stored
     a, _, _ = load_stored("small_random")[5]
-    prob = plq.LqrProblem.from_arrays(a)
+    prob = plq.problem_from_arrays(a)
     aff = plq.solve_endpoint_affine(prob)
     v0, mm = aff.values[0], aff.multipliers
     tol = 1e-7 * _scale(a)
@@ -167,7 +167,7 @@ def test_endpoint_exactness_over_many_targets():
     import paper_1809_06360_b200 as plq
     from conftest import load_stored
     a, _, _ = load_stored("small_random")[9]
-    prob = plq.LqrProblem.from_arrays(a)
+    prob = plq.problem_from_arrays(a)
     aff = plq.solve_endpoint_affine(prob)
     rng = np.random.default_rng(5)
     n = a["x_init"].shape[0]

@@ -136,7 +136,7 @@ def test_solve_parallel_drop_in_api():
     import paper_1809_06360_b200 as plq
     from paper_1809_06360_b200 import synth
     a = synth.generate_one(12, 4, 64, seed=3)
-    prob = plq.LqrProblem.from_arrays(a)
+    prob = plq.problem_from_arrays(a)
     sol = plq.solve_parallel(prob, J=4, workers=8)
     ref = O.solve(a, J=4)
     assert isinstance(sol, plq.LqrSolution)
@@ -163,7 +163,7 @@ def test_solve_parallel_drop_in_api():
 def test_partition_errors_match_reference():
     import paper_1809_06360_b200 as plq
     from paper_1809_06360_b200 import synth
-    prob = plq.LqrProblem.from_arrays(synth.generate_one(3, 1, 6, seed=1))
+    prob = plq.problem_from_arrays(synth.generate_one(3, 1, 6, seed=1))
     with pytest.raises(ValueError):
         plq.solve_parallel(prob, J=7)
     with pytest.raises(ValueError):
@@ -301,3 +301,41 @@ def test_large_n_split_link_vs_oracle(n, m, T, J, kernel_path):
     ref = O.solve(prob, J=J)
     floors = _floor(prob, J, ref)
     _check(g, 0, ref, floors)
+
+
+@pytest.mark.parametrize("n,m,T,J", [(12, 4, 64, 8), (32, 8, 256, 4), (64, 32, 64, 2), (6, 2, 40, 4)])
+def test_understated_max_seg_len_is_flagged_not_overrun(n, m, T, J):
+    """The C ABI trusts max_seg_len for buffer sizing only after the device
+    checked each segment against it: an understated value (or splits that do
+    not run 0..T) flags PLQ_STATUS_BAD_PARTITION and the host raises
+    ValueError -- no shared-memory overrun."""
+    import ctypes
+    import torch
+    from paper_1809_06360_b200 import BatchSolver, _native, synth
+    from paper_1809_06360_b200.parallel import _ptr
+    from paper_1809_06360_b200.parallel import raise_for_status
+    cfg = synth.Config("bad", 2, n, m, T, J)
+    batch = synth.generate_batch(cfg, seed=3, count=2)
+    dev = torch.device("cuda", 0)
+    s = BatchSolver(2, T, n, m, J=J, device=dev)
+    inputs = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
+    for empty_first, msl in ((False, T // J - 1), (True, T // J)):
+        P = s._problem_struct(inputs)
+        if empty_first:
+            sp = list(s.partition.split_times)
+            sp[1] = sp[0]                 # an empty first segment
+            splits = torch.tensor(sp, dtype=torch.int32, device=dev)
+            P.split_times = _ptr(splits)
+        P.max_seg_len = msl
+        s.out["status"].zero_()
+        rc = s.lib.plq_solve_parallel(ctypes.byref(P), ctypes.byref(s._outs), _ptr(s.workspace), s.ws_bytes,
+                                      ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+        assert rc == _native.PLQ_OK
+        torch.cuda.synchronize()
+        st = s.out["status"].cpu().numpy()
+        assert np.any(st == _native.PLQ_STATUS_BAD_PARTITION)
+        with pytest.raises(ValueError):
+            raise_for_status(st)
+    # the solver is still healthy afterwards
+    s.run(inputs)
+    s.raise_for_status()

@@ -106,7 +106,7 @@ def test_smooth_drop_in_api_on_demo():
     import paper_1809_06360_b200 as plq
     z = np.load(os.path.join(GOLDEN, "demo_double_integrator.npz"))
     a = {k[3:]: z[k] for k in z.files if k.startswith("in/")}
-    prob = plq.LqrProblem.from_arrays(a)
+    prob = plq.problem_from_arrays(a)
     psol = plq.solve_parallel(prob, J=int(z["J"]))
     sm = plq.smooth(prob, psol, workers=1)
     K = np.stack([p.Kx for p in sm.policies])
@@ -132,7 +132,7 @@ def test_smooth_drop_in_api_on_demo():
 
 def _problem(a):
     import paper_1809_06360_b200 as plq
-    return plq.LqrProblem.from_arrays(a)
+    return plq.problem_from_arrays(a)
 
 
 def test_two_way_smoothing_recovers_global_gain():

@@ -92,7 +92,7 @@ class TestStatusMapping:
 class TestDataModel:
     def test_stack_problem_layout_and_memo(self):
         a = synth.generate_one(3, 2, 5, seed=1)
-        prob = plq.LqrProblem.from_arrays(a)
+        prob = plq.problem_from_arrays(a)
         st1 = plq.stack_problem(prob)
         assert st1 is plq.stack_problem(prob)
         for k in a:
@@ -101,7 +101,7 @@ class TestDataModel:
 
     def test_symmetrization_is_a_no_op_on_generated_data(self):
         a = synth.generate_one(6, 2, 4, seed=2)
-        prob = plq.LqrProblem.from_arrays(a)
+        prob = plq.problem_from_arrays(a)
         assert all(np.array_equal(c.Qxx, a["Qxx"][t]) for t, (c, _) in enumerate(prob.stages))
 
     def test_lazy_policies(self):
@@ -203,6 +203,6 @@ def test_product_path_refuses_without_gpu():
     import torch
     if torch.cuda.is_available():
         pytest.skip("GPU present")
-    prob = plq.LqrProblem.from_arrays(synth.generate_one(3, 1, 6, seed=1))
+    prob = plq.problem_from_arrays(synth.generate_one(3, 1, 6, seed=1))
     with pytest.raises(RuntimeError, match="CUDA"):
         plq.solve_parallel(prob, J=2)
