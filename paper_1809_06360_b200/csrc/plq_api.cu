@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "plq_internal.h"
+#include "plq_rank.cuh"
 
 namespace {
 
@@ -49,7 +50,9 @@ struct Plan {
   size_t smem = 0;
   int grid_max = 0;
   size_t off_Kz = 0, off_k1 = 0, off_gh = 0, off_xend = 0, off_part = 0, off_gs = 0, off_link = 0, off_smap = 0;
-  size_t off_mucorr = 0, off_lfpool = 0, off_ctr = 0;
+  size_t off_mucorr = 0, off_lfpool = 0, off_ctr = 0, off_rlist = 0, off_rank = 0;
+  size_t rank_doubles = 0;   // per repair CTA
+  int repair_grid = 0;
   size_t total_doubles = 0;
 };
 
@@ -97,7 +100,15 @@ Plan make_plan(const plq_problem_t* p) {
   off += up2(std::max(plq::link_workspace_doubles(B, p->J, p->n),
                       use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0)));
   P.off_ctr = off;
-  off += 2;
+  off += 2;   // [0] dynamic segment queue, [1] rank-repair count
+  P.off_rlist = off;
+  off += up2(B * J);   // rank-repair list (long long per entry)
+  // rank-revealing repair launch (plq_rank.cuh): one resident wave of the
+  // generic kernel at most, each CTA with its own slow-path scratch
+  P.repair_grid = std::min(P.grid_max, sms);
+  P.rank_doubles = up2(plq::rank_scratch_doubles(p->n, p->m, P.lay.large ? 2 * p->n + 2 : 2 * p->n + 1));
+  P.off_rank = off;
+  off += (size_t)P.repair_grid * P.rank_doubles;
   P.off_mucorr = off;
   off += up2(B * J * n);
   P.off_lfpool = off;
@@ -148,11 +159,27 @@ int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
   a.endpoint_terminal = endpoint_terminal;
   a.feas = o->feas;
   a.feas_rows = o->feas_rows;
+  a.repair_ctr = reinterpret_cast<unsigned long long*>(c.ws + c.P.off_ctr) + 1;
+  a.repair_list = reinterpret_cast<long long*>(c.ws + c.P.off_rlist);
+  a.rank_scratch = c.ws + c.P.off_rank;
+  a.rank_scratch_doubles = (int64_t)c.P.rank_doubles;
+  // endpoint segments (tail stages) may need the rank-revealing repair pass
+  const bool tails = endpoint_terminal || j0 < p->J - 1;
+  if (tails && cudaMemsetAsync(a.repair_ctr, 0, sizeof(unsigned long long), c.s) != cudaSuccess)
+    return cuda_fail("repair counter reset");
   const int64_t tasks = p->B * (int64_t)(j1 - j0);
   const int grid = (int)std::min<int64_t>(tasks, c.P.grid_max);
   const int rc = use_small_sweep(p) ? plq::launch_sweep_small(a, c.s) : plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s);
   if (rc) return cuda_fail("sweep launch");
   ++g_launches;
+  if (tails) {
+    // re-solve (exact SVD rank decision) the segments whose tail-stage rank
+    // the fast sweep could not certify; exits at once when there are none
+    plq::SweepArgs ra = a;
+    ra.repair = 1;
+    if (plq::launch_sweep(ra, c.P.repair_grid, c.P.threads, c.P.smem, c.s)) return cuda_fail("rank repair launch");
+    ++g_launches;
+  }
   return PLQ_OK;
 }
 

@@ -82,7 +82,29 @@ struct SweepArgs {
   // dynamic task queue of the specialized sweep (reset by the launcher);
   // null: static round-robin
   unsigned long long* task_ctr;
+  // Rank-revealing repair (plq_rank.cuh): a sweep that cannot certify the
+  // rank of a tail stage's Nu marks the segment PLQ_STATUS_RANK_REPAIR and
+  // appends b*J+j to repair_list; the repair launch of the generic kernel
+  // (repair = 1) re-solves exactly those segments with the SVD decision,
+  // using rank_scratch (rank_scratch_doubles per CTA).  The counter is reset
+  // before every sweep.
+  int repair;
+  unsigned long long* repair_ctr;
+  long long* repair_list;      // (B*J)
+  double* rank_scratch;
+  int64_t rank_scratch_doubles;
 };
+
+// internal status: segment awaits the rank-revealing repair pass (never
+// returned to the caller: the repair pass overwrites it)
+#define PLQ_STATUS_RANK_REPAIR (-5)
+
+__device__ __forceinline__ void push_repair(const SweepArgs& a, int64_t b, int j) {
+  if (!a.repair && a.repair_ctr) {
+    const unsigned long long i = atomicAdd(a.repair_ctr, 1ULL);
+    a.repair_list[i] = (long long)(b * a.p.J + j);
+  }
+}
 
 struct LinkFeasArgs {
   plq_problem_t p;

@@ -10,6 +10,7 @@ namespace plq {
 
 #define PLQ_SWEEP_DECLARE(NT)                                                    \
   int launch_sweep_##NT(const SweepArgs& a, int grid, size_t smem, cudaStream_t s); \
+  int launch_sweep_repair_##NT(const SweepArgs& a, int grid, size_t smem, cudaStream_t s); \
   int sweep_occupancy_##NT(size_t smem);
 PLQ_SWEEP_DECLARE(32)
 PLQ_SWEEP_DECLARE(128)
@@ -73,6 +74,14 @@ SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
 }
 
 int launch_sweep(const SweepArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
+  if (a.repair) {
+    switch (threads) {
+      case 32: return launch_sweep_repair_32(a, grid, smem, s);
+      case 128: return launch_sweep_repair_128(a, grid, smem, s);
+      case 256: return launch_sweep_repair_256(a, grid, smem, s);
+      default: return launch_sweep_repair_512(a, grid, smem, s);
+    }
+  }
   switch (threads) {
     case 32: return launch_sweep_32(a, grid, smem, s);
     case 128: return launch_sweep_128(a, grid, smem, s);

@@ -23,6 +23,7 @@
 #include "plq_device.cuh"
 #include "plq_gemm.cuh"
 #include "plq_internal.h"
+#include "plq_rank.cuh"
 #include "plq_tma.cuh"
 
 #include <algorithm>
@@ -70,7 +71,7 @@ __device__ __forceinline__ void cho_solve_x(const double* L, int m, int ldl, dou
     cta_cho_solve(L, m, ldl, X, W, ldx);
 }
 
-__device__ void wide_branch(const plq_problem_t& p, int n, int m, int r, int W, int ldw, int Fw, double* VF,
+__device__ int wide_branch(const plq_problem_t& p, int n, int m, int r, int W, int ldw, int Fw, double* VF,
                             double* H, double* P, double* G, double* Muu, double* WIDE, double* tau, double* rdiag,
                             double* red, int* iflag, double thr_scale, int* status_out, int stage) {
   // Mixed branch 0 < p = r < m (endpoint.py:234-250): Nu (r x m) has full
@@ -86,16 +87,29 @@ __device__ void wide_branch(const plq_problem_t& p, int n, int m, int r, int W, 
   }
   __syncthreads();
   cta_householder_qr(X, m, r, r, nullptr, 0, 1, tau, rdiag, red);
-  double rmax = 0.0, rmin = 1e308;
-  for (int i = 0; i < r; ++i) {
-    rmax = fmax(rmax, fabs(rdiag[i]));
-    rmin = fmin(rmin, fabs(rdiag[i]));
+  // rank certificates (plq_rank.cuh): ||Rw||_F <= thr -> p = 0 for sure;
+  // 1 / ||Rw^{-1}||_F > thr -> p = r for sure; otherwise the SVD decides
+  double rmax = 0.0, pf = 0.0, pi = 0.0;
+  for (int i = 0; i < r; ++i) rmax = fmax(rmax, fabs(rdiag[i]));
+  for (int idx = tid; idx < r * r; idx += nt) {
+    const int i = idx / r, c = idx % r;
+    if (c > i) pf += X[i * r + c] * X[i * r + c];
+    if (c == i) pf += rdiag[i] * rdiag[i];
   }
-  if (!(rmin > p.rank_tol * fmax(thr_scale, rmax))) {
-    if (tid == 0) *status_out = PLQ_STATUS_DEGENERATE;
-    __syncthreads();
-    return;
+  for (int c = tid; c < r; c += nt) {   // column c of Rw^{-1} into BASE (free here)
+    for (int i = c; i >= 0; --i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = i + 1; k <= c; ++k) v -= X[i * r + k] * BASE[k * ldw + c];
+      v /= rdiag[i];
+      BASE[i * ldw + c] = v;
+      pi += v * v;
+    }
   }
+  const double rf2 = block_sum(pf, red);
+  const double ri2 = block_sum(pi, red);
+  const double thr = p.rank_tol * fmax(thr_scale, rmax);
+  if (sqrt(rf2) <= thr) return 1;                 // p = 0: Cholesky gains, all rows stay
+  if (!(ri2 * thr * thr < 1.0)) return 2;         // undecided: rank-revealing path
   // y = R^{-T} stack (forward substitution), BASE = Q [y; 0]
   for (int c = tid; c < W; c += nt) {
     for (int i = 0; i < r; ++i) {
@@ -133,7 +147,7 @@ __device__ void wide_branch(const plq_problem_t& p, int n, int m, int r, int W, 
   if (!cta_cholesky(Wn, q, m, iflag)) {
     if (tid == 0) *status_out = 1 + stage;
     __syncthreads();
-    return;
+    return -1;
   }
   cta_cho_solve(Wn, q, m, C + r * ldw, W, ldw);
   for (int idx = tid; idx < r * W; idx += nt) C[(idx / W) * ldw + idx % W] = 0.0;
@@ -144,9 +158,10 @@ __device__ void wide_branch(const plq_problem_t& p, int n, int m, int r, int W, 
     G[i * ldw + j] = -(BASE[i * ldw + j] + C[i * ldw + j]);
   }
   __syncthreads();
+  return 0;
 }
 
-template <int NT>
+template <int NT, bool REPAIR>
 __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int j) {
   const plq_problem_t& p = a.p;
   const int n = p.n, m = p.m, J = p.J, T = p.T;
@@ -183,6 +198,9 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   double* red = rdiag + m;
   int* iflag = reinterpret_cast<int*>(red + 32);
   int* sflag = iflag + 1;
+  // rank-revealing slow path scratch (repair launches only, plq_rank.cuh)
+  const RankScratch rsc =
+      rank_scratch(a.rank_scratch + (REPAIR ? (int64_t)blockIdx.x * a.rank_scratch_doubles : 0), n, m, ldw);
   // blocked-factorization scratch (plq_blocked.cuh): block inverses, per-warp
   // tiles, V T' of the QR panel
   double* binv = red + 34;
@@ -377,23 +395,36 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           gqr8<NT / 32>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync);
         else
           cta_householder_qr(VF + n, r, m, Fw, H, W, ldw, tau, rdiag, red);
-        double rmax = 0.0, rmin = 1e308;
-        for (int i = 0; i < m; ++i) {
-          rmax = fmax(rmax, fabs(rdiag[i]));
-          rmin = fmin(rmin, fabs(rdiag[i]));
+        double rmax = 0.0, pf = 0.0;
+        for (int i = 0; i < m; ++i) rmax = fmax(rmax, fabs(rdiag[i]));
+        for (int idx = tid; idx < m * m; idx += nt) {
+          const int i = idx / m, c = idx % m;
+          const double v = c > i ? VF[i * Fw + n + c] : (c == i ? rdiag[i] : 0.0);
+          pf += v * v;
         }
         const double thr = p.rank_tol * fmax(nu_scale, rmax);
-        if (rmax <= thr) {
-          // p = 0 (Nu numerically zero, e.g. a segment without control
-          // authority): the reflectors are the identity, all r rows stay
-          // and the gains are the null-space solve with Zw = I
-          // (endpoint.py:239-250)
-          chol = true;
-        } else if (!(rmin > thr)) {
-          // 0 < p < m: rank-revealing branch not built
-          if (tid == 0) *sflag = PLQ_STATUS_DEGENERATE;
+        const double rf2 = block_sum(pf, red);
+        if constexpr (REPAIR) {
+          // rank-revealing path (plq_rank.cuh): SVD of R decides p exactly as
+          // the reference does; gains, surviving rows, r - p rows left
+          const double* Rv = VF + n;
+          const int pr = rank_tail_solve(
+              m, m, r, W, ldw, [&](int i, int c) { return c > i ? Rv[i * Fw + c] : (c == i ? rdiag[i] : 0.0); }, H, P,
+              Muu, m, nu_scale, p.rank_tol, G, rsc, red);
+          if (pr < 0) {
+            if (tid == 0) *sflag = 1 + s;
+            __syncthreads();
+            break;
+          }
+          r -= pr;
           __syncthreads();
-          break;
+        } else {
+        if (sqrt(rf2) <= thr) {
+          // p = 0 for sure (sigma_max <= ||R||_F <= thr; Nu numerically zero,
+          // e.g. a segment without control authority): the reflectors are
+          // the identity, all r rows stay and the gains are the null-space
+          // solve with Zw = I (endpoint.py:239-250)
+          chol = true;
         } else {
           // G = -R^{-1} (Q1' stack): back substitution, thread per column
           // (blocked: in place on H's first m rows, DMMA tiles)
@@ -409,11 +440,22 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
             }
           }
           __syncthreads();
+          double pz = 0.0;
           for (int idx = tid; idx < m * W; idx += nt) {
             const int u = idx / W, c = idx % W;
-            G[u * ldw + c] = -(blocked ? H[u * ldw + c] : G[u * ldw + c]);
+            const double g = -(blocked ? H[u * ldw + c] : G[u * ldw + c]);
+            G[u * ldw + c] = g;
+            if (c >= n && c < 2 * n) pz += g * g;
           }
-          __syncthreads();
+          // p = m for sure iff sigma_min >= 1 / ||R^{-1}||_F = 1 / ||Kz||_F > thr
+          // (plq_rank.cuh); otherwise the rank-revealing repair pass re-solves
+          // this segment (NaN / Inf from an exactly singular R fail the test)
+          const double kz2 = block_sum(pz, red);
+          if (!(kz2 * thr * thr < 1.0)) {
+            if (tid == 0) *sflag = PLQ_STATUS_RANK_REPAIR;
+            __syncthreads();
+            break;
+          }
           // surviving rows Q2' stack: shift rows m..r-1 up by m, one block of
           // m rows at a time so sources and destinations never overlap
           for (int blk = 0; blk < r - m; blk += m) {
@@ -427,10 +469,58 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           r -= m;
           __syncthreads();
         }
+        }
+      } else if (REPAIR) {
+        // r < m, rank-revealing: QR of Nu' = Qw [Rw; 0], SVD of Rw' in the
+        // Qw-rotated control coordinates (plq_rank.cuh), G = Qw G'
+        double* X = rsc.wX;   // (the WIDE buffer exists only when n % m != 0)
+        double* Mp = rsc.wM;
+        double* Pp = rsc.wP;
+        for (int idx = tid; idx < m * r; idx += nt) {
+          const int c = idx / r, i = idx % r;
+          X[c * r + i] = VF[i * Fw + n + c];
+        }
+        __syncthreads();
+        cta_householder_qr(X, m, r, r, nullptr, 0, 1, tau, rdiag, red);
+        for (int idx = tid; idx < m * m; idx += nt) Mp[idx] = Muu[idx];
+        for (int idx = tid; idx < m * W; idx += nt) Pp[(idx / W) * ldw + idx % W] = P[(idx / W) * ldw + idx % W];
+        __syncthreads();
+        cta_apply_q(X, m, r, r, tau, Mp, m, m, false);
+        for (int idx = tid; idx < m * m; idx += nt) {
+          const int i = idx / m, c = idx % m;
+          if (i < c) {
+            const double t = Mp[i * m + c];
+            Mp[i * m + c] = Mp[c * m + i];
+            Mp[c * m + i] = t;
+          }
+        }
+        __syncthreads();
+        cta_apply_q(X, m, r, r, tau, Mp, m, m, false);
+        cta_apply_q(X, m, r, r, tau, Pp, W, ldw, false);
+        const int pr = rank_tail_solve(
+            r, m, r, W, ldw, [&](int i, int c) { return c < i ? X[c * r + i] : (c == i ? rdiag[i] : 0.0); }, H, Pp,
+            Mp, m, nu_scale, p.rank_tol, G, rsc, red);
+        if (pr < 0) {
+          if (tid == 0) *sflag = 1 + s;
+          __syncthreads();
+          break;
+        }
+        cta_apply_q(X, m, r, r, tau, G, W, ldw, true);
+        r -= pr;
       } else {
-        wide_branch(p, n, m, r, W, ldw, Fw, VF, H, P, G, Muu, bf.WIDE, tau, rdiag, red, iflag, nu_scale, sflag, s);
-        if (*sflag) break;
-        r = 0;
+        const int wr = wide_branch(p, n, m, r, W, ldw, Fw, VF, H, P, G, Muu, bf.WIDE, tau, rdiag, red, iflag,
+                                   nu_scale, sflag, s);
+        if (wr < 0) break;
+        if (wr == 2) {
+          if (tid == 0) *sflag = PLQ_STATUS_RANK_REPAIR;
+          __syncthreads();
+          break;
+        }
+        if (wr == 1) {
+          chol = true;   // p = 0: all rows stay
+        } else {
+          r = 0;
+        }
       }
     }
     if (chol) {
@@ -555,11 +645,12 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     if (a.feas_rows) a.feas_rows[b * J + j] = (!serial && st == 0) ? r : 0;
     if (st == 0 && !serial && r > 0 && !a.feas) st = PLQ_STATUS_DEGENERATE;   // feasibility rows left
     a.status[b * J + j] = st;
+    if (st == PLQ_STATUS_RANK_REPAIR) push_repair(a, b, j);
   }
   __syncthreads();
 }
 
-template <int NT>
+template <int NT, bool REPAIR>
 __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(16) double smem[];
   Bufs bf;
@@ -578,6 +669,15 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArg
   bf.H = ptrs[SB_H];
   bf.WIDE = ptrs[SB_WIDE];
   bf.tiles = a.lay.large ? smem + a.lay.tiles_off : nullptr;
+  if constexpr (REPAIR) {
+    // re-solve the segments the fast sweep could not decide (PLQ_STATUS_RANK_REPAIR)
+    const long long flagged = (long long)*a.repair_ctr;
+    for (long long i = blockIdx.x; i < flagged; i += gridDim.x) {
+      const long long bj = a.repair_list[i];
+      sweep_segment<NT, true>(a, bf, bj / a.p.J, (int)(bj % a.p.J));
+    }
+    return;
+  }
   const int nloc = a.seg_end - a.seg_begin;
   const int64_t total = a.p.B * nloc;
   for (int64_t task = blockIdx.x; task < total; task += gridDim.x) {
@@ -587,7 +687,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArg
       if (threadIdx.x == 0) a.status[b * a.p.J + j] = PLQ_STATUS_BAD_PARTITION;
       continue;
     }
-    sweep_segment<NT>(a, bf, b, j);
+    sweep_segment<NT, false>(a, bf, b, j);
   }
 }
 
@@ -597,15 +697,21 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArg
 // in its own translation unit (plq_sweep_t<NT>.cu) so the build parallelizes.
 #define PLQ_SWEEP_INSTANTIATE(NT)                                                          \
   int launch_sweep_##NT(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {       \
-    sweep_kernel<NT><<<grid, NT, smem, s>>>(a);                                            \
+    sweep_kernel<NT, false><<<grid, NT, smem, s>>>(a);                                     \
     return cudaGetLastError() == cudaSuccess ? 0 : -1;                                     \
   }                                                                                        \
   int sweep_occupancy_##NT(size_t smem) {                                                  \
     int nb = 0;                                                                            \
-    cudaFuncSetAttribute(sweep_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+    cudaFuncSetAttribute(sweep_kernel<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          (int)smem);                                                       \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel<NT>, NT, smem);        \
+    cudaFuncSetAttribute(sweep_kernel<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                       \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel<NT, false>, NT, smem); \
     return nb;                                                                             \
+  }                                                                                        \
+  int launch_sweep_repair_##NT(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) { \
+    sweep_kernel<NT, true><<<grid, NT, smem, s>>>(a);                                      \
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;                                     \
   }
 
 }  // namespace plq

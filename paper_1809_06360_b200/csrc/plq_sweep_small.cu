@@ -531,27 +531,27 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         // (measured faster here than gqr8: 2.46 vs 2.51 ms cfg2 sweep)
         gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
-      double rmax = 0.0, rmin = 1e308;
+      // rank certificates (plq_rank.cuh): p = 0 for sure when ||R||_F <= thr,
+      // p = M for sure when 1 / ||R^{-1}||_F = 1 / ||Kz||_F > thr; anything
+      // else is re-solved by the rank-revealing repair pass (SVD decision,
+      // the reference's endpoint.py:226-231)
+      const double* Rm = NTb + N;   // R (upper) with stride LDF
+      double rmax = 0.0, pf = 0.0;
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        rmax = fmax(rmax, fabs(rdiag[i]));
-        rmin = fmin(rmin, fabs(rdiag[i]));
+      for (int i = 0; i < M; ++i) rmax = fmax(rmax, fabs(rdiag[i]));
+      for (int idx = gt; idx < M * M; idx += NT) {
+        const int i = idx / M, c = idx % M;
+        const double v = c > i ? Rm[i * LDF + c] : (c == i ? rdiag[i] : 0.0);
+        pf += v * v;
       }
+      const double rf2 = gsum<NWG>(pf, red, grp, gw);
+      gsync<NWG>(grp);
       const double thr = p.rank_tol * fmax(nu_scale, rmax);
-      if (rmax <= thr) {
+      if (sqrt(rf2) <= thr) {
         // p = 0 (Nu numerically zero): identity reflectors, all r rows stay,
         // gains by the null-space solve with Zw = I (endpoint.py:239-250)
         chol = true;
-      } else if (!(rmin > thr)) {
-        // 0 < p < m: rank-revealing branch not built
-        status = PLQ_STATUS_DEGENERATE;
-        if (s > 0) {
-          mbar_wait(bar, phase);
-          phase ^= 1u;
-        }
-        break;
       } else {
-        const double* Rm = NTb + N;   // R (upper) with stride LDF
         int ldr = LDF;
         if constexpr (S::BIG) {
           // G = -R^{-1} (Q1' stack): blocked back substitution in place on
@@ -579,6 +579,21 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
         }
         gsync<NWG>(grp);
+        }
+        double pz = 0.0;
+        for (int idx = gt; idx < M * N; idx += NT) {
+          const double g = G[(idx / N) * LDW + N + idx % N];
+          pz += g * g;
+        }
+        const double kz2 = gsum<NWG>(pz, red, grp, gw);
+        gsync<NWG>(grp);
+        if (!(kz2 * thr * thr < 1.0)) {
+          status = PLQ_STATUS_RANK_REPAIR;
+          if (s > 0) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+          }
+          break;
         }
         // the surviving rows Q2' stack are rows M..r-1: advance the row base
         // instead of moving them (H is re-based at every segment start and
@@ -786,6 +801,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     if (a.feas_rows) a.feas_rows[b * J + j] = (!SERIAL && status == 0) ? r : 0;
     if (status == 0 && !SERIAL && r > 0 && !a.feas) status = PLQ_STATUS_DEGENERATE;
     a.status[b * J + j] = status;
+    if (status == PLQ_STATUS_RANK_REPAIR) push_repair(a, b, j);
   }
   gsync<NWG>(grp);
 }

@@ -226,7 +226,92 @@ def endpoint_goldens():
              input_sha256=np.array(digest(batch)), **endpoint_case(a, 200 + cid))
 
 
+def _with_singular_values(Fu, sig, seed):
+    """Fu replaced by U diag(sig) V' with the same shape (random orthogonal
+    U, V from a seeded QR)."""
+    rng = np.random.default_rng(seed)
+    n, m = Fu.shape
+    U, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    S = np.zeros((n, m))
+    S[np.arange(len(sig)), np.arange(len(sig))] = sig
+    return U @ S @ V.T
+
+
+def rank_goldens():
+    """Constrained tail stages whose Nu = Hx Fu sits at the reference's rank
+    threshold (endpoint.py:226-231): at a segment's last stage Hx = I, so
+    Nu = Fu and thr = rank_tol * sqrt(n) * ||Fu||_F.  Singular values below
+    it make the reference take its mixed range/null-space branch (0 < p < m);
+    values just above it with sigma_min inside the sqrt(m) band of the
+    certificate exercise the GPU's rank-revealing repair pass."""
+    tol = parlqr.DEFAULT_TOLERANCES.rank_tol
+    probs, Js = [], []
+
+    def case(a, J, t, sig_big, small, seed):
+        n, m = a["Fu"].shape[1:]
+        nb = len(sig_big)
+        fro = np.sqrt(np.sum(np.square(sig_big)))
+        thr = tol * np.sqrt(n) * fro
+        sig = list(sig_big) + [c * thr for c in small]
+        assert len(sig) == m
+        a["Fu"][t] = _with_singular_values(a["Fu"][t], sig, seed)
+        probs.append(a)
+        Js.append(J)
+        return nb
+
+    # generic path: n=6, m=2 (partial p = 1, exactly deficient p = 1)
+    case(from_problem(ref_generate(6, 2, 24, seed=301)), 3, 7, [1.0], [0.3], 1)
+    case(from_problem(ref_generate(6, 2, 24, seed=302)), 3, 15, [0.8], [0.0], 2)
+    # n % m != 0: the wide branch (r < m) with a rank-1 Fu two stages into
+    # the tail of segment 0 (T=10, J=2: r = 5 -> 2 -> wide with p = 1)
+    for seed in range(303, 340):     # first seed whose reference solve has no CholeskyFailure
+        a = from_problem(ref_generate(5, 3, 10, seed=seed))
+        rng = np.random.default_rng(seed)
+        a["Fu"][3] = np.outer(rng.standard_normal(5), rng.standard_normal(3))
+        try:
+            ref_solve(a, 2)
+        except parlqr.errors.SolverError:
+            continue
+        probs.append(a)
+        Js.append(2)
+        break
+    # specialised kernels: cfg1 / cfg2 / cfg4 shapes (BASELINE recipe)
+    for cid, over, J, t, seed in ((1, dict(B=1), 8, 15, 5), (2, dict(T=64, J=4), 4, 31, 6),
+                                  (4, dict(T=16, J=2), 2, 7, 7)):
+        cfg = synth.CONFIGS[cid].scaled(**over)
+        for s in range(seed, seed + 40):   # first seed the reference solves without CholeskyFailure
+            if cid == 4:
+                # the reference's own generator at the (64, 32) shape: with the
+                # cfg4 recipe (R = VV'/m + 1e-4 I) the reference itself fails
+                # its Cholesky after a partial-rank tail
+                b = from_problem(ref_generate(cfg.n, cfg.m, cfg.T, seed=s))
+            else:
+                b = {k: v[0] for k, v in synth.generate_batch(cfg, seed=s, count=1).items()}
+            scale = float(np.linalg.norm(b["Fu"][t], 2))
+            case(b, J, t, [scale] * (cfg.m - 1), [0.3], 10 + s)            # partial: p = m - 1
+            try:
+                ref_solve(b, J)
+                break
+            except parlqr.errors.SolverError:
+                probs.pop()
+                Js.pop()
+    # (a stage whose sigma_min sits just above the threshold, inside the
+    # certificate band, gives gains ~1e10 and the reference itself fails a
+    # later Cholesky on every seed tried; the repair pass's p = m decision is
+    # exercised by the other tail stages of the repaired segments above)
+    for i, (a, J) in enumerate(zip(probs, Js)):
+        try:
+            ref_solve(a, J)
+        except parlqr.errors.SolverError as exc:
+            print("rank case", i, "fails:", exc)
+    stored_case("rank_near", probs, Js)
+
+
 def main():
+    if "--only" in sys.argv:
+        {"rank": rank_goldens}[sys.argv[sys.argv.index("--only") + 1]]()
+        return
     # 1. hand example of test_parallel.py:48-54 (J=2 scalar problem)
     stored_case("hand_scalar", [from_problem(scalar_problem(2))], [2])
     # 2. the reference's small random pool (conftest.py:53-63) for J=2,3,4
@@ -316,6 +401,8 @@ def main():
     stored_case("uncontrollable", probs, Js)
     # two-point-boundary solves (endpoint.py:603-653) by the reference itself
     endpoint_goldens()
+    # tail stages at the rank threshold (mixed branch 0 < p < m, repair pass)
+    rank_goldens()
     # JSON problem / solution files written by the reference itself
     # (fileio.save_problem, cli solve --solver parallel --J 3, cli.py:26-59)
     from parlqr import cli as ref_cli

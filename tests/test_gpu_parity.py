@@ -339,3 +339,20 @@ def test_understated_max_seg_len_is_flagged_not_overrun(n, m, T, J):
     # the solver is still healthy afterwards
     s.run(inputs)
     s.raise_for_status()
+
+
+def test_rank_threshold_tail_stages(kernel_path):
+    """Tail stages whose Nu sits at the reference's rank threshold
+    (tests/golden/rank_near.npz, written by the reference): a singular value
+    below rank_tol * ||Hx||_F ||Fu||_F makes the reference take its mixed
+    range/null-space branch (0 < p < m, endpoint.py:234-250).  The GPU's fast
+    sweeps cannot certify such a rank, flag the segment, and the rank-
+    revealing repair pass (SVD decision, plq_rank.cuh) re-solves it; the
+    n % m != 0 case goes through the wide branch (r < m) with p < r."""
+    for a, o, J in load_stored("rank_near"):
+        splits = tuple(int(s) for s in o["splits"])
+        g, _ = _gpu_batch({k: v[None] for k, v in a.items()}, splits=splits)
+        assert not bool(o["degenerate"])
+        floors = _floor(a, None, O.solve(a, splits=splits), splits=splits)
+        _check(g, 0, o, floors)
+        assert rel_err(g["Kz"][0], o["Kz"]) <= max(K_TOL, 10 * floors.get("K", 0.0))
