@@ -203,7 +203,7 @@ def time_cpu_endpoint(cfg, seed, budget_s=4.0):
             "sample": f"{done} two-point-boundary solves of the config's problems"}
 
 
-def parity_sample(cfg, host, out, B_loc):
+def parity_sample(cfg, host, out, B_loc, stages=None):
     """A sample of the solved problems against the CPU oracle, computed
     outside the timed region (the oracle is the checker here, never the
     thing measured).  ``K`` and the objective are gated at 1e-9 (SURVEY.md
@@ -224,13 +224,14 @@ def parity_sample(cfg, host, out, B_loc):
         return float(np.abs(a - b).max()) / d if d else float(np.abs(a - b).max())
 
     errs = {}
+    lo, hi = stages if stages is not None else (0, cfg.T)   # this rank's stages (horizon sharding)
     for i, ref in zip(picks, refs):
         for key, rk in (("K", "K"), ("k", "k"), ("x", "states"), ("u", "controls"), ("lam", "lambdas")):
-            errs[key] = max(errs.get(key, 0.0), rel(out[key][i].cpu().numpy(), ref[rk]))
+            errs[key] = max(errs.get(key, 0.0), rel(out[key][i][lo:hi].cpu().numpy(), ref[rk][lo:hi]))
         errs["objective"] = max(errs.get("objective", 0.0),
                                 rel(out["objective"][i:i + 1].cpu().numpy(), np.array([ref["objective"]])))
     ok = errs["K"] <= 1e-9 and errs["objective"] <= 1e-9
-    return {"problems": picks, "max_rel_err": errs, "pass_K_objective_1e-9": ok,
+    return {"problems": picks, "stages": [int(lo), int(hi)], "max_rel_err": errs, "pass_K_objective_1e-9": ok,
             "oracle": "oracle/parlqr_oracle.py (the reference's call sequence restated)",
             "oracle_seconds": time.perf_counter() - t0}
 
@@ -281,17 +282,29 @@ def run_ours(args):
     # seeded host inputs (fork-pool generator), pinned once: the e2e leg reads
     # them as its host buffers, the device-resident leg copies them to HBM
     gen = synth.generate_batch_parallel(cfg, seed=args.seed, count=B_loc, first=first)
-    host = {k: torch.from_numpy(v).pin_memory() for k, v in gen.items()}
+    solver = BatchSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev, degenerate=not sharded)
+    j0, j1, t0 = 0, cfg.J, 0
+    full = None
+    if sharded:
+        # horizon sharding: this rank uploads and holds only its segments'
+        # stages (shifted pointers, DeviceBackend(t0=...))
+        from paper_1809_06360_b200.sharded import shard_range, stage_window
+        j0, j1 = shard_range(cfg.J, world, rank)
+        full = gen if rank == 0 else None       # rank 0 keeps the whole problem for the parity check
+        gen, t0 = stage_window(gen, solver.partition.split_times, j0, j1)
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in gen.items()}
     del gen
     inputs = {k: v.to(dev) for k, v in host.items()}
-    solver = BatchSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev)
     stream = torch.cuda.current_stream(dev)
     if sharded:
-        from paper_1809_06360_b200.sharded import DeviceBackend, solve_sharded
-        backend = DeviceBackend(solver, inputs)
+        from paper_1809_06360_b200.sharded import DeviceBackend, raise_sharded_status, solve_sharded
+        backend = DeviceBackend(solver, inputs, t0=t0)
 
         def one_step():
-            solve_sharded(backend, dist)
+            # no host synchronization inside the step: status rows travel
+            # with the value blocks and are checked after the timed region
+            solve_sharded(backend, dist, check=False)
+            solver.launches = backend.launches
     elif args.graph:
         # the whole solve captured once into a CUDA graph, replayed per step
         graph = solver.capture(inputs)
@@ -303,9 +316,15 @@ def run_ours(args):
     else:
         def one_step():
             solver.run(inputs)
+    def check_status():
+        if sharded:
+            raise_sharded_status(backend)
+        else:
+            solver.raise_for_status()
+
     for _ in range(max(args.warmup, 1)):
         one_step()
-    solver.raise_for_status()
+    check_status()
     in_bytes = sum(v.numel() * 8 for v in inputs.values())
     flush = None
     if in_bytes < 2 * L2_BYTES:
@@ -323,7 +342,7 @@ def run_ours(args):
         ev[i][0].record(stream)
         one_step()
         ev[i][1].record(stream)
-        launches += solver.launches if not sharded else 6
+        launches += solver.launches
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -337,21 +356,21 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
     knots = cfg.B * cfg.T
     value = knots / (ms_per_step / 1000.0)
-    solver.raise_for_status()
+    check_status()
 
     # ---- dominant kernel (the segment sweep) timed on its own stream, and the other phases
     import ctypes
     lib = _native.lib()
-    prob = solver._problem_struct(inputs)
+    prob = solver._problem_struct(inputs, t0=t0)
     phase_ms = {}
     phases = {
-        "sweep": lambda: lib.plq_sweep_segments(ctypes.byref(prob), ctypes.byref(solver._outs), 0, cfg.J,
+        "sweep": lambda: lib.plq_sweep_segments(ctypes.byref(prob), ctypes.byref(solver._outs), j0, j1,
                                                 ctypes.c_void_p(solver.workspace.data_ptr()), solver.ws_bytes,
                                                 ctypes.c_void_p(stream.cuda_stream)),
         "link": lambda: lib.plq_link_solve(ctypes.byref(prob), ctypes.byref(solver._outs),
                                            ctypes.c_void_p(solver.workspace.data_ptr()), solver.ws_bytes,
                                            ctypes.c_void_p(stream.cuda_stream)),
-        "recon": lambda: lib.plq_reconstruct_segments(ctypes.byref(prob), ctypes.byref(solver._outs), 0, cfg.J,
+        "recon": lambda: lib.plq_reconstruct_segments(ctypes.byref(prob), ctypes.byref(solver._outs), j0, j1,
                                                       None, ctypes.c_void_p(solver.workspace.data_ptr()),
                                                       solver.ws_bytes, ctypes.c_void_p(stream.cuda_stream)),
     }
@@ -368,11 +387,16 @@ def run_ours(args):
             es.append((a, b))
         torch.cuda.synchronize()
         phase_ms[name] = statistics.mean(x.elapsed_time(y) for x, y in es)
-    _, sweep_fl = perfmodel.problem_flops(cfg.n, cfg.m, cfg.T, cfg.J)
+    # algorithmic work of this rank's sweep launch (all segments, or the
+    # rank's segment range when the horizon is sharded)
+    Fe, Fs, _, _ = perfmodel.stage_flops(cfg.n, cfg.m)
+    L = cfg.T / cfg.J
+    n_end = min(j1, cfg.J - 1) - j0
+    sweep_fl = L * (n_end * Fe + (Fs if j1 == cfg.J else 0.0))
     peak_f64 = perfmodel.fp64_peak_tflops()
     achieved = B_loc * sweep_fl / (phase_ms["sweep"] / 1000.0) / 1e12
     hbm_peak, hbm_src = perfmodel.hbm_peak_gbs(ROOT)
-    sweep_b = B_loc * perfmodel.sweep_bytes(cfg.n, cfg.m, cfg.T, cfg.J)
+    sweep_b = B_loc * perfmodel.sweep_bytes(cfg.n, cfg.m, cfg.T, cfg.J) * (j1 - j0) / cfg.J
     kernel = perfmodel.sweep_kernel_name(cfg.n, cfg.m)
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -389,20 +413,49 @@ def run_ours(args):
     # (outside the timed region; the tests gate every output at the floor)
     parity = None
     if not args.no_parity and rank == 0:
-        parity = parity_sample(cfg, host, solver.out, B_loc)
+        if sharded:
+            parity = parity_sample(cfg, {k: torch.from_numpy(v) for k, v in full.items()}, solver.out, 1,
+                                   stages=(t0, solver.partition.split_times[j1]))
+        else:
+            parity = parity_sample(cfg, host, solver.out, B_loc)
+    # whole-job algorithmic rates (all ranks) against world x the peaks
     total_fl, _ = perfmodel.problem_flops(cfg.n, cfg.m, cfg.T, cfg.J)
     bin_, bout = perfmodel.knot_bytes(cfg.n, cfg.m)
+    sec = ms_per_step / 1000.0
     whole = {
-        "fp64_tflops": B_loc * total_fl / (ms_per_step / 1000.0) / 1e12,
-        "fp64_frac": B_loc * total_fl / (ms_per_step / 1000.0) / 1e12 / peak_f64,
-        "hbm_gbs": B_loc * cfg.T * (bin_ + bout) / (ms_per_step / 1000.0) / 1e9,
+        "fp64_tflops": cfg.B * total_fl / sec / 1e12,
+        "fp64_frac": cfg.B * total_fl / sec / 1e12 / (peak_f64 * world),
+        "hbm_gbs": cfg.B * cfg.T * (bin_ + bout) / sec / 1e9,
     }
-    whole["hbm_frac"] = whole["hbm_gbs"] / hbm_peak
+    whole["hbm_frac"] = whole["hbm_gbs"] / (hbm_peak * world)
 
     # ---- end-to-end: host buffers through plq_solve_parallel_host
     e2e = None
     if not args.no_e2e:
-        hs = HostSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev, pin=True)
+        if sharded:
+            # horizon-sharded end to end: each rank copies its window of
+            # stages in, runs the phases with the exchanges, and copies its
+            # stages' K, k, x, u, lam back (pinned buffers, host wall clock)
+            lo_t, hi_t = t0, solver.partition.split_times[j1]
+            outs_h = {k: torch.empty(tuple(solver.out[k][0, lo_t:hi_t].shape), dtype=torch.float64).pin_memory()
+                      for k in ("K", "k", "x", "u", "lam")}
+
+            class _ShardedE2E:
+                h2d_bytes = sum(v.numel() * 8 for v in host.values())
+                d2h_bytes = sum(v.numel() * 8 for v in outs_h.values())
+
+                def run(self, pinned_in):
+                    for k, v in pinned_in.items():
+                        inputs[k].copy_(v, non_blocking=True)
+                    solve_sharded(backend, dist, check=False)
+                    for k, v in outs_h.items():
+                        v.copy_(solver.out[k][0, lo_t:hi_t], non_blocking=True)
+                    torch.cuda.synchronize()
+            hs = _ShardedE2E()
+            e2e_api = "sharded phases (pinned window in -> this rank's K, k, x, u, lam out)"
+        else:
+            hs = HostSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev, pin=True)
+            e2e_api = "plq_solve_parallel_host (pinned host inputs -> host LqrSolution arrays)"
         pinned = host
         for _ in range(max(1, min(args.warmup, 3))):
             hs.run(pinned)
@@ -412,9 +465,11 @@ def run_ours(args):
         e_steps = max(3, min(args.steps, 10))
         per = []
         for _ in range(e_steps):
-            t0 = time.perf_counter()
+            tic = time.perf_counter()
             hs.run(pinned)                 # synchronizes on the result copy
-            per.append(time.perf_counter() - t0)
+            per.append(time.perf_counter() - tic)
+        if sharded:
+            raise_sharded_status(backend)
         # host wall clock per step (the copies are the host's): median, so a
         # stall of the shared VM host does not stand for the path
         el = statistics.median(per)
@@ -442,7 +497,7 @@ def run_ours(args):
                "d2h_bytes_per_step": int(hs.d2h_bytes) * world, "ms_per_step": el * 1000.0,
                "ms_per_step_min_mean_max": [1000 * min(per), 1000 * statistics.mean(per), 1000 * max(per)],
                "steps": e_steps, "statistic": "median of per-step host wall clock",
-               "api": "plq_solve_parallel_host (pinned host inputs -> host LqrSolution arrays)",
+               "api": e2e_api,
                "copy_roofline": {"h2d_gbs": bw["h2d"], "d2h_gbs": bw["d2h"],
                                  "floor_ms": 1000.0 * copy_floor, "frac": copy_floor / el,
                                  "note": "pinned-copy bandwidth measured in this run; floor = max(H2D, D2H) "

@@ -216,22 +216,38 @@ class BatchSolver:
             self.workspace = torch.empty((self.ws_bytes,), dtype=torch.uint8, device=self.device)
         self.launches = 0
 
-    def _problem_struct(self, inputs):
+    def _problem_struct(self, inputs, t0=0):
+        """C-ABI problem struct over device ``inputs``.  ``t0 > 0`` (B = 1,
+        horizon sharding): the stage arrays hold only a window of stages
+        starting at ``t0``; their pointers are shifted back by ``t0`` stages
+        so the kernels' global stage index lands in the window (the phase
+        entry points read only the stages of their segment range,
+        include/parlqr_b200.h)."""
         splits = np.asarray(self.partition.split_times)
         P = _native.PlqProblem()
         P.B, P.T, P.n, P.m, P.J = self.B, self.T, self.n, self.m, self.J
         P.max_seg_len = int(np.diff(splits).max())
         P.split_times = _ptr(self.split_times)
         dummy = self.split_times   # non-null placeholder for sizing queries
+        if t0 and self.B != 1:
+            raise ValueError("stage windows are for single-problem horizon sharding (B = 1)")
         for f in INPUT_FIELDS:
-            setattr(P, f, _ptr(inputs[f]) if inputs is not None else _ptr(dummy))
+            if inputs is None:
+                setattr(P, f, _ptr(dummy))
+            elif t0 and f in STAGE_FIELDS:
+                t = inputs[f]
+                stride = t[0, 0].numel() * t.element_size()
+                setattr(P, f, ctypes.c_void_p(t.data_ptr() - t0 * stride))
+            else:
+                setattr(P, f, _ptr(inputs[f]))
         P.rank_tol = float(self.tolerances.rank_tol)
         P.feas_tol = float(self.tolerances.feas_tol)
         return P
 
-    def check_inputs(self, inputs):
+    def check_inputs(self, inputs, T_held=None):
         torch = self.torch
-        B, T, n, m = self.B, self.T, self.n, self.m
+        B, n, m = self.B, self.n, self.m
+        T = self.T if T_held is None else int(T_held)
         shapes = {"Qxx": (B, T, n, n), "Qux": (B, T, m, n), "Quu": (B, T, m, m), "qx1": (B, T, n),
                   "qu1": (B, T, m), "Fx": (B, T, n, n), "Fu": (B, T, n, m), "f1": (B, T, n),
                   "QxxT": (B, n, n), "qx1T": (B, n), "x_init": (B, n)}

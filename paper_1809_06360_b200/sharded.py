@@ -57,23 +57,29 @@ def _gather_rows(dist, group, local, J, world, torch):
     return out
 
 
-def solve_sharded(backend, dist, group=None):
-    """Run one sharded solve; every rank returns the same scalar results."""
+def solve_sharded(backend, dist, group=None, check=True):
+    """Run one sharded solve; every rank returns the same scalar results.
+
+    The per-segment status rows are exchanged with the value blocks and kept
+    on the device: with ``check=False`` the solve makes no host
+    synchronization (stream-ordered launches and collectives only) and the
+    caller raises the reference's exceptions afterwards with
+    :func:`raise_sharded_status`.  ``check=True`` does that at the end.
+    """
     torch = backend.torch
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     J = backend.J
     j0, j1 = shard_range(J, world, rank)
+    backend.launches = 0
     # 1. local sweeps, exchange of segment-start value blocks and status
     if j1 > j0:
         backend.sweep(j0, j1)
     vf0 = _gather_rows(dist, group, backend.vf0_rows(j0, j1), J, world, torch)
-    status = _gather_rows(dist, group, backend.status_rows(j0, j1), J, world, torch)
+    backend.seg_status = _gather_rows(dist, group, backend.status_rows(j0, j1), J, world, torch)
     backend.set_vf0(vf0)
-    raise_for_status(status[:, :, 0].cpu().numpy())
     # 2. replicated coupling solve
     backend.link()
-    raise_for_status(backend.status_all())
     # 3. local reconstruction, multiplier rows, link-stage KKT rows, partials
     if j1 > j0:
         backend.recon(j0, j1)
@@ -84,20 +90,38 @@ def solve_sharded(backend, dist, group=None):
     parts = _gather_rows(dist, group, backend.partial_rows(j0, j1), J, world, torch)
     backend.set_partials(parts)
     backend.finalize()
+    if check:
+        raise_sharded_status(backend)
     return backend.results()
+
+
+def raise_sharded_status(backend):
+    """The reference's exceptions for a finished sharded solve, in the
+    reference's order: segment sweeps first (gathered rows), then the link
+    solve (this rank's replicated flags)."""
+    raise_for_status(backend.seg_status[:, :, 0].cpu().numpy())
+    raise_for_status(backend.status_all())
 
 
 class DeviceBackend:
     """GPU backend: a :class:`BatchSolver`'s buffers driven phase by phase."""
 
-    def __init__(self, solver: BatchSolver, inputs):
+    def __init__(self, solver: BatchSolver, inputs, t0=0):
+        """``inputs``: the full stacked device arrays, or (``t0`` > 0, B = 1)
+        only this rank's window of stages starting at stage ``t0``
+        (:func:`stage_window`) -- each rank then uploads and holds only its
+        segments' stage data."""
         self.solver = solver
         self.torch = solver.torch
         self.lib = solver.lib
         self.J = solver.J
         self.n = solver.n
-        solver.check_inputs(inputs)
-        self.prob = solver._problem_struct(inputs)
+        solver.check_inputs(inputs, T_held=inputs["qx1"].shape[1])
+        self.prob = solver._problem_struct(inputs, t0=t0)
+        self.inputs = inputs          # keep the (windowed) buffers alive
+        self.t0 = t0
+        self.seg_status = None
+        self.launches = 0
         torch = self.torch
         self.partials = torch.zeros((solver.B, solver.J, 3), dtype=torch.float64, device=solver.device)
         self.stream = torch.cuda.current_stream(solver.device)
@@ -108,6 +132,7 @@ class DeviceBackend:
         head = (ctypes.byref(self.prob), ctypes.byref(s._outs))
         rc = fn(*head, *args)
         _native.check(rc, name)
+        self.launches += int(self.lib.plq_last_launch_count())
 
     def _ws(self):
         s = self.solver
@@ -175,6 +200,18 @@ class DeviceBackend:
         return {k: o[k] for k in ("objective", "kkt_inf", "link_mismatch", "link_residual", "links")}
 
 
+def stage_window(arrays, splits, j0, j1):
+    """Host arrays of one problem (B = 1) cut to the stages of segments
+    [j0, j1) -- what a rank of a horizon-sharded solve needs (its sweeps,
+    reconstruction and link-stage KKT rows read nothing else; terminal cost
+    and x_init are replicated).  Returns (window arrays, first stage)."""
+    t0, t1 = int(splits[j0]), int(splits[j1])
+    out = {}
+    for k, v in arrays.items():
+        out[k] = v[:, t0:t1] if v.ndim >= 2 and k not in ("QxxT", "qx1T", "x_init") else v
+    return out, t0
+
+
 def sharded_solve_device(inputs, J=None, partition=None, dist=None, group=None, device=None, tolerances=None):
     """Convenience wrapper: a horizon-sharded solve of device ``inputs`` (each
     rank holds the full stacked inputs; it only reads its segments')."""
@@ -188,4 +225,5 @@ def sharded_solve_device(inputs, J=None, partition=None, dist=None, group=None, 
     return solver, res
 
 
-__all__ = ["shard_range", "solve_sharded", "DeviceBackend", "sharded_solve_device"]
+__all__ = ["shard_range", "solve_sharded", "raise_sharded_status", "DeviceBackend", "stage_window",
+           "sharded_solve_device"]
