@@ -1,7 +1,18 @@
 import os
 import sys
 
-import numpy as np
+# the CPU oracle runs many tiny BLAS calls (and fork pools of them):
+# multi-threaded OpenBLAS is pathologically slow there
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np  # noqa: E402
+
+try:  # numpy may already be loaded by a plugin: limit its BLAS pool too
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+except Exception:  # noqa: BLE001
+    pass
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -45,8 +45,8 @@ def _report(tag, g, i, ref, floors):
             (("K", "K", "K"), ("x", "x", "states"), ("u", "u", "controls"), ("lam", "lam", "lambdas"),
              ("k", "k", "k"))}
     errs["obj"] = rel_err(g["objective"][i], ref["objective"])
-    print(f"{tag}: " + " ".join(f"{k}={v:.2e}(fl {floors.get(k if k != 'x' else 'states', 0):.1e})"
-                               for k, v in errs.items()))
+    fk = {"x": "states", "u": "controls", "lam": "lambdas", "obj": "objective"}
+    print(f"{tag}: " + " ".join(f"{k}={v:.2e}(fl {floors.get(fk.get(k, k), 0):.1e})" for k, v in errs.items()))
 
 
 @pytest.mark.slow
