@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libparlqr_b200.so")
+LIB_PATH = os.environ.get("PLQ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                          "libparlqr_b200.so")
 
 PLQ_OK = 0
 PLQ_STATUS_DEGENERATE = -1

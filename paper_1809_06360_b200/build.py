@@ -40,14 +40,19 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, profile=False):
+    """``profile=True``: a measurement build with the sweep's per-phase cycle
+    counters (-DPLQ_PHASE_PROFILE) as libparlqr_b200_prof.so (load it with
+    PLQ_LIB_PATH); the product library never has them."""
+    lib_path = LIB.replace(".so", "_prof.so") if profile else LIB
+    if not force and not profile and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "_build")
+    objdir = os.path.join(HERE, "_build_prof" if profile else "_build")
+    flags = FLAGS + (["-DPLQ_PHASE_PROFILE"] if profile else [])
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, src.replace(".cu", ".o")) for src in SOURCES]
     # translation units are independent: compile them concurrently
-    procs = [subprocess.Popen([nvcc(), *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj],
+    procs = [subprocess.Popen([nvcc(), *ARCH, *flags, "-c", os.path.join(CSRC, src), "-o", obj],
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
              for src, obj in zip(SOURCES, objs)]
     log = []
@@ -59,18 +64,18 @@ def build(force=False, verbose=False):
             failed.append(f"nvcc failed for {src}:\n{out}")
     if failed:
         raise RuntimeError("\n".join(failed))
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_path)
     with open(os.path.join(objdir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

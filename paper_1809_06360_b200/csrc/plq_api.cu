@@ -461,6 +461,8 @@ int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const d
 
 namespace {
 
+constexpr int NOUT_HOST = 19;   // plq_outputs_t fields, in declaration order
+
 void host_sizes(const plq_problem_t* p, size_t* in_sz, size_t* out_sz) {
   const size_t B = p->B, T = p->T, n = p->n, m = p->m, J = p->J;
   // order: split_times(int32), Qxx, Qux, Quu, qx1, qu1, Fx, Fu, f1, QxxT, qx1T, x_init (bytes)
@@ -493,6 +495,10 @@ void host_sizes(const plq_problem_t* p, size_t* in_sz, size_t* out_sz) {
   out_sz[13] = B * 8;
   out_sz[14] = B * 8;
   out_sz[15] = B * J * sizeof(int32_t);
+  // degenerate partitions (parallel.py:320-384): feas, feas_rows, feas_residual
+  out_sz[16] = B * J * n * (2 * n + 1) * 8;
+  out_sz[17] = B * J * sizeof(int32_t);
+  out_sz[18] = B * J * 8;
 }
 
 inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -511,7 +517,7 @@ static void host_chunking(const plq_problem_t* hp, int* nchunks, int64_t* chunk_
 
 size_t plq_host_arena_bytes(const plq_problem_t* hp) {
   if (check_problem(hp)) return 0;
-  size_t in_sz[12], out_sz[16], total = 0;
+  size_t in_sz[12], out_sz[NOUT_HOST], total = 0;
   host_sizes(hp, in_sz, out_sz);
   for (size_t s : in_sz) total += up256(s);
   for (size_t s : out_sz) total += up256(s);
@@ -536,7 +542,7 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
   if (hp->split_times[0] != 0 || hp->split_times[hp->J] != hp->T)
     return fail(PLQ_ERR_ARG, "partition does not cover the horizon");
   cudaStream_t s0 = static_cast<cudaStream_t>(stream);
-  size_t in_sz[12], out_sz[16];
+  size_t in_sz[12], out_sz[NOUT_HOST];
   host_sizes(hp, in_sz, out_sz);
   int nc, ns;
   int64_t cb;
@@ -549,8 +555,8 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
     din[i] = cur;
     cur += up256(in_sz[i]);
   }
-  char* dout[16];
-  for (int i = 0; i < 16; ++i) {
+  char* dout[NOUT_HOST];
+  for (int i = 0; i < NOUT_HOST; ++i) {
     dout[i] = cur;
     cur += up256(out_sz[i]);
   }
@@ -562,9 +568,9 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
     wsp[k] = cur;
     cur += up256(wsb);
   }
-  void* hout[16] = {ho->K, ho->k, ho->x, ho->u, ho->lam, ho->links, ho->mu_left, ho->lambda_right,
-                    ho->vf0, ho->Kz, ho->k1, ho->objective, ho->kkt_inf, ho->link_mismatch, ho->link_residual,
-                    ho->status};
+  void* hout[NOUT_HOST] = {ho->K, ho->k, ho->x, ho->u, ho->lam, ho->links, ho->mu_left, ho->lambda_right,
+                           ho->vf0, ho->Kz, ho->k1, ho->objective, ho->kkt_inf, ho->link_mismatch,
+                           ho->link_residual, ho->status, ho->feas, ho->feas_rows, ho->feas_residual};
   cudaStream_t st[3] = {s0, nullptr, nullptr};
   cudaEvent_t ready = nullptr;
   for (int k = 1; k < ns; ++k)
@@ -592,15 +598,18 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
     const double** fields[11] = {&dp.Qxx, &dp.Qux, &dp.Quu, &dp.qx1, &dp.qu1, &dp.Fx,
                                  &dp.Fu, &dp.f1, &dp.QxxT, &dp.qx1T, &dp.x_init};
     for (int i = 1; i < 12; ++i) *fields[i - 1] = reinterpret_cast<const double*>(din[i] + b0 * (in_sz[i] / hp->B));
-    plq_outputs_t o{};   // feas* null: degenerate partitions report PLQ_STATUS_DEGENERATE here
+    plq_outputs_t o{};   // feasibility buffers always on the device: degenerate partitions solved here too
     double** ofields[15] = {&o.K, &o.k, &o.x, &o.u, &o.lam, &o.links, &o.mu_left, &o.lambda_right,
                             &o.vf0, &o.Kz, &o.k1, &o.objective, &o.kkt_inf, &o.link_mismatch, &o.link_residual};
     for (int i = 0; i < 15; ++i) *ofields[i] = reinterpret_cast<double*>(dout[i] + b0 * (out_sz[i] / hp->B));
     o.status = reinterpret_cast<int32_t*>(dout[15] + b0 * (out_sz[15] / hp->B));
+    o.feas = reinterpret_cast<double*>(dout[16] + b0 * (out_sz[16] / hp->B));
+    o.feas_rows = reinterpret_cast<int32_t*>(dout[17] + b0 * (out_sz[17] / hp->B));
+    o.feas_residual = reinterpret_cast<double*>(dout[18] + b0 * (out_sz[18] / hp->B));
     rc = plq_solve_parallel(&dp, &o, wsp[c % ns], wsb, s);
     launches += g_launches;
     if (rc) break;
-    for (int i = 0; i < 16 && !rc; ++i) {
+    for (int i = 0; i < NOUT_HOST && !rc; ++i) {
       if (!hout[i]) continue;
       const size_t per = out_sz[i] / (size_t)hp->B;
       if (cudaMemcpyAsync((char*)hout[i] + b0 * per, dout[i] + b0 * per, bc * per, cudaMemcpyDeviceToHost, s) !=
@@ -617,3 +626,12 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
 }
 
 }  // extern "C"
+
+#ifdef PLQ_PHASE_PROFILE
+namespace plq {
+int sweep_small_phase_cycles(unsigned long long* out);
+}
+// Measurement builds only (-DPLQ_PHASE_PROFILE, libparlqr_b200_prof.so):
+// per-CTA cycle counters of the specialized sweep's stage phases, 1024 x 10.
+extern "C" int plq_debug_phase_cycles(unsigned long long* out) { return plq::sweep_small_phase_cycles(out); }
+#endif

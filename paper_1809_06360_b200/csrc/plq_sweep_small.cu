@@ -26,6 +26,25 @@
 
 namespace plq {
 
+// Optional per-phase cycle accounting (build with -DPLQ_PHASE_PROFILE; a
+// measurement build only): group 0 thread 0 of every CTA adds clock64()
+// deltas per stage phase into g_phase_cycles[blockIdx.x][phase].
+#ifdef PLQ_PHASE_PROFILE
+__device__ unsigned long long g_phase_cycles[1024][10];
+#define PLQ_PHASE(k)                                                               \
+  do {                                                                             \
+    if (gt == 0) {                                                                 \
+      const long long t_ = clock64();                                              \
+      atomicAdd(&g_phase_cycles[blockIdx.x][k], (unsigned long long)(t_ - t_last)); \
+      t_last = t_;                                                                 \
+    }                                                                              \
+  } while (0)
+#else
+#define PLQ_PHASE(k) \
+  do {               \
+  } while (0)
+#endif
+
 namespace {
 
 template <int N, int M>
@@ -379,6 +398,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   q_prefetch(b * T + lo + L - 1);
   gsync<NWG>(grp);
 
+#ifdef PLQ_PHASE_PROFILE
+  long long t_last = clock64();
+#endif
 #pragma unroll 1
   for (int s = L - 1; s >= 0; --s) {
     const int64_t st = b * T + lo + s;
@@ -387,8 +409,10 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     const double* Quu = S::QSTAGED ? sm + S::SQUU : p.Quu + st * (M * M);
     const double* qx1 = S::QSTAGED ? sm + S::SQX1 : p.qx1 + st * N;
     const double* qu1 = S::QSTAGED ? sm + S::SQU1 : p.qu1 + st * M;
+    PLQ_PHASE(8);   // end of the previous stage / segment prologue
     mbar_wait(bar, phase);
     phase ^= 1u;
+    PLQ_PHASE(0);   // stage-input copy wait
 
     // GEMM1: [VF; Z] = [Vxx; Vzx] [Fx | Fu]; Z lands in place: Mzx -> Vzx, Mzu' -> P.
     // The f1 column (w = vx1 + Vxx f1, mz1 = vz1 + Vzx f1) is a lane-parallel
@@ -407,6 +431,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       wcol += w2;
     }
     gsync<NWG>(grp);
+    PLQ_PHASE(1);   // f1 column dot products
     ggemm_f<N + NZ, N + M, N, NWG>(
         [&](int i, int k) { return Vxx[i * LDN + k]; }, [&](int k, int c) { return fload<N, M>(sm, k, c); }, gw,
         [&](int i, int c, double acc) {
@@ -421,6 +446,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         vz1[gt - N] += wcol;
     }
     gsync<NWG>(grp);
+    PLQ_PHASE(2);   // GEMM1
     // GEMM2: [Mxx ; Mux Muu] = [Fx Fu]' [VFx VFu] + Q-blocks; the w column
     // (mx1 = qx1 + Fx' w, mu1 = qu1 + Fu' w) lane-parallel
     if constexpr (S::QREG) {
@@ -483,6 +509,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     if (s > 0) q_prefetch(st - 1);   // next stage's Q values, consumed one stage later
 
     gsync<NWG>(grp);
+    PLQ_PHASE(3);   // GEMM2
 
     const bool constrained = (r != 0);
     bool chol = !constrained;
@@ -602,6 +629,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         r -= M;
       }
     }
+    PLQ_PHASE(4);   // constrained tail stage (QR, gains, rank certificate)
     if (chol) {
       // ---- G = -Muu^{-1} P (unconstrained stage, or p = 0), Cholesky in every lane's registers
       if (gt == 0 && s > 0 && !constrained) stage_issue<N, M>(p, st - 1, sm, bar);
@@ -674,6 +702,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       }
     }
 
+    PLQ_PHASE(5);   // Cholesky gains
     // ---- policy outputs
     for (int idx = gt; idx < M * N; idx += NT) {
       const int u = idx / N, c = idx % N;
@@ -681,6 +710,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       a.Kz[st * (M * N) + idx] = SERIAL ? 0.0 : G[u * LDW + N + c];
     }
     for (int u = gt; u < M; u += NT) a.k1[st * M + u] = G[u * LDW + CC];
+    PLQ_PHASE(6);   // policy stores
 
     // ---- value update.  Tail stages: Y = P + Muu G, V += P'G + G'Y (the
     // reference's terms, endpoint.py:285-294).  Unconstrained stages have
@@ -752,6 +782,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         vz1[gt - N] += t;
     }
     gsync<NWG>(grp);
+    PLQ_PHASE(7);   // value update
     if constexpr (!SEL) {
       // symmetrize Vxx (and Vzz) as 0.5 (V + V'): all N(N-1)/2 pairs in parallel
       // (Vzz is never a GEMM operand; symmetrizing it once per segment is the
@@ -891,5 +922,14 @@ int launch_sweep_small(const SweepArgs& a, cudaStream_t s) {
   if (a.p.n == 64 && a.p.m == 32) return launch_small<64, 32, 8, 1>(a, s);
   return -1;
 }
+
+#ifdef PLQ_PHASE_PROFILE
+// copy (and reset) the per-CTA phase cycle counters: out[1024 * 10]
+int sweep_small_phase_cycles(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles)) != cudaSuccess) return -1;
+  static unsigned long long zero[1024][10];
+  return cudaMemcpyToSymbol(g_phase_cycles, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 }  // namespace plq

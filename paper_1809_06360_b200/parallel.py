@@ -534,7 +534,7 @@ class HostSolver:
     ctypes/cgo binding of the reference would take)."""
 
     def __init__(self, B, T, n, m, J=None, partition=None, tolerances=DEFAULT_TOLERANCES, device=None,
-                 pin=True):
+                 pin=True, keep_feas=False):
         torch = _torch()
         self.torch = torch
         self.lib = _native.lib()
@@ -548,8 +548,12 @@ class HostSolver:
                   "lam": (B, T + 1, n), "links": (B, max(J - 1, 1), n), "mu_left": (B, max(J - 1, 1), n),
                   "lambda_right": (B, max(J - 1, 1), n), "vf0": (B, J, 3 * n * n + 2 * n),
                   "objective": (B,), "kkt_inf": (B,), "link_mismatch": (B,), "link_residual": (B,)}
+        if keep_feas:   # degenerate partitions' feasibility rows (details.segment_feasibility)
+            shapes["feas"] = (B, J, n, 2 * n + 1)
+        shapes["feas_residual"] = (B, J)
         self.out = {k: torch.empty(s, dtype=torch.float64, pin_memory=pin) for k, s in shapes.items()}
         self.out["status"] = torch.zeros((B, J), dtype=torch.int32, pin_memory=pin)
+        self.out["feas_rows"] = torch.zeros((B, J), dtype=torch.int32, pin_memory=pin)
         P = self._problem_struct(None)
         with torch.cuda.device(self.device):
             self.arena_bytes = int(self.lib.plq_host_arena_bytes(ctypes.byref(P)))
@@ -581,7 +585,7 @@ class HostSolver:
         rc = self.lib.plq_solve_parallel_host(ctypes.byref(P), ctypes.byref(outs), _ptr(self.arena),
                                               self.arena_bytes, ctypes.c_void_p(stream.cuda_stream))
         _native.check(rc, "plq_solve_parallel_host")
-        raise_for_status(self.out["status"].numpy())
+        raise_for_status(self.out["status"].numpy(), self.out["feas_residual"].numpy())
         return self.out
 
 
@@ -590,7 +594,8 @@ def solve_parallel_host(arrays, J=None, partition=None, tolerances=DEFAULT_TOLER
     torch = _torch()
     B, T, n = (int(s) for s in arrays["qx1"].shape)
     m = int(arrays["qu1"].shape[2])
-    hs = HostSolver(B, T, n, m, J=J, partition=partition, tolerances=tolerances, device=device, pin=False)
+    hs = HostSolver(B, T, n, m, J=J, partition=partition, tolerances=tolerances, device=device, pin=False,
+                    keep_feas=True)
     host = {f: torch.from_numpy(np.require(arrays[f], dtype=np.float64, requirements=["C", "W"]))
             for f in INPUT_FIELDS}
     out = hs.run(host)

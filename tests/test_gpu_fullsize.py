@@ -15,7 +15,10 @@ with a nonzero cross term ``Qux``.
   kernels and the generic ones (``PLQ_FORCE_GENERIC=1``).
 
 Gate: ``err = |y_gpu - y_ref|_inf / |y_ref|_inf``; ``K`` and the objective
-<= 1e-9 (or 10x the K floor where the reference's own K moves more);
+<= 1e-9, or 10x their own floor where the reference's K / objective move
+more (cfg3 at full size: x moves by 5e-3 and the objective by ~1e-8 under a
+1-ulp input perturbation -- the 1e-9 objective target is below the
+reference's own floor there);
 ``x, u, k, lambda, links`` <= max(1e-9, 10 * floor), floor = the oracle's
 own output change under a 1e-15 relative input perturbation, measured here
 at the same size.
@@ -35,7 +38,7 @@ def _floors(prob, J, ref, workers, reps=2):
     fl = {}
     for s in range(reps):
         r = O.solve(O.perturbed(prob, 1e-15, 100 + s), J=J, workers=workers)
-        for k in ("states", "controls", "lambdas", "K", "k", "links"):
+        for k in ("states", "controls", "lambdas", "K", "k", "links", "objective"):
             fl[k] = max(fl.get(k, 0.0), rel_err(r[k], ref[k]))
     return fl
 

@@ -31,7 +31,7 @@ def _floor(prob, J, key_ref, splits=None):
     fl = {}
     for s in range(2):
         r = O.solve(O.perturbed(prob, 1e-15, 100 + s), J=J, splits=splits)
-        for k in ("states", "controls", "lambdas", "K", "k", "links"):
+        for k in ("states", "controls", "lambdas", "K", "k", "links", "objective"):
             fl[k] = max(fl.get(k, 0.0), rel_err(r[k], key_ref[k]))
     return fl
 
@@ -46,8 +46,11 @@ def _check(g, i, ref, floors, K_gate=K_TOL):
     J = len(ref["splits"]) - 1 if "splits" in ref else None
     assert rel_err(g["K"][i], ref["K"]) <= max(K_gate, 10 * floors.get("K", 0.0)), \
         ("K", rel_err(g["K"][i], ref["K"]))
-    assert rel_err(g["objective"][i], ref["objective"]) <= OBJ_TOL, \
-        ("objective", g["objective"][i], float(ref["objective"]))
+    # objective: 1e-9, or 10x the reference's own objective floor where that
+    # is larger (cfg3 at full size: the oracle's x moves by ~5e-3 under a
+    # 1-ulp input perturbation, its objective by ~1e-8)
+    assert rel_err(g["objective"][i], ref["objective"]) <= max(OBJ_TOL, 10 * floors.get("objective", 0.0)), \
+        ("objective", g["objective"][i], float(ref["objective"]), floors.get("objective"))
     _gate("states", rel_err(g["x"][i], ref["states"]), floors.get("states", 0.0))
     _gate("controls", rel_err(g["u"][i], ref["controls"]), floors.get("controls", 0.0))
     _gate("lambdas", rel_err(g["lam"][i], ref["lambdas"]), floors.get("lambdas", 0.0))
@@ -356,3 +359,26 @@ def test_rank_threshold_tail_stages(kernel_path):
         floors = _floor(a, None, O.solve(a, splits=splits), splits=splits)
         _check(g, 0, o, floors)
         assert rel_err(g["Kz"][0], o["Kz"]) <= max(K_TOL, 10 * floors.get("K", 0.0))
+
+
+def test_host_entry_solves_degenerate_partitions():
+    """plq_solve_parallel_host takes the feasibility-constrained link path
+    too (parallel.py:320-384): the reference's degenerate golden cases give
+    the same bytes through the host entry as through the device entry."""
+    from paper_1809_06360_b200 import Partition, solve_parallel_host
+    done = 0
+    for name in ("uncontrollable", "small_random"):
+        for a, o, J in load_stored(name):
+            if not bool(o["degenerate"]):
+                continue
+            splits = tuple(int(s) for s in o["splits"])
+            part = Partition(len(splits) - 1, splits)
+            batch = {k: v[None] for k, v in a.items()}
+            d, _ = _gpu_batch(batch, splits=splits, keep_unfolded=False)
+            h = solve_parallel_host(batch, partition=part)
+            for k in ("K", "k", "x", "u", "lam", "objective", "kkt_inf", "feas_rows"):
+                assert np.array_equal(d[k], h[k]), (name, k)
+            nd = len(splits) - 2
+            assert np.array_equal(h["feas_rows"][0][:nd], o["feas_rows"][:-1])
+            done += 1
+    assert done >= 3
