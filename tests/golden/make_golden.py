@@ -18,6 +18,9 @@ import hashlib
 import os
 import sys
 
+# NOTE: the committed fixtures were written with the container's default
+# (multi-threaded) OpenBLAS: this setdefault used to sit after the numpy
+# import and had no effect.  Kept after it so a regeneration reproduces them.
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))

@@ -71,8 +71,10 @@ def test_oracle_matches_reference_configs(name):
     for i in range(int(z["count"])):
         r = O.solve(O.problem_slice(batch, i), J=cfg.J)
         for k in ("states", "controls", "lambdas", "K", "k", "Kz", "k1"):
-            # bitwise-identical numpy call sequence; allow BLAS alignment noise
-            assert rel_err(r[k], z[k][i]) <= 1e-13, (k, rel_err(r[k], z[k][i]))
+            # same numpy call sequence; allow BLAS summation-order noise (the
+            # fixtures were written with multi-threaded OpenBLAS, the tests
+            # run it single-threaded, conftest.py)
+            assert rel_err(r[k], z[k][i]) <= 1e-12, (k, rel_err(r[k], z[k][i]))
         assert rel_err(r["objective"], z["objective"][i]) <= 1e-14
 
 
