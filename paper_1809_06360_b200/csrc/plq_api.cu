@@ -632,6 +632,6 @@ namespace plq {
 int sweep_small_phase_cycles(unsigned long long* out);
 }
 // Measurement builds only (-DPLQ_PHASE_PROFILE, libparlqr_b200_prof.so):
-// per-CTA cycle counters of the specialized sweep's stage phases, 1024 x 10.
+// per-CTA cycle counters of the specialized sweep's stage phases, 1024 x 16.
 extern "C" int plq_debug_phase_cycles(unsigned long long* out) { return plq::sweep_small_phase_cycles(out); }
 #endif

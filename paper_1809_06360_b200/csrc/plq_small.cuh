@@ -43,6 +43,33 @@ __device__ __forceinline__ double gsum(double v, double* red, int grp, int gw) {
   }
 }
 
+// Two group sums in one reduction pass (independent shuffle chains).
+template <int NWG>
+__device__ __forceinline__ double2 gsum2(double a, double b, double* red, int grp, int gw) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if constexpr (NWG == 1) {
+    return make_double2(a, b);
+  } else {
+    gsync<NWG>(grp);
+    if ((threadIdx.x & 31) == 0) {
+      red[2 * gw] = a;
+      red[2 * gw + 1] = b;
+    }
+    gsync<NWG>(grp);
+    double ta = 0.0, tb = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWG; ++w) {
+      ta += red[2 * w];
+      tb += red[2 * w + 1];
+    }
+    return make_double2(ta, tb);
+  }
+}
+
 // C(M x N) = A (M x K) * B (K x N) on the FP64 tensor pipe (DMMA 8x8x4),
 // compile-time shapes, operands supplied by loader functors aload(i, k) /
 // bload(k, j) (only called in range).  Rows are processed in 8-row bands,

@@ -30,7 +30,7 @@ namespace plq {
 // measurement build only): group 0 thread 0 of every CTA adds clock64()
 // deltas per stage phase into g_phase_cycles[blockIdx.x][phase].
 #ifdef PLQ_PHASE_PROFILE
-__device__ unsigned long long g_phase_cycles[1024][10];
+__device__ unsigned long long g_phase_cycles[1024][16];
 #define PLQ_PHASE(k)                                                               \
   do {                                                                             \
     if (gt == 0) {                                                                 \
@@ -542,6 +542,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           },
           r);
       gsync<NWG>(grp);
+      PLQ_PHASE(10);   // tail: norms + N = Hx F
       if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
       if constexpr (NWG == 1) {
         // tau slot holds T (M*M); NTb columns 0..M-1 (free: Nx went to H) take V T',
@@ -558,6 +559,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         // (measured faster here than gqr8: 2.46 vs 2.51 ms cfg2 sweep)
         gqr<M, W, LDF, LDW, NWG>(NTb + N, r, H, tau, rdiag, red, grp, gw, gt);
       }
+      PLQ_PHASE(11);   // tail: QR of Nu applied to the rows
       // rank certificates (plq_rank.cuh): p = 0 for sure when ||R||_F <= thr,
       // p = M for sure when 1 / ||R^{-1}||_F = 1 / ||Kz||_F > thr; anything
       // else is re-solved by the rank-revealing repair pass (SVD decision,
@@ -571,22 +573,33 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         const double v = c > i ? Rm[i * LDF + c] : (c == i ? rdiag[i] : 0.0);
         pf += v * v;
       }
-      const double rf2 = gsum<NWG>(pf, red, grp, gw);
-      gsync<NWG>(grp);
       const double thr = p.rank_tol * fmax(nu_scale, rmax);
-      if (sqrt(rf2) <= thr) {
+      double rf2 = 0.0;
+      if constexpr (S::BIG) {
+        // the blocked back substitution below overwrites H's first M rows,
+        // which a p = 0 stage keeps: decide p = 0 first
+        rf2 = gsum<NWG>(pf, red, grp, gw);
+        gsync<NWG>(grp);
+      }
+      if (S::BIG && sqrt(rf2) <= thr) {
         // p = 0 (Nu numerically zero): identity reflectors, all r rows stay,
         // gains by the null-space solve with Zw = I (endpoint.py:239-250)
         chol = true;
       } else {
         int ldr = LDF;
+        double pz = 0.0;   // ||Kz||_F^2 partial (the z columns of G)
         if constexpr (S::BIG) {
           // G = -R^{-1} (Q1' stack): blocked back substitution in place on
           // H's first M rows (R stays in NTb, which G overlays), then G = -H
           auto sy = [&] { gsync<NWG>(grp); };
           gtri_inv_upper8<NWG>(Rm, M, ldr, rdiag, tau, gt, sy);
           gtrsm8<2, NWG>(Rm, M, ldr, tau, H, W, LDW, tau + 256, gt, sy);
-          for (int idx = gt; idx < M * W; idx += NT) G[(idx / W) * LDW + idx % W] = -H[(idx / W) * LDW + idx % W];
+          for (int idx = gt; idx < M * W; idx += NT) {
+            const int c = idx % W;
+            const double g = -H[(idx / W) * LDW + c];
+            G[(idx / W) * LDW + c] = g;
+            if (c >= N && c < 2 * N) pz += g * g;
+          }
           gsync<NWG>(grp);
         } else {
         // reciprocal pivots off the dependent chain (independent divisions)
@@ -604,29 +617,41 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           }
   #pragma unroll
           for (int i = 0; i < M; ++i) G[i * LDW + c] = -x[i];
+          if (c >= N && c < 2 * N) {
+  #pragma unroll
+            for (int i = 0; i < M; ++i) pz += x[i] * x[i];
+          }
         }
         gsync<NWG>(grp);
         }
-        double pz = 0.0;
-        for (int idx = gt; idx < M * N; idx += NT) {
-          const double g = G[(idx / N) * LDW + N + idx % N];
-          pz += g * g;
+        // one group reduction for both certificates (BIG: ||R||_F done above)
+        double kz2;
+        if constexpr (S::BIG) {
+          kz2 = gsum<NWG>(pz, red, grp, gw);
+        } else {
+          const double2 t = gsum2<NWG>(pf, pz, red, grp, gw);
+          rf2 = t.x;
+          kz2 = t.y;
         }
-        const double kz2 = gsum<NWG>(pz, red, grp, gw);
         gsync<NWG>(grp);
-        if (!(kz2 * thr * thr < 1.0)) {
+        if (!S::BIG && sqrt(rf2) <= thr) {
+          // p = 0: the gains come from the Cholesky branch below (G is
+          // recomputed), all r rows stay (rotated by the QR: same row space)
+          chol = true;
+        } else if (!(kz2 * thr * thr < 1.0)) {
           status = PLQ_STATUS_RANK_REPAIR;
           if (s > 0) {
             mbar_wait(bar, phase);
             phase ^= 1u;
           }
           break;
-        }
+        } else {
         // the surviving rows Q2' stack are rows M..r-1: advance the row base
         // instead of moving them (H is re-based at every segment start and
         // r + offset never exceeds the N-row buffer)
         H += M * LDW;
         r -= M;
+        }
       }
     }
     PLQ_PHASE(4);   // constrained tail stage (QR, gains, rank certificate)
@@ -649,6 +674,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           }
           break;
         }
+        PLQ_PHASE(9);   // Cholesky + fused forward solve
         gtrsm8<1, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);   // G = -Muu^{-1} P
       } else {
       double Lr[M][M], id[M];
@@ -671,6 +697,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           }
         }
       }
+      PLQ_PHASE(9);   // register Cholesky
       if (fail) {
         status = 1 + s;
         if (s > 0) {   // drain the copy in flight so the barrier phase stays in step
@@ -924,10 +951,10 @@ int launch_sweep_small(const SweepArgs& a, cudaStream_t s) {
 }
 
 #ifdef PLQ_PHASE_PROFILE
-// copy (and reset) the per-CTA phase cycle counters: out[1024 * 10]
+// copy (and reset) the per-CTA phase cycle counters: out[1024 * 16]
 int sweep_small_phase_cycles(unsigned long long* out) {
   if (cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles)) != cudaSuccess) return -1;
-  static unsigned long long zero[1024][10];
+  static unsigned long long zero[1024][16];
   return cudaMemcpyToSymbol(g_phase_cycles, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
 }
 #endif

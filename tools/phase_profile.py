@@ -18,8 +18,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-NAMES = ["copy wait", "f1 column", "GEMM1", "GEMM2", "tail (QR)", "Cholesky gains", "policy stores",
-         "value update", "stage end / prologue", "-"]
+NAMES = ["copy wait", "f1 column", "GEMM1", "GEMM2", "tail (QR)", "Cholesky solve", "policy stores",
+         "value update", "stage end / prologue", "Cholesky factor (+fused fwd solve)",
+         "tail: norms + N = Hx F", "tail: QR", "-", "-", "-", "-"]
 
 
 def main():
@@ -42,7 +43,7 @@ def main():
     lib = _native.lib()
     lib.plq_debug_phase_cycles.argtypes = [ctypes.c_void_p]
     lib.plq_debug_phase_cycles.restype = ctypes.c_int
-    buf = np.zeros((1024, 10), dtype=np.uint64)
+    buf = np.zeros((1024, 16), dtype=np.uint64)
     prob = s._problem_struct(inputs)
     stream = torch.cuda.current_stream(dev)
     run = lambda: lib.plq_sweep_segments(ctypes.byref(prob), ctypes.byref(s._outs), 0, cfg.J,
@@ -64,8 +65,8 @@ def main():
     stages = B * cfg.T * args.reps
     out = {"config": cfg.name, "B": B, "sweep_ms": ms, "ctas": ctas,
            "cycles_per_stage": float(tot.sum() / stages) * ctas / max(ctas, 1),
-           "share": {NAMES[k]: float(tot[k] / tot.sum()) for k in range(10) if tot[k] > 0},
-           "cycles_per_stage_by_phase": {NAMES[k]: float(tot[k] / stages) for k in range(10) if tot[k] > 0}}
+           "share": {NAMES[k]: float(tot[k] / tot.sum()) for k in range(16) if tot[k] > 0},
+           "cycles_per_stage_by_phase": {NAMES[k]: float(tot[k] / stages) for k in range(16) if tot[k] > 0}}
     print(json.dumps(out, indent=1))
 
 
