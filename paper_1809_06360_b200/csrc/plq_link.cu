@@ -311,11 +311,13 @@ __host__ __device__ inline void link_slab(int w, int sidx, int* c0, int* c1) {
 __device__ __forceinline__ void stage_rows(double* dst, int ld, const double* src, int n, double* xdst,
                                            const double* xsrc, int xcount, uint64_t* bar, uint32_t& phase) {
   if ((n % 2) == 0 && (ld % 2) == 0 && (xcount % 2) == 0) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {   // row copies spread over warp 0's lanes (one issuer serializes them)
+      const int lane = threadIdx.x;
       fence_proxy_async();
-      mbar_arrive_tx(bar, 8u * (uint32_t)(n * n + xcount));
-      for (int r = 0; r < n; ++r) bulk_g2s(dst + (size_t)r * ld, src + (size_t)r * n, 8u * n, bar);
-      if (xcount) bulk_g2s(xdst, xsrc, 8u * xcount, bar);
+      if (lane == 0) mbar_arrive_tx(bar, 8u * (uint32_t)(n * n + xcount));
+      __syncwarp();
+      for (int r = lane; r < n; r += 32) bulk_g2s(dst + (size_t)r * ld, src + (size_t)r * n, 8u * n, bar);
+      if (xcount && lane == 0) bulk_g2s(xdst, xsrc, 8u * xcount, bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1u;
@@ -384,11 +386,13 @@ __global__ void __launch_bounds__(256) link_trsm_big(plq_problem_t p, LinkLevel 
   __syncthreads();
   uint32_t phase = 0;
   // factor rows and the block inverses by bulk copies, overlapping the slab assembly
-  if ((n % 2) == 0 && threadIdx.x == 0) {
+  if ((n % 2) == 0 && threadIdx.x < 32) {   // row copies over warp 0's lanes
+    const int lane = threadIdx.x;
     fence_proxy_async();
-    mbar_arrive_tx(&bar, 8u * (uint32_t)(nn + nbk * 64));
-    for (int r = 0; r < n; ++r) bulk_g2s(Ls + (size_t)r * lls, gLc + (size_t)r * n, 8u * n, &bar);
-    bulk_g2s(Li, L.Linv + (b * E + o) * nbk * 64, 8u * nbk * 64, &bar);
+    if (lane == 0) mbar_arrive_tx(&bar, 8u * (uint32_t)(nn + nbk * 64));
+    __syncwarp();
+    for (int r = lane; r < n; r += 32) bulk_g2s(Ls + (size_t)r * lls, gLc + (size_t)r * n, 8u * n, &bar);
+    if (lane == 0) bulk_g2s(Li, L.Linv + (b * E + o) * nbk * 64, 8u * nbk * 64, &bar);
   }
   if ((n % 2) != 0) {
     for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Ls[(idx / n) * lls + idx % n] = gLc[idx];

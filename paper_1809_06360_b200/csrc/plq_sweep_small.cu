@@ -105,32 +105,38 @@ struct SL {
                 "bulk copies need 16-byte alignment");
 };
 
-// issue the bulk copies of stage `st` into the staging fields (one thread)
+// Bulk copies of stage `st` into the staging fields, issued by the 32 lanes
+// of one warp (all lanes must call):
+// the padded-row layouts (Fx / Fu rows at n = 32, 64) are N row copies each,
+// which one thread issuing serially put on the critical path of the stage
+// (~130 UBLKCP per stage at n = 64).  Lane 0 posts the byte count first.
 template <int N, int M>
-__device__ __forceinline__ void stage_issue(const plq_problem_t& p, int64_t st, double* sm, uint64_t* bar) {
+__device__ __forceinline__ void stage_issue_warp(const plq_problem_t& p, int64_t st, double* sm, uint64_t* bar,
+                                                 int lane) {
   using S = SL<N, M>;
   constexpr int NN = N * N, NM = N * M, MM = M * M;
   fence_proxy_async();
-  mbar_arrive_tx(bar, S::STAGE_BYTES);
+  if (lane == 0) mbar_arrive_tx(bar, S::STAGE_BYTES);
+  __syncwarp();
   if constexpr (S::FX_ROWS) {
 #pragma unroll 1
-    for (int r = 0; r < N; ++r) bulk_g2s(sm + S::SFX + r * S::LFX, p.Fx + st * NN + r * N, 8u * N, bar);
+    for (int r = lane; r < N; r += 32) bulk_g2s(sm + S::SFX + r * S::LFX, p.Fx + st * NN + r * N, 8u * N, bar);
   } else {
-    bulk_g2s(sm + S::SFX, p.Fx + st * NN, 8u * NN, bar);
+    if (lane == 0) bulk_g2s(sm + S::SFX, p.Fx + st * NN, 8u * NN, bar);
   }
   if constexpr (S::FU_ROWS) {
 #pragma unroll 1
-    for (int r = 0; r < N; ++r) bulk_g2s(sm + S::SFU + r * S::LFU, p.Fu + st * NM + r * M, 8u * M, bar);
+    for (int r = lane; r < N; r += 32) bulk_g2s(sm + S::SFU + r * S::LFU, p.Fu + st * NM + r * M, 8u * M, bar);
   } else {
-    bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
+    if (lane == 1) bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
   }
-  bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
+  if (lane == 2) bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
   if constexpr (S::QSTAGED) {
-    bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
-    bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
-    bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
-    bulk_g2s(sm + S::SQX1, p.qx1 + st * N, 8u * N, bar);
-    bulk_g2s(sm + S::SQU1, p.qu1 + st * M, 8u * M, bar);
+    if (lane == 3) bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
+    if (lane == 4) bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
+    if (lane == 5) bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
+    if (lane == 6) bulk_g2s(sm + S::SQX1, p.qx1 + st * N, 8u * N, bar);
+    if (lane == 7) bulk_g2s(sm + S::SQU1, p.qu1 + st * M, 8u * M, bar);
   }
 }
 
@@ -336,7 +342,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   double* dum = S::QREG ? sm + S::VF + (lane % N) * S::LDF + S::FW + lane / N : sm + S::DUM + lane;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
 
-  if (gt == 0) stage_issue<N, M>(p, b * T + lo + L - 1, sm, bar);
+  if (gw == 0) stage_issue_warp<N, M>(p, b * T + lo + L - 1, sm, bar, lane);
   for (int idx = gt; idx < S::VZ1 + N; idx += NT) sm[idx] = 0.0;
   if constexpr (S::BIG)
     for (int idx = gt; idx < N * LDN; idx += NT) Vzz[idx] = 0.0;
@@ -543,7 +549,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           r);
       gsync<NWG>(grp);
       PLQ_PHASE(10);   // tail: norms + N = Hx F
-      if (gt == 0 && s > 0) stage_issue<N, M>(p, st - 1, sm, bar);   // F consumed
+      if (gw == 0 && s > 0) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);   // F consumed
       if constexpr (NWG == 1) {
         // tau slot holds T (M*M); NTb columns 0..M-1 (free: Nx went to H) take V T',
         // the Y slot (dead until the value update) takes V'X
@@ -657,7 +663,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     PLQ_PHASE(4);   // constrained tail stage (QR, gains, rank certificate)
     if (chol) {
       // ---- G = -Muu^{-1} P (unconstrained stage, or p = 0), Cholesky in every lane's registers
-      if (gt == 0 && s > 0 && !constrained) stage_issue<N, M>(p, st - 1, sm, bar);
+      if (gw == 0 && s > 0 && !constrained) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);
       if constexpr (S::BIG) {
         // CTA Cholesky of Muu in place (not needed again in this stage) and
         // a blocked DMMA solve of the m x W right-hand side
