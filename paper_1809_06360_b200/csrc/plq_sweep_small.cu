@@ -35,7 +35,7 @@ __device__ unsigned long long g_phase_cycles[1024][16];
   do {                                                                             \
     if (gt == 0) {                                                                 \
       const long long t_ = clock64();                                              \
-      atomicAdd(&g_phase_cycles[blockIdx.x][k], (unsigned long long)(t_ - t_last)); \
+      atomicAdd(&g_phase_cycles[blockIdx.x & 1023][k], (unsigned long long)(t_ - t_last)); \
       t_last = t_;                                                                 \
     }                                                                              \
   } while (0)
@@ -131,6 +131,15 @@ __device__ __forceinline__ void stage_issue_warp(const plq_problem_t& p, int64_t
     if (lane == 1) bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
   }
   if (lane == 2) bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
+  if constexpr (S::BIG) {
+    // the Q blocks are not staged (GEMM2 loads them as epilogue addends):
+    // pull them into L2 now, a stage ahead, so those loads hit L2 not HBM
+    if (lane == 3) bulk_prefetch_l2(p.Qxx + st * NN, 8u * NN);
+    if (lane == 4) bulk_prefetch_l2(p.Qux + st * NM, 8u * NM);
+    if (lane == 5) bulk_prefetch_l2(p.Quu + st * MM, 8u * MM);
+    if (lane == 6) bulk_prefetch_l2(p.qx1 + st * N, 8u * N);
+    if (lane == 7) bulk_prefetch_l2(p.qu1 + st * M, 8u * M);
+  }
   if constexpr (S::QSTAGED) {
     if (lane == 3) bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
     if (lane == 4) bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
@@ -549,7 +558,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           r);
       gsync<NWG>(grp);
       PLQ_PHASE(10);   // tail: norms + N = Hx F
-      if (gw == 0 && s > 0) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);   // F consumed
+      // F consumed: the next stage's copies, issued by the LAST warp (warp 0
+      // factors the QR panels next)
+      if (gw == NWG - 1 && s > 0) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);
       if constexpr (NWG == 1) {
         // tau slot holds T (M*M); NTb columns 0..M-1 (free: Nx went to H) take V T',
         // the Y slot (dead until the value update) takes V'X
@@ -663,7 +674,9 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     PLQ_PHASE(4);   // constrained tail stage (QR, gains, rank certificate)
     if (chol) {
       // ---- G = -Muu^{-1} P (unconstrained stage, or p = 0), Cholesky in every lane's registers
-      if (gw == 0 && s > 0 && !constrained) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);
+      // next stage's copies from the LAST warp: warp 0 factors the first
+      // diagonal blocks of the Cholesky right after this
+      if (gw == NWG - 1 && s > 0 && !constrained) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);
       if constexpr (S::BIG) {
         // CTA Cholesky of Muu in place (not needed again in this stage) and
         // a blocked DMMA solve of the m x W right-hand side

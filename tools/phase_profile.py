@@ -61,7 +61,7 @@ def main():
     ms = ev0.elapsed_time(ev1) / args.reps
     assert lib.plq_debug_phase_cycles(ctypes.c_void_p(buf.ctypes.data)) == 0
     tot = buf.sum(axis=0).astype(np.float64)
-    ctas = int((buf.sum(axis=1) > 0).sum())
+    ctas = int((buf.sum(axis=1) > 0).sum())   # CTAs >= 1024 fold onto blockIdx % 1024
     stages = B * cfg.T * args.reps
     out = {"config": cfg.name, "B": B, "sweep_ms": ms, "ctas": ctas,
            "cycles_per_stage": float(tot.sum() / stages) * ctas / max(ctas, 1),
