@@ -105,48 +105,64 @@ struct SL {
                 "bulk copies need 16-byte alignment");
 };
 
-// Bulk copies of stage `st` into the staging fields, issued by the 32 lanes
-// of one warp (all lanes must call):
-// the padded-row layouts (Fx / Fu rows at n = 32, 64) are N row copies each,
-// which one thread issuing serially put on the critical path of the stage
-// (~130 UBLKCP per stage at n = 64).  Lane 0 posts the byte count first.
+// Stage `st`'s inputs into the staging fields, issued by EVERY thread of the
+// group (all must call).  Contiguous fields go by one bulk copy each (TMA
+// 1-D, complete_tx on the stage mbarrier); the row-padded Fx / Fu layouts
+// (n = 32, 64: conflict-free DMMA fragment strides) go by 16-byte cp.async
+// spread over the group, each thread then arriving on the same mbarrier when
+// its copies land (cp.async.mbarrier.arrive.noinc; the barrier counts 1 + NT
+// arrivals).  One bulk copy per row instead -- ~130 UBLKCP per n = 64 stage,
+// ~70 at n = 32 -- was issue-bound (measured: ~4k cycles per n = 32 stage).
 template <int N, int M>
-__device__ __forceinline__ void stage_issue_warp(const plq_problem_t& p, int64_t st, double* sm, uint64_t* bar,
-                                                 int lane) {
+__host__ __device__ constexpr uint32_t stage_bulk_bytes() {
+  using S = SL<N, M>;
+  return S::STAGE_BYTES - (S::FX_ROWS ? 8u * N * N : 0u) - (S::FU_ROWS ? 8u * N * M : 0u);
+}
+
+template <int N, int M, int NT>
+__device__ __forceinline__ void stage_issue_group(const plq_problem_t& p, int64_t st, double* sm, uint64_t* bar,
+                                                  int gt) {
   using S = SL<N, M>;
   constexpr int NN = N * N, NM = N * M, MM = M * M;
-  fence_proxy_async();
-  if (lane == 0) mbar_arrive_tx(bar, S::STAGE_BYTES);
-  __syncwarp();
+  if (gt < 8) fence_proxy_async();   // the bulk-copy issuers: generic reads before async writes
+  if (gt == 0) mbar_arrive_tx(bar, stage_bulk_bytes<N, M>());
   if constexpr (S::FX_ROWS) {
+    constexpr int CR = N / 2;   // 16-byte chunks per row
+    const double* src = p.Fx + st * NN;
 #pragma unroll 1
-    for (int r = lane; r < N; r += 32) bulk_g2s(sm + S::SFX + r * S::LFX, p.Fx + st * NN + r * N, 8u * N, bar);
-  } else {
-    if (lane == 0) bulk_g2s(sm + S::SFX, p.Fx + st * NN, 8u * NN, bar);
+    for (int c = gt; c < N * CR; c += NT) cp_async16(sm + S::SFX + (c / CR) * S::LFX + 2 * (c % CR), src + 2 * c);
+  } else if (gt == 0) {
+    bulk_g2s(sm + S::SFX, p.Fx + st * NN, 8u * NN, bar);
   }
   if constexpr (S::FU_ROWS) {
+    constexpr int CR = M / 2;
+    const double* src = p.Fu + st * NM;
 #pragma unroll 1
-    for (int r = lane; r < N; r += 32) bulk_g2s(sm + S::SFU + r * S::LFU, p.Fu + st * NM + r * M, 8u * M, bar);
-  } else {
-    if (lane == 1) bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
+    for (int c = gt; c < N * CR; c += NT) cp_async16(sm + S::SFU + (c / CR) * S::LFU + 2 * (c % CR), src + 2 * c);
+  } else if (gt == (NT > 1 ? 1 : 0)) {
+    bulk_g2s(sm + S::SFU, p.Fu + st * NM, 8u * NM, bar);
   }
-  if (lane == 2) bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
-  if constexpr (S::BIG) {
-    // the Q blocks are not staged (GEMM2 loads them as epilogue addends):
-    // pull them into L2 now, a stage ahead, so those loads hit L2 not HBM
-    if (lane == 3) bulk_prefetch_l2(p.Qxx + st * NN, 8u * NN);
-    if (lane == 4) bulk_prefetch_l2(p.Qux + st * NM, 8u * NM);
-    if (lane == 5) bulk_prefetch_l2(p.Quu + st * MM, 8u * MM);
-    if (lane == 6) bulk_prefetch_l2(p.qx1 + st * N, 8u * N);
-    if (lane == 7) bulk_prefetch_l2(p.qu1 + st * M, 8u * M);
+  const int lane = gt & 31;
+  if (gt < 32) {
+    if (lane == 2 % NT) bulk_g2s(sm + S::SF1, p.f1 + st * N, 8u * N, bar);
+    if constexpr (S::BIG) {
+      // the Q blocks are not staged (GEMM2 loads them as epilogue addends):
+      // pull them into L2 now, a stage ahead, so those loads hit L2 not HBM
+      if (lane == 3) bulk_prefetch_l2(p.Qxx + st * NN, 8u * NN);
+      if (lane == 4) bulk_prefetch_l2(p.Qux + st * NM, 8u * NM);
+      if (lane == 5) bulk_prefetch_l2(p.Quu + st * MM, 8u * MM);
+      if (lane == 6) bulk_prefetch_l2(p.qx1 + st * N, 8u * N);
+      if (lane == 7) bulk_prefetch_l2(p.qu1 + st * M, 8u * M);
+    }
+    if constexpr (S::QSTAGED) {
+      if (lane == 3) bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
+      if (lane == 4) bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
+      if (lane == 5) bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
+      if (lane == 6) bulk_g2s(sm + S::SQX1, p.qx1 + st * N, 8u * N, bar);
+      if (lane == 7) bulk_g2s(sm + S::SQU1, p.qu1 + st * M, 8u * M, bar);
+    }
   }
-  if constexpr (S::QSTAGED) {
-    if (lane == 3) bulk_g2s(sm + S::SQXX, p.Qxx + st * NN, 8u * NN, bar);
-    if (lane == 4) bulk_g2s(sm + S::SQUX, p.Qux + st * NM, 8u * NM, bar);
-    if (lane == 5) bulk_g2s(sm + S::SQUU, p.Quu + st * MM, 8u * MM, bar);
-    if (lane == 6) bulk_g2s(sm + S::SQX1, p.qx1 + st * N, 8u * N, bar);
-    if (lane == 7) bulk_g2s(sm + S::SQU1, p.qu1 + st * M, 8u * M, bar);
-  }
+  cp_async_arrive_noinc(bar);
 }
 
 // F(k, j) = [Fx | Fu | f1](k, j) from the staged fields
@@ -351,7 +367,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
   double* dum = S::QREG ? sm + S::VF + (lane % N) * S::LDF + S::FW + lane / N : sm + S::DUM + lane;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::BAR);
 
-  if (gw == 0) stage_issue_warp<N, M>(p, b * T + lo + L - 1, sm, bar, lane);
+  stage_issue_group<N, M, NT>(p, b * T + lo + L - 1, sm, bar, gt);
   for (int idx = gt; idx < S::VZ1 + N; idx += NT) sm[idx] = 0.0;
   if constexpr (S::BIG)
     for (int idx = gt; idx < N * LDN; idx += NT) Vzz[idx] = 0.0;
@@ -558,9 +574,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           r);
       gsync<NWG>(grp);
       PLQ_PHASE(10);   // tail: norms + N = Hx F
-      // F consumed: the next stage's copies, issued by the LAST warp (warp 0
-      // factors the QR panels next)
-      if (gw == NWG - 1 && s > 0) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);
+      if (s > 0) stage_issue_group<N, M, NT>(p, st - 1, sm, bar, gt);   // F consumed
       if constexpr (NWG == 1) {
         // tau slot holds T (M*M); NTb columns 0..M-1 (free: Nx went to H) take V T',
         // the Y slot (dead until the value update) takes V'X
@@ -674,9 +688,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     PLQ_PHASE(4);   // constrained tail stage (QR, gains, rank certificate)
     if (chol) {
       // ---- G = -Muu^{-1} P (unconstrained stage, or p = 0), Cholesky in every lane's registers
-      // next stage's copies from the LAST warp: warp 0 factors the first
-      // diagonal blocks of the Cholesky right after this
-      if (gw == NWG - 1 && s > 0 && !constrained) stage_issue_warp<N, M>(p, st - 1, sm, bar, lane);
+      if (s > 0 && !constrained) stage_issue_group<N, M, NT>(p, st - 1, sm, bar, gt);
       if constexpr (S::BIG) {
         // CTA Cholesky of Muu in place (not needed again in this stage) and
         // a blocked DMMA solve of the m x W right-hand side
@@ -897,7 +909,7 @@ __global__ void __launch_bounds__(NWG * 32 * GROUPS, (NWG == 1 ? 16 : 1)) sweep_
     if (i < c) pairs[i * (2 * N - i - 1) / 2 + (c - i - 1)] = (unsigned short)((i << 8) | c);
   }
   __shared__ long long next_task[GROUPS];
-  if (gt == 0) mbar_init(bar, 1);
+  if (gt == 0) mbar_init(bar, 1 + NWG * 32);   // the bulk-copy arrive + every thread's cp.async arrive
   __syncthreads();
   uint32_t phase = 0;
   const int nloc = a.seg_end - a.seg_begin;

@@ -60,6 +60,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Arrive on `bar` once all of this thread's prior cp.async copies have
+// landed; the arrival is NOT pre-counted (.noinc): the barrier's expected
+// count includes it.
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Bulk prefetch of a global range into L2 (no shared-memory destination,
 // no completion tracking): the next stage's operands are in L2 by the time
 // the stage starts.  `src` and `bytes` must be multiples of 16.
