@@ -256,6 +256,86 @@ __device__ __forceinline__ void ggemm_sel(AL aload, BL bload, int gw, BandOf ban
   }
 }
 
+// Two row bands of a tile-selective GEMM in ONE k-loop: band tmA (column
+// tiles tn < TNA with on(tmA, tn)) and band tmB (tn < TNB with on(tmB, tn);
+// tmB < 0: band A only).  Every k-step issues the DMMAs of both bands' tiles
+// back to back, so a band with few tiles (the short end of a triangular
+// block) no longer runs its K/4-deep accumulation chain alone.  Addends:
+// pre(i, j) is loaded before the k-loop for every band-A tile when PREA and
+// for the band-B tiles tn >= PRE_FROM (latency hidden behind the DMMAs);
+// epi(i, j, v, has_pre) gets v = pre + acc for those and v = acc otherwise
+// (the epilogue then adds its on-chip addend itself, which keeps the
+// register footprint down).
+template <int M, int N, int K, int TNA, int TNB, bool PREA, int PRE_FROM, class AL, class BL, class On, class Pre,
+          class Epi>
+__device__ __forceinline__ void ggemm_sel2(AL aload, BL bload, int tmA, int tmB, On on, Pre pre, Epi epi) {
+  constexpr int KS = (K + 3) / 4;
+  constexpr int TNX = TNA > TNB ? TNA : TNB;
+  constexpr int TPA = PREA ? TNA : 1, TPB = TNB > PRE_FROM ? TNB - PRE_FROM : 1;
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int iA = tmA * 8 + g, iB = tmB * 8 + g;
+  const bool okA = iA < M, hasB = tmB >= 0, okB = hasB && iB < M;
+  double accA[TNA][2], accB[TNB > 0 ? TNB : 1][2], addA[TPA][2], addB[TPB][2];
+#pragma unroll
+  for (int tn = 0; tn < TNA; ++tn) accA[tn][0] = accA[tn][1] = 0.0;
+#pragma unroll
+  for (int tn = 0; tn < TNB; ++tn) accB[tn][0] = accB[tn][1] = 0.0;
+  if constexpr (PREA) {
+#pragma unroll
+    for (int tn = 0; tn < TNA; ++tn)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tn * 8 + 2 * q + e;
+        addA[tn][e] = (okA && j < N && on(tmA, tn)) ? pre(iA, j) : 0.0;
+      }
+  }
+#pragma unroll
+  for (int tn = PRE_FROM; tn < TNB; ++tn)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = tn * 8 + 2 * q + e;
+      addB[tn - PRE_FROM][e] = (okB && j < N && on(tmB, tn)) ? pre(iB, j) : 0.0;
+    }
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + q;
+    const bool kok = (K % 4 == 0) || (k < K);
+    const double a = (okA && kok) ? aload(iA, k) : 0.0;
+    const double ab = (okB && kok) ? aload(iB, k) : 0.0;
+#pragma unroll
+    for (int tn = 0; tn < TNX; ++tn) {
+      const int j = tn * 8 + g;
+      const bool useA = tn < TNA && on(tmA, tn), useB = tn < TNB && hasB && on(tmB, tn);
+      if (useA || useB) {
+        const double b = (((N % 8 == 0) || (j < N)) && kok) ? bload(k, j) : 0.0;
+        if (tn < TNA && useA) dmma884(accA[tn < TNA ? tn : 0][0], accA[tn < TNA ? tn : 0][1], a, b);
+        if (tn < TNB && useB) dmma884(accB[tn < TNB ? tn : 0][0], accB[tn < TNB ? tn : 0][1], ab, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int tn = 0; tn < TNA; ++tn) {
+    if (on(tmA, tn)) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tn * 8 + 2 * q + e;
+        if (okA && j < N) epi(iA, j, accA[tn][e] + (PREA ? addA[PREA ? tn : 0][e] : 0.0), PREA);
+      }
+    }
+  }
+#pragma unroll
+  for (int tn = 0; tn < TNB; ++tn) {
+    if (hasB && on(tmB, tn)) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tn * 8 + 2 * q + e;
+        const bool hp = tn >= PRE_FROM;
+        if (okB && j < N) epi(iB, j, accB[tn][e] + (hp ? addB[hp ? tn - PRE_FROM : 0][e] : 0.0), hp);
+      }
+    }
+  }
+}
+
 // pointer-operand form: A row-major (or transposed, TA) with stride LDA, B row-major stride LDB
 template <int M, int N, int K, bool TA, int LDA, int LDB, int NWG, class Epi>
 __device__ __forceinline__ void ggemm(const double* __restrict__ A, const double* __restrict__ B, int gw, Epi epi,

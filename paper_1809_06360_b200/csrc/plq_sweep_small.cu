@@ -494,24 +494,28 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       // V), no Mxu block; u bands: Mux | Muu in full.  Warps 0-3 take a u
       // band (12 tiles), warps 4-7 a pair of x bands (9 tiles).  The Q-block
       // addends are loaded from global memory before each band's k-loop.
-      ggemm_sel<N + M, N + M, N, 2>(
-          [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
-          [](int w, int slot) { return w < 4 ? (slot == 0 ? XB + w : -1) : (slot == 0 ? w - 4 : XB + 3 - w); },
-          [](int tm, int tn) { return tm >= XB || tn <= tm; },
-          [&](int i, int c) {
-            const int u = i - N;
-            return i < N ? __ldg(Qxx + i * N + c) : (c < N ? __ldg(Qux + u * N + c) : __ldg(Quu + u * M + (c - N)));
-          },
-          [&](int i, int c, double v) {
-            const int u = i - N;
-            if (i < N) {
-              if (c <= i) Vxx[i * LDN + c] = v;
-            } else if (c < N) {
-              P[u * LDW + c] = v;
-            } else {
-              Muu[u * LDM + (c - N)] = v;
-            }
-          });
+      auto fa = [&](int i, int k) { return fload<N, M>(sm, k, i); };
+      auto fb = [&](int k, int c) { return VF[k * LDF + c]; };
+      auto on2 = [](int tm, int tn) { return tm >= XB || tn <= tm; };
+      auto qpre = [&](int i, int c) {
+        const int u = i - N;
+        return i < N ? __ldg(Qxx + i * N + c) : (c < N ? __ldg(Qux + u * N + c) : __ldg(Quu + u * M + (c - N)));
+      };
+      auto mepi = [&](int i, int c, double v, bool) {
+        const int u = i - N;
+        if (i < N) {
+          if (c <= i) Vxx[i * LDN + c] = v;
+        } else if (c < N) {
+          P[u * LDW + c] = v;
+        } else {
+          Muu[u * LDM + (c - N)] = v;
+        }
+      };
+      // both x bands of a warp in one k-loop (joint accumulation chains)
+      if (gw < 4)
+        ggemm_sel2<N + M, N + M, N, (N + M) / 8, 0, true, 0>(fa, fb, XB + gw, -1, on2, qpre, mepi);
+      else
+        ggemm_sel2<N + M, N + M, N, XB, XB, true, 0>(fa, fb, gw - 4, XB + 3 - gw, on2, qpre, mepi);
     } else {
       ggemm_f<N + M, N + M, N, NWG>(
           [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
@@ -809,6 +813,24 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           Vzz[zi * LDN + (c - N)] = v;
       }
     };
+    // SEL epilogue of the joint-band update: Vxx / Vzx read-modify-written
+    // on chip, Vzz (L2 scratch) pre-loaded before the k-loop (has_pre)
+    auto vsel2 = [&](int i, int c, double v, bool has_pre) {
+      if (i < N) {
+        if (c <= i) {
+          const double w = Vxx[i * LDN + c] + v;
+          Vxx[i * LDN + c] = w;
+          Vxx[c * LDN + i] = w;
+        }
+      } else {
+        const int zi = i - N;
+        if (c < N)
+          Vzx[zi * LDN + c] += v;
+        else if (c - N <= zi)
+          Vzz[zi * LDN + (c - N)] = has_pre ? v : Vzz[zi * LDN + (c - N)] + v;
+      }
+    };
+    auto vzz_pre = [&](int i, int c) { return Vzz[(i - N) * LDN + (c - N)]; };
     if (constrained) {
       ggemm<M, W, M, false, LDM, LDW, NWG>(Muu, G, gw,
                                            [&](int i, int c, double acc) { Y[i * LDW + c] = P[i * LDW + c] + acc; });
@@ -816,12 +838,13 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       auto aP = [&](int i, int k) { return k < M ? P[k * LDW + i] : G[(k - M) * LDW + i]; };
       auto bG = [&](int k, int c) { return k < M ? G[k * LDW + c] : Y[(k - M) * LDW + c]; };
       if constexpr (SEL)
-        ggemm_sel<N + NZ, W - 1, 2 * M, 2>(aP, bG, gw, vband, von, vzero, vsel);
+        ggemm_sel2<N + NZ, W - 1, 2 * M, XB, 2 * XB, false, XB>(aP, bG, gw, (VTM > NWG ? VTM - 1 - gw : -1), von, vzz_pre, vsel2);
       else
         ggemm_f<N + NZ, W - 1, 2 * M, NWG>(aP, bG, gw, vupd);
     } else if constexpr (SEL) {
-      ggemm_sel<N + NZ, W - 1, M, 2>([&](int i, int k) { return P[k * LDW + i]; },
-                                     [&](int k, int c) { return G[k * LDW + c]; }, gw, vband, von, vzero, vsel);
+      ggemm_sel2<N + NZ, W - 1, M, XB, 2 * XB, false, XB>([&](int i, int k) { return P[k * LDW + i]; },
+                                                         [&](int k, int c) { return G[k * LDW + c]; }, gw,
+                                                         (VTM > NWG ? VTM - 1 - gw : -1), von, vzz_pre, vsel2);
     } else {
       ggemm<N + NZ, W - 1, M, true, LDW, LDW, NWG>(P, G, gw, vupd);
     }
