@@ -6,6 +6,8 @@
 
 #include "plq_device.cuh"
 
+#include <type_traits>
+
 namespace plq {
 
 // smallest v >= x with v % 8 == 4: row strides (in doubles) for which the
@@ -266,15 +268,19 @@ __device__ __forceinline__ void ggemm_sel(AL aload, BL bload, int gw, BandOf ban
 // epi(i, j, v, has_pre) gets v = pre + acc for those and v = acc otherwise
 // (the epilogue then adds its on-chip addend itself, which keeps the
 // register footprint down).
-template <int M, int N, int K, int TNA, int TNB, bool PREA, int PRE_FROM, class AL, class BL, class On, class Pre,
-          class Epi>
-__device__ __forceinline__ void ggemm_sel2(AL aload, BL bload, int tmA, int tmB, On on, Pre pre, Epi epi) {
+// The bands are template parameters (tmA, tmB; tmB < 0: none) so that, once
+// the tile loops are unrolled, on(tm, tn) folds to a constant: no runtime
+// tile predicates in the k-loop (callers dispatch on the warp index).
+template <int M, int N, int K, int TNA, int TNB, bool PREA, int PRE_FROM, int tmA, int tmB, class AL, class BL,
+          class On, class Pre, class Epi>
+__device__ __forceinline__ void ggemm_sel2(AL aload, BL bload, On on, Pre pre, Epi epi) {
   constexpr int KS = (K + 3) / 4;
   constexpr int TNX = TNA > TNB ? TNA : TNB;
   constexpr int TPA = PREA ? TNA : 1, TPB = TNB > PRE_FROM ? TNB - PRE_FROM : 1;
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int iA = tmA * 8 + g, iB = tmB * 8 + g;
-  const bool okA = iA < M, hasB = tmB >= 0, okB = hasB && iB < M;
+  constexpr bool hasB = tmB >= 0;
+  const bool okA = iA < M, okB = hasB && iB < M;
   double accA[TNA][2], accB[TNB > 0 ? TNB : 1][2], addA[TPA][2], addB[TPB][2];
 #pragma unroll
   for (int tn = 0; tn < TNA; ++tn) accA[tn][0] = accA[tn][1] = 0.0;
@@ -333,6 +339,22 @@ __device__ __forceinline__ void ggemm_sel2(AL aload, BL bload, int tmA, int tmB,
         if (okB && j < N) epi(iB, j, accB[tn][e] + (hp ? addB[hp ? tn - PRE_FROM : 0][e] : 0.0), hp);
       }
     }
+  }
+}
+
+// f(std::integral_constant<int, w>{}) for the runtime warp index w < 8:
+// lets a group hand each warp a compile-time role.
+template <class F>
+__device__ __forceinline__ void warp_dispatch8(int w, F&& f) {
+  switch (w) {
+    case 0: f(std::integral_constant<int, 0>{}); break;
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 5: f(std::integral_constant<int, 5>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    default: f(std::integral_constant<int, 7>{}); break;
   }
 }
 

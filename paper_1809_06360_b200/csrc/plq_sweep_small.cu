@@ -470,6 +470,7 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           double* d = (i < N) ? VF + i * LDF + c : ((c < N) ? Vzx + zi * LDN + c : P + (c - N) * LDW + N + zi);
           *d = acc;
         });
+    PLQ_PHASE(14);   // GEMM1 k-loops (warp 0's bands)
     if (wrow) {
       if (gt < N)
         VF[gt * LDF + N + M] = vx1[gt] + wcol;
@@ -511,11 +512,17 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           Muu[u * LDM + (c - N)] = v;
         }
       };
-      // both x bands of a warp in one k-loop (joint accumulation chains)
-      if (gw < 4)
-        ggemm_sel2<N + M, N + M, N, (N + M) / 8, 0, true, 0>(fa, fb, XB + gw, -1, on2, qpre, mepi);
-      else
-        ggemm_sel2<N + M, N + M, N, XB, XB, true, 0>(fa, fb, gw - 4, XB + 3 - gw, on2, qpre, mepi);
+      // warps 0-3: one u band; warps 4-7: an x-band pair in one k-loop
+      // (bands fixed per warp at compile time: no runtime tile predicates)
+      auto g2 = [&](auto w) {
+        constexpr int WI = decltype(w)::value;
+        if constexpr (WI < 4)
+          ggemm_sel2<N + M, N + M, N, (N + M) / 8, 0, true, 0, XB + WI, -1>(fa, fb, on2, qpre, mepi);
+        else
+          ggemm_sel2<N + M, N + M, N, XB, XB, true, 0, WI - 4, XB + 3 - WI>(fa, fb, on2, qpre, mepi);
+      };
+      warp_dispatch8(gw, g2);
+      PLQ_PHASE(12);   // GEMM2 k-loops (warp 0's band)
     } else {
       ggemm_f<N + M, N + M, N, NWG>(
           [&](int i, int k) { return fload<N, M>(sm, k, i); }, [&](int k, int c) { return VF[k * LDF + c]; }, gw,
@@ -696,7 +703,18 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       if constexpr (S::BIG) {
         // CTA Cholesky of Muu in place (not needed again in this stage) and
         // a blocked DMMA solve of the m x W right-hand side
+#ifdef PLQ_PHASE_PROFILE
+        int nsync = 0;   // gchol8 syncs alternate: diagonal factor + panel | trailing tiles
+        auto sy = [&] {
+          gsync<NWG>(grp);
+          if (nsync++ & 1)
+            PLQ_PHASE(11);
+          else
+            PLQ_PHASE(15);
+        };
+#else
         auto sy = [&] { gsync<NWG>(grp); };
+#endif
         static_assert(M * M >= 256 + NWG * 64, "TAU slot too small for the blocked solve");
         // Cholesky with the forward solve fused in: G <- L^{-1} (-P), block
         // row k in step k (no copy / negation passes)
@@ -837,14 +855,24 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
       gsync<NWG>(grp);
       auto aP = [&](int i, int k) { return k < M ? P[k * LDW + i] : G[(k - M) * LDW + i]; };
       auto bG = [&](int k, int c) { return k < M ? G[k * LDW + c] : Y[(k - M) * LDW + c]; };
-      if constexpr (SEL)
-        ggemm_sel2<N + NZ, W - 1, 2 * M, XB, 2 * XB, false, XB>(aP, bG, gw, (VTM > NWG ? VTM - 1 - gw : -1), von, vzz_pre, vsel2);
-      else
+      if constexpr (SEL) {
+        auto vu = [&](auto w) {
+          constexpr int WI = decltype(w)::value;
+          ggemm_sel2<N + NZ, W - 1, 2 * M, XB, 2 * XB, false, XB, WI, (VTM > NWG ? VTM - 1 - WI : -1)>(
+              aP, bG, von, vzz_pre, vsel2);
+        };
+        warp_dispatch8(gw, vu);
+      } else
         ggemm_f<N + NZ, W - 1, 2 * M, NWG>(aP, bG, gw, vupd);
     } else if constexpr (SEL) {
-      ggemm_sel2<N + NZ, W - 1, M, XB, 2 * XB, false, XB>([&](int i, int k) { return P[k * LDW + i]; },
-                                                         [&](int k, int c) { return G[k * LDW + c]; }, gw,
-                                                         (VTM > NWG ? VTM - 1 - gw : -1), von, vzz_pre, vsel2);
+      auto vu = [&](auto w) {
+        constexpr int WI = decltype(w)::value;
+        ggemm_sel2<N + NZ, W - 1, M, XB, 2 * XB, false, XB, WI, (VTM > NWG ? VTM - 1 - WI : -1)>(
+            [&](int i, int k) { return P[k * LDW + i]; }, [&](int k, int c) { return G[k * LDW + c]; }, von,
+            vzz_pre, vsel2);
+      };
+      warp_dispatch8(gw, vu);
+      PLQ_PHASE(13);   // value-update k-loops (warp 0's bands)
     } else {
       ggemm<N + NZ, W - 1, M, true, LDW, LDW, NWG>(P, G, gw, vupd);
     }

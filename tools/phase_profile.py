@@ -20,7 +20,8 @@ sys.path.insert(0, ROOT)
 
 NAMES = ["copy wait", "f1 column", "GEMM1", "GEMM2", "tail (QR)", "Cholesky solve", "policy stores",
          "value update", "stage end / prologue", "Cholesky factor (+fused fwd solve)",
-         "tail: norms + N = Hx F", "tail: QR", "-", "-", "-", "-"]
+         "tail: norms + N = Hx F", "tail: QR (n=64: + Cholesky trailing tiles)", "GEMM2 k-loops (warp 0)",
+         "value-update k-loops (warp 0)", "GEMM1 k-loops (warp 0)", "Cholesky diag factor + panel (n=64)"]
 
 
 def main():
