@@ -718,8 +718,11 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         static_assert(M * M >= 256 + NWG * 64, "TAU slot too small for the blocked solve");
         // Cholesky with the forward solve fused in: G <- L^{-1} (-P), block
         // row k in step k (no copy / negation passes)
-        if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy, nullptr, G, W, LDW,
-                         tau + 256, P, -1.0)) {
+        // (look-ahead variant: the next diagonal block is factored by warp 0
+        // during the trailing phase; L_kk staged at tau + 768)
+        static_assert(M * M >= 256 + NWG * 64 + 72, "TAU slot too small for the look-ahead Cholesky");
+        if (!gchol8_la<NWG>(Muu, M, LDM, tau, tau + 256 + NWG * 64, reinterpret_cast<int*>(sm + S::FLAG), gt, sy, G,
+                            W, LDW, tau + 256, P, -1.0)) {
           status = 1 + s;
           if (s > 0) {
             mbar_wait(bar, phase);
