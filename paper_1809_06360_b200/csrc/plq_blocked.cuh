@@ -176,168 +176,6 @@ __device__ __forceinline__ bool gchol8(double* A, int m, int lda, double* Linv, 
   return true;
 }
 
-// gchol8 with look-ahead (same results bit for bit, same outputs: L below
-// the diagonal blocks of A, the block inverses in Linv, the fused forward
-// solve X <- L^{-1} (xscale * Xsrc); the diagonal blocks of A untouched).
-// In gchol8 the next step's 8 x 8 diagonal factorization (a dependent chain
-// of 8 reciprocal square roots) runs while every other warp waits at the
-// barrier.  Here warp 0 applies the last Schur update to the NEXT diagonal
-// block first and factors it right away -- inside the trailing phase, while
-// warps 1.. do the fused-solve and remaining Schur tiles -- and publishes
-// L_kk (Lbuf: 64 doubles + 8 reciprocal pivots) and L_kk^{-1} (Linv) for the
-// next step's panel solves.  Needs NWG >= 2.  `Lbuf`: 72 doubles.
-template <int NWG, class Sync>
-__device__ __forceinline__ bool gchol8_la(double* A, int m, int lda, double* Linv, double* Lbuf, int* flag, int gt,
-                                          Sync sync, double* X, int W, int ldx, double* wsc, const double* Xsrc,
-                                          double xscale) {
-  static_assert(NWG >= 2, "look-ahead needs a second warp");
-  constexpr int NT = NWG * 32;
-  const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, q = lane & 3;
-  // warp 0: factor the diagonal block at k0 (after its last Schur update):
-  // every lane redundantly in registers (ragged block padded with I), lanes
-  // 0..7 solve unit rows -> the columns of L_kk^{-1}
-  auto factor_diag = [&](int k0) {
-    const int rb = min(8, m - k0);
-    double L[8][8], ri[8];
-    bool ok = true;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-#pragma unroll
-      for (int i = j; i < 8; ++i) {
-        double v = (i < rb && j < rb) ? A[(k0 + i) * lda + k0 + j] : (i == j ? 1.0 : 0.0);
-#pragma unroll
-        for (int c = 0; c < j; ++c) v -= L[i][c] * L[j][c];
-        if (i == j) {
-          ok = ok && (v > 0.0);
-          const double vv = v > 0.0 ? v : 1.0;
-          const double rs = rsqrt(vv);
-          L[j][j] = vv * rs;
-          ri[j] = rs;
-        } else {
-          L[i][j] = v * ri[j];
-        }
-      }
-    }
-    if (lane < 8) {
-      const int u = lane;
-      double a[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        double v = (j == u) ? 1.0 : 0.0;
-#pragma unroll
-        for (int c = 0; c < j; ++c) v -= L[j][c] * a[c];
-        a[j] = v * ri[j];
-      }
-      double* Li = Linv + (k0 >> 3) * 64;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) Li[i * 8 + u] = a[i];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {   // row u of L (constant register indices)
-        if (i == u) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) Lbuf[i * 8 + j] = (j <= i) ? L[i][j] : 0.0;
-          Lbuf[64 + i] = ri[i];
-        }
-      }
-    }
-    if (lane == 0) *flag = ok ? 0 : 1;
-  };
-  if (gw == 0) factor_diag(0);
-  sync();
-  for (int k0 = 0; k0 < m; k0 += 8) {
-    if (*flag) {
-      sync();
-      return false;
-    }
-    const int rb = min(8, m - k0);
-    const int below = m - k0 - rb;
-    // panel rows l = a L_kk^{-T} (forward substitution against Lbuf)
-    for (int t = gt; t < below; t += NT) {
-      double a[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) a[c] = c < rb ? A[(k0 + rb + t) * lda + k0 + c] : 0.0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        double v = a[j];
-#pragma unroll
-        for (int c = 0; c < j; ++c) v -= Lbuf[j * 8 + c] * a[c];
-        a[j] = v * Lbuf[64 + j];
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < rb) A[(k0 + rb + t) * lda + k0 + c] = a[c];
-    }
-    sync();
-    const int r0 = k0 + rb;
-    const int tt = (below + 7) >> 3;
-    const int nschur = tt * (tt + 1) / 2, nrhs = X != nullptr ? (W + 7) >> 3 : 0;
-    // Schur tile (ti, tj) of the trailing block: A[i][j] -= sum_c l_ic l_jc (lower part)
-    auto schur_tile = [&](int tile) {
-      int ti = 0;
-      while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
-      const int tj = tile - ti * (ti + 1) / 2;
-      const int i = r0 + ti * 8 + g, jb = r0 + tj * 8;
-      double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < 8; kk += 4) {
-        const int k = kk + q;
-        const double av = (i < m && k < rb) ? A[i * lda + k0 + k] : 0.0;
-        const double bv = (jb + g < m && k < rb) ? A[(jb + g) * lda + k0 + k] : 0.0;
-        dmma884(c0, c1, av, bv);
-      }
-      const int j0 = jb + 2 * q;
-      if (i < m) {
-        if (j0 < m && (ti != tj || j0 <= i)) A[i * lda + j0] -= c0;
-        if (j0 + 1 < m && (ti != tj || j0 + 1 <= i)) A[i * lda + j0 + 1] -= c1;
-      }
-    };
-    if (gw == 0) {
-      if (below > 0) {
-        schur_tile(0);   // the next diagonal block's last update ...
-        __syncwarp();
-        factor_diag(r0);   // ... and its factorization, off the other warps' critical path
-      }
-    } else {
-      for (int t = gw - 1; t < nrhs + nschur - 1; t += NWG - 1) {
-        if (t >= nrhs) {
-          schur_tile(t - nrhs + 1);
-          continue;
-        }
-        // X_k = Linv_kk (xscale Xsrc_k - sum_{c < k0} L[k][c] X_c)
-        double* ws = wsc + gw * 64;
-        const double* D = Linv + (k0 >> 3) * 64;
-        const int j0 = t * 8;
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll 4
-        for (int kk = 0; kk < k0; kk += 4) {
-          const int k = kk + q;
-          const double av = (g < rb) ? A[(k0 + g) * lda + k] : 0.0;
-          const double bv = (j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
-          dmma884(c0, c1, av, bv);
-        }
-        const int j = j0 + 2 * q;
-        const double* Xs = Xsrc != nullptr ? Xsrc : X;
-        ws[g * 8 + 2 * q] = (g < rb && j < W) ? xscale * Xs[(k0 + g) * ldx + j] - c0 : 0.0;
-        ws[g * 8 + 2 * q + 1] = (g < rb && j + 1 < W) ? xscale * Xs[(k0 + g) * ldx + j + 1] - c1 : 0.0;
-        __syncwarp();
-        double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 8; kk += 4) {
-          const int k = kk + q;
-          dmma884(d0, d1, D[g * 8 + k], ws[k * 8 + g]);
-        }
-        if (g < rb) {
-          if (j < W) X[(k0 + g) * ldx + j] = d0;
-          if (j + 1 < W) X[(k0 + g) * ldx + j + 1] = d1;
-        }
-        __syncwarp();
-      }
-    }
-    sync();
-  }
-  return true;
-}
-
 // Inverses of the 8 x 8 diagonal blocks of an upper-triangular R (m x m,
 // diagonal taken from rdiag): block kb at Rinv + 64 kb (row-major, upper).
 // Thread (kb, u) back-substitutes the unit column e_u.
