@@ -520,31 +520,73 @@ __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X
       }
       // Y = V' C (8 x 8, K = rows): V'(i, l) = v_i(l)
       double y0 = 0.0, y1 = 0.0;
+      if constexpr (RS > 0 && RS <= 2) {
+        // rows <= 64: every C load of the tile issued up front (C may live in
+        // L2 scratch: one latency exposure instead of one per 4 k-steps)
+        constexpr int KS = 8 * RS;
+        double avs[KS], bvs[KS];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int l = 4 * ks + q;
+          avs[ks] = (l < rows && g < pb) ? ((l == g) ? 1.0 : (l > g ? A[(p0 + l) * lda + p0 + g] : 0.0)) : 0.0;
+          bvs[ks] = (l < rows && g < ncol) ? C[l * ldc + g] : 0.0;
+        }
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) dmma884(y0, y1, avs[ks], bvs[ks]);
+      } else {
 #pragma unroll 4
-      for (int kk = 0; kk < rows; kk += 4) {
-        const int l = kk + q;
-        double av = 0.0;
-        if (l < rows && g < pb) av = (l == g) ? 1.0 : (l > g ? A[(p0 + l) * lda + p0 + g] : 0.0);
-        const double bv = (l < rows && g < ncol) ? C[l * ldc + g] : 0.0;
-        dmma884(y0, y1, av, bv);
+        for (int kk = 0; kk < rows; kk += 4) {
+          const int l = kk + q;
+          double av = 0.0;
+          if (l < rows && g < pb) av = (l == g) ? 1.0 : (l > g ? A[(p0 + l) * lda + p0 + g] : 0.0);
+          const double bv = (l < rows && g < ncol) ? C[l * ldc + g] : 0.0;
+          dmma884(y0, y1, av, bv);
+        }
       }
       ws[g * 8 + 2 * q] = y0;
       ws[g * 8 + 2 * q + 1] = y1;
       __syncwarp();
       // C -= VT Y, 8-row bands
-#pragma unroll 2
-      for (int b0 = 0; b0 < rows; b0 += 8) {
-        double c0 = 0.0, c1 = 0.0;
+      if constexpr (RS > 0 && RS <= 2) {
+        constexpr int NB = 4 * RS;   // 8-row bands of <= 32 RS rows
+        const int j = 2 * q;
+        double cur[NB][2];
 #pragma unroll
-        for (int kk = 0; kk < 8; kk += 4) {
-          const int k = kk + q;
-          const double av = (b0 + g < rows) ? VT[(b0 + g) * 8 + k] : 0.0;
-          dmma884(c0, c1, av, ws[k * 8 + g]);
+        for (int bb = 0; bb < NB; ++bb) {   // loads first (L2 latency once)
+          const int i = bb * 8 + g;
+          cur[bb][0] = (i < rows && j < ncol) ? C[i * ldc + j] : 0.0;
+          cur[bb][1] = (i < rows && j + 1 < ncol) ? C[i * ldc + j + 1] : 0.0;
         }
-        const int i = b0 + g, j = 2 * q;
-        if (i < rows) {
-          if (j < ncol) C[i * ldc + j] -= c0;
-          if (j + 1 < ncol) C[i * ldc + j + 1] -= c1;
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 8; kk += 4) {
+            const int k = kk + q;
+            const double av = (bb * 8 + g < rows) ? VT[(bb * 8 + g) * 8 + k] : 0.0;
+            dmma884(c0, c1, av, ws[k * 8 + g]);
+          }
+          const int i = bb * 8 + g;
+          if (i < rows) {
+            if (j < ncol) C[i * ldc + j] = cur[bb][0] - c0;
+            if (j + 1 < ncol) C[i * ldc + j + 1] = cur[bb][1] - c1;
+          }
+        }
+      } else {
+#pragma unroll 2
+        for (int b0 = 0; b0 < rows; b0 += 8) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 8; kk += 4) {
+            const int k = kk + q;
+            const double av = (b0 + g < rows) ? VT[(b0 + g) * 8 + k] : 0.0;
+            dmma884(c0, c1, av, ws[k * 8 + g]);
+          }
+          const int i = b0 + g, j = 2 * q;
+          if (i < rows) {
+            if (j < ncol) C[i * ldc + j] -= c0;
+            if (j + 1 < ncol) C[i * ldc + j + 1] -= c1;
+          }
         }
       }
       __syncwarp();
