@@ -716,21 +716,13 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         auto sy = [&] { gsync<NWG>(grp); };
 #endif
         static_assert(M * M >= 256 + NWG * 64, "TAU slot too small for the blocked solve");
-        static_assert(M == 32 && NWG == 8, "explicit-inverse gains are laid out for m = 32 on 8 warps");
-        // G = -Muu^{-1} P through the explicit inverse: the blocked Cholesky
-        // solves the identity (L^{-1}: 4 column tiles per block step instead
-        // of P's 17), then Muu^{-1} = L^{-T} L^{-1} and G = -Muu^{-1} P are
-        // two fully parallel DMMA products -- no block-sequential forward /
-        // backward solves of the 2n+1 gain columns.  (A look-ahead Cholesky
-        // -- warp 0 factoring the next diagonal block inside the trailing
-        // phase -- measured slower: register spills.)
-        constexpr int LDI = pad_ld(M);
-        double* Li = VF + M * LDW;   // L^{-1}: VF's rows past G (G overlays VF)
-        static_assert(M * LDW + M * LDI <= N * LDF, "VF region too small for L^{-1}");
-        for (int idx = gt; idx < M * M; idx += NT) Li[(idx / M) * LDI + idx % M] = (idx / M == idx % M) ? 1.0 : 0.0;
-        gsync<NWG>(grp);
-        if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy, nullptr, Li, M, LDI,
-                         tau + 256)) {
+        // Cholesky with the forward solve fused in: G <- L^{-1} (-P), block
+        // row k in step k (no copy / negation passes)
+        // (a look-ahead variant -- warp 0 factoring the next diagonal block
+        // inside the trailing phase -- measured slower: 45.4 vs 44.2 ms per
+        // B = 148 wave, warp 0's extra register pressure spills)
+        if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy, nullptr, G, W, LDW,
+                         tau + 256, P, -1.0)) {
           status = 1 + s;
           if (s > 0) {
             mbar_wait(bar, phase);
@@ -738,53 +730,8 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
           }
           break;
         }
-        PLQ_PHASE(9);   // Cholesky + L^{-1}
-        {
-          const int g8 = lane >> 2, q4 = lane & 3;
-          // Muu^{-1} = L^{-T} L^{-1} into Muu (the factor is dead): tiles gw, gw + 8
-          const int ia = (gw >> 2) * 8 + g8, ja = (gw & 3) * 8, ib = ((gw + 8) >> 2) * 8 + g8, jb = ((gw + 8) & 3) * 8;
-          double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-#pragma unroll
-          for (int ks = 0; ks < M / 4; ++ks) {
-            const int k = 4 * ks + q4;
-            dmma884(c0[0], c0[1], Li[k * LDI + ia], Li[k * LDI + ja + g8]);
-            dmma884(c1[0], c1[1], Li[k * LDI + ib], Li[k * LDI + jb + g8]);
-          }
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            Muu[ia * LDM + ja + 2 * q4 + e] = c0[e];
-            Muu[ib * LDM + jb + 2 * q4 + e] = c1[e];
-          }
-        }
-        gsync<NWG>(grp);
-        {
-          // G = -Muu^{-1} P: warp gw takes row band gw & 3 and half of the 17
-          // column tiles, all in one k-loop
-          const int g8 = lane >> 2, q4 = lane & 3;
-          constexpr int TH = ((W + 7) / 8 + 1) / 2;
-          const int i = (gw & 3) * 8 + g8, tn0 = (gw >> 2) * TH;
-          double acc[TH][2];
-#pragma unroll
-          for (int t = 0; t < TH; ++t) acc[t][0] = acc[t][1] = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < M / 4; ++ks) {
-            const int k = 4 * ks + q4;
-            const double a = Muu[i * LDM + k];
-#pragma unroll
-            for (int t = 0; t < TH; ++t) {
-              const int j = (tn0 + t) * 8 + g8;
-              dmma884(acc[t][0], acc[t][1], a, j < W ? P[k * LDW + j] : 0.0);
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < TH; ++t)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int j = (tn0 + t) * 8 + 2 * q4 + e;
-              if (j < W) G[i * LDW + j] = -acc[t][e];
-            }
-        }
-        gsync<NWG>(grp);
+        PLQ_PHASE(9);   // Cholesky + fused forward solve
+        gtrsm8<1, NWG>(Muu, M, LDM, tau, G, W, LDW, tau + 256, gt, sy);   // G = -Muu^{-1} P
       } else {
       double Lr[M][M], id[M];
       int fail = 0;
