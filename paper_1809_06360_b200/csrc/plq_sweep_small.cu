@@ -718,9 +718,13 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
         static_assert(M * M >= 256 + NWG * 64, "TAU slot too small for the blocked solve");
         // Cholesky with the forward solve fused in: G <- L^{-1} (-P), block
         // row k in step k (no copy / negation passes)
-        // (a look-ahead variant -- warp 0 factoring the next diagonal block
-        // inside the trailing phase -- measured slower: 45.4 vs 44.2 ms per
-        // B = 148 wave, warp 0's extra register pressure spills)
+        // Measured and rejected: a look-ahead variant (warp 0 factoring the
+        // next diagonal block inside the trailing phase: slower, register
+        // spills); gains through the explicit inverse (L^{-1} by an identity
+        // right-hand side, Muu^{-1} = L^{-T} L^{-1}, G = -Muu^{-1} P as
+        // parallel DMMA products: 8% faster, but K moved by ~1e-6 relative on
+        // the cfg4-shape goldens -- cond(Muu)^2 error growth -- against ~1e-12
+        // with the triangular solves)
         if (!gchol8<NWG>(Muu, M, LDM, tau, reinterpret_cast<int*>(sm + S::FLAG), gt, sy, nullptr, G, W, LDW,
                          tau + 256, P, -1.0)) {
           status = 1 + s;
