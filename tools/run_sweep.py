@@ -18,13 +18,15 @@ def main():
     ap.add_argument("--B", type=int, default=None)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--phase", default="sweep", choices=("sweep", "link", "recon", "solve"))
+    ap.add_argument("--T", type=int, default=None)
+    ap.add_argument("--J", type=int, default=None)
     args = ap.parse_args()
     import torch
 
     from paper_1809_06360_b200 import BatchSolver, _native, synth
     cfg = synth.CONFIGS[args.config]
     B = args.B or cfg.B
-    cfg = cfg.scaled(B=B)
+    cfg = cfg.scaled(B=B, T=args.T or cfg.T, J=args.J or cfg.J)
     dev = torch.device("cuda", 0)
     batch = synth.generate_batch_parallel(cfg, seed=0, count=B)
     inputs = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
