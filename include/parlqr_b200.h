@@ -60,7 +60,9 @@ typedef struct plq_problem {
   int32_t T, n, m, J;        /* horizon, state dim, control dim, segments (1 <= J <= T) */
   int32_t max_seg_len;       /* max(split_times[j+1]-split_times[j]) */
   const int32_t* split_times;/* J+1 increasing stage indices, 0 .. T (Partition.split_times) */
-  const double* Qxx;         /* (B,T,n,n) symmetric */
+  const double* Qxx;         /* (B,T,n,n) symmetric -- PRECONDITION: Qxx, Quu, QxxT must be exactly
+                                symmetric, as the reference's constructors make them (problem.py:106-116);
+                                some kernels read one triangle only.  The Python layer symmetrizes. */
   const double* Qux;         /* (B,T,m,n) */
   const double* Quu;         /* (B,T,m,m) symmetric */
   const double* qx1;         /* (B,T,n) */

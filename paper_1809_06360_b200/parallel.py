@@ -355,11 +355,36 @@ def _to_device(arrays, device, torch):
     return out
 
 
+def _symmetrize_blocks(inputs, torch, chunk=1 << 24):
+    """The reference symmetrizes ``Qxx`` / ``Quu`` when a problem is built
+    (problem.py:106-116, 129-133); raw stacked arrays skip those constructors,
+    and the kernels read only one triangle of the symmetric blocks on some
+    paths.  Blocks that are already symmetric (the usual case) are left
+    untouched and unallocated; others are replaced by ``0.5 (Q + Q')``."""
+    for f in ("Qxx", "Quu", "QxxT"):
+        t = inputs[f]
+        d = t.shape[-1]
+        flat = t.reshape(-1, d, d)
+        step = max(1, chunk // (d * d))
+        fixed = None
+        for i in range(0, flat.shape[0], step):
+            blk = flat[i:i + step]
+            if not torch.equal(blk, blk.transpose(1, 2)):
+                if fixed is None:
+                    fixed = flat.clone()
+                fixed[i:i + step] = 0.5 * (blk + blk.transpose(1, 2))
+        if fixed is not None:
+            inputs[f] = fixed.reshape(t.shape)
+    return inputs
+
+
 def solve_parallel_batch(arrays, J=None, partition=None, tolerances=DEFAULT_TOLERANCES, device=None,
-                         keep_unfolded=False, check=True):
+                         keep_unfolded=False, check=True, symmetrize=True):
     """Solve ``B`` stacked problems (dict of ``(B, T, ...)`` arrays or
     tensors).  Returns the :class:`BatchSolver` whose ``out`` dict holds the
-    device results."""
+    device results.  ``symmetrize`` applies the reference constructors'
+    ``0.5 (Q + Q')`` to unsymmetric quadratic blocks (a C-ABI caller must
+    pass symmetric blocks, include/parlqr_b200.h)."""
     torch = _torch()
     B, T, n = (int(s) for s in arrays["qx1"].shape)
     m = int(arrays["qu1"].shape[2])
@@ -367,6 +392,8 @@ def solve_parallel_batch(arrays, J=None, partition=None, tolerances=DEFAULT_TOLE
                          keep_unfolded=keep_unfolded)
     inputs = _to_device(arrays, solver.device, torch)
     solver.check_inputs(inputs)
+    if symmetrize:
+        inputs = _symmetrize_blocks(inputs, torch)
     with torch.cuda.device(solver.device):
         solver.run(inputs)
     if check:

@@ -382,3 +382,22 @@ def test_host_entry_solves_degenerate_partitions():
             assert np.array_equal(h["feas_rows"][0][:nd], o["feas_rows"][:-1])
             done += 1
     assert done >= 3
+
+
+@pytest.mark.parametrize("cfg_id,T,J", [(4, 64, 2), (1, 64, 8)])
+def test_unsymmetric_quadratic_blocks_are_symmetrized(cfg_id, T, J):
+    """problem.py:106-116: the reference symmetrizes Qxx / Quu on construction.
+    The batch layer does the same for raw stacked arrays, so the result does not
+    depend on which triangle a kernel path reads (n = 64 reads the lower one)."""
+    from paper_1809_06360_b200 import synth
+    cfg = synth.CONFIGS[cfg_id].scaled(B=2, T=T, J=J)
+    batch = synth.generate_batch(cfg, seed=3, count=2)
+    rng = np.random.default_rng(0)
+    skew = {f: 1e-3 * rng.standard_normal(batch[f].shape) for f in ("Qxx", "Quu", "QxxT")}
+    bad = dict(batch)
+    for f, s in skew.items():
+        bad[f] = batch[f] + (s - np.swapaxes(s, -1, -2))      # same symmetric part
+    g0, _ = _gpu_batch(batch, J=J)
+    g1, _ = _gpu_batch(bad, J=J)
+    for key in ("K", "k", "x", "u", "lam", "objective"):
+        assert rel_err(g1[key], g0[key]) <= 1e-6, key      # 1e-3 skew ignored; rounding-level input change only
