@@ -162,6 +162,33 @@ int plq_boundary_segments(const plq_problem_t* problem, const plq_outputs_t* out
 int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const double* partials, void* workspace,
                  size_t workspace_bytes, void* stream);
 
+/* Horizon-sharded solve across the ranks of an NCCL communicator (one process
+ * per GPU): the five phases above with their three exchanges issued by the
+ * library on `stream` -- no host synchronization, no allocation.  Replaces the
+ * reference's worker pool over segments (_run_tasks, parallel.py:168-207,
+ * 446-449) for horizons too long for one GPU's latency budget (cfg2, cfg3).
+ *   * rank r sweeps / reconstructs the balanced contiguous segment range
+ *     [r*(J/nranks) + min(r, J%nranks), ...) (remainder to the early ranks);
+ *     it reads only its own segments' stages, so `problem`'s stage arrays may
+ *     hold just that window (pointers shifted back by the window's first
+ *     stage); QxxT, qx1T, x_init are replicated.
+ *   * exchanges (in place, on the full-size output arrays every rank holds):
+ *     vf0 + status (+ feas, feas_rows when given) rows after the sweeps;
+ *     mu_left / lambda_right rows after the reconstruction; the (B,J,3)
+ *     partials before the fixed-order reduction.  Equal shards of one problem
+ *     travel as one in-place ncclAllGather per array, anything else as grouped
+ *     in-place ncclBroadcast calls.  The link solve is replicated, so links,
+ *     objective, kkt_inf, link_mismatch, status are bitwise identical on every
+ *     rank and identical for any rank count.
+ *   * K, k, x, u, lam hold this rank's segments only (the caller gathers them
+ *     if it wants the whole trajectory in one place).
+ * `nccl_comm` is an ncclComm_t whose rank/size are `rank`/`nranks` (NULL is
+ * allowed for nranks == 1: the phases run without NCCL).  NCCL is bound at run
+ * time with dlopen("libnccl.so.2") (override: PLQ_NCCL_LIB); this library has
+ * no link-time NCCL dependency. */
+int plq_solve_parallel_sharded(const plq_problem_t* problem, const plq_outputs_t* out, void* workspace,
+                               size_t workspace_bytes, void* nccl_comm, int32_t rank, int32_t nranks, void* stream);
+
 /* Device outputs of the smoothing pass (parlqr.parallel.smooth,
  * parallel.py:567-633): the smoothed LqrSolution's policies, trajectory and
  * diagnostics.  Its lambdas are the parent's (unchanged). */

@@ -25,7 +25,7 @@ EXPORTS = (
     "plq_host_arena_bytes", "plq_solve_parallel_host", "plq_sweep_segments",
     "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
     "plq_finalize", "plq_last_launch_count", "plq_smooth", "plq_endpoint_workspace_bytes",
-    "plq_endpoint_affine", "plq_endpoint_evaluate",
+    "plq_endpoint_affine", "plq_endpoint_evaluate", "plq_solve_parallel_sharded",
 )
 
 _vp = ctypes.c_void_p
@@ -108,7 +108,8 @@ def lib():
     L.plq_endpoint_workspace_bytes.argtypes = [P]
     L.plq_endpoint_affine.argtypes = [P, EO, _vp, ctypes.c_size_t, _vp]
     L.plq_endpoint_evaluate.argtypes = [P, EO, ctypes.POINTER(PlqEndpointPoint), _vp, ctypes.c_size_t, _vp]
-    for name in ("plq_solve_parallel", "plq_solve_parallel_host", "plq_sweep_segments",
+    L.plq_solve_parallel_sharded.argtypes = [P, O, _vp, ctypes.c_size_t, _vp, ctypes.c_int32, ctypes.c_int32, _vp]
+    for name in ("plq_solve_parallel", "plq_solve_parallel_host", "plq_sweep_segments", "plq_solve_parallel_sharded",
                  "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
                  "plq_finalize", "plq_smooth", "plq_endpoint_affine", "plq_endpoint_evaluate"):
         getattr(L, name).restype = ctypes.c_int

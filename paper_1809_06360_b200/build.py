@@ -52,12 +52,19 @@ def build(force=False, verbose=False, profile=False):
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, src.replace(".cu", ".o")) for src in SOURCES]
     # translation units are independent: compile them concurrently
+    # (objects newer than their source and every header are kept unless forced)
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    hdrs.append(os.path.join(ROOT, "include", "parlqr_b200.h"))
+    hdr_t = max(os.path.getmtime(h) for h in hdrs)
+    todo = [(src, obj) for src, obj in zip(SOURCES, objs)
+            if force or not os.path.exists(obj)
+            or os.path.getmtime(obj) <= max(hdr_t, os.path.getmtime(os.path.join(CSRC, src)))]
     procs = [subprocess.Popen([nvcc(), *ARCH, *flags, "-c", os.path.join(CSRC, src), "-o", obj],
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
-             for src, obj in zip(SOURCES, objs)]
+             for src, obj in todo]
     log = []
     failed = []
-    for src, p in zip(SOURCES, procs):
+    for (src, _), p in zip(todo, procs):
         out, _ = p.communicate()
         log.append(out)
         if p.returncode:
@@ -65,7 +72,7 @@ def build(force=False, verbose=False, profile=False):
     if failed:
         raise RuntimeError("\n".join(failed))
     tmp = lib_path + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

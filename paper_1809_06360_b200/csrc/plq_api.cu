@@ -1,5 +1,6 @@
 // C-ABI layer (include/parlqr_b200.h): argument checks, workspace carving,
 // and the stream-ordered phase sequence of one partitioned solve.
+#include <dlfcn.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -455,6 +456,158 @@ int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const d
   if (rc) return rc;
   return phase_finalize(problem, out, c, partials);
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// horizon-sharded solve over an NCCL communicator
+
+namespace {
+
+// NCCL is bound at run time from the library the host process already uses
+// (torch ships libnccl.so.2), so loading this library never needs NCCL.
+struct NcclApi {
+  void* h = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*Broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool ok = false;
+};
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8;   // ncclDataType_t (nccl.h)
+
+NcclApi& nccl_api() {
+  static NcclApi a = [] {
+    NcclApi x;
+    const char* names[] = {getenv("PLQ_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      if (!nm) continue;
+      if ((x.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    }
+    if (!x.h) return x;
+    x.GroupStart = reinterpret_cast<int (*)()>(dlsym(x.h, "ncclGroupStart"));
+    x.GroupEnd = reinterpret_cast<int (*)()>(dlsym(x.h, "ncclGroupEnd"));
+    x.Broadcast = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(x.h, "ncclBroadcast"));
+    x.AllGather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
+        dlsym(x.h, "ncclAllGather"));
+    x.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(x.h, "ncclGetErrorString"));
+    x.ok = x.GroupStart && x.GroupEnd && x.Broadcast && x.AllGather;
+    return x;
+  }();
+  return a;
+}
+
+inline void shard_range(int J, int nranks, int r, int* lo, int* hi) {
+  const int base = J / nranks, extra = J % nranks;
+  *lo = r * base + (r < extra ? r : extra);
+  *hi = *lo + base + (r < extra ? 1 : 0);
+}
+
+// One in-place exchange of per-segment rows: buffer (B, Jrows, width) of
+// `dtype`, rank r owning rows [lo_r + shift_lo, hi_r + shift_hi) clipped to
+// [0, Jrows).  Equal contiguous shards of a single problem go as one in-place
+// all-gather; everything else as grouped in-place broadcasts (one per owner
+// and problem), which NCCL aggregates into one launch.
+struct RowXfer {
+  void* base;
+  int64_t Jrows, width;   // rows per problem, elements per row
+  int dtype, elem;        // NCCL type, bytes per element
+  int shift;              // row index = segment index + shift (lambda_right rows: -1)
+  int seg_lo_min, seg_hi_max;   // owned segments are clipped to [seg_lo_min, seg_hi_max)
+};
+
+int exchange_rows(const NcclApi& N, void* comm, int J, int nranks, int rank, int64_t B, const RowXfer* xs, int nx,
+                  cudaStream_t s) {
+  int rc = 0;
+  const bool even = (J % nranks == 0) && B == 1;
+  if ((rc = N.GroupStart())) return rc;
+  for (int i = 0; i < nx && !rc; ++i) {
+    const RowXfer& x = xs[i];
+    const bool whole = even && x.shift == 0 && x.seg_lo_min == 0 && x.seg_hi_max == J;
+    if (whole) {
+      const size_t cnt = (size_t)(J / nranks) * x.width;
+      char* b = static_cast<char*>(x.base);
+      rc = N.AllGather(b + (size_t)rank * cnt * x.elem, b, cnt, x.dtype, comm, s);
+      continue;
+    }
+    for (int r = 0; r < nranks && !rc; ++r) {
+      int lo, hi;
+      shard_range(J, nranks, r, &lo, &hi);
+      lo = lo < x.seg_lo_min ? x.seg_lo_min : lo;
+      hi = hi > x.seg_hi_max ? x.seg_hi_max : hi;
+      if (hi <= lo) continue;
+      for (int64_t b = 0; b < B && !rc; ++b) {
+        char* ptr = static_cast<char*>(x.base) + ((size_t)b * x.Jrows + (lo + x.shift)) * x.width * x.elem;
+        rc = N.Broadcast(ptr, ptr, (size_t)(hi - lo) * x.width, x.dtype, r, comm, s);
+      }
+    }
+  }
+  const int rc2 = N.GroupEnd();
+  return rc ? rc : rc2;
+}
+
+}  // namespace
+
+extern "C" int plq_solve_parallel_sharded(const plq_problem_t* problem, const plq_outputs_t* out, void* workspace,
+                                          size_t workspace_bytes, void* nccl_comm, int32_t rank, int32_t nranks,
+                                          void* stream) {
+  g_launches = 0;
+  Ctx c;
+  int rc = setup(problem, out, workspace, workspace_bytes, stream, &c);
+  if (rc) return rc;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PLQ_ERR_ARG, "bad rank / nranks");
+  if (nranks > 1 && !nccl_comm) return fail(PLQ_ERR_ARG, "null communicator with nranks > 1");
+  const bool feas = out->feas && out->feas_rows && out->feas_residual;
+  if (!feas && (out->feas || out->feas_rows || out->feas_residual))
+    return fail(PLQ_ERR_ARG, "feas, feas_rows and feas_residual go together");
+  const NcclApi* N = nullptr;
+  if (nccl_comm) {
+    N = &nccl_api();
+    if (!N->ok) return fail(PLQ_ERR_ARG, "NCCL (libnccl.so.2) could not be loaded; set PLQ_NCCL_LIB");
+  }
+  auto nccl_fail = [&](int e, const char* where) {
+    snprintf(g_err, sizeof(g_err), "%s: NCCL error %d (%s)", where, e,
+             N && N->GetErrorString ? N->GetErrorString(e) : "?");
+    return PLQ_ERR_CUDA;
+  };
+  const int J = problem->J, n = problem->n;
+  const int64_t B = problem->B;
+  int j0, j1;
+  shard_range(J, nranks, rank, &j0, &j1);
+  double* part = c.ws + c.P.off_part;
+  // 1. local sweeps; exchange of the segment-start value blocks, status and feasibility rows
+  if (j1 > j0 && (rc = phase_sweep(problem, out, c, j0, j1))) return rc;
+  if (N) {
+    RowXfer xs[4] = {{out->vf0, J, (int64_t)3 * n * n + 2 * n, kNcclFloat64, 8, 0, 0, J},
+                     {out->status, J, 1, kNcclInt32, 4, 0, 0, J},
+                     {out->feas, J, (int64_t)n * (2 * n + 1), kNcclFloat64, 8, 0, 0, J},
+                     {out->feas_rows, J, 1, kNcclInt32, 4, 0, 0, J}};
+    const int e = exchange_rows(*N, nccl_comm, J, nranks, rank, B, xs, feas ? 4 : 2, c.s);
+    if (e) return nccl_fail(e, "value-block exchange");
+  }
+  // 2. replicated coupling solve (bitwise identical on every rank)
+  if ((rc = phase_link(problem, out, c))) return rc;
+  // 3. local reconstruction; exchange of the multiplier rows at the links
+  if (j1 > j0 && (rc = phase_recon(problem, out, c, j0, j1, part))) return rc;
+  if (N && J > 1) {
+    RowXfer xs[2] = {{out->mu_left, J - 1, n, kNcclFloat64, 8, 0, 0, J - 1},
+                     {out->lambda_right, J - 1, n, kNcclFloat64, 8, -1, 1, J}};
+    const int e = exchange_rows(*N, nccl_comm, J, nranks, rank, B, xs, 2, c.s);
+    if (e) return nccl_fail(e, "multiplier-row exchange");
+  }
+  // 4. link-stage KKT rows; exchange of the per-segment partials; fixed-order reduction
+  if (j1 > j0 && (rc = phase_boundary(problem, out, c, j0, j1, part))) return rc;
+  if (N) {
+    RowXfer xs[1] = {{part, J, 3, kNcclFloat64, 8, 0, 0, J}};
+    const int e = exchange_rows(*N, nccl_comm, J, nranks, rank, B, xs, 1, c.s);
+    if (e) return nccl_fail(e, "partials exchange");
+  }
+  return phase_finalize(problem, out, c, part);
+}
+
+extern "C" {
 
 // ---------------------------------------------------------------------------
 // host-buffer entry

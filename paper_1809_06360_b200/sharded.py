@@ -200,6 +200,82 @@ class DeviceBackend:
         return {k: o[k] for k in ("objective", "kkt_inf", "link_mismatch", "link_residual", "links")}
 
 
+class NcclComm:
+    """An ``ncclComm_t`` of this process's own, for ``plq_solve_parallel_sharded``
+    (torch does not expose its communicators).  The 128-byte unique id is made
+    on rank 0 and broadcast through the given ``torch.distributed`` group (any
+    backend); every rank then calls ``ncclCommInitRank`` on its current CUDA
+    device.  The library is the one torch already loaded (``libnccl.so.2``)."""
+
+    def __init__(self, dist=None, group=None, rank=0, world=1):
+        import torch
+        name = None
+        for cand in ("libnccl.so.2", "libnccl.so"):
+            try:
+                self.nccl = ctypes.CDLL(cand)
+                name = cand
+                break
+            except OSError:
+                continue
+        if name is None:
+            raise RuntimeError("libnccl.so.2 not found (import torch with CUDA support first)")
+        if dist is not None:
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.rank, self.world = int(rank), int(world)
+
+        class UniqueId(ctypes.Structure):
+            _fields_ = [("internal", ctypes.c_char * 128)]
+
+        uid = UniqueId()
+        self.nccl.ncclGetErrorString.restype = ctypes.c_char_p
+        if self.rank == 0:
+            self._ok(self.nccl.ncclGetUniqueId(ctypes.byref(uid)), "ncclGetUniqueId")
+        if self.world > 1:
+            box = [bytes(uid.internal) if self.rank == 0 else None]
+            src = 0 if group is None else dist.get_global_rank(group, 0)
+            dist.broadcast_object_list(box, src=src, group=group)
+            ctypes.memmove(ctypes.byref(uid), box[0], 128)
+        self.comm = ctypes.c_void_p()
+        self.nccl.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, UniqueId, ctypes.c_int]
+        torch.cuda.current_stream().synchronize()
+        self._ok(self.nccl.ncclCommInitRank(ctypes.byref(self.comm), self.world, uid, self.rank), "ncclCommInitRank")
+
+    def _ok(self, rc, what):
+        if rc != 0:
+            raise RuntimeError(f"{what}: NCCL error {rc} ({self.nccl.ncclGetErrorString(rc).decode()})")
+
+    def close(self):
+        if getattr(self, "comm", None):
+            self.nccl.ncclCommDestroy.argtypes = [ctypes.c_void_p]
+            self.nccl.ncclCommDestroy(self.comm)
+            self.comm = None
+
+
+def solve_sharded_native(solver: BatchSolver, inputs, comm: NcclComm = None, t0=0, stream=None, check=True):
+    """One horizon-sharded solve through ``plq_solve_parallel_sharded``: the
+    library runs the phases and issues the NCCL exchanges itself on one stream
+    (no host synchronization, no temporaries).  ``inputs``: full stacked device
+    arrays, or this rank's stage window (``t0`` = its first stage, B = 1).
+    Degenerate partitions are supported (the feasibility rows travel with the
+    value blocks).  Returns the replicated scalar results; ``solver.out`` holds
+    this rank's segments of ``K, k, x, u, lam``."""
+    torch = solver.torch
+    solver.check_inputs(inputs, T_held=inputs["qx1"].shape[1])
+    prob = solver._problem_struct(inputs, t0=t0)
+    stream = torch.cuda.current_stream(solver.device) if stream is None else stream
+    rank, world = (comm.rank, comm.world) if comm is not None else (0, 1)
+    rc = solver.lib.plq_solve_parallel_sharded(
+        ctypes.byref(prob), ctypes.byref(solver._outs), ctypes.c_void_p(solver.workspace.data_ptr()),
+        solver.ws_bytes, comm.comm if comm is not None else None, rank, world,
+        ctypes.c_void_p(stream.cuda_stream))
+    _native.check(rc, "plq_solve_parallel_sharded")
+    solver.launches = int(solver.lib.plq_last_launch_count())
+    if check:
+        solver.raise_for_status()
+    o = solver.out
+    return {k: o[k] for k in ("objective", "kkt_inf", "link_mismatch", "link_residual", "links")}
+
+
 def stage_window(arrays, splits, j0, j1):
     """Host arrays of one problem (B = 1) cut to the stages of segments
     [j0, j1) -- what a rank of a horizon-sharded solve needs (its sweeps,
@@ -226,4 +302,4 @@ def sharded_solve_device(inputs, J=None, partition=None, dist=None, group=None, 
 
 
 __all__ = ["shard_range", "solve_sharded", "raise_sharded_status", "DeviceBackend", "stage_window",
-           "sharded_solve_device"]
+           "sharded_solve_device", "NcclComm", "solve_sharded_native"]

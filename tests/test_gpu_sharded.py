@@ -121,3 +121,179 @@ def test_two_ranks_windowed_inputs_equal_one_call_solve(world, cfg_id, T, J):
         for k in ("objective", "kkt_inf", "link_mismatch", "link_residual"):
             assert np.array_equal(o[k], ref[k]), k
         assert np.array_equal(o["links"], ref["links"])
+
+
+@pytest.mark.parametrize("cfg_id,T,J,count", [(2, 512, 16, 1), (1, 64, 8, 3), (4, 64, 4, 2), (0, 96, 6, 1)])
+def test_native_sharded_entry_equals_one_call_solve(cfg_id, T, J, count):
+    """plq_solve_parallel_sharded over a real (one-rank) NCCL communicator:
+    the in-place all-gather (B = 1, equal shards) and grouped-broadcast
+    (B > 1) exchanges run, and every output equals the one-call solve bit
+    for bit.  NULL communicator with nranks = 1 takes the same phases."""
+    import torch
+
+    from paper_1809_06360_b200 import BatchSolver, solve_parallel_batch, synth
+    from paper_1809_06360_b200.sharded import NcclComm, solve_sharded_native
+    cfg = synth.CONFIGS[cfg_id].scaled(T=T, J=J)
+    batch = synth.generate_batch(cfg, seed=5, count=count)
+    ref = solve_parallel_batch(batch, J=J)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    inputs = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
+    comm = NcclComm()
+    try:
+        for c in (comm, None):
+            solver = BatchSolver(count, T, cfg.n, cfg.m, J=J, device=dev)
+            solve_sharded_native(solver, inputs, c)
+            torch.cuda.synchronize()
+            assert solver.launches == ref.launches
+            for k in ("K", "k", "x", "u", "lam", "links", "objective", "kkt_inf", "link_mismatch",
+                      "link_residual", "status"):
+                assert np.array_equal(solver.out[k].cpu().numpy(), ref.out[k].cpu().numpy()), k
+    finally:
+        comm.close()
+
+
+def test_native_sharded_entry_degenerate_partition():
+    """A partition with segments too short to reach arbitrary endpoints
+    (feasibility rows, parallel.py:320-384) through the sharded entry: the rows
+    travel with the value blocks and the constrained link solve is replicated."""
+    import torch
+
+    from paper_1809_06360_b200 import BatchSolver, Partition, solve_parallel_batch, synth
+    from paper_1809_06360_b200.sharded import NcclComm, solve_sharded_native
+    cfg = synth.CONFIGS[0].scaled(T=24, J=4)
+    batch = synth.generate_batch(cfg, seed=2, count=2)
+    part = Partition(4, (0, 2, 12, 14, 24))          # L = 2 stages of m = 4 controls < n = 12
+    ref = solve_parallel_batch(batch, partition=part)
+    assert int(ref.out["feas_rows"].sum()) > 0
+    dev = torch.device("cuda", 0)
+    inputs = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
+    comm = NcclComm()
+    try:
+        solver = BatchSolver(2, 24, cfg.n, cfg.m, partition=part, device=dev)
+        solve_sharded_native(solver, inputs, comm)
+        torch.cuda.synchronize()
+        for k in ("K", "k", "x", "u", "lam", "links", "objective", "kkt_inf", "feas_rows", "feas_residual"):
+            assert np.array_equal(solver.out[k].cpu().numpy(), ref.out[k].cpu().numpy()), k
+    finally:
+        comm.close()
+
+
+# ---------------------------------------------------------------------------
+# plq_solve_parallel_sharded across several ranks on ONE GPU: the library's
+# NCCL binding is pointed (PLQ_NCCL_LIB) at tests/nccl_host_shim.c, which
+# stages every collective through host shared memory between kernel launches.
+
+SHIM_CAP = 64 << 20
+
+
+def _build_shim(workdir):
+    import os
+    import subprocess
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "nccl_host_shim.c")
+    so = os.path.join(workdir, "libnccl_host_shim.so")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.run(["gcc", "-shared", "-fPIC", "-O1", f"-I{cuda}/include", src, "-o", so, f"-L{cuda}/lib64",
+                    f"-Wl,-rpath,{cuda}/lib64", "-lcudart", "-lpthread", "-lrt"], check=True)
+    return so
+
+
+class _ShimComm:
+    def __init__(self, so, name, rank, world):
+        import ctypes
+        self.lib = ctypes.CDLL(so)
+        self.lib.shim_attach.restype = ctypes.c_void_p
+        self.lib.shim_attach.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_size_t]
+        self.lib.shim_calls.restype = ctypes.c_ulonglong
+        self.lib.shim_calls.argtypes = [ctypes.c_void_p]
+        self.comm = ctypes.c_void_p(self.lib.shim_attach(name.encode(), rank, world, SHIM_CAP))
+        assert self.comm.value, "shim attach failed"
+        self.rank, self.world = rank, world
+
+    def calls(self):
+        return int(self.lib.shim_calls(self.comm))
+
+
+def _native_rank_worker(rank, world, so, name, case, outdir):
+    import os
+    os.environ["PLQ_NCCL_LIB"] = so          # read once, at the library's first sharded call
+    import torch
+
+    from paper_1809_06360_b200 import BatchSolver, Partition, synth
+    from paper_1809_06360_b200.sharded import shard_range, solve_sharded_native, stage_window
+    cfg_id, T, J, count, splits, windowed = case
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[cfg_id].scaled(T=T, J=J)
+    batch = synth.generate_batch(cfg, seed=5, count=count)
+    part = None if splits is None else Partition(J, tuple(splits))
+    solver = BatchSolver(count, T, cfg.n, cfg.m, J=J, partition=part, device=dev)
+    j0, j1 = shard_range(J, world, rank)
+    t0 = 0
+    if windowed:
+        batch, t0 = stage_window(batch, solver.partition.split_times, j0, j1)
+    inputs = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in batch.items()}
+    comm = _ShimComm(so, name, rank, world)
+    res = solve_sharded_native(solver, inputs, comm, t0=t0)
+    torch.cuda.synchronize()
+    st = solver.partition.split_times
+    lo, hi = int(st[j0]), int(st[j1])
+    o = solver.out
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), lo=lo, hi=hi, calls=comm.calls(),
+             status=o["status"].cpu().numpy(), feas_rows=o["feas_rows"].cpu().numpy(),
+             **{k: o[k][:, lo:hi].cpu().numpy() for k in ("K", "k", "x", "u", "lam")},
+             **{k: v.cpu().numpy() for k, v in res.items()})
+
+
+@pytest.mark.parametrize("world,case", [
+    (2, (2, 512, 16, 1, None, True)),                      # equal shards, B = 1: in-place all-gathers, stage windows
+    (4, (0, 96, 6, 1, None, True)),                        # unequal shards (2,2,1,1): grouped broadcasts
+    (2, (1, 64, 8, 3, None, False)),                       # B > 1: one broadcast per owner and problem
+    (3, (3, 64, 8, 1, None, True)),                        # n = 128 generic kernels, shards (3,3,2)
+    (2, (0, 24, 4, 2, (0, 2, 12, 14, 24), False)),         # degenerate partition: feasibility rows exchanged
+])
+def test_native_sharded_entry_multi_rank(world, case):
+    """Every rank's slice of K, k, x, u, lambda and the replicated links /
+    scalars / status equal the one-call solve bit for bit, for any rank count."""
+    import ctypes
+    import os
+    import tempfile
+
+    import torch.multiprocessing as mp
+
+    from paper_1809_06360_b200 import Partition, solve_parallel_batch, synth
+    cfg_id, T, J, count, splits, _ = case
+    cfg = synth.CONFIGS[cfg_id].scaled(T=T, J=J)
+    batch = synth.generate_batch(cfg, seed=5, count=count)
+    part = None if splits is None else Partition(J, tuple(splits))
+    ref = {k: v.cpu().numpy() for k, v in solve_parallel_batch(batch, J=J, partition=part).out.items()
+           if v is not None}
+    if splits is not None:
+        assert int(ref["feas_rows"].sum()) > 0
+    name = f"/plq_shim_{os.getpid()}_{world}_{cfg_id}"
+    with tempfile.TemporaryDirectory() as d:
+        so = _build_shim(d)
+        parent = ctypes.CDLL(so)
+        parent.shim_create.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_size_t]
+        assert parent.shim_create(name.encode(), world, SHIM_CAP) == 0
+        try:
+            ctx = mp.get_context("spawn")
+            procs = [ctx.Process(target=_native_rank_worker, args=(r, world, so, name, case, d)) for r in range(world)]
+            for p in procs:
+                p.start()
+            for p in procs:
+                p.join(240)
+            hung = [p for p in procs if p.is_alive()]
+            for p in hung:                       # a rank that died leaves its peers in the barrier
+                p.kill()
+            assert not hung and all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+            outs = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
+        finally:
+            parent.shim_destroy(name.encode())
+    for o in outs:
+        lo, hi = int(o["lo"]), int(o["hi"])
+        assert int(o["calls"]) > 0
+        for k in ("K", "k", "x", "u", "lam"):
+            assert np.array_equal(o[k], ref[k][:, lo:hi]), k
+        for k in ("objective", "kkt_inf", "link_mismatch", "link_residual", "links", "status", "feas_rows"):
+            assert np.array_equal(o[k], ref[k]), k
