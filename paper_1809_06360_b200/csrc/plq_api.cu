@@ -31,6 +31,14 @@ bool force_bcr() {
 bool use_seq_link(const plq_problem_t* p) {
   return !force_generic() && !force_bcr() && plq::link_seq_supported(p->n, p->J);
 }
+// one CTA per problem running the reference's sequential block Cholesky
+// (16 <= n <= 64): when the batch is at least as large as the chain is long,
+// or forced with PLQ_LINK=chain
+bool use_chain_link(const plq_problem_t* p) {
+  if (force_generic() || force_bcr() || !plq::link_chain_supported(p->n, p->J)) return false;
+  const char* e = getenv("PLQ_LINK");
+  return (e && e[0] == 'c') || plq::link_chain_preferred(p->B, p->J);
+}
 
 int fail(int code, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -98,8 +106,9 @@ Plan make_plan(const plq_problem_t* p) {
   off += up2(std::max((size_t)P.grid_max * P.lay.gmem_doubles,
                       (size_t)sms * 2 * plq::sweep_small_gscratch_doubles(p->n, p->m)));
   P.off_link = off;
-  off += up2(std::max(plq::link_workspace_doubles(B, p->J, p->n),
-                      use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0)));
+  off += up2(std::max({plq::link_workspace_doubles(B, p->J, p->n),
+                       use_seq_link(p) ? plq::link_seq_workspace_doubles(B, p->J, p->n) : size_t(0),
+                       use_chain_link(p) ? plq::link_chain_workspace_doubles(B, p->J, p->n) : size_t(0)}));
   P.off_ctr = off;
   off += 2;   // [0] dynamic segment queue, [1] rank-repair count
   P.off_rlist = off;
@@ -190,6 +199,10 @@ int phase_link(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c) {
   if (p->J < 2) return PLQ_OK;
   if (use_seq_link(p)) {
     if (plq::launch_link_seq(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s))
+      return cuda_fail("link launch");
+    nl = 1;
+  } else if (use_chain_link(p)) {
+    if (plq::launch_link_chain(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s))
       return cuda_fail("link launch");
     nl = 1;
   } else if (plq::launch_link_solve(*p, o->vf0, o->links, o->link_residual, o->status, c.ws + c.P.off_link, c.s,

@@ -205,6 +205,13 @@ size_t link_seq_workspace_doubles(int64_t B, int J, int n);
 int launch_link_seq(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
                     int32_t* status, double* ws, cudaStream_t s);
 
+// Link solve of a batch of short chains, one CTA per problem (plq_linkchain.cu).
+bool link_chain_supported(int n, int J);
+bool link_chain_preferred(int64_t B, int J);
+size_t link_chain_workspace_doubles(int64_t B, int J, int n);
+int launch_link_chain(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
+                      int32_t* status, double* ws, cudaStream_t s);
+
 // Link (coupling) solve by block cyclic reduction.
 size_t link_workspace_doubles(int64_t B, int J, int n);
 int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,

@@ -401,3 +401,51 @@ def test_unsymmetric_quadratic_blocks_are_symmetrized(cfg_id, T, J):
     g1, _ = _gpu_batch(bad, J=J)
     for key in ("K", "k", "x", "u", "lam", "objective"):
         assert rel_err(g1[key], g0[key]) <= 1e-6, key      # 1e-3 skew ignored; rounding-level input change only
+
+
+@pytest.mark.parametrize("n,m,T,J,B", [(64, 32, 128, 4, 5), (32, 8, 96, 6, 9), (20, 6, 60, 5, 8), (40, 10, 64, 4, 8)])
+def test_chain_link_solve_equals_cyclic_reduction(n, m, T, J, B, monkeypatch):
+    """The one-CTA-per-problem sequential block Cholesky of the link system
+    (plq_linkchain.cu, the reference's own recurrence endpoint.py:410-438) and
+    block cyclic reduction solve the same equations: links within 1e-9 of each
+    other (both are gated against the oracle by the parity tests), residuals
+    at rounding level, and a non-SPD pivot flags LinkSingular for that problem
+    only (parallel.py:267-271)."""
+    import ctypes
+
+    import torch
+
+    from paper_1809_06360_b200 import _native, synth
+    cfg = synth.Config(f"chain_n{n}", B, n, m, T, J, cross=0.3)
+    batch = synth.generate_batch(cfg, seed=11, count=B)
+    outs = {}
+    for mode in ("chain", "bcr"):
+        monkeypatch.setenv("PLQ_LINK", mode)
+        g, s = _gpu_batch(batch, J=J)
+        outs[mode] = g
+        if mode == "chain":
+            chain_launches = s.launches
+        else:
+            assert s.launches > chain_launches      # BCR: ~4 log2(J) launches; the chain: one
+    scale = np.abs(outs["bcr"]["links"]).max()
+    assert np.abs(outs["chain"]["links"] - outs["bcr"]["links"]).max() <= 1e-9 * scale
+    for k in ("x", "u", "lam"):
+        assert rel_err(outs["chain"][k], outs["bcr"][k]) <= 1e-8, k
+    assert outs["chain"]["link_residual"].max() <= 1e-9 * (1 + np.abs(batch["Qxx"]).max() * scale * n)
+    ref = O.solve(O.problem_slice(batch, B - 1), J=J)
+    assert rel_err(outs["chain"]["links"][B - 1], ref["links"]) <= 1e-7
+    # a non-SPD pivot in problem 1's chain
+    monkeypatch.setenv("PLQ_LINK", "chain")
+    g, s = _gpu_batch(batch, J=J)
+    vf0 = s.out["vf0"]
+    vf0[1, 1, 2 * n * n:3 * n * n] = -torch.eye(n, dtype=torch.float64, device=vf0.device).reshape(-1) * 1e6
+    s.out["status"].zero_()
+    inputs = {k: torch.from_numpy(v).to(vf0.device) for k, v in batch.items()}
+    prob = s._problem_struct(inputs)
+    rc = _native.lib().plq_link_solve(ctypes.byref(prob), ctypes.byref(s._outs), ctypes.c_void_p(s.workspace.data_ptr()),
+                                      s.ws_bytes, None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    st = s.out["status"].cpu().numpy()
+    assert st[1, 0] == _native.PLQ_STATUS_LINK_SINGULAR and (np.delete(st, 1, axis=0) == 0).all()
+    assert rel_err(s.out["links"][0].cpu().numpy(), outs["chain"]["links"][0]) == 0.0
