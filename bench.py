@@ -58,6 +58,11 @@ def parse():
     ap.add_argument("--no-smooth", action="store_true")
     ap.add_argument("--no-endpoint", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--gen", default="device", choices=("device", "host"),
+                    help="inputs from the device-side seeded generator (plq_generate_batch) or the numpy one")
+    ap.add_argument("--native-sharded", action="store_true",
+                    help="horizon-sharded runs through plq_solve_parallel_sharded (library-issued NCCL exchanges) "
+                         "instead of the torch.distributed orchestration")
     ap.add_argument("--graph", type=int, default=1, help="replay the solve as one CUDA graph (1) or launch eagerly (0)")
     return ap.parse_args()
 
@@ -295,24 +300,37 @@ def run_ours(args):
     scaling = "strong"
     # seeded host inputs (fork-pool generator), pinned once: the e2e leg reads
     # them as its host buffers, the device-resident leg copies them to HBM
-    gen = synth.generate_batch_parallel(cfg, seed=args.seed, count=B_loc, first=first)
+    device_gen = args.gen == "device" and not sharded
+    gen = None if device_gen else synth.generate_batch_parallel(cfg, seed=args.seed, count=B_loc, first=first)
     solver = BatchSolver(B_loc, cfg.T, cfg.n, cfg.m, J=cfg.J, device=dev, degenerate=not sharded)
     j0, j1, t0 = 0, cfg.J, 0
     full = None
-    if sharded:
+    if device_gen:
+        # the batch is generated in HBM (plq_generate_batch: same recipe, counter-based stream) and
+        # copied once to pinned host memory for the e2e leg and the oracle parity sample
+        inputs = synth.generate_batch_device(cfg, seed=args.seed, count=B_loc, first=first, device=dev)
+        host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v) for k, v in inputs.items()}
+    elif sharded:
         # horizon sharding: this rank uploads and holds only its segments'
         # stages (shifted pointers, DeviceBackend(t0=...))
         from paper_1809_06360_b200.sharded import shard_range, stage_window
         j0, j1 = shard_range(cfg.J, world, rank)
         full = gen if rank == 0 else None       # rank 0 keeps the whole problem for the parity check
         gen, t0 = stage_window(gen, solver.partition.split_times, j0, j1)
-    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in gen.items()}
-    del gen
-    inputs = {k: v.to(dev) for k, v in host.items()}
+    if not device_gen:
+        host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in gen.items()}
+        del gen
+        inputs = {k: v.to(dev) for k, v in host.items()}
     stream = torch.cuda.current_stream(dev)
     if sharded:
         from paper_1809_06360_b200.sharded import DeviceBackend, raise_sharded_status, solve_sharded
         backend = DeviceBackend(solver, inputs, t0=t0)
+        if args.native_sharded:
+            from paper_1809_06360_b200.sharded import NcclComm, solve_sharded_native
+            comm = NcclComm(dist)
+
+        def one_step_native():
+            solve_sharded_native(solver, inputs, comm, t0=t0, check=False)
 
         def one_step():
             # no host synchronization inside the step: status rows travel
@@ -330,8 +348,13 @@ def run_ours(args):
     else:
         def one_step():
             solver.run(inputs)
+    if sharded and args.native_sharded:
+        one_step = one_step_native
+
     def check_status():
-        if sharded:
+        if sharded and args.native_sharded:
+            solver.raise_for_status()
+        elif sharded:
             raise_sharded_status(backend)
         else:
             solver.raise_for_status()
@@ -589,7 +612,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "knots/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (BASELINE.json recipe, seeded numpy generator, see synth.py)",
+            "data": ("synthetic (BASELINE.json recipe, seeded; generated on the device by plq_generate_batch, "
+                     "Philox-4x32-10 + Box-Muller)" if device_gen else
+                     "synthetic (BASELINE.json recipe, seeded numpy generator, see synth.py)"),
             "config": {"workload": cfg.name, "B": cfg.B, "n": cfg.n, "m": cfg.m, "T": cfg.T, "J": cfg.J,
                        "global_batch": cfg.B,
                        "parallelism": (f"batch-shard x{world}" if cfg.B > 1 else f"segment-shard x{world}"),

@@ -189,6 +189,27 @@ int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const d
 int plq_solve_parallel_sharded(const plq_problem_t* problem, const plq_outputs_t* out, void* workspace,
                                size_t workspace_bytes, void* nccl_comm, int32_t rank, int32_t nranks, void* stream);
 
+/* Device-side seeded generator of the benchmark inputs (
+ * the reference generates its benchmark problems on the host, bench.py:38-60
+ * via generate.py:14-47, and BASELINE.json gives the recipe used here): fills
+ * the ARRAYS NAMED BY `problem` (device pointers; they are outputs of this
+ * call, split_times / J / max_seg_len are ignored) with problems
+ * first_problem .. first_problem + B - 1 of the seeded family
+ *   Fx = I + a_scale G/sqrt(n), Fu = 0.1 Bu/sqrt(n), f1 = 0.1 c,
+ *   Qxx = W W'/n + q_eps I, Quu = V V'/m + r_eps I, Qux = 0, qx1, qu1 ~ N(0,1),
+ *   QxxT = WT WT'/n + q_eps I, qx1T, x_init ~ N(0,1)
+ * (all capitals / lowercase letters independent N(0,1) arrays; Qxx, Quu, QxxT
+ * exactly symmetric).  Counter-based (Philox-4x32-10 + Box-Muller, stream
+ * documented in csrc/plq_generate.cu): the values depend only on (seed,
+ * problem index, field, element), so a batch generated in pieces equals one
+ * generated in one call. */
+typedef struct plq_recipe {
+  double a_scale, q_eps, r_eps;
+  uint64_t seed;
+  int64_t first_problem;
+} plq_recipe_t;
+int plq_generate_batch(const plq_problem_t* problem, const plq_recipe_t* recipe, void* stream);
+
 /* Device outputs of the smoothing pass (parlqr.parallel.smooth,
  * parallel.py:567-633): the smoothed LqrSolution's policies, trajectory and
  * diagnostics.  Its lambdas are the parent's (unchanged). */

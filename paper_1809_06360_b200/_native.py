@@ -26,6 +26,7 @@ EXPORTS = (
     "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
     "plq_finalize", "plq_last_launch_count", "plq_smooth", "plq_endpoint_workspace_bytes",
     "plq_endpoint_affine", "plq_endpoint_evaluate", "plq_solve_parallel_sharded",
+    "plq_generate_batch",
 )
 
 _vp = ctypes.c_void_p
@@ -71,6 +72,11 @@ class PlqEndpointPoint(ctypes.Structure):
     _fields_ = [(f, _vp) for f in POINT_FIELDS]
 
 
+class PlqRecipe(ctypes.Structure):
+    _fields_ = [("a_scale", ctypes.c_double), ("q_eps", ctypes.c_double), ("r_eps", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("first_problem", ctypes.c_int64)]
+
+
 _LIB = None
 
 
@@ -108,6 +114,8 @@ def lib():
     L.plq_endpoint_workspace_bytes.argtypes = [P]
     L.plq_endpoint_affine.argtypes = [P, EO, _vp, ctypes.c_size_t, _vp]
     L.plq_endpoint_evaluate.argtypes = [P, EO, ctypes.POINTER(PlqEndpointPoint), _vp, ctypes.c_size_t, _vp]
+    L.plq_generate_batch.argtypes = [P, ctypes.POINTER(PlqRecipe), _vp]
+    L.plq_generate_batch.restype = ctypes.c_int
     L.plq_solve_parallel_sharded.argtypes = [P, O, _vp, ctypes.c_size_t, _vp, ctypes.c_int32, ctypes.c_int32, _vp]
     for name in ("plq_solve_parallel", "plq_solve_parallel_host", "plq_sweep_segments", "plq_solve_parallel_sharded",
                  "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",

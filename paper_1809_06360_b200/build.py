@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparlqr_b200.so")
 SOURCES = ("plq_sweep.cu", "plq_sweep_t32.cu", "plq_sweep_t128.cu", "plq_sweep_t256.cu", "plq_sweep_t512.cu", "plq_sweep_small.cu", "plq_link.cu", "plq_recon.cu", "plq_recon_small.cu", "plq_recon_ring.cu",
-           "plq_smooth.cu", "plq_endpoint.cu", "plq_linkfeas.cu", "plq_linkchain.cu",
+           "plq_smooth.cu", "plq_endpoint.cu", "plq_linkfeas.cu", "plq_linkchain.cu", "plq_generate.cu",
            "plq_api.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

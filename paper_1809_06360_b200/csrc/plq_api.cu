@@ -473,6 +473,27 @@ int plq_finalize(const plq_problem_t* problem, const plq_outputs_t* out, const d
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
+// device-side seeded generator
+
+extern "C" int plq_generate_batch(const plq_problem_t* problem, const plq_recipe_t* recipe, void* stream) {
+  g_launches = 0;
+  const plq_problem_t* p = problem;
+  if (!p || !recipe) return fail(PLQ_ERR_ARG, "null problem or recipe");
+  if (p->B < 1 || p->T < 1 || p->n < 1 || p->m < 1 || p->n > 128 || p->m > 128)
+    return fail(PLQ_ERR_ARG, "B, T >= 1 and 1 <= n, m <= 128");
+  if (!p->Qxx || !p->Qux || !p->Quu || !p->qx1 || !p->qu1 || !p->Fx || !p->Fu || !p->f1 || !p->QxxT || !p->qx1T ||
+      !p->x_init)
+    return fail(PLQ_ERR_ARG, "null problem array");
+  if (recipe->first_problem < 0 || recipe->first_problem + p->B > 0xffffffffLL)
+    return fail(PLQ_ERR_ARG, "problem index out of range");
+  if (plq::launch_generate(*p, recipe->a_scale, recipe->q_eps, recipe->r_eps, recipe->seed, recipe->first_problem,
+                           static_cast<cudaStream_t>(stream)))
+    return cuda_fail("generator launch");
+  g_launches = 2;
+  return PLQ_OK;
+}
+
+// ---------------------------------------------------------------------------
 // horizon-sharded solve over an NCCL communicator
 
 namespace {

@@ -205,6 +205,10 @@ size_t link_seq_workspace_doubles(int64_t B, int J, int n);
 int launch_link_seq(const plq_problem_t& p, const double* vf0, double* links, double* link_residual,
                     int32_t* status, double* ws, cudaStream_t s);
 
+// Device-side seeded generator of the BASELINE recipe (plq_generate.cu).
+int launch_generate(const plq_problem_t& p, double a_scale, double q_eps, double r_eps, uint64_t seed, int64_t first,
+                    cudaStream_t s);
+
 // Link solve of a batch of short chains, one CTA per problem (plq_linkchain.cu).
 bool link_chain_supported(int n, int J);
 bool link_chain_preferred(int64_t B, int J);

@@ -215,3 +215,101 @@ def batch_nbytes(cfg, B=None):
     n, m, T = cfg.n, cfg.m, cfg.T
     per_stage = 8 * (2 * n * n + 2 * n * m + m * m + 2 * n + m)
     return B * (T * per_stage + 8 * (n * n + 2 * n))
+
+
+# ---------------------------------------------------------------------------
+# device-side generator (plq_generate_batch) and the host restatement of its
+# random stream
+
+_FIELD_IDS = {"G": 0, "Bu": 1, "c": 2, "W": 3, "V": 4, "q": 5, "r": 6, "WT": 7, "qT": 8, "x0": 9}
+
+
+def generate_batch_device(cfg, seed=0, count=None, first=0, device=None, out=None):
+    """Problems ``first .. first+count-1`` of ``cfg``'s seeded family generated
+    ON THE DEVICE (``plq_generate_batch``, csrc/plq_generate.cu): a dict of
+    ``(B, T, ...)`` float64 CUDA tensors in the solver's input layout.  The
+    family has the distributions of :func:`generate_one` (BASELINE.json recipe,
+    ``Qux = 0``) but its own counter-based stream (Philox-4x32-10 + Box-Muller,
+    restated in :func:`device_stream_reference`), so the values differ from the
+    numpy generator's for the same seed.  ``out``: tensors to fill in place."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+    if cfg.cross:
+        raise ValueError("the device generator has no cross term (BASELINE recipe: Qux = 0)")
+    count = cfg.B if count is None else count
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    n, m, T = cfg.n, cfg.m, cfg.T
+    shapes = {"Qxx": (count, T, n, n), "Qux": (count, T, m, n), "Quu": (count, T, m, m), "qx1": (count, T, n),
+              "qu1": (count, T, m), "Fx": (count, T, n, n), "Fu": (count, T, n, m), "f1": (count, T, n),
+              "QxxT": (count, n, n), "qx1T": (count, n), "x_init": (count, n)}
+    if out is None:
+        out = {k: torch.empty(s, dtype=torch.float64, device=dev) for k, s in shapes.items()}
+    P = _native.PlqProblem()
+    P.B, P.T, P.n, P.m, P.J, P.max_seg_len = count, T, n, m, 1, T
+    for k, s in shapes.items():
+        t = out[k]
+        if tuple(t.shape) != s or t.dtype != torch.float64 or not t.is_contiguous() or not t.is_cuda:
+            raise ValueError(f"{k}: expected a contiguous float64 CUDA tensor of shape {s}")
+        setattr(P, k, ctypes.c_void_p(t.data_ptr()))
+    R = _native.PlqRecipe(cfg.a_scale, cfg.q_eps, cfg.r_eps, int(seed) & (2 ** 64 - 1), int(first))
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        rc = _native.lib().plq_generate_batch(ctypes.byref(P), ctypes.byref(R), ctypes.c_void_p(stream.cuda_stream))
+    _native.check(rc, "plq_generate_batch")
+    return out
+
+
+def _philox4x32_10(c0, c1, c2, c3, k0, k1):
+    M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    mask = np.uint64(0xFFFFFFFF)
+    c = [np.asarray(x, dtype=np.uint64) & mask for x in (c0, c1, c2, c3)]
+    k0, k1 = np.uint64(k0), np.uint64(k1)
+    for _ in range(10):
+        p0, p1 = M0 * c[0], M1 * c[2]
+        hi0, lo0, hi1, lo1 = p0 >> np.uint64(32), p0 & mask, p1 >> np.uint64(32), p1 & mask
+        c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
+        k0 = (k0 + np.uint64(0x9E3779B9)) & mask
+        k1 = (k1 + np.uint64(0xBB67AE85)) & mask
+    return c
+
+
+def _device_normals(seed, problem, field, count):
+    """The first ``count`` standard normals of (seed, problem, field) in the
+    device generator's stream (csrc/plq_generate.cu: normal_at)."""
+    e = np.arange(count, dtype=np.uint64)
+    k = e >> np.uint64(1)
+    seed = int(seed) & (2 ** 64 - 1)
+    w = _philox4x32_10(k & np.uint64(0xFFFFFFFF), k >> np.uint64(32), np.full(count, _FIELD_IDS[field], np.uint64),
+                       np.full(count, problem, np.uint64), seed & 0xFFFFFFFF, seed >> 32)
+    u0 = (w[0] >> np.uint64(5)).astype(np.float64) / 134217728.0 + (w[1] >> np.uint64(6)).astype(np.float64) / 9007199254740992.0
+    u1 = (w[2] >> np.uint64(5)).astype(np.float64) / 134217728.0 + (w[3] >> np.uint64(6)).astype(np.float64) / 9007199254740992.0
+    r = np.sqrt(-2.0 * np.log(1.0 - u0))
+    return np.where(e & np.uint64(1), r * np.sin(2.0 * np.pi * u1), r * np.cos(2.0 * np.pi * u1))
+
+
+def device_stream_reference(cfg, seed=0, problem=0):
+    """Host (numpy) restatement of ONE problem of the device generator's
+    family: same Philox counters, Box-Muller pairing and recipe, so the
+    device output can be checked to rounding (libm vs CUDA ``log`` /
+    ``sincospi`` differ in the last bits).  Test infrastructure."""
+    n, m, T = cfg.n, cfg.m, cfg.T
+    nrm = lambda f, shape: _device_normals(seed, problem, f, int(np.prod(shape))).reshape(shape)  # noqa: E731
+    G, Bu, c = nrm("G", (T, n, n)), nrm("Bu", (T, n, m)), nrm("c", (T, n))
+    W, V = nrm("W", (T, n, n)), nrm("V", (T, m, m))
+    WT = nrm("WT", (n, n))
+    return {
+        "Fx": np.eye(n) + (cfg.a_scale / np.sqrt(n)) * G,
+        "Fu": (0.1 / np.sqrt(n)) * Bu,
+        "f1": 0.1 * c,
+        "Qxx": W @ np.swapaxes(W, 1, 2) / n + cfg.q_eps * np.eye(n),
+        "Qux": np.zeros((T, m, n)),
+        "Quu": V @ np.swapaxes(V, 1, 2) / m + cfg.r_eps * np.eye(m),
+        "qx1": nrm("q", (T, n)),
+        "qu1": nrm("r", (T, m)),
+        "QxxT": WT @ WT.T / n + cfg.q_eps * np.eye(n),
+        "qx1T": nrm("qT", (n,)),
+        "x_init": nrm("x0", (n,)),
+    }

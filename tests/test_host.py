@@ -206,3 +206,19 @@ def test_product_path_refuses_without_gpu():
     prob = plq.problem_from_arrays(synth.generate_one(3, 1, 6, seed=1))
     with pytest.raises(RuntimeError, match="CUDA"):
         plq.solve_parallel(prob, J=2)
+
+
+def test_device_generator_stream_restatement():
+    """Philox-4x32-10 known answers (the algorithm's published test vectors)
+    and the moments of the Box-Muller normals the device generator draws."""
+    from paper_1809_06360_b200 import synth
+    w = synth._philox4x32_10([0], [0], [0], [0], 0, 0)
+    assert [int(x[0]) for x in w] == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    w = synth._philox4x32_10([0xFFFFFFFF], [0xFFFFFFFF], [0xFFFFFFFF], [0xFFFFFFFF], 0xFFFFFFFF, 0xFFFFFFFF)
+    assert [int(x[0]) for x in w] == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    z = synth._device_normals(5, 2, "W", 400_000)
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01 and abs((z ** 4).mean() - 3) < 0.1
+    assert not np.array_equal(z[:100], synth._device_normals(5, 3, "W", 100))
+    cfg = synth.CONFIGS[1].scaled(T=4, J=1)
+    p = synth.device_stream_reference(cfg, seed=0, problem=1)
+    assert p["Qxx"].shape == (4, 12, 12) and np.linalg.eigvalsh(p["Qxx"][0]).min() > 0
