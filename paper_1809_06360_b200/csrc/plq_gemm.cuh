@@ -27,13 +27,17 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int NW>
+// NS = stages of the cp.async ring (2 = double buffering; deeper rings keep
+// NS - 1 chunks in flight, which is what hides DRAM latency when the operands'
+// L2-resident scratch spills)
+template <int NW, int NS = 2>
 struct TileCfg {
   static constexpr int BM = 8 * NW, BN = 64, BK = 16;
   static constexpr int LDA = 20, LDB = 68;   // = 4 (mod 8): conflict-free fragment loads
   static constexpr int LDAT = BM + 4;        // transposed A tile (BK x BM), also = 4 (mod 8)
   static_assert(BK * LDAT <= BM * LDA, "transposed A tile fits the A buffer");
-  static constexpr int DOUBLES = 2 * (BM * LDA + BK * LDB);
+  static constexpr int STAGE = BM * LDA + BK * LDB;
+  static constexpr int DOUBLES = NS * STAGE;
 };
 
 struct NoPre {
@@ -42,19 +46,16 @@ struct NoPre {
 
 // PRE: pre(i, j) (e.g. a Q-block entry in HBM) is loaded before each tile's
 // k-loop and the epilogue receives pre(i, j) + acc
-template <bool TA, int NW, class Epi, bool PRE = false, class Pre = NoPre>
+template <bool TA, int NW, class Epi, bool PRE = false, class Pre = NoPre, int NS = 2>
 __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double* __restrict__ A, int lda,
                                                const double* __restrict__ B, int ldb, double* tiles, Epi epi,
                                                Pre pre = Pre()) {
-  using C = TileCfg<NW>;
+  using C = TileCfg<NW, NS>;
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, LDA = C::LDA, LDB = C::LDB, NT = NW * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int wr = warp >> 1, wc = warp & 1;
-  double* As0 = tiles;
-  double* As1 = tiles + BM * LDA;
-  double* Bs0 = tiles + 2 * BM * LDA;
-  double* Bs1 = Bs0 + BK * LDB;
+  // stage s: A tile at tiles + s * STAGE, B tile behind it
   const int tmc = (M + BM - 1) / BM, tnc = (N + BN - 1) / BN, kc = (K + BK - 1) / BK;
   // 16-byte copies when both operands have even leading dimensions and
   // 16-byte-aligned bases (large-mode scratch); the A tile of a transposed
@@ -76,8 +77,8 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
       }
     auto load_vec = [&](int c, int buf) {
       const int k0 = c * BK;
-      double* as = buf ? As1 : As0;
-      double* bs = buf ? Bs1 : Bs0;
+      double* as = tiles + buf * C::STAGE;
+      double* bs = as + BM * LDA;
       for (int e = tid; e < BM * BK / 2; e += NT) {
         int i, k;
         if (TA) {
@@ -119,7 +120,6 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
           cp_async8(dst + 1, gk < K && gj + 1 < N ? src + 1 : B, gk < K && gj + 1 < N);
         }
       }
-      cp_async_commit();
     };
     auto load = [&](int c, int buf) {
       if (vec) {
@@ -127,8 +127,8 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
         return;
       }
       const int k0 = c * BK;
-      double* as = buf ? As1 : As0;
-      double* bs = buf ? Bs1 : Bs0;
+      double* as = tiles + buf * C::STAGE;
+      double* bs = as + BM * LDA;
       for (int e = tid; e < BM * BK; e += NT) {
         int i, k;
         if (TA) {
@@ -149,19 +149,22 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
         const bool v = gk < K && gj < N;
         cp_async8(bs + k * LDB + j, v ? B + (size_t)gk * ldb + gj : B, v);
       }
-      cp_async_commit();
     };
-    load(0, 0);
+    // ring of NS stages: chunks c .. c + NS - 2 in flight while chunk c is
+    // consumed; one commit group per chunk slot (empty past the end), so
+    // wait_group<NS - 2> always means "chunk c has landed"
+#pragma unroll
+    for (int st = 0; st < NS - 1; ++st) {
+      if (st < kc) load(st, st);
+      cp_async_commit();
+    }
     for (int c = 0; c < kc; ++c) {
-      if (c + 1 < kc) {
-        load(c + 1, (c + 1) & 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncthreads();
-      const double* as = (c & 1) ? As1 : As0;
-      const double* bs = (c & 1) ? Bs1 : Bs0;
+      cp_async_wait<NS - 2>();
+      __syncthreads();   // chunk c visible to all; everyone is done with chunk c - 1's buffer
+      if (c + NS - 1 < kc) load(c + NS - 1, (c + NS - 1) % NS);
+      cp_async_commit();
+      const double* as = tiles + (c % NS) * C::STAGE;
+      const double* bs = as + BM * LDA;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
         double af[2], bf[4];
@@ -175,8 +178,9 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
 #pragma unroll
           for (int t = 0; t < 4; ++t) dmma884(acc[r][t][0], acc[r][t][1], af[r], bf[t]);
       }
-      __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();   // the next tile's prologue reuses the buffers
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll

@@ -37,6 +37,10 @@ enum SweepBuf {
   SB_COUNT
 };
 
+// stages of the tiled GEMM's cp.async ring in the large-mode sweep: 8-warp
+// CTAs (two per SM) take four (75 KB of the SM's 227 KB each), 16-warp CTAs two
+constexpr int sweep_tile_stages(int threads) { return threads == 256 ? 4 : 2; }
+
 struct SweepLayout {
   int64_t off[SB_COUNT];     // offset in doubles within its space
   int in_smem[SB_COUNT];

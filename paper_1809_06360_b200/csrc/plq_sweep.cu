@@ -53,7 +53,8 @@ SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
     L.large = 1;
     const int nw = threads / 32;
     L.tiles_off = 0;
-    so = nw >= 16 ? TileCfg<16>::DOUBLES : (nw >= 8 ? TileCfg<8>::DOUBLES : TileCfg<4>::DOUBLES);
+    so = nw >= 16 ? TileCfg<16, sweep_tile_stages(512)>::DOUBLES
+                  : (nw >= 8 ? TileCfg<8, sweep_tile_stages(256)>::DOUBLES : TileCfg<4>::DOUBLES);
     budget = so + ((sz[SB_MISC] + 1) & ~1LL);
   }
   for (int i = 0; i < SB_COUNT; ++i) {

@@ -44,7 +44,7 @@ __device__ __forceinline__ void gemm_x(int M, int N, int K, const double* A, int
                                        double* tiles, Epi epi) {
   if constexpr (NT >= 256) {
     if (tiles != nullptr && (long long)M * N * K >= 16384) {
-      cta_gemm_tiled<TA, NT / 32>(M, N, K, A, lda, B, ldb, tiles, epi);
+      cta_gemm_tiled<TA, NT / 32, Epi, false, NoPre, sweep_tile_stages(NT)>(M, N, K, A, lda, B, ldb, tiles, epi);
       return;
     }
   }
@@ -57,7 +57,7 @@ __device__ __forceinline__ void gemm_x_pre(int M, int N, int K, const double* A,
                                            double* tiles, Pre pre, Epi epi) {
   if constexpr (NT >= 256) {
     if (tiles != nullptr && (long long)M * N * K >= 16384) {
-      cta_gemm_tiled<TA, NT / 32, Epi, true, Pre>(M, N, K, A, lda, B, ldb, tiles, epi, pre);
+      cta_gemm_tiled<TA, NT / 32, Epi, true, Pre, sweep_tile_stages(NT)>(M, N, K, A, lda, B, ldb, tiles, epi, pre);
       return;
     }
   }
@@ -578,15 +578,21 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     }
     // x rows over the x columns only (no discarded Vxz block), z rows over
     // [x | z] columns, the constant column as a matvec
-    gemm_x<true, NT>(n, n, KV, P, ldw, G, ldw, bf.tiles,
-                     [&](int i, int c, double acc) { Vxx[i * n + c] += acc; });
+    // (the addends -- Mxx in Vxx, Mzx in Z, Vzz -- are loaded before each
+    // tile's k-loop: L2 / DRAM latency of the scratch hides behind the DMMAs)
+    gemm_x_pre<true, NT>(
+        n, n, KV, P, ldw, G, ldw, bf.tiles, [&](int i, int c) { return Vxx[i * n + c]; },
+        [&](int i, int c, double v) { Vxx[i * n + c] = v; });
     if (nz)
-      gemm_x<true, NT>(nz, 2 * n, KV, P + n, ldw, G, ldw, bf.tiles, [&](int zi, int c, double acc) {
-        if (c < n)
-          Vzx[zi * n + c] = Z[zi * Fw + c] + acc;
-        else
-          Vzz[zi * n + (c - n)] += acc;
-      });
+      gemm_x_pre<true, NT>(
+          nz, 2 * n, KV, P + n, ldw, G, ldw, bf.tiles,
+          [&](int zi, int c) { return c < n ? Z[zi * Fw + c] : Vzz[zi * n + (c - n)]; },
+          [&](int zi, int c, double v) {
+            if (c < n)
+              Vzx[zi * n + c] = v;
+            else
+              Vzz[zi * n + (c - n)] = v;
+          });
     for (int i = tid; i < n + nz; i += nt) {
       double t0 = 0.0, t1 = 0.0;
       int k = 0;
