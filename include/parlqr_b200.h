@@ -249,8 +249,15 @@ typedef struct plq_endpoint_outputs {
   double* Lam;            /* (B,T+1,n,W) multipliers: lam_t = [La|Lz|l1] [...] */
   double* E;              /* (B,n,W)     mu = [Ea|Ez|e1] [...] */
   int32_t* status;        /* (B) backward pass: 0, 1+t CholeskyFailure(t), -1 unreachable endpoint
-                             directions (feasibility rows; not solved on the GPU) */
-  int32_t* gram_status;   /* (B) multiplier Gram system: 0, or 1+i FactorizationFailure(block i) */
+                             directions (feasibility rows) when feas / feas_rows are NULL */
+  int32_t* gram_status;   /* (B) multiplier Gram system: 0, 1+i FactorizationFailure(block i), or -1 = not
+                             computed (feasibility rows: the boundary constraints are linearly dependent,
+                             solve_endpoint_affine endpoint.py:589-620 leaves multipliers = None) */
+  /* Unreachable endpoint directions (T m < n, or no control authority): the rows [Hx | Hz | h1] any
+   * (x_init, x_term) pair must satisfy (BackwardResult.feasibility, endpoint.py:124-127; an orthonormal
+   * rotation of the reference's rows).  Both NULL: such problems report status -1. */
+  double* feas;           /* (B,n,W) */
+  int32_t* feas_rows;     /* (B) */
 } plq_endpoint_outputs_t;
 
 /* Evaluation at concrete endpoints (EndpointAffineSolution.evaluate,
@@ -264,6 +271,11 @@ typedef struct plq_endpoint_point {
   double* mu;             /* (B,n) */
   double* objective;      /* (B) */
   double* kkt_inf;        /* (B) */
+  double* feas_residual;  /* (B) max |Hx x_init + Hz x_term + h1| over the feasibility rows (0 without rows);
+                             may be NULL.  The caller raises Infeasible above feas_tol * scale
+                             (endpoint.py:516-523).  Problems with rows take their multipliers from the
+                             value-function gradient and the stationarity recursion (gradient_duals,
+                             endpoint.py:566-587). */
 } plq_endpoint_point_t;
 
 size_t plq_endpoint_workspace_bytes(const plq_problem_t* problem);

@@ -332,31 +332,57 @@ def full_kkt_residual(prob, states, controls, lambdas, mu, x_term):
 
 
 def solve_endpoint_affine(prob, rank_tol=RANK_TOL):
-    """solve_endpoint_affine (endpoint.py:603-636) for reachable problems
-    (empty feasibility triple; the GPU path raises otherwise)."""
+    """solve_endpoint_affine (endpoint.py:589-620).  With feasibility rows
+    left at t = 0 (unreachable endpoint directions) the boundary constraints
+    are linearly dependent and no multiplier maps are computed (``Lam``/``E``
+    absent); ``feas`` holds the rows."""
     st = {f: np.asarray(prob[f]) for f in STAGE_FIELDS}
     sw = endpoint_sweep(st, rank_tol, prob["QxxT"], prob["qx1T"])
-    if sw["feas"][0].shape[0]:
-        raise OracleDegenerate(0)
     X, S = forward_maps(st, sw["Kx"], sw["Kz"], sw["k1"])
-    Lam, E = multiplier_maps(st, prob["QxxT"], prob["qx1T"], X, S)
-    return {"Kx": sw["Kx"], "Kz": sw["Kz"], "k1": sw["k1"], "vf0": sw["vf0"], "X": X, "S": S,
-            "Lam": Lam, "E": E}
+    out = {"Kx": sw["Kx"], "Kz": sw["Kz"], "k1": sw["k1"], "vf0": sw["vf0"], "X": X, "S": S,
+           "feas": sw["feas"]}
+    if sw["feas"][0].shape[0] == 0:
+        out["Lam"], out["E"] = multiplier_maps(st, prob["QxxT"], prob["qx1T"], X, S)
+    return out
+
+
+def gradient_duals(prob, vf0, states, controls, x_init, x_term):
+    """Multipliers from the value-function gradient and the backward
+    stationarity recursion (endpoint.py:566-587)."""
+    Vxx, Vzx, Vzz, vx1, vz1 = vf0
+    mu = -(Vzx @ x_init + Vzz @ x_term + vz1)
+    T, n = controls.shape[0], states.shape[1]
+    lambdas = np.empty((T + 1, n))
+    lambdas[T] = -(prob["QxxT"] @ states[T] + prob["qx1T"]) - mu
+    for t in range(T - 1, -1, -1):
+        lambdas[t] = prob["Fx"][t].T @ lambdas[t + 1] - (
+            prob["Qxx"][t] @ states[t] + prob["Qux"][t].T @ controls[t] + prob["qx1"][t])
+    return lambdas, mu
 
 
 def evaluate_endpoint(prob, aff, x_init, x_term):
-    """EndpointAffineSolution.evaluate (endpoint.py:538-575) with multiplier
-    maps: states, controls, lambdas, mu, objective, full KKT residual."""
+    """EndpointAffineSolution.evaluate (endpoint.py:507-546): states,
+    controls, lambdas, mu, objective, full KKT residual, and the residual of
+    the feasibility rows at the endpoint pair; multipliers from the maps, or
+    from :func:`gradient_duals` when there are none."""
+    x_init = np.asarray(x_init, dtype=float)
+    x_term = np.asarray(x_term, dtype=float)
     v = np.concatenate([x_init, x_term, [1.0]])
     states = aff["X"] @ v
     controls = aff["S"] @ v
-    lambdas = aff["Lam"] @ v
-    mu = aff["E"] @ v
+    Hx, Hz, h1 = aff["feas"]
+    res = Hx @ x_init + Hz @ x_term + h1
+    if "Lam" in aff:
+        lambdas = aff["Lam"] @ v
+        mu = aff["E"] @ v
+    else:
+        lambdas, mu = gradient_duals(prob, aff["vf0"], states, controls, x_init, x_term)
     p = dict(prob)
-    p["x_init"] = np.asarray(x_init, dtype=float)
+    p["x_init"] = x_init
     return {"states": states, "controls": controls, "lambdas": lambdas, "mu": mu,
             "objective": objective(p, states, controls),
-            "kkt": full_kkt_residual(p, states, controls, lambdas, mu, x_term)}
+            "kkt": full_kkt_residual(p, states, controls, lambdas, mu, x_term),
+            "feas_residual": float(np.abs(res).max()) if res.size else 0.0}
 
 
 def link_system(vf0, x_init):

@@ -58,14 +58,14 @@ class PlqSmoothOutputs(ctypes.Structure):
     _fields_ = [(f, _vp) for f in SMOOTH_FIELDS]
 
 
-ENDPOINT_FIELDS = ("Kx", "Kz", "k1", "value0", "X", "S", "Lam", "E", "status", "gram_status")
+ENDPOINT_FIELDS = ("Kx", "Kz", "k1", "value0", "X", "S", "Lam", "E", "status", "gram_status", "feas", "feas_rows")
 
 
 class PlqEndpointOutputs(ctypes.Structure):
     _fields_ = [(f, _vp) for f in ENDPOINT_FIELDS]
 
 
-POINT_FIELDS = ("x_init", "x_term", "x", "u", "lam", "mu", "objective", "kkt_inf")
+POINT_FIELDS = ("x_init", "x_term", "x", "u", "lam", "mu", "objective", "kkt_inf", "feas_residual")
 
 
 class PlqEndpointPoint(ctypes.Structure):

@@ -397,6 +397,9 @@ int plq_endpoint_affine(const plq_problem_t* problem, const plq_endpoint_outputs
   o.k1 = out->k1;
   o.vf0 = out->value0;
   o.status = out->status;
+  if ((out->feas != nullptr) != (out->feas_rows != nullptr)) return fail(PLQ_ERR_ARG, "feas and feas_rows go together");
+  o.feas = out->feas;            // (B, J = 1, n, 2n+1): rows instead of PLQ_STATUS_DEGENERATE
+  o.feas_rows = out->feas_rows;
   Ctx c;
   int rc = setup(problem, &o, workspace, workspace_bytes, stream, &c);
   if (rc) return rc;

@@ -199,6 +199,13 @@ __global__ void __launch_bounds__(EP_NT) ep_mult_kernel(EpArgs a) {
   double* Xb = a.Xb + b * (T + 1) * nn;
   double* Lam = a.o.Lam + b * (T + 1) * n * W;
   double* E = a.o.E + b * n * W;
+  if (a.o.feas_rows != nullptr && a.o.feas_rows[b] > 0) {
+    // unreachable endpoint rows: the boundary constraints are linearly
+    // dependent, the Gram system is singular and the reference computes no
+    // multiplier maps (endpoint.py:607-613); evaluate uses gradient duals
+    if (tid == 0) a.o.gram_status[b] = -1;
+    return;
+  }
   int fail = 0;
   for (int i = 0; i <= T + 1 && !fail; ++i) {
     double* dg = (i <= T) ? Lam + (int64_t)i * n * W : E;   // d_i's home
@@ -283,6 +290,8 @@ __global__ void __launch_bounds__(EP_NT) ep_point_kernel(EpArgs a) {
   const int n = p.n, m = p.m, T = p.T, W = 2 * n + 1, tid = threadIdx.x;
   const int64_t b = blockIdx.x / a.nch;
   const int c = (int)(blockIdx.x % a.nch);
+  // problems with feasibility rows have no multiplier maps: ep_dual_kernel fills lam / mu
+  const bool dual = a.o.feas_rows != nullptr && a.o.feas_rows[b] > 0;
   for (int i = tid; i < W; i += EP_NT)
     v[i] = i < n ? a.x_init[b * n + i] : (i < 2 * n ? a.x_term[b * n + i - n] : 1.0);
   __syncthreads();
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(EP_NT) ep_point_kernel(EpArgs a) {
   for (int t = t0; t < t1; ++t) {
     const double* X = a.o.X + (b * (T + 1) + t) * n * W;
     const double* L = a.o.Lam + (b * (T + 1) + t) * n * W;
-    for (int r = tid; r < 2 * n; r += EP_NT) {
+    for (int r = tid; r < (dual ? n : 2 * n); r += EP_NT) {
       const double* row = (r < n ? X : L) + (r % n) * W;
       double s = 0.0;
       for (int k = 0; k < W; ++k) s += row[k] * v[k];
@@ -303,13 +312,84 @@ __global__ void __launch_bounds__(EP_NT) ep_point_kernel(EpArgs a) {
         for (int k = 0; k < W; ++k) s += S[r * W + k] * v[k];
         a.pt.u[(b * T + t) * m + r] = s;
       }
-    } else {
+    } else if (!dual) {
       for (int r = tid; r < n; r += EP_NT) {
         double s = 0.0;
         for (int k = 0; k < W; ++k) s += a.o.E[(b * n + r) * W + k] * v[k];
         a.pt.mu[b * n + r] = s;
       }
     }
+  }
+}
+
+// Problems with feasibility rows (unreachable endpoint directions): the
+// residual of the rows at (x_init, x_term) (feasibility_residual,
+// endpoint.py:507-511) and the multipliers from the value-function gradient
+// and the stationarity recursion (gradient_duals, endpoint.py:566-587):
+//   mu = -(Vzx0 x_init + Vzz0 x_term + vz10),  lam_T = -(QxxT x_T + qx1T) - mu,
+//   lam_t = Fx_t' lam_{t+1} - (Qxx_t x_t + Qux_t' u_t + qx1_t).
+// One CTA per problem (the recursion is sequential in t); no-op without rows.
+__global__ void __launch_bounds__(EP_NT) ep_dual_kernel(EpArgs a) {
+  extern __shared__ double dsm[];   // lam ping | lam pong | x_init | x_term
+  __shared__ double red[32];
+  const plq_problem_t& p = a.p;
+  const int n = p.n, m = p.m, T = p.T, W = 2 * n + 1, tid = threadIdx.x;
+  const int64_t b = blockIdx.x, nn = (int64_t)n * n, nm = (int64_t)n * m;
+  const int rows = a.o.feas_rows != nullptr ? a.o.feas_rows[b] : 0;
+  if (rows <= 0) {
+    if (tid == 0 && a.pt.feas_residual != nullptr) a.pt.feas_residual[b] = 0.0;
+    return;
+  }
+  double* l0 = dsm;
+  double* l1 = dsm + n;
+  double* xi = l1 + n;
+  double* xt = xi + n;
+  for (int i = tid; i < n; i += EP_NT) {
+    xi[i] = a.x_init[b * n + i];
+    xt[i] = a.x_term[b * n + i];
+  }
+  __syncthreads();
+  double worst = 0.0;
+  const double* H = a.o.feas + b * n * W;
+  for (int r = tid; r < rows; r += EP_NT) {
+    double s = H[r * W + 2 * n];
+    for (int k = 0; k < n; ++k) s += H[r * W + k] * xi[k] + H[r * W + n + k] * xt[k];
+    worst = fmax(worst, fabs(s));
+  }
+  worst = block_max(worst, red);
+  if (tid == 0 && a.pt.feas_residual != nullptr) a.pt.feas_residual[b] = worst;
+  const double* v0 = a.o.value0 + b * (3 * nn + 2 * n);
+  const double* xT = a.pt.x + (b * (T + 1) + T) * n;
+  for (int i = tid; i < n; i += EP_NT) {
+    double mu = v0[3 * nn + n + i];
+    for (int k = 0; k < n; ++k) mu += v0[nn + i * n + k] * xi[k] + v0[2 * nn + i * n + k] * xt[k];
+    mu = -mu;
+    double g = p.qx1T[b * n + i];
+    for (int k = 0; k < n; ++k) g += p.QxxT[b * nn + i * n + k] * xT[k];
+    a.pt.mu[b * n + i] = mu;
+    const double lt = -g - mu;
+    l0[i] = lt;
+    a.pt.lam[(b * (T + 1) + T) * n + i] = lt;
+  }
+  __syncthreads();
+  double* cur = l0;
+  double* nxt = l1;
+  for (int t = T - 1; t >= 0; --t) {
+    const int64_t bt = b * T + t;
+    const double* x = a.pt.x + (b * (T + 1) + t) * n;
+    const double* u = a.pt.u + bt * m;
+    const double *Fx = p.Fx + bt * nn, *Qxx = p.Qxx + bt * nn, *Qux = p.Qux + bt * nm;
+    for (int i = tid; i < n; i += EP_NT) {
+      double s = -p.qx1[bt * n + i];
+      for (int k = 0; k < n; ++k) s += Fx[k * n + i] * cur[k] - Qxx[i * n + k] * x[k];
+      for (int k = 0; k < m; ++k) s -= Qux[k * n + i] * u[k];
+      nxt[i] = s;
+      a.pt.lam[(b * (T + 1) + t) * n + i] = s;
+    }
+    __syncthreads();
+    double* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
   }
 }
 
@@ -453,6 +533,11 @@ int launch_endpoint_evaluate(const plq_problem_t& p, const plq_endpoint_outputs_
   const unsigned grid = (unsigned)(p.B * a.nch);
   ep_point_kernel<<<grid, EP_NT, sizeof(double) * (2 * p.n + 1), s>>>(a);
   if (cudaGetLastError() != cudaSuccess) return -1;
+  if (o.feas_rows != nullptr) {
+    ep_dual_kernel<<<(unsigned)p.B, EP_NT, sizeof(double) * 4 * p.n, s>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    ++*launches;
+  }
   ep_eval_kernel<<<grid, EP_NT, 0, s>>>(a);
   if (cudaGetLastError() != cudaSuccess) return -1;
   ep_fin_kernel<<<(unsigned)p.B, 256, 0, s>>>(a);

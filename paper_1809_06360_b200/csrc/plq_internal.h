@@ -37,9 +37,11 @@ enum SweepBuf {
   SB_COUNT
 };
 
-// stages of the tiled GEMM's cp.async ring in the large-mode sweep: 8-warp
-// CTAs (two per SM) take four (75 KB of the SM's 227 KB each), 16-warp CTAs two
-constexpr int sweep_tile_stages(int threads) { return threads == 256 ? 4 : 2; }
+// stages of the tiled GEMM's cp.async ring in the large-mode sweep.  Measured
+// on the cfg3 sweep (B200): 2 stages 13.0 ms, 4 stages 13.3 ms -- the deeper
+// ring's shared memory comes out of the L1 the panel / epilogue loads use, and
+// the GEMM k-loops were not waiting on their copies.
+constexpr int sweep_tile_stages(int threads) { return threads == 256 ? 2 : 2; }
 
 struct SweepLayout {
   int64_t off[SB_COUNT];     // offset in doubles within its space

@@ -297,11 +297,12 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         Z[(i - n) * Fw + c] = acc;
       }
     });
+    // (Mzu = Vzx Fu feeds only P's z-block, as Mzu': stored there directly)
     gemm_x<false, NT>(n + nz, m, n, bf.V, n, fup, ldfu, bf.tiles, [&](int i, int c, double acc) {
       if (i < n) {
         VF[i * Fw + n + c] = acc;
       } else {
-        Z[(i - n) * Fw + n + c] = acc;
+        P[c * ldw + n + (i - n)] = acc;
       }
     });
     for (int i = tid; i < n + nz; i += nt) {
@@ -348,11 +349,6 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           else
             Muu[u * m + (c - n)] = v;
         });
-    // P z-block = Mzu' (Mzu = Vzx Fu lives in Z's middle columns)
-    for (int idx = tid; idx < m * nz; idx += nt) {
-      const int u = idx / nz, c = idx % nz;
-      P[u * ldw + n + c] = Z[c * Fw + n + u];
-    }
     __syncthreads();
 
     // ---- gains

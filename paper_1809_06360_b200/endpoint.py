@@ -10,8 +10,11 @@ and the evaluation at concrete endpoints all run on the device
 * ``values`` / ``constraints`` hold the t = 0 entries only (the ones
   ``evaluate`` needs; ``values[0].const`` is not computed);
 * problems whose endpoint cannot be reached in every direction (feasibility
-  rows) raise :class:`UnsupportedPartition` instead of taking the reference's
-  value-gradient dual path (``gradient_duals``, ``endpoint.py:578-600``);
+  rows, e.g. ``T m < n``) are solved like the reference does: no multiplier
+  maps, ``evaluate`` checks the rows (``Infeasible``) and takes the
+  multipliers from the value-function gradient and the stationarity recursion
+  (``gradient_duals``, ``endpoint.py:566-587``) on the device; the rows in
+  ``constraints[0]`` are an orthonormal rotation of the reference's;
 * ``collect_diagnostics`` raises ``NotImplementedError`` (SVD defects).
 """
 
@@ -23,7 +26,7 @@ import dataclasses
 import numpy as np
 
 from . import _native
-from .errors import CholeskyFailure, FactorizationFailure, UnsupportedPartition
+from .errors import CholeskyFailure, FactorizationFailure, Infeasible, UnsupportedPartition
 from .parallel import INPUT_FIELDS, _ptr, _to_device, _torch, stack_problem
 from .problem import DEFAULT_TOLERANCES, AffinePolicy, LqrSolution
 
@@ -48,7 +51,7 @@ class ValueFunction:
 
 @dataclasses.dataclass(frozen=True, eq=False, repr=False)
 class ConstraintToGo:
-    """endpoint.py:86-105 (always empty on the GPU path)."""
+    """endpoint.py:86-105."""
 
     Hx: np.ndarray
     Hz: np.ndarray
@@ -57,6 +60,11 @@ class ConstraintToGo:
     @property
     def rows(self):
         return self.Hx.shape[0]
+
+    def residual(self, x, z):
+        if self.rows == 0:
+            return np.zeros(0)
+        return self.Hx @ x + self.Hz @ z + self.h1
 
     def residual(self, x, z):
         return np.zeros(0) if self.rows == 0 else self.Hx @ x + self.Hz @ z + self.h1
@@ -124,11 +132,14 @@ class EndpointBatch:
                 "Lam": torch.empty((B, T + 1, n, W), **f64), "E": torch.empty((B, n, W), **f64),
                 "status": torch.zeros((B,), dtype=torch.int32, device=self.device),
                 "gram_status": torch.zeros((B,), dtype=torch.int32, device=self.device),
+                "feas": torch.zeros((B, n, W), **f64),
+                "feas_rows": torch.zeros((B,), dtype=torch.int32, device=self.device),
             }
             self.point = {
                 "x": torch.empty((B, T + 1, n), **f64), "u": torch.empty((B, T, m), **f64),
                 "lam": torch.empty((B, T + 1, n), **f64), "mu": torch.empty((B, n), **f64),
                 "objective": torch.empty((B,), **f64), "kkt_inf": torch.empty((B,), **f64),
+                "feas_residual": torch.zeros((B,), **f64),
             }
         self._outs = _native.PlqEndpointOutputs(**{f: _ptr(self.out[f]) for f in _native.ENDPOINT_FIELDS})
         P = self._problem_struct(None)
@@ -171,23 +182,36 @@ class EndpointBatch:
                                             _ptr(self.workspace), self.ws_bytes, ctypes.c_void_p(stream.cuda_stream))
         _native.check(rc, "plq_endpoint_evaluate")
         self.launches = int(self.lib.plq_last_launch_count())
+        xi = x_init if x_init is not None else self._inputs["x_init"]
+        self._last_endpoints = (xi.cpu().numpy(), x_term.cpu().numpy())
         return self.point
 
-    def raise_for_status(self, require_multipliers=True):
+    def raise_for_status(self, require_multipliers=True, check_feasibility=False):
+        """Map the device status to the reference's exceptions.  ``require_multipliers``:
+        ``"strict"`` = ``solve_endpoint_affine(require_multipliers=True)`` (rows raise
+        ``FactorizationFailure``, endpoint.py:614-617); truthy = a failed Gram factorization
+        raises.  ``check_feasibility``: after ``evaluate``, rows violated by the endpoint pair
+        raise ``Infeasible`` (endpoint.py:516-523)."""
         st = self.out["status"].cpu().numpy()
         gs = self.out["gram_status"].cpu().numpy()
+        rows = self.out["feas_rows"].cpu().numpy()
         for b in range(self.B):
             if st[b] > 0:
                 raise CholeskyFailure(int(st[b]) - 1)
             if st[b] < 0:
-                if require_multipliers == "strict":
-                    # solve_endpoint_affine(require_multipliers=True), endpoint.py:628-631
-                    raise FactorizationFailure(None, "boundary constraints are linearly dependent "
-                                                     "(unreachable endpoint rows)")
-                raise UnsupportedPartition(0, "the endpoint cannot be reached in every direction "
-                                              "(feasibility rows); not supported on the GPU path")
+                raise UnsupportedPartition(0, "feasibility rows left but no buffer to return them")
+            if rows[b] > 0 and require_multipliers == "strict":
+                raise FactorizationFailure(None, "boundary constraints are linearly dependent "
+                                                 f"({int(rows[b])} unreachable endpoint rows)")
             if gs[b] > 0 and require_multipliers:
                 raise FactorizationFailure(int(gs[b]) - 1)
+        if check_feasibility and rows.any():
+            res = self.point["feas_residual"].cpu().numpy()
+            xi, xt = self._last_endpoints
+            for b in range(self.B):
+                scale = 1.0 + float(np.abs(xi[b]).max(initial=0.0)) + float(np.abs(xt[b]).max(initial=0.0))
+                if rows[b] > 0 and res[b] > self.tolerances.feas_tol * scale:
+                    raise Infeasible(float(res[b]))
 
 
 class EndpointAffineSolution:
@@ -204,11 +228,13 @@ class EndpointAffineSolution:
         v = o["value0"]
         self.values = (ValueFunction(v[:nn].reshape(n, n), v[nn:2 * nn].reshape(n, n),
                                      v[2 * nn:3 * nn].reshape(n, n), v[3 * nn:3 * nn + n], v[3 * nn + n:]),)
-        self.constraints = (ConstraintToGo(np.zeros((0, n)), np.zeros((0, n)), np.zeros(0)),)
+        r = int(o["feas_rows"])
+        Hf = o["feas"][:r]
+        self.constraints = (ConstraintToGo(Hf[:, :n].copy(), Hf[:, n:2 * n].copy(), Hf[:, 2 * n].copy()),)
         X, S, L, E = o["X"], o["S"], o["Lam"], o["E"]
         self.maps = TrajectoryMaps(X[:, :, :n], X[:, :, n:2 * n], X[:, :, 2 * n],
                                    S[:, :, :n], S[:, :, n:2 * n], S[:, :, 2 * n])
-        self.multipliers = None if int(o["gram_status"]) else MultiplierMaps(
+        self.multipliers = None if (int(o["gram_status"]) or r) else MultiplierMaps(
             L[:, :, :n], L[:, :, n:2 * n], L[:, :, 2 * n], E[:, :n], E[:, n:2 * n], E[:, 2 * n])
         self.diagnostics = None
         self._batch, self._index, self._problem = batch, index, problem
@@ -218,11 +244,21 @@ class EndpointAffineSolution:
         return self.constraints[0]
 
     def feasibility_residual(self, x_init, x_term):
-        return 0.0
+        res = self.feasibility.residual(np.asarray(x_init, float), np.asarray(x_term, float))
+        return float(np.abs(res).max()) if res.size else 0.0
 
     def evaluate(self, x_init, x_term, tolerances=DEFAULT_TOLERANCES):
-        """Numeric solution at concrete endpoints (endpoint.py:538-575)."""
-        if self.multipliers is None:
+        """Numeric solution at concrete endpoints (endpoint.py:507-546).  With
+        feasibility rows: ``Infeasible`` when the pair violates them, else the
+        multipliers come from ``gradient_duals`` (computed on the device)."""
+        x_init = np.asarray(x_init, dtype=np.float64)
+        x_term = np.asarray(x_term, dtype=np.float64)
+        if self.feasibility.rows:
+            residual = self.feasibility_residual(x_init, x_term)
+            scale = 1.0 + float(np.abs(x_init).max(initial=0.0)) + float(np.abs(x_term).max(initial=0.0))
+            if residual > tolerances.feas_tol * scale:
+                raise Infeasible(residual)
+        elif self.multipliers is None:
             raise FactorizationFailure(int(self._batch.out["gram_status"][self._index]) - 1)
         torch = self._batch.torch
         B, n = self._batch.B, self._batch.n
@@ -266,7 +302,7 @@ def solve_endpoint(problem, x_init, x_term, tolerances=DEFAULT_TOLERANCES, *, de
     ``problem.x_init`` is ignored in favour of ``x_init``."""
     batch = _batch_for(problem, tolerances, device)
     batch.raise_for_status(require_multipliers=True)
-    return EndpointAffineSolution(problem, batch).evaluate(x_init, x_term, tolerances)
+    return EndpointAffineSolution(problem, batch).evaluate(x_init, x_term, tolerances)   # Infeasible inside
 
 
 def solve_endpoint_batch(arrays, x_term, x_init=None, tolerances=DEFAULT_TOLERANCES, device=None):
@@ -285,7 +321,7 @@ def solve_endpoint_batch(arrays, x_term, x_init=None, tolerances=DEFAULT_TOLERAN
     with torch.cuda.device(dev):
         batch.affine(inputs)
         batch.evaluate(xt, xi)
-    batch.raise_for_status()
+    batch.raise_for_status(check_feasibility=True)
     batch._keep = (inputs, xt, xi)
     return batch
 

@@ -229,6 +229,57 @@ def endpoint_goldens():
              input_sha256=np.array(digest(batch)), **endpoint_case(a, 200 + cid))
 
 
+def endpoint_unreachable_goldens():
+    """Two-point-boundary problems whose horizon is too short to reach every
+    endpoint direction (T m < n): feasibility rows, no multiplier maps,
+    multipliers from gradient_duals (endpoint.py:566-587), Infeasible for a
+    pair that violates the rows -- all by the reference itself."""
+    from parlqr import endpoint as ref_endpoint
+    from parlqr.errors import Infeasible
+    rec = {}
+    cases = [("ref", 3, 1, 1, 61), ("ref", 5, 2, 2, 62), ("ref", 6, 2, 2, 63), ("ref", 4, 1, 3, 64),
+             ("cfg", 12, 4, 2, 65), ("cfg", 32, 8, 3, 66)]
+    for i, (kind, n, m, T, seed) in enumerate(cases):
+        if kind == "ref":
+            a = from_problem(ref_generate(n, m, T, seed=seed))
+        else:
+            a = synth.generate_one(n, m, T, seed)
+        prob = to_problem(a)
+        aff = ref_endpoint.solve_endpoint_affine(prob)
+        assert aff.multipliers is None and aff.feasibility.rows == n - T * m
+        rng = np.random.default_rng(300 + i)
+        x = prob.x_init.copy()
+        for _, dyn in prob.stages:
+            x = dyn.Fx @ x + dyn.Fu @ (0.3 * rng.standard_normal(prob.m)) + dyn.f1
+        z = x
+        sol = ref_endpoint.solve_endpoint(prob, prob.x_init, z)
+        bad = z + rng.standard_normal(n)
+        try:
+            ref_endpoint.solve_endpoint(prob, prob.x_init, bad)
+            raise AssertionError("expected Infeasible")
+        except Infeasible as exc:
+            bad_res = exc.residual
+        v0, mp = aff.values[0], aff.maps
+        out = {
+            "Kx": np.stack([p.Kx for p in aff.policies]), "Kz": np.stack([p.Kz for p in aff.policies]),
+            "k1": np.stack([p.k1 for p in aff.policies]),
+            "Vxx0": v0.Vxx, "Vzx0": v0.Vzx, "Vzz0": v0.Vzz, "vx10": v0.vx1, "vz10": v0.vz1,
+            "X": np.concatenate([mp.Ra, mp.Rz, mp.r1[:, :, None]], axis=2),
+            "S": np.concatenate([mp.Sa, mp.Sz, mp.s1[:, :, None]], axis=2),
+            "feas_rows": np.int64(aff.feasibility.rows),
+            "Hx": aff.feasibility.Hx, "Hz": aff.feasibility.Hz, "h1": aff.feasibility.h1,
+            "x_term": z, "states": sol.states, "controls": sol.controls, "lambdas": sol.lambdas,
+            "mu": sol.mu, "objective": np.float64(sol.objective), "kkt": np.float64(sol.kkt_residual_inf),
+            "x_bad": bad, "bad_residual": np.float64(bad_res),
+        }
+        for k, v in a.items():
+            rec[f"{i}/in/{k}"] = v
+        for k, v in out.items():
+            rec[f"{i}/out/{k}"] = v
+    rec["num"] = np.int64(len(cases))
+    save("endpoint_unreachable", **rec)
+
+
 def _with_singular_values(Fu, sig, seed):
     """Fu replaced by U diag(sig) V' with the same shape (random orthogonal
     U, V from a seeded QR)."""
@@ -404,6 +455,7 @@ def main():
     stored_case("uncontrollable", probs, Js)
     # two-point-boundary solves (endpoint.py:603-653) by the reference itself
     endpoint_goldens()
+    endpoint_unreachable_goldens()
     # tail stages at the rank threshold (mixed branch 0 < p < m, repair pass)
     rank_goldens()
     # JSON problem / solution files written by the reference itself
@@ -431,4 +483,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:           # regenerate single fixtures: make_golden.py endpoint_unreachable_goldens
+        for fn in sys.argv[1:]:
+            globals()[fn]()
+    else:
+        main()

@@ -88,7 +88,7 @@ def test_endpoint_reference_goldens_configs(name, kernel_path):
     batch = synth.generate_batch(cfg, seed=int(z["seed"]), count=1)
     a = O.problem_slice(batch, 0)
     out, pt, eb = _run(batch, z["x_term"][None])
-    assert eb.launches == 3
+    assert eb.launches == 4                      # point, duals (no-op without rows), evaluation, reduction
     ref = {k: z[k] for k in z.files}
     aff = O.solve_endpoint_affine(a)
     _check(out, pt, 0, ref, a, _floor(a, z["x_term"], aff, O.evaluate_endpoint(a, aff, a["x_init"], z["x_term"])))
@@ -144,8 +144,73 @@ def test_dependent_constraints():
     prob = plq.problem_from_arrays(synth.generate_one(3, 1, 1, seed=61))
     with pytest.raises(plq.FactorizationFailure):
         plq.solve_endpoint_affine(prob, require_multipliers=True)
-    with pytest.raises(plq.SolverError):
+    with pytest.raises(plq.Infeasible):
         plq.solve_endpoint(prob, np.zeros(3), np.ones(3))
+    aff = plq.solve_endpoint_affine(prob)
+    assert aff.multipliers is None and aff.feasibility.rows == 2
+
+
+def test_endpoint_unreachable_directions_reference_goldens(kernel_path):
+    """Horizons too short to reach every endpoint direction (T m < n): the
+    rows are returned, no multiplier maps are computed, and evaluate takes the
+    multipliers from gradient_duals (endpoint.py:566-587) on the device --
+    against the reference's own outputs, batched and through the drop-in."""
+    import paper_1809_06360_b200 as plq
+    z = np.load(os.path.join(GOLDEN, "endpoint_unreachable.npz"))
+    for i in range(int(z["num"])):
+        a = {k.split("/")[-1]: z[k] for k in z.files if k.startswith(f"{i}/in/")}
+        o = {k.split("/")[-1]: z[k] for k in z.files if k.startswith(f"{i}/out/")}
+        out, pt, eb = _run({k: v[None] for k, v in a.items()}, o["x_term"][None])
+        assert eb.launches == 4                      # point, duals, evaluation, reduction
+        r = int(o["feas_rows"])
+        assert int(out["feas_rows"][0]) == r and int(out["gram_status"][0]) == -1
+        sc = _scale(a)
+        for k in ("Kx", "Kz", "k1", "X", "S"):
+            assert rel_err(out[k][0], o[k]) <= 1e-9 * sc, (k, rel_err(out[k][0], o[k]))
+        # the rows span the reference's row space (an orthonormal rotation of them)
+        mine = out["feas"][0][:r]
+        ref_rows = np.concatenate([o["Hx"], o["Hz"], o["h1"][:, None]], axis=1)
+        coef = np.linalg.lstsq(ref_rows.T, mine.T, rcond=None)[0]
+        assert np.abs(ref_rows.T @ coef - mine.T).max() <= 1e-9 * sc
+        assert np.abs(coef @ coef.T - np.eye(r)).max() <= 1e-8 * sc
+        for k, rk in PT + (("objective", "objective"),):
+            assert rel_err(pt[k][0], o[rk]) <= 1e-8 * sc, (k, rel_err(pt[k][0], o[rk]))
+        assert pt["kkt_inf"][0] <= max(10 * float(o["kkt"]), 1e-8 * sc)
+        assert pt["feas_residual"][0] <= 1e-9 * sc
+        # drop-in: same solution, Infeasible for a pair off the rows, strict mode raises
+        prob = plq.problem_from_arrays(a)
+        sol = plq.solve_endpoint(prob, a["x_init"], o["x_term"])
+        assert rel_err(sol.lambdas, o["lambdas"]) <= 1e-8 * sc and rel_err(sol.mu, o["mu"]) <= 1e-8 * sc
+        with pytest.raises(plq.Infeasible) as ei:
+            plq.solve_endpoint(prob, a["x_init"], o["x_bad"])
+        assert 0.2 * float(o["bad_residual"]) <= ei.value.residual <= 5 * float(o["bad_residual"])
+        with pytest.raises(plq.FactorizationFailure):
+            plq.solve_endpoint_affine(prob, require_multipliers=True)
+    # a batch mixing reachable and unreachable problems is not possible (one T per batch);
+    # mixed ROW COUNTS are: an uncontrollable direction in one problem of a reachable batch
+    from paper_1809_06360_b200 import solve_endpoint_batch, synth
+    cfg = synth.CONFIGS[1].scaled(T=8, J=1)
+    batch = synth.generate_batch(cfg, seed=31, count=3)
+    batch["Fu"][1][:, 0, :] = 0.0                  # state 0 of problem 1 gets no direct control ...
+    batch["Fx"][1][:, 0, :] = 0.0                  # ... and no coupling: x0' = f1 only
+    batch["Fx"][1][:, 0, 0] = 1.0
+    zt = np.zeros((3, cfg.n))
+    for i in range(3):
+        a = O.problem_slice(batch, i)
+        x = a["x_init"].copy()
+        for t in range(cfg.T):
+            x = a["Fx"][t] @ x + a["f1"][t]
+        zt[i] = x                                     # reachable with u = 0
+    eb = solve_endpoint_batch(batch, zt)
+    rows = eb.out["feas_rows"].cpu().numpy()
+    assert rows[0] == 0 and rows[2] == 0 and rows[1] >= 1
+    for i in range(3):
+        a = O.problem_slice(batch, i)
+        aff = O.solve_endpoint_affine(a)
+        ev = O.evaluate_endpoint(a, aff, a["x_init"], zt[i])
+        assert aff["feas"][0].shape[0] == rows[i]
+        for k, rk in PT:
+            assert rel_err(eb.point[k][i].cpu().numpy(), ev[rk]) <= 1e-7, (i, k)
 
 
 def test_map_boundary_blocks_equal_value_gradients():

@@ -126,3 +126,30 @@ def test_oracle_smooth_matches_reference():
             assert rel_err(sm[k], zz[k]) <= 1e-12, (name, k)
         assert abs(sm["objective"] - float(zz["objective"])) <= 1e-12 * abs(float(zz["objective"]))
         assert sm["smooth_deviation"] <= 1e-8 and float(zz["deviation"]) <= 1e-8
+
+
+def test_oracle_endpoint_unreachable_matches_reference():
+    """Two-point-boundary problems with unreachable endpoint directions
+    (T m < n): the reference's own gains, maps, gradient-dual multipliers
+    (endpoint.py:566-587) and trajectories (tests/golden/endpoint_unreachable.npz)."""
+    import os
+
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "endpoint_unreachable.npz"))
+    for i in range(int(z["num"])):
+        a = {k.split("/")[-1]: z[k] for k in z.files if k.startswith(f"{i}/in/")}
+        o = {k.split("/")[-1]: z[k] for k in z.files if k.startswith(f"{i}/out/")}
+        aff = O.solve_endpoint_affine(a)
+        assert "Lam" not in aff and aff["feas"][0].shape[0] == int(o["feas_rows"])
+        scale = 1.0 + max(float(np.abs(v).max()) for v in a.values())
+        for k in ("Kx", "Kz", "k1", "X", "S"):
+            assert np.abs(aff[k] - o[k]).max() <= 1e-12 * scale * (1 + np.abs(o[k]).max()), k
+        for k, v in zip(("Hx", "Hz", "h1"), aff["feas"]):
+            assert np.abs(v - o[k]).max() <= 1e-11 * scale, k
+        ev = O.evaluate_endpoint(a, aff, a["x_init"], o["x_term"])
+        for k in ("states", "controls", "lambdas", "mu"):
+            assert np.abs(ev[k] - o[k]).max() <= 1e-11 * scale * (1 + np.abs(o[k]).max()), k
+        assert abs(ev["objective"] - float(o["objective"])) <= 1e-11 * scale * (1 + abs(float(o["objective"])))
+        assert ev["feas_residual"] <= 1e-9 * scale
+        bad = O.evaluate_endpoint(a, aff, a["x_init"], o["x_bad"])
+        assert bad["feas_residual"] == pytest.approx(float(o["bad_residual"]), rel=1e-9)
