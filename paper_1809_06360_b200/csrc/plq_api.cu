@@ -820,8 +820,11 @@ int plq_solve_parallel_host(const plq_problem_t* hp, const plq_outputs_t* ho, vo
 #ifdef PLQ_PHASE_PROFILE
 namespace plq {
 int sweep_small_phase_cycles(unsigned long long* out);
+int sweep_phase_cycles_256(unsigned long long* out);
 }
 // Measurement builds only (-DPLQ_PHASE_PROFILE, libparlqr_b200_prof.so):
 // per-CTA cycle counters of the specialized sweep's stage phases, 1024 x 16.
 extern "C" int plq_debug_phase_cycles(unsigned long long* out) { return plq::sweep_small_phase_cycles(out); }
+// the generic sweep's counters (256-thread instantiation)
+extern "C" int plq_debug_phase_cycles_generic(unsigned long long* out) { return plq::sweep_phase_cycles_256(out); }
 #endif

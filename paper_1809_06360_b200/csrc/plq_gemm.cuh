@@ -46,7 +46,10 @@ struct NoPre {
 
 // PRE: pre(i, j) (e.g. a Q-block entry in HBM) is loaded before each tile's
 // k-loop and the epilogue receives pre(i, j) + acc
-template <bool TA, int NW, class Epi, bool PRE = false, class Pre = NoPre, int NS = 2>
+// LOWER: tiles that lie entirely above the diagonal (n0 >= m0 + BM) are
+// skipped -- for symmetric results whose epilogue writes (i, j <= i) and
+// mirrors it.
+template <bool TA, int NW, class Epi, bool PRE = false, class Pre = NoPre, int NS = 2, bool LOWER = false>
 __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double* __restrict__ A, int lda,
                                                const double* __restrict__ B, int ldb, double* tiles, Epi epi,
                                                Pre pre = Pre()) {
@@ -63,6 +66,7 @@ __device__ __forceinline__ void cta_gemm_tiled(int M, int N, int K, const double
   const bool vec = ((lda | ldb) & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
   for (int tile = 0; tile < tmc * tnc; ++tile) {
     const int m0 = (tile / tnc) * BM, n0 = (tile % tnc) * BN;
+    if (LOWER && n0 >= m0 + BM) continue;
     double acc[2][4][2], pv[2][4][2];
 #pragma unroll
     for (int r = 0; r < 2; ++r)

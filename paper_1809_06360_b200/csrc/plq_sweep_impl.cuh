@@ -32,6 +32,25 @@ namespace plq {
 
 namespace {
 
+// Optional per-phase cycle accounting of the generic sweep (measurement build
+// -DPLQ_PHASE_PROFILE only): thread 0 of every CTA adds clock64() deltas per
+// stage phase into g_gen_phase[blockIdx.x][phase].
+#ifdef PLQ_PHASE_PROFILE
+__device__ unsigned long long g_gen_phase[1024][16];
+#define PLQ_GPH(k)                                                                              \
+  do {                                                                                          \
+    if (threadIdx.x == 0) {                                                                     \
+      const long long t_ = clock64();                                                           \
+      atomicAdd(&g_gen_phase[blockIdx.x & 1023][k], (unsigned long long)(t_ - t_last));         \
+      t_last = t_;                                                                              \
+    }                                                                                           \
+  } while (0)
+#else
+#define PLQ_GPH(k) \
+  do {             \
+  } while (0)
+#endif
+
 struct Bufs {
   double *V, *IN, *PGY, *MUU, *MISC, *VF, *Z, *MX, *H, *WIDE;
   double* tiles;   // tiled-GEMM staging (large mode) or nullptr
@@ -62,6 +81,23 @@ __device__ __forceinline__ void gemm_x_pre(int M, int N, int K, const double* A,
     }
   }
   cta_gemm<TA, false, 1, 1>(M, N, K, A, lda, B, ldb, [&](int i, int j, double acc) { epi(i, j, pre(i, j) + acc); });
+}
+
+// Symmetric result C = pre + op(A) B (Mxx = Qxx + Fx' VFx, Vxx += P'G): in
+// large mode only the tiles on / below the diagonal are computed and the
+// epilogue mirrors (i, j <= i) into (j, i), so C is exactly symmetric and no
+// symmetrization pass is needed (what the n = 64 kernel does); returns false
+// when the shape takes the direct path (caller symmetrizes as before).
+template <bool TA, int NT, class Pre, class Epi>
+__device__ __forceinline__ bool gemm_x_pre_sym(int N, int K, const double* A, int lda, const double* B, int ldb,
+                                               double* tiles, Pre pre, Epi epi) {
+  if constexpr (NT >= 256) {
+    if (tiles != nullptr && (long long)N * N * K >= 16384) {
+      cta_gemm_tiled<TA, NT / 32, Epi, true, Pre, sweep_tile_stages(NT), true>(N, N, K, A, lda, B, ldb, tiles, epi, pre);
+      return true;
+    }
+  }
+  return false;
 }
 
 __device__ __forceinline__ void cho_solve_x(const double* L, int m, int ldl, double* X, int W, int ldx) {
@@ -249,6 +285,9 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   int r = serial ? 0 : n;
   __syncthreads();
 
+#ifdef PLQ_PHASE_PROFILE
+  long long t_last = clock64();
+#endif
   for (int s = L - 1; s >= 0; --s) {
     const int64_t st = b * T + (lo + s);
     // ---- stage inputs -> shared/scratch (coalesced global reads)
@@ -287,6 +326,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     }
     __syncthreads();
 
+    PLQ_GPH(0);
     // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217).
     // The f1 column ([w; mz1] = [Vxx; Vzx] f1 + [vx1; vz1]) is a thread-per-row
     // matvec, so the GEMM's N is n + m (a whole 64-wide tile less in large mode)
@@ -320,6 +360,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         Z[(i - n) * Fw + n + m] = vz1[i - n] + (t0 + t1);
     }
     __syncthreads();
+    PLQ_GPH(1);
     // ---- GEMM2: M-terms (endpoint.py:209-211, 215-216); the w column
     // (mx1 = qx1 + Fx' w, mu1 = qu1 + Fu' w) again as a matvec
     for (int i = tid; i < n + m; i += nt) {
@@ -337,9 +378,17 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     }
     // x rows over the x columns only (the Mxu block is never used), u rows
     // over all columns
-    gemm_x_pre<true, NT>(
-        n, n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return Qxx_s[i * n + c]; },
-        [&](int i, int c, double v) { Vxx[i * n + c] = v; });   // Mxx in place (Vxx was consumed by GEMM1)
+    if (!gemm_x_pre_sym<true, NT>(
+            n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return c <= i ? Qxx_s[i * n + c] : 0.0; },
+            [&](int i, int c, double v) {
+              if (c <= i) {
+                Vxx[i * n + c] = v;
+                Vxx[c * n + i] = v;
+              }
+            }))
+      gemm_x_pre<true, NT>(
+          n, n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return Qxx_s[i * n + c]; },
+          [&](int i, int c, double v) { Vxx[i * n + c] = v; });   // Mxx in place (Vxx was consumed by GEMM1)
     gemm_x_pre<true, NT>(
         m, n + m, n, fup, ldfu, VF, Fw, bf.tiles,
         [&](int u, int c) { return c < n ? Qux_s[u * n + c] : Quu_s[u * m + (c - n)]; },
@@ -351,6 +400,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         });
     __syncthreads();
 
+    PLQ_GPH(2);
     // ---- gains
     bool chol = (r == 0);
     if (r != 0) {
@@ -519,6 +569,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         }
       }
     }
+    PLQ_GPH(3);
     if (chol) {
       // G = -Muu^{-1} P: unconstrained stage, or p = 0 in a constrained one
       // (endpoint.py:239-250 with Zw = I; serial.py:63-70)
@@ -540,6 +591,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         __syncthreads();
         break;
       }
+      PLQ_GPH(4);
       if (blocked) {
         gtrsm8<1, NT / 32>(Muu, m, m, binv, G, W, ldw, wsc, tid, csync);
       } else {
@@ -552,6 +604,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
     }
 
+    PLQ_GPH(5);
     // ---- policy outputs (parallel.py:224-236 stacking)
     for (int idx = tid; idx < m * n; idx += nt) {
       const int u = idx / n, c = idx % n;
@@ -566,6 +619,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     // have G = -Muu^{-1} P, so Y = 0 in exact arithmetic and the update is the
     // standard Riccati form V += P'G (K = m: half the update, no Y GEMM), as
     // in the specialized kernels.
+    PLQ_GPH(6);
     const int KV = chol ? m : 2 * m;
     if (!chol) {
       gemm_x<false, NT>(m, W, m, Muu, m, G, ldw, bf.tiles,
@@ -574,11 +628,21 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     }
     // x rows over the x columns only (no discarded Vxz block), z rows over
     // [x | z] columns, the constant column as a matvec
+    PLQ_GPH(7);
     // (the addends -- Mxx in Vxx, Mzx in Z, Vzz -- are loaded before each
     // tile's k-loop: L2 / DRAM latency of the scratch hides behind the DMMAs)
-    gemm_x_pre<true, NT>(
-        n, n, KV, P, ldw, G, ldw, bf.tiles, [&](int i, int c) { return Vxx[i * n + c]; },
-        [&](int i, int c, double v) { Vxx[i * n + c] = v; });
+    const bool vsym = gemm_x_pre_sym<true, NT>(
+        n, KV, P, ldw, G, ldw, bf.tiles, [&](int i, int c) { return c <= i ? Vxx[i * n + c] : 0.0; },
+        [&](int i, int c, double v) {
+          if (c <= i) {
+            Vxx[i * n + c] = v;
+            Vxx[c * n + i] = v;
+          }
+        });
+    if (!vsym)
+      gemm_x_pre<true, NT>(
+          n, n, KV, P, ldw, G, ldw, bf.tiles, [&](int i, int c) { return Vxx[i * n + c]; },
+          [&](int i, int c, double v) { Vxx[i * n + c] = v; });
     if (nz)
       gemm_x_pre<true, NT>(
           nz, 2 * n, KV, P + n, ldw, G, ldw, bf.tiles,
@@ -603,8 +667,9 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         vz1[i - n] = Z[(i - n) * Fw + n + m] + (t0 + t1);
     }
     __syncthreads();
-    // symmetrize Vxx: 0.5 * (V + V')
-    for (int idx = tid; idx < nn; idx += nt) {
+    PLQ_GPH(8);
+    // symmetrize Vxx: 0.5 * (V + V') (large mode: mirrored in the epilogues above)
+    for (int idx = tid; idx < nn && !vsym; idx += nt) {
       const int i = idx / n, c = idx % n;
       if (i < c) {
         const double v = 0.5 * (Vxx[i * n + c] + Vxx[c * n + i]);
@@ -697,7 +762,19 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) sweep_kernel(SweepArg
 
 // Launch / occupancy wrappers of one CTA size; each instantiation is compiled
 // in its own translation unit (plq_sweep_t<NT>.cu) so the build parallelizes.
+#ifdef PLQ_PHASE_PROFILE
+#define PLQ_SWEEP_PHASE_ACCESSOR(NT)                                                                 \
+  int sweep_phase_cycles_##NT(unsigned long long* out) {                                             \
+    if (cudaMemcpyFromSymbol(out, g_gen_phase, sizeof(g_gen_phase)) != cudaSuccess) return -1;       \
+    static unsigned long long zero[1024][16];                                                        \
+    return cudaMemcpyToSymbol(g_gen_phase, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;              \
+  }
+#else
+#define PLQ_SWEEP_PHASE_ACCESSOR(NT)
+#endif
+
 #define PLQ_SWEEP_INSTANTIATE(NT)                                                          \
+  PLQ_SWEEP_PHASE_ACCESSOR(NT)                                                             \
   int launch_sweep_##NT(const SweepArgs& a, int grid, size_t smem, cudaStream_t s) {       \
     sweep_kernel<NT, false><<<grid, NT, smem, s>>>(a);                                     \
     return cudaGetLastError() == cudaSuccess ? 0 : -1;                                     \

@@ -24,8 +24,15 @@ NAMES = ["copy wait", "f1 column", "GEMM1", "GEMM2", "tail (QR)", "Cholesky solv
          "value-update k-loops (warp 0)", "GEMM1 k-loops (warp 0)", "Cholesky diag factor + panel (n=64)"]
 
 
+GENERIC_NAMES = ["stage start (input staging / loop)", "GEMM1 (+ f1 column)", "GEMM2 (+ w column)",
+                 "constrained-stage gains (QR tail)", "Cholesky factor (+ fused forward solve)", "backward solve",
+                 "policy stores", "Y = P + Muu G (constrained stages)", "value update (+ constant column)",
+                 "symmetrize / stage end"] + ["-"] * 6
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--generic", action="store_true", help="the generic sweep's counters (plq_sweep_impl.cuh)")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--B", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
@@ -52,7 +59,10 @@ def main():
                                          ctypes.c_void_p(stream.cuda_stream))
     run()
     torch.cuda.synchronize()
-    lib.plq_debug_phase_cycles(ctypes.c_void_p(buf.ctypes.data))   # reset
+    reader = lib.plq_debug_phase_cycles_generic if args.generic else lib.plq_debug_phase_cycles
+    reader.argtypes = [ctypes.c_void_p]
+    reader.restype = ctypes.c_int
+    reader(ctypes.c_void_p(buf.ctypes.data))   # reset
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.reps):
@@ -60,8 +70,11 @@ def main():
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.reps
-    assert lib.plq_debug_phase_cycles(ctypes.c_void_p(buf.ctypes.data)) == 0
+    assert reader(ctypes.c_void_p(buf.ctypes.data)) == 0
     tot = buf.sum(axis=0).astype(np.float64)
+    global NAMES
+    if args.generic:
+        NAMES = GENERIC_NAMES
     ctas = int((buf.sum(axis=1) > 0).sum())   # CTAs >= 1024 fold onto blockIdx % 1024
     stages = B * cfg.T * args.reps
     out = {"config": cfg.name, "B": B, "sweep_ms": ms, "ctas": ctas,
