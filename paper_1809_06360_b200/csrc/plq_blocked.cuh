@@ -276,9 +276,11 @@ __device__ __forceinline__ void warp_sum_batch(double (&v)[N8]) {
 
 // TS != nullptr keeps T (8 x 8) in shared memory instead of registers (for
 // register-capped 16-warp CTAs).
+// VS != nullptr: the reflectors V (rows x 8, explicit unit diagonal / zeros)
+// are also stored there, so the trailing update reads them from shared memory.
 template <int RS>
 __device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb, int rows, double* rdiag,
-                                              double* VT, int lane, double* TS = nullptr) {
+                                              double* VT, int lane, double* TS = nullptr, double* VS = nullptr) {
   double a[RS][8];
 #pragma unroll
   for (int s = 0; s < RS; ++s)
@@ -393,6 +395,10 @@ __device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb
       double v[8];
 #pragma unroll
       for (int l = 0; l < 8; ++l) v[l] = (l >= pb || li < l) ? 0.0 : (li == l ? 1.0 : a[s][l]);
+      if (VS != nullptr) {
+#pragma unroll
+        for (int l = 0; l < 8; ++l) VS[li * 8 + l] = v[l];
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         double sacc = 0.0;
@@ -406,14 +412,15 @@ __device__ __forceinline__ void qr_panel_regs(double* A, int lda, int p0, int pb
 
 template <int NWG, class Sync, int RS = 0>
 __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X, int W, int ldx, double* rdiag,
-                                     double* VT, double* wsc, int gt, Sync sync, double* TS = nullptr) {
+                                     double* VT, double* wsc, int gt, Sync sync, double* TS = nullptr,
+                                     double* VS = nullptr) {
   const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, q = lane & 3;
   double* ws = wsc + gw * 64;
   for (int p0 = 0; p0 < M; p0 += 8) {
     const int pb = min(8, M - p0);
     const int rows = r - p0;   // panel rows p0 .. r-1 (local index li)
     if constexpr (RS > 0) {
-      if (gw == 0) qr_panel_regs<RS>(A, lda, p0, pb, rows, rdiag, VT, lane, TS);
+      if (gw == 0) qr_panel_regs<RS>(A, lda, p0, pb, rows, rdiag, VT, lane, TS, VS);
     } else if (gw == 0) {
       double tau[8];
 #pragma unroll
@@ -533,6 +540,23 @@ __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X
         }
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) dmma884(y0, y1, avs[ks], bvs[ks]);
+      } else if (VS != nullptr) {
+        // any row count: C (L2 / DRAM scratch) loaded 8 k-steps at a time
+        // before their DMMAs -- a quarter of the latency exposures of a
+        // load-per-step loop; the reflectors come from shared memory
+        for (int kk0 = 0; kk0 < rows; kk0 += 32) {
+          double bvs[8];
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int l = kk0 + 4 * ks + q;
+            bvs[ks] = (l < rows && g < ncol) ? C[l * ldc + g] : 0.0;
+          }
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int l = kk0 + 4 * ks + q;
+            dmma884(y0, y1, l < rows ? VS[l * 8 + g] : 0.0, bvs[ks]);
+          }
+        }
       } else {
 #pragma unroll 4
         for (int kk = 0; kk < rows; kk += 4) {
@@ -570,6 +594,31 @@ __device__ __forceinline__ void gqr8(double* A, int r, int M, int lda, double* X
           if (i < rows) {
             if (j < ncol) C[i * ldc + j] = cur[bb][0] - c0;
             if (j + 1 < ncol) C[i * ldc + j + 1] = cur[bb][1] - c1;
+          }
+        }
+      } else if (VS != nullptr) {
+        const int j = 2 * q;
+        for (int b00 = 0; b00 < rows; b00 += 32) {   // four 8-row bands: loads first
+          double cur[4][2];
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int i = b00 + bb * 8 + g;
+            cur[bb][0] = (i < rows && j < ncol) ? C[i * ldc + j] : 0.0;
+            cur[bb][1] = (i < rows && j + 1 < ncol) ? C[i * ldc + j + 1] : 0.0;
+          }
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int i = b00 + bb * 8 + g;
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 4) {
+              const int k = kk + q;
+              dmma884(c0, c1, i < rows ? VT[i * 8 + k] : 0.0, ws[k * 8 + g]);
+            }
+            if (i < rows) {
+              if (j < ncol) C[i * ldc + j] = cur[bb][0] - c0;
+              if (j + 1 < ncol) C[i * ldc + j + 1] = cur[bb][1] - c1;
+            }
           }
         }
       } else {

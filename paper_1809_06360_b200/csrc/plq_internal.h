@@ -43,6 +43,11 @@ enum SweepBuf {
 // the GEMM k-loops were not waiting on their copies.
 constexpr int sweep_tile_stages(int threads) { return threads == 256 ? 2 : 2; }
 
+// large mode, blocked factorizations, m <= 64: the Cholesky of Muu runs on a
+// shared-memory copy (m x (m + 4) doubles behind the MISC scratch) instead of
+// the L2-resident scratch -- its 8 block steps are latency chains
+__host__ __device__ inline bool sweep_muu_in_smem(int n, int m) { return n >= 48 && m >= 16 && m <= 64; }
+
 struct SweepLayout {
   int64_t off[SB_COUNT];     // offset in doubles within its space
   int in_smem[SB_COUNT];

@@ -37,7 +37,8 @@ SweepLayout plan_sweep(int n, int m, int threads, size_t smem_budget) {
   sz[SB_MUU] = 2LL * m * m;
   // tau, rdiag, reduction (32), flags (2), blocked scratch: block inverses,
   // per-warp tiles, V T' (plq_blocked.cuh)
-  sz[SB_MISC] = 2LL * m + 32 + 2 + ((m + 7) / 8) * 64LL + (threads / 32) * 64LL + 8LL * n + 64;
+  sz[SB_MISC] = 2LL * m + 32 + 2 + ((m + 7) / 8) * 64LL + (threads / 32) * 64LL + 16LL * n + 64 +
+                (sweep_muu_in_smem(n, m) ? (int64_t)m * (m + 4) + 2 : 0);
   sz[SB_VF] = n * Fw;
   sz[SB_Z] = n * Fw;
   sz[SB_MX] = 0;   // Mxx / mx1 are written into Vxx / vx1 in place

@@ -242,6 +242,9 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
   double* binv = red + 34;
   double* wsc = binv + ((m + 7) / 8) * 64;
   double* vts = wsc + (NT / 32) * 64;
+  // shared-memory home of Muu for the blocked Cholesky (large mode, m <= 64), 16-byte aligned
+  // (every MISC sub-buffer has an even length, so this stays 16-byte aligned)
+  double* muus = (a.lay.large && sweep_muu_in_smem(n, m)) ? vts + 16 * n + 64 : nullptr;
   auto csync = [] { __syncthreads(); };
   const bool blocked = m >= 16;
   double* VF = bf.VF;
@@ -345,19 +348,49 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         P[c * ldw + n + (i - n)] = acc;
       }
     });
-    for (int i = tid; i < n + nz; i += nt) {
-      const double* vr = bf.V + (size_t)i * n;
-      double t0 = 0.0, t1 = 0.0;
-      int k = 0;
-      for (; k + 1 < n; k += 2) {
-        t0 += vr[k] * f1at(k);
-        t1 += vr[k + 1] * f1at(k + 1);
+    if (qdirect) {
+      // warp per row, lanes over k: coalesced reads of V's rows (the scratch is in L2 / DRAM)
+      const int lane = tid & 31, wp = tid >> 5, nwp = nt >> 5;
+      for (int i0 = wp; i0 < n + nz; i0 += 2 * nwp) {
+        const int i1 = i0 + nwp;
+        const double* v0 = bf.V + (size_t)i0 * n;
+        const double* v1 = bf.V + (size_t)(i1 < n + nz ? i1 : i0) * n;
+        double t0 = 0.0, t1 = 0.0;
+        for (int k = lane; k < n; k += 32) {
+          const double f = f1p[k];
+          t0 += v0[k] * f;
+          t1 += v1[k] * f;
+        }
+        t0 = warp_sum(t0);
+        t1 = warp_sum(t1);
+        if (lane == 0) {
+          if (i0 < n)
+            VF[i0 * Fw + n + m] = vx1[i0] + t0;
+          else
+            Z[(i0 - n) * Fw + n + m] = vz1[i0 - n] + t0;
+          if (i1 < n + nz) {
+            if (i1 < n)
+              VF[i1 * Fw + n + m] = vx1[i1] + t1;
+            else
+              Z[(i1 - n) * Fw + n + m] = vz1[i1 - n] + t1;
+          }
+        }
       }
-      if (k < n) t0 += vr[k] * f1at(k);
-      if (i < n)
-        VF[i * Fw + n + m] = vx1[i] + (t0 + t1);
-      else
-        Z[(i - n) * Fw + n + m] = vz1[i - n] + (t0 + t1);
+    } else {
+      for (int i = tid; i < n + nz; i += nt) {
+        const double* vr = bf.V + (size_t)i * n;
+        double t0 = 0.0, t1 = 0.0;
+        int k = 0;
+        for (; k + 1 < n; k += 2) {
+          t0 += vr[k] * f1at(k);
+          t1 += vr[k + 1] * f1at(k + 1);
+        }
+        if (k < n) t0 += vr[k] * f1at(k);
+        if (i < n)
+          VF[i * Fw + n + m] = vx1[i] + (t0 + t1);
+        else
+          Z[(i - n) * Fw + n + m] = vz1[i - n] + (t0 + t1);
+      }
     }
     __syncthreads();
     PLQ_GPH(1);
@@ -427,6 +460,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         VF[i * Fw + n + m] = t;
       }
       __syncthreads();
+      PLQ_GPH(9);
       // stack [Nx | Nz=Hz | n1 = Hx f1 + h1] in place in H
       for (int idx = tid; idx < r * n; idx += nt) {
         const int i = idx / n, c = idx % n;
@@ -434,13 +468,16 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       for (int i = tid; i < r; i += nt) H[i * ldw + cc] += VF[i * Fw + n + m];
       __syncthreads();
+      PLQ_GPH(10);
       if (r >= m) {
         if (blocked && NT >= 256 && r <= 128)
-          gqr8<NT / 32, decltype(csync), 4>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync, vts + 8 * n);
+          gqr8<NT / 32, decltype(csync), 4>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync, vts + 8 * n,
+                                            vts + 8 * n + 64);
         else if (blocked)
           gqr8<NT / 32>(VF + n, r, m, Fw, H, W, ldw, rdiag, vts, wsc, tid, csync);
         else
           cta_householder_qr(VF + n, r, m, Fw, H, W, ldw, tau, rdiag, red);
+        PLQ_GPH(11);
         double rmax = 0.0, pf = 0.0;
         for (int i = 0; i < m; ++i) rmax = fmax(rmax, fabs(rdiag[i]));
         for (int idx = tid; idx < m * m; idx += nt) {
@@ -486,6 +523,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
             }
           }
           __syncthreads();
+          PLQ_GPH(12);
           double pz = 0.0;
           for (int idx = tid; idx < m * W; idx += nt) {
             const int u = idx / W, c = idx % W;
@@ -583,9 +621,16 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           G[u * ldw + c] = P[u * ldw + c];
         }
       }
+      double* Mc = Muu;   // the factorization's working copy
+      int ldm = m;
+      if (blocked && muus != nullptr) {
+        ldm = m + 4;
+        Mc = muus;
+        for (int idx = tid; idx < m * m; idx += nt) Mc[(idx / m) * ldm + idx % m] = Muu[idx];
+      }
       if (tid == 0) *iflag = 0;
       __syncthreads();
-      if (!(blocked ? gchol8<NT / 32>(Muu, m, m, binv, iflag, tid, csync, nullptr, G, W, ldw, wsc, P, -1.0)
+      if (!(blocked ? gchol8<NT / 32>(Mc, m, ldm, binv, iflag, tid, csync, nullptr, G, W, ldw, wsc, P, -1.0)
                     : cta_cholesky(Lm, m, m, iflag))) {
         if (tid == 0) *sflag = 1 + s;
         __syncthreads();
@@ -593,7 +638,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       PLQ_GPH(4);
       if (blocked) {
-        gtrsm8<1, NT / 32>(Muu, m, m, binv, G, W, ldw, wsc, tid, csync);
+        gtrsm8<1, NT / 32>(Mc, m, ldm, binv, G, W, ldw, wsc, tid, csync);
       } else {
         cho_solve_x(Lm, m, m, G, W, ldw);
         for (int idx = tid; idx < m * W; idx += nt) {

@@ -25,9 +25,10 @@ NAMES = ["copy wait", "f1 column", "GEMM1", "GEMM2", "tail (QR)", "Cholesky solv
 
 
 GENERIC_NAMES = ["stage start (input staging / loop)", "GEMM1 (+ f1 column)", "GEMM2 (+ w column)",
-                 "constrained-stage gains (QR tail)", "Cholesky factor (+ fused forward solve)", "backward solve",
+                 "tail: negate / certificates / row shift (rest of the constrained stage)", "Cholesky factor (+ fused forward solve)", "backward solve",
                  "policy stores", "Y = P + Muu G (constrained stages)", "value update (+ constant column)",
-                 "symmetrize / stage end"] + ["-"] * 6
+                 "tail: norms + N = Hx F", "tail: stack copy", "tail: Householder QR (gqr8)",
+                 "tail: R inverse + back substitution", "-", "-", "-"]
 
 
 def main():
