@@ -39,7 +39,9 @@ namespace plq {
 // Xsrc (optional, same stride) supplies the right-hand side instead of X's
 // own contents, scaled by xscale: X <- L^{-1} (xscale * Xsrc) with no copy
 // pass (block row k of Xsrc is read once, in step k).
-template <int NWG, class Sync>
+// BATCH: the k-loops over already-solved rows of X load 8 k-steps of X before
+// their DMMAs (X in L2 / DRAM scratch: a quarter of the latency exposures).
+template <int NWG, bool BATCH = false, class Sync>
 __device__ __forceinline__ bool gchol8(double* A, int m, int lda, double* Linv, int* flag, int gt, Sync sync,
                                        double* Ld = nullptr, double* X = nullptr, int W = 0, int ldx = 0,
                                        double* wsc = nullptr, const double* Xsrc = nullptr, double xscale = 1.0) {
@@ -119,12 +121,28 @@ __device__ __forceinline__ bool gchol8(double* A, int m, int lda, double* Linv, 
       const double* D = Linv + (k0 >> 3) * 64;
       const int j0 = (t - nschur) * 8;
       double c0 = 0.0, c1 = 0.0;
+      if constexpr (BATCH) {
+        for (int kk0 = 0; kk0 < k0; kk0 += 32) {
+          double bvs[8];
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int k = kk0 + 4 * ks + q;
+            bvs[ks] = (k < k0 && j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
+          }
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int k = kk0 + 4 * ks + q;
+            dmma884(c0, c1, (k < k0 && g < rb) ? A[(k0 + g) * lda + k] : 0.0, bvs[ks]);
+          }
+        }
+      } else {
 #pragma unroll 4
-      for (int kk = 0; kk < k0; kk += 4) {
-        const int k = kk + q;
-        const double av = (g < rb) ? A[(k0 + g) * lda + k] : 0.0;
-        const double bv = (j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
-        dmma884(c0, c1, av, bv);
+        for (int kk = 0; kk < k0; kk += 4) {
+          const int k = kk + q;
+          const double av = (g < rb) ? A[(k0 + g) * lda + k] : 0.0;
+          const double bv = (j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
+          dmma884(c0, c1, av, bv);
+        }
       }
       const int j = j0 + 2 * q;
       const double* Xs = Xsrc != nullptr ? Xsrc : X;
@@ -208,7 +226,7 @@ __device__ __forceinline__ void gtri_inv_upper8(const double* R, int m, int ldr,
 // MODE 0: L x = b (L lower, forward; T(k,c) = L[k][c], D = Linv)
 // MODE 1: L' x = b (backward; T(k,c) = L[c][k], D = Linv')
 // MODE 2: R x = b (R upper, backward; T(k,c) = R[k][c], D = Rinv)
-template <int MODE, int NWG, class Sync>
+template <int MODE, int NWG, bool BATCH = false, class Sync>
 __device__ __forceinline__ void gtrsm8(const double* T, int m, int ldt, const double* Dinv, double* X, int W, int ldx,
                                        double* wsc, int gt, Sync sync) {
   const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, q = lane & 3;
@@ -223,15 +241,34 @@ __device__ __forceinline__ void gtrsm8(const double* T, int m, int ldt, const do
     for (int tj = gw; tj < tn; tj += NWG) {
       const int j0 = tj * 8;
       double c0 = 0.0, c1 = 0.0;
+      if constexpr (BATCH) {
+        for (int kk0 = c_lo; kk0 < c_hi; kk0 += 32) {
+          double bvs[8];
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int k = kk0 + 4 * ks + q;
+            bvs[ks] = (k < c_hi && j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
+          }
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int k = kk0 + 4 * ks + q;
+            const int i = k0 + g;
+            double av = 0.0;
+            if (k < c_hi && g < rb) av = (MODE == 1) ? T[k * ldt + i] : T[i * ldt + k];
+            dmma884(c0, c1, av, bvs[ks]);
+          }
+        }
+      } else {
 #pragma unroll 4
-      for (int kk = c_lo; kk < c_hi; kk += 4) {
-        const int k = kk + q;
-        const bool kv = k < c_hi;
-        const int i = k0 + g;
-        double av = 0.0;
-        if (kv && g < rb) av = (MODE == 1) ? T[k * ldt + i] : T[i * ldt + k];
-        const double bv = (kv && j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
-        dmma884(c0, c1, av, bv);
+        for (int kk = c_lo; kk < c_hi; kk += 4) {
+          const int k = kk + q;
+          const bool kv = k < c_hi;
+          const int i = k0 + g;
+          double av = 0.0;
+          if (kv && g < rb) av = (MODE == 1) ? T[k * ldt + i] : T[i * ldt + k];
+          const double bv = (kv && j0 + g < W) ? X[k * ldx + j0 + g] : 0.0;
+          dmma884(c0, c1, av, bv);
+        }
       }
       // R tile (rows g < rb of block k, columns j0 + 2q + e) -> warp scratch
       const int j = j0 + 2 * q;

@@ -330,107 +330,143 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     __syncthreads();
 
     PLQ_GPH(0);
-    // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217).
-    // The f1 column ([w; mz1] = [Vxx; Vzx] f1 + [vx1; vz1]) is a thread-per-row
-    // matvec, so the GEMM's N is n + m (a whole 64-wide tile less in large mode)
-    gemm_x<false, NT>(n + nz, n, n, bf.V, n, fxp, ldfx, bf.tiles, [&](int i, int c, double acc) {
-      if (i < n) {
-        VF[i * Fw + c] = acc;
-      } else {
-        Z[(i - n) * Fw + c] = acc;
+    // First stage of an endpoint segment: V = 0, [vx1; vz1] = 0 and the rows are
+    // H = [I | -I | 0] (endpoint.py:182-191), so every product with V is an
+    // exact zero and N = Hx F = F: the GEMMs of this stage reduce to copies.
+    const bool vzero = a.lay.large && s == L - 1 && !serial && !(a.endpoint_terminal && j == J - 1);
+    if (vzero) {
+      for (int idx = tid; idx < n * Fw; idx += nt) {
+        VF[idx] = 0.0;
+        Z[idx] = 0.0;
       }
-    });
-    // (Mzu = Vzx Fu feeds only P's z-block, as Mzu': stored there directly)
-    gemm_x<false, NT>(n + nz, m, n, bf.V, n, fup, ldfu, bf.tiles, [&](int i, int c, double acc) {
-      if (i < n) {
-        VF[i * Fw + n + c] = acc;
-      } else {
-        P[c * ldw + n + (i - n)] = acc;
-      }
-    });
-    if (qdirect) {
-      // warp per row, lanes over k: coalesced reads of V's rows (the scratch is in L2 / DRAM)
-      const int lane = tid & 31, wp = tid >> 5, nwp = nt >> 5;
-      for (int i0 = wp; i0 < n + nz; i0 += 2 * nwp) {
-        const int i1 = i0 + nwp;
-        const double* v0 = bf.V + (size_t)i0 * n;
-        const double* v1 = bf.V + (size_t)(i1 < n + nz ? i1 : i0) * n;
-        double t0 = 0.0, t1 = 0.0;
-        for (int k = lane; k < n; k += 32) {
-          const double f = f1p[k];
-          t0 += v0[k] * f;
-          t1 += v1[k] * f;
+      for (int idx = tid; idx < m * nz; idx += nt) P[(idx / nz) * ldw + n + idx % nz] = 0.0;
+    } else {
+      // ---- GEMM1: [VF; Z] = [Vxx; Vzx] F  (endpoint.py:206-208, 212-213, 217).
+      // The f1 column ([w; mz1] = [Vxx; Vzx] f1 + [vx1; vz1]) is a thread-per-row
+      // matvec, so the GEMM's N is n + m (a whole 64-wide tile less in large mode)
+      gemm_x<false, NT>(n + nz, n, n, bf.V, n, fxp, ldfx, bf.tiles, [&](int i, int c, double acc) {
+        if (i < n) {
+          VF[i * Fw + c] = acc;
+        } else {
+          Z[(i - n) * Fw + c] = acc;
         }
-        t0 = warp_sum(t0);
-        t1 = warp_sum(t1);
-        if (lane == 0) {
-          if (i0 < n)
-            VF[i0 * Fw + n + m] = vx1[i0] + t0;
-          else
-            Z[(i0 - n) * Fw + n + m] = vz1[i0 - n] + t0;
-          if (i1 < n + nz) {
-            if (i1 < n)
-              VF[i1 * Fw + n + m] = vx1[i1] + t1;
+      });
+      // (Mzu = Vzx Fu feeds only P's z-block, as Mzu': stored there directly)
+      gemm_x<false, NT>(n + nz, m, n, bf.V, n, fup, ldfu, bf.tiles, [&](int i, int c, double acc) {
+        if (i < n) {
+          VF[i * Fw + n + c] = acc;
+        } else {
+          P[c * ldw + n + (i - n)] = acc;
+        }
+      });
+      if (qdirect) {
+        // warp per row, lanes over k: coalesced reads of V's rows (the scratch is in L2 / DRAM)
+        const int lane = tid & 31, wp = tid >> 5, nwp = nt >> 5;
+        for (int i0 = wp; i0 < n + nz; i0 += 2 * nwp) {
+          const int i1 = i0 + nwp;
+          const double* v0 = bf.V + (size_t)i0 * n;
+          const double* v1 = bf.V + (size_t)(i1 < n + nz ? i1 : i0) * n;
+          double t0 = 0.0, t1 = 0.0;
+          for (int k = lane; k < n; k += 32) {
+            const double f = f1p[k];
+            t0 += v0[k] * f;
+            t1 += v1[k] * f;
+          }
+          t0 = warp_sum(t0);
+          t1 = warp_sum(t1);
+          if (lane == 0) {
+            if (i0 < n)
+              VF[i0 * Fw + n + m] = vx1[i0] + t0;
             else
-              Z[(i1 - n) * Fw + n + m] = vz1[i1 - n] + t1;
+              Z[(i0 - n) * Fw + n + m] = vz1[i0 - n] + t0;
+            if (i1 < n + nz) {
+              if (i1 < n)
+                VF[i1 * Fw + n + m] = vx1[i1] + t1;
+              else
+                Z[(i1 - n) * Fw + n + m] = vz1[i1 - n] + t1;
+            }
           }
         }
-      }
-    } else {
-      for (int i = tid; i < n + nz; i += nt) {
-        const double* vr = bf.V + (size_t)i * n;
-        double t0 = 0.0, t1 = 0.0;
-        int k = 0;
-        for (; k + 1 < n; k += 2) {
-          t0 += vr[k] * f1at(k);
-          t1 += vr[k + 1] * f1at(k + 1);
+      } else {
+        for (int i = tid; i < n + nz; i += nt) {
+          const double* vr = bf.V + (size_t)i * n;
+          double t0 = 0.0, t1 = 0.0;
+          int k = 0;
+          for (; k + 1 < n; k += 2) {
+            t0 += vr[k] * f1at(k);
+            t1 += vr[k + 1] * f1at(k + 1);
+          }
+          if (k < n) t0 += vr[k] * f1at(k);
+          if (i < n)
+            VF[i * Fw + n + m] = vx1[i] + (t0 + t1);
+          else
+            Z[(i - n) * Fw + n + m] = vz1[i - n] + (t0 + t1);
         }
-        if (k < n) t0 += vr[k] * f1at(k);
-        if (i < n)
-          VF[i * Fw + n + m] = vx1[i] + (t0 + t1);
-        else
-          Z[(i - n) * Fw + n + m] = vz1[i - n] + (t0 + t1);
       }
+    
     }
     __syncthreads();
     PLQ_GPH(1);
-    // ---- GEMM2: M-terms (endpoint.py:209-211, 215-216); the w column
-    // (mx1 = qx1 + Fx' w, mu1 = qu1 + Fu' w) again as a matvec
-    for (int i = tid; i < n + m; i += nt) {
-      double t0 = 0.0, t1 = 0.0;
-      int k = 0;
-      for (; k + 1 < n; k += 2) {
-        t0 += fat(k, i) * VF[k * Fw + n + m];
-        t1 += fat(k + 1, i) * VF[(k + 1) * Fw + n + m];
+    if (vzero) {
+      // M-terms with V = 0: the stage's own Q blocks (Mxx mirrored like the GEMM epilogue does)
+      for (int i = tid; i < n + m; i += nt) {
+        if (i < n)
+          vx1[i] = qx1_s[i];
+        else
+          P[(i - n) * ldw + cc] = qu1_s[i - n];
       }
-      if (k < n) t0 += fat(k, i) * VF[k * Fw + n + m];
-      if (i < n)
-        vx1[i] = qx1_s[i] + (t0 + t1);   // mx1 in place (vx1 was consumed by GEMM1's f1 column)
-      else
-        P[(i - n) * ldw + cc] = qu1_s[i - n] + (t0 + t1);
-    }
-    // x rows over the x columns only (the Mxu block is never used), u rows
-    // over all columns
-    if (!gemm_x_pre_sym<true, NT>(
-            n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return c <= i ? Qxx_s[i * n + c] : 0.0; },
-            [&](int i, int c, double v) {
-              if (c <= i) {
-                Vxx[i * n + c] = v;
-                Vxx[c * n + i] = v;
-              }
-            }))
+      for (int idx = tid; idx < nn; idx += nt) {
+        const int i = idx / n, c = idx % n;
+        if (c <= i) {
+          const double v = __ldcs(Qxx_s + idx);
+          Vxx[i * n + c] = v;
+          Vxx[c * n + i] = v;
+        }
+      }
+      for (int idx = tid; idx < m * n; idx += nt) P[(idx / n) * ldw + idx % n] = __ldcs(Qux_s + idx);
+      for (int idx = tid; idx < m * m; idx += nt) Muu[idx] = __ldcs(Quu_s + idx);
+    } else {
+      // ---- GEMM2: M-terms (endpoint.py:209-211, 215-216); the w column
+      // (mx1 = qx1 + Fx' w, mu1 = qu1 + Fu' w) again as a matvec
+      for (int i = tid; i < n + m; i += nt) {
+        double t0 = 0.0, t1 = 0.0;
+        int k = 0;
+        for (; k + 1 < n; k += 2) {
+          t0 += fat(k, i) * VF[k * Fw + n + m];
+          t1 += fat(k + 1, i) * VF[(k + 1) * Fw + n + m];
+        }
+        if (k < n) t0 += fat(k, i) * VF[k * Fw + n + m];
+        if (i < n)
+          vx1[i] = qx1_s[i] + (t0 + t1);   // mx1 in place (vx1 was consumed by GEMM1's f1 column)
+        else
+          P[(i - n) * ldw + cc] = qu1_s[i - n] + (t0 + t1);
+      }
+      // x rows over the x columns only (the Mxu block is never used), u rows
+      // over all columns
+      if (!gemm_x_pre_sym<true, NT>(
+              n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return c <= i ? __ldcs(Qxx_s + i * n + c) : 0.0; },
+              [&](int i, int c, double v) {
+                if (c <= i) {
+                  Vxx[i * n + c] = v;
+                  Vxx[c * n + i] = v;
+                }
+              }))
+        gemm_x_pre<true, NT>(
+            n, n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return Qxx_s[i * n + c]; },
+            [&](int i, int c, double v) { Vxx[i * n + c] = v; });   // Mxx in place (Vxx was consumed by GEMM1)
       gemm_x_pre<true, NT>(
-          n, n, n, fxp, ldfx, VF, Fw, bf.tiles, [&](int i, int c) { return Qxx_s[i * n + c]; },
-          [&](int i, int c, double v) { Vxx[i * n + c] = v; });   // Mxx in place (Vxx was consumed by GEMM1)
-    gemm_x_pre<true, NT>(
-        m, n + m, n, fup, ldfu, VF, Fw, bf.tiles,
-        [&](int u, int c) { return c < n ? Qux_s[u * n + c] : Quu_s[u * m + (c - n)]; },
-        [&](int u, int c, double v) {
-          if (c < n)
-            P[u * ldw + c] = v;
-          else
-            Muu[u * m + (c - n)] = v;
-        });
+          m, n + m, n, fup, ldfu, VF, Fw, bf.tiles,
+          // (Q blocks are read once: streaming loads keep them from evicting the L2-resident scratch)
+          [&](int u, int c) { return qdirect ? (c < n ? __ldcs(Qux_s + u * n + c) : __ldcs(Quu_s + u * m + (c - n)))
+                                             : (c < n ? Qux_s[u * n + c] : Quu_s[u * m + (c - n)]); },
+          [&](int u, int c, double v) {
+            if (c < n)
+              P[u * ldw + c] = v;
+            else
+              Muu[u * m + (c - n)] = v;
+          });
+    
+    }
     __syncthreads();
 
     PLQ_GPH(2);
@@ -451,13 +487,19 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       const double fu2 = block_sum(part_u, red);
       const double nu_scale = sqrt(hx2) * sqrt(fu2);
       // N = Hx F -> VF (r x Fw): [Nx | Nu | Hx f1]
-      gemm_x<false, NT>(r, n, n, H, ldw, fxp, ldfx, bf.tiles, [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
-      gemm_x<false, NT>(r, m, n, H, ldw, fup, ldfu, bf.tiles,
-                        [&](int i, int c, double acc) { VF[i * Fw + n + c] = acc; });
-      for (int i = tid; i < r; i += nt) {
-        double t = 0.0;
-        for (int k = 0; k < n; ++k) t += H[i * ldw + k] * f1at(k);
-        VF[i * Fw + n + m] = t;
+      if (vzero) {   // Hx = I
+        for (int idx = tid; idx < nn; idx += nt) VF[(idx / n) * Fw + idx % n] = fxp[(idx / n) * ldfx + idx % n];
+        for (int idx = tid; idx < n * m; idx += nt) VF[(idx / m) * Fw + n + idx % m] = fup[(idx / m) * ldfu + idx % m];
+        for (int i = tid; i < n; i += nt) VF[i * Fw + n + m] = f1at(i);
+      } else {
+        gemm_x<false, NT>(r, n, n, H, ldw, fxp, ldfx, bf.tiles, [&](int i, int c, double acc) { VF[i * Fw + c] = acc; });
+        gemm_x<false, NT>(r, m, n, H, ldw, fup, ldfu, bf.tiles,
+                          [&](int i, int c, double acc) { VF[i * Fw + n + c] = acc; });
+        for (int i = tid; i < r; i += nt) {
+          double t = 0.0;
+          for (int k = 0; k < n; ++k) t += H[i * ldw + k] * f1at(k);
+          VF[i * Fw + n + m] = t;
+        }
       }
       __syncthreads();
       PLQ_GPH(9);
@@ -513,7 +555,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           // (blocked: in place on H's first m rows, DMMA tiles)
           if (blocked) {
             gtri_inv_upper8<NT / 32>(VF + n, m, Fw, rdiag, binv, tid, csync);
-            gtrsm8<2, NT / 32>(VF + n, m, Fw, binv, H, W, ldw, wsc, tid, csync);
+            gtrsm8<2, NT / 32, true>(VF + n, m, Fw, binv, H, W, ldw, wsc, tid, csync);
           }
           for (int c = tid; c < W && !blocked; c += nt) {
             for (int i = m - 1; i >= 0; --i) {
@@ -630,7 +672,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       if (tid == 0) *iflag = 0;
       __syncthreads();
-      if (!(blocked ? gchol8<NT / 32>(Mc, m, ldm, binv, iflag, tid, csync, nullptr, G, W, ldw, wsc, P, -1.0)
+      if (!(blocked ? gchol8<NT / 32, true>(Mc, m, ldm, binv, iflag, tid, csync, nullptr, G, W, ldw, wsc, P, -1.0)
                     : cta_cholesky(Lm, m, m, iflag))) {
         if (tid == 0) *sflag = 1 + s;
         __syncthreads();
@@ -638,7 +680,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       }
       PLQ_GPH(4);
       if (blocked) {
-        gtrsm8<1, NT / 32>(Mc, m, ldm, binv, G, W, ldw, wsc, tid, csync);
+        gtrsm8<1, NT / 32, true>(Mc, m, ldm, binv, G, W, ldw, wsc, tid, csync);
       } else {
         cho_solve_x(Lm, m, m, G, W, ldw);
         for (int idx = tid; idx < m * W; idx += nt) {
@@ -651,10 +693,25 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
 
     PLQ_GPH(5);
     // ---- policy outputs (parallel.py:224-236 stacking)
-    for (int idx = tid; idx < m * n; idx += nt) {
-      const int u = idx / n, c = idx % n;
-      a.Kx[st * m * n + idx] = G[u * ldw + c];
-      a.Kz[st * m * n + idx] = serial ? 0.0 : G[u * ldw + n + c];   // serial segment: Kz = 0
+    for (int idx0 = tid; idx0 < m * n; idx0 += 4 * nt) {
+      // four elements per trip, loads first (G is in L2 scratch); streaming
+      // stores: the policies are not read again by this kernel
+      double gx[4], gz[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int idx = idx0 + e * nt;
+        const int u = idx / n, c = idx % n;
+        gx[e] = idx < m * n ? G[u * ldw + c] : 0.0;
+        gz[e] = (idx < m * n && !serial) ? G[u * ldw + n + c] : 0.0;   // serial segment: Kz = 0
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int idx = idx0 + e * nt;
+        if (idx < m * n) {
+          __stcs(a.Kx + st * m * n + idx, gx[e]);
+          __stcs(a.Kz + st * m * n + idx, gz[e]);
+        }
+      }
     }
     for (int u = tid; u < m; u += nt) a.k1[st * m + u] = G[u * ldw + cc];
 
