@@ -86,15 +86,24 @@ __device__ __forceinline__ void bwd_issue(const ReconArgs& A, double* slot, uint
   bulk_g2s(slot + R::GH, A.gh + st * (N + M), 8u * (N + M), bar);
 }
 
-// row dot product rp . vec over K entries, two accumulators (as the fused
-// single-kernel passes)
+// Row dot product with a per-lane rotated column order.  The bulk copies land
+// the matrices unpadded, so the rows of consecutive lanes are K doubles apart
+// and a plain rp[c] loop puts all 32 lanes of a load on the same bank (a
+// 32-way conflict: ~6 k shared-memory wavefronts per n = 64 stage, more than
+// the stage's HBM time).  Starting lane t at column pair (c + t) and loading
+// 16 bytes spreads every quarter-warp over all eight 16-byte bank groups.
 template <int K>
-__device__ __forceinline__ double rdot(const double* rp, const double* vec) {
+__device__ __forceinline__ double rdot_rot(const double* rp, const double* vec, int rot) {
+  static_assert(K % 2 == 0 && ((K / 2) & (K / 2 - 1)) == 0, "row length: twice a power of two");
+  const double2* r2 = reinterpret_cast<const double2*>(rp);
+  const double2* v2 = reinterpret_cast<const double2*>(vec);
   double t = 0.0, t_ = 0.0;
 #pragma unroll 8
-  for (int c = 0; c < K; c += 2) {
-    t += rp[c] * vec[c];
-    t_ += rp[c + 1] * vec[c + 1];
+  for (int c = 0; c < K / 2; ++c) {
+    const int k = (c + rot) & (K / 2 - 1);
+    const double2 a = r2[k], b = v2[k];
+    t += a.x * b.x;
+    t_ += a.y * b.y;
   }
   return t + t_;
 }
@@ -144,11 +153,11 @@ __global__ void __launch_bounds__(NT) recon_fwd_kernel(ReconArgs A) {
       const int64_t st = s0 + s;
       // pass 1: Fx x | Kx x | Kz z
       if (tid < N)
-        tf[tid] = rdot<N>(sl + R::FX + tid * N, x);
+        tf[tid] = rdot_rot<N>(sl + R::FX + tid * N, x, tid);
       else if (tid < N + M)
-        tu[tid - N] = rdot<N>(sl + R::KX + (tid - N) * N, x);
+        tu[tid - N] = rdot_rot<N>(sl + R::KX + (tid - N) * N, x, tid);
       else if (tid < N + 2 * M)
-        tk[tid - N - M] = rdot<N>(sl + R::KZ + (tid - N - M) * N, z);
+        tk[tid - N - M] = rdot_rot<N>(sl + R::KZ + (tid - N - M) * N, z, tid);
       __syncthreads();
       if (tid < M) {
         const double kk = tk[tid] + sl[R::K1 + tid];   // k = Kz z + k1 (parallel.py:495)
@@ -162,9 +171,7 @@ __global__ void __launch_bounds__(NT) recon_fwd_kernel(ReconArgs A) {
       }
       __syncthreads();
       if (tid < N) {
-        double t = 0.0;
-#pragma unroll
-        for (int q = 0; q < M; ++q) t += sl[R::FU + tid * M + q] * uu[q];
+        const double t = rdot_rot<M>(sl + R::FU + tid * M, uu, tid);
         xn[tid] = (tf[tid] + t) + sl[R::F1 + tid];
       }
       __syncthreads();
@@ -217,9 +224,9 @@ __global__ void __launch_bounds__(NT) recon_eval_kernel(ReconArgs A) {
       phases ^= 1u << slot;
       const int64_t st = s0 + s;
       if (tid < N)
-        t0[tid] = rdot<N>(sl + R::QXX + tid * N, sl + R::X);
+        t0[tid] = rdot_rot<N>(sl + R::QXX + tid * N, sl + R::X, tid);
       else if (tid < N + M)
-        t2[tid - N] = rdot<N>(sl + R::QUX + (tid - N) * N, sl + R::X);
+        t2[tid - N] = rdot_rot<N>(sl + R::QUX + (tid - N) * N, sl + R::X, tid);
       __syncthreads();
       if (tid < N) {
         // g = Qxx x + Qux' u + qx1; objective 1/2 x'Qxx x + qx1'x
@@ -232,9 +239,7 @@ __global__ void __launch_bounds__(NT) recon_eval_kernel(ReconArgs A) {
       } else if (tid < N + M) {
         // h = Qux x + Quu u + qu1; objective 1/2 u'Quu u + u'Qux x + qu1'u
         const int u = tid - N;
-        double t = 0.0;
-#pragma unroll
-        for (int q = 0; q < M; ++q) t += sl[R::QUU + u * M + q] * sl[R::U + q];
+        const double t = rdot_rot<M>(sl + R::QUU + u * M, sl + R::U, u);
         const double ui = sl[R::U + u], qu = sl[R::QU1 + u];
         A.gh[st * (N + M) + N + u] = (t2[u] + t) + qu;
         obj += 0.5 * ui * t + ui * t2[u] + qu * ui;
