@@ -539,16 +539,41 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
     // stage the factor (coalesced) for the blocked solve below; v by one
     // warp per row with the lanes over the (coalesced) columns of W
     double* Lsb = v + ((n + 16) & ~1);
-    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lsb[(idx / n) * (n + 1) + idx % n] = Lc[idx];
-    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int r = threadIdx.x >> 5; r < n; r += nw) {
-      double t = 0.0;
-      for (int c = lane; c < n; c += 32) {
-        if (has_l) t += Wm[r * w + c] * xl[c];
-        if (has_r) t += Wm[r * w + n + c] * xr[c];
+    // (eight loads in flight per thread: the factor comes from L2)
+    for (int idx0 = threadIdx.x; idx0 < nn; idx0 += 8 * blockDim.x) {
+      double lv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int64_t idx = idx0 + (int64_t)e * blockDim.x;
+        lv[e] = idx < nn ? Lc[idx] : 0.0;
       }
-      t = warp_sum(t);
-      if (lane == 0) v[r] = Wm[r * w + 2 * n] - t;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int64_t idx = idx0 + (int64_t)e * blockDim.x;
+        if (idx < nn) Lsb[(idx / n) * (n + 1) + idx % n] = lv[e];
+      }
+    }
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // four rows of W per warp trip (independent loads, one latency for four rows)
+    for (int r0 = threadIdx.x >> 5; r0 < n; r0 += 4 * nw) {
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int c = lane; c < n; c += 32) {
+        const double xlc = has_l ? xl[c] : 0.0, xrc = has_r ? xr[c] : 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = r0 + e * nw;
+          if (r < n) {
+            if (has_l) t[e] += Wm[r * w + c] * xlc;
+            if (has_r) t[e] += Wm[r * w + n + c] * xrc;
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = r0 + e * nw;
+        const double ts = warp_sum(t[e]);
+        if (lane == 0 && r < n) v[r] = Wm[r * w + 2 * n] - ts;
+      }
     }
   } else {
     for (int r = threadIdx.x; r < n; r += blockDim.x) {

@@ -19,11 +19,24 @@ namespace {
 __device__ __forceinline__ void gemv_rows(int R, int C, const double* __restrict__ A, const double* x, double* y,
                                           const double* add, double sign = 1.0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = warp; i < R; i += nw) {
-    double s = 0.0;
-    for (int k = lane; k < C; k += 32) s += A[(int64_t)i * C + k] * x[k];
-    s = warp_sum(s);
-    if (lane == 0) y[i] = sign * s + (add ? add[i] : 0.0);
+  // four rows per trip: their loads are independent, so one memory latency
+  // covers four rows instead of one (the matrices stream from HBM / L2)
+  for (int i0 = warp; i0 < R; i0 += 4 * nw) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = lane; k < C; k += 32) {
+      const double xv = x[k];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = i0 + e * nw;
+        s[e] += (i < R ? A[(int64_t)i * C + k] : 0.0) * xv;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = i0 + e * nw;
+      const double t = warp_sum(s[e]);
+      if (lane == 0 && i < R) y[i] = sign * t + (add ? add[i] : 0.0);
+    }
   }
 }
 
@@ -54,6 +67,17 @@ __device__ __forceinline__ void gemv_cols_par(int R, int C, const double* __rest
     const int r0 = (int)((int64_t)R * chunk / S), r1 = (int)((int64_t)R * (chunk + 1) / S);
     double t0 = 0.0, t1 = 0.0;
     int k = r0;
+    // eight rows per trip, loads first: one memory latency per eight rows
+    for (; k + 7 < r1; k += 8) {
+      double av[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) av[e] = A[(int64_t)(k + e) * C + i];
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        t0 += av[e] * x[k + e];
+        t1 += av[e + 1] * x[k + e + 1];
+      }
+    }
     for (; k + 1 < r1; k += 2) {
       t0 += A[(int64_t)k * C + i] * x[k];
       t1 += A[(int64_t)(k + 1) * C + i] * x[k + 1];
