@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define PLQ_ABI_VERSION 1
+#define PLQ_ABI_VERSION 2
 
 /* Return codes of the entry points (launch / argument errors only; numerical
  * failures are reported per segment in plq_outputs_t.status). */
@@ -105,6 +105,16 @@ typedef struct plq_outputs {
                              rotation of the reference's rows; row counts in feas_rows) */
   int32_t* feas_rows;     /* (B,J) */
   double* feas_residual;  /* (B,J) details.feasibility_residuals */
+  /* collect_diagnostics=True (StageDiagnostics, endpoint.py:108-115, 258-299).  Both NULL: not
+   * collected.  Given: every endpoint segment is solved by the rank-revealing kernel (SVD of the
+   * triangular factor of Nu, csrc/plq_rank.cuh) and reports the worst defects over its constrained
+   * stages: [0] basis_defect = |V V' - I|_max of the right singular basis [Py | Zw], [1]
+   * projector_defect = |P P - P|_max of the row projector P = I - U_p U_p' (both in the
+   * QR-rotated coordinates of that kernel); diag_rows = max_rows, the largest constraint-to-go row
+   * count.  The last (serial) segment has no diagnostics (zeros; the reference returns None).
+   * Not copied back by plq_solve_parallel_host. */
+  double* diag;           /* (B,J,2) */
+  int32_t* diag_rows;     /* (B,J) */
 } plq_outputs_t;
 
 /* Library identification. */
@@ -258,6 +268,9 @@ typedef struct plq_endpoint_outputs {
    * rotation of the reference's rows).  Both NULL: such problems report status -1. */
   double* feas;           /* (B,n,W) */
   int32_t* feas_rows;     /* (B) */
+  /* collect_diagnostics=True (as plq_outputs_t::diag / diag_rows): both NULL = not collected */
+  double* diag;           /* (B,2) basis / projector defects */
+  int32_t* diag_rows;     /* (B) max_rows */
 } plq_endpoint_outputs_t;
 
 /* Evaluation at concrete endpoints (EndpointAffineSolution.evaluate,

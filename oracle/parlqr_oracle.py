@@ -109,6 +109,8 @@ def endpoint_sweep(st, rank_tol=RANK_TOL, QxxT=None, qx1T=None):
     Kz_all = np.empty((L, m, n))
     k1_all = np.empty((L, m))
     eye_m = np.eye(m)
+    # StageDiagnostics (endpoint.py:108-115, 200): worst defects, largest row count
+    diag = {"basis_defect": 0.0, "projector_defect": 0.0, "max_rows": int(Hx.shape[0])}
     for t in range(L - 1, -1, -1):
         Fx, Fu, f1 = st["Fx"][t], st["Fu"][t], st["f1"][t]
         # M-terms (endpoint.py:206-217)
@@ -158,6 +160,12 @@ def endpoint_sweep(st, rank_tol=RANK_TOL, QxxT=None, qx1T=None):
             G = -base
         Kx, Kz, k1 = G[:, :n], G[:, n:2 * n], G[:, 2 * n]
         Kx_all[t], Kz_all[t], k1_all[t] = Kx, Kz, k1
+        if p:   # endpoint.py:258-265, 275-277
+            Zfull = Vt[p:].T if p < m else np.zeros((m, 0))
+            comp = Vt[:p].T @ Vt[:p] + Zfull @ Zfull.T - eye_m
+            diag["basis_defect"] = max(diag["basis_defect"], float(np.abs(comp).max()))
+            Pr = np.eye(r) - U[:, :p] @ U[:, :p].T
+            diag["projector_defect"] = max(diag["projector_defect"], float(np.abs(Pr @ Pr - Pr).max()))
         # constraint projection + compression (endpoint.py:267-281)
         if r:
             pre = float(np.linalg.norm(np.concatenate([Nx, Nz], axis=1)))
@@ -182,8 +190,9 @@ def endpoint_sweep(st, rank_tol=RANK_TOL, QxxT=None, qx1T=None):
         vx1 = mx1 + Kx.T @ mu1 + (Mux.T + Kx.T @ Muu) @ k1
         vz1 = mz1 + Mzu @ k1 + Kz.T @ mu1 + Kz.T @ (Muu @ k1)
         Vzx = Vzx_new
+        diag["max_rows"] = max(diag["max_rows"], int(Hx.shape[0]))   # endpoint.py:298-299
     return {"Kx": Kx_all, "Kz": Kz_all, "k1": k1_all,
-            "vf0": (Vxx, Vzx, Vzz, vx1, vz1), "feas": (Hx, Hz, h1)}
+            "vf0": (Vxx, Vzx, Vzz, vx1, vz1), "feas": (Hx, Hz, h1), "diagnostics": diag}
 
 
 def serial_sweep(st, QxxT, qx1T):

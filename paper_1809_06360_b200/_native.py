@@ -44,7 +44,7 @@ class PlqProblem(ctypes.Structure):
 
 OUTPUT_FIELDS = ("K", "k", "x", "u", "lam", "links", "mu_left", "lambda_right", "vf0",
                  "Kz", "k1", "objective", "kkt_inf", "link_mismatch", "link_residual",
-                 "status", "feas", "feas_rows", "feas_residual")
+                 "status", "feas", "feas_rows", "feas_residual", "diag", "diag_rows")
 
 
 class PlqOutputs(ctypes.Structure):
@@ -58,7 +58,8 @@ class PlqSmoothOutputs(ctypes.Structure):
     _fields_ = [(f, _vp) for f in SMOOTH_FIELDS]
 
 
-ENDPOINT_FIELDS = ("Kx", "Kz", "k1", "value0", "X", "S", "Lam", "E", "status", "gram_status", "feas", "feas_rows")
+ENDPOINT_FIELDS = ("Kx", "Kz", "k1", "value0", "X", "S", "Lam", "E", "status", "gram_status", "feas", "feas_rows",
+                   "diag", "diag_rows")
 
 
 class PlqEndpointOutputs(ctypes.Structure):
@@ -121,7 +122,7 @@ def lib():
                  "plq_link_solve", "plq_reconstruct_segments", "plq_boundary_segments",
                  "plq_finalize", "plq_smooth", "plq_endpoint_affine", "plq_endpoint_evaluate"):
         getattr(L, name).restype = ctypes.c_int
-    if L.plq_abi_version() != 1:
+    if L.plq_abi_version() != 2:
         raise RuntimeError("libparlqr_b200.so ABI version mismatch; rebuild it")
     _LIB = L
     return L

@@ -173,13 +173,26 @@ int phase_sweep(const plq_problem_t* p, const plq_outputs_t* o, Ctx& c, int j0, 
   a.repair_list = reinterpret_cast<long long*>(c.ws + c.P.off_rlist);
   a.rank_scratch = c.ws + c.P.off_rank;
   a.rank_scratch_doubles = (int64_t)c.P.rank_doubles;
+  // collect_diagnostics: endpoint segments solved by the rank-revealing launch of the generic kernel
+  if ((o->diag != nullptr) != (o->diag_rows != nullptr)) return fail(PLQ_ERR_ARG, "diag and diag_rows go together");
+  const bool diag = o->diag != nullptr;
+  a.force_repair = diag ? 1 : 0;
+  a.diag = diag ? o->diag : nullptr;
+  a.diag_rows = diag ? o->diag_rows : nullptr;
+  if (diag) {
+    const size_t cells = (size_t)p->B * p->J;
+    if (cudaMemsetAsync(o->diag, 0, cells * 2 * sizeof(double), c.s) != cudaSuccess ||
+        cudaMemsetAsync(o->diag_rows, 0, cells * sizeof(int32_t), c.s) != cudaSuccess)
+      return cuda_fail("diagnostics reset");
+  }
   // endpoint segments (tail stages) may need the rank-revealing repair pass
   const bool tails = endpoint_terminal || j0 < p->J - 1;
   if (tails && cudaMemsetAsync(a.repair_ctr, 0, sizeof(unsigned long long), c.s) != cudaSuccess)
     return cuda_fail("repair counter reset");
   const int64_t tasks = p->B * (int64_t)(j1 - j0);
   const int grid = (int)std::min<int64_t>(tasks, c.P.grid_max);
-  const int rc = use_small_sweep(p) ? plq::launch_sweep_small(a, c.s) : plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s);
+  const int rc = (use_small_sweep(p) && !diag) ? plq::launch_sweep_small(a, c.s)
+                                               : plq::launch_sweep(a, grid, c.P.threads, c.P.smem, c.s);
   if (rc) return cuda_fail("sweep launch");
   ++g_launches;
   if (tails) {
@@ -400,6 +413,8 @@ int plq_endpoint_affine(const plq_problem_t* problem, const plq_endpoint_outputs
   if ((out->feas != nullptr) != (out->feas_rows != nullptr)) return fail(PLQ_ERR_ARG, "feas and feas_rows go together");
   o.feas = out->feas;            // (B, J = 1, n, 2n+1): rows instead of PLQ_STATUS_DEGENERATE
   o.feas_rows = out->feas_rows;
+  o.diag = out->diag;            // (B, J = 1, 2) / (B, J = 1)
+  o.diag_rows = out->diag_rows;
   Ctx c;
   int rc = setup(problem, &o, workspace, workspace_bytes, stream, &c);
   if (rc) return rc;
@@ -651,7 +666,7 @@ extern "C" {
 
 namespace {
 
-constexpr int NOUT_HOST = 19;   // plq_outputs_t fields, in declaration order
+constexpr int NOUT_HOST = 19;   // plq_outputs_t fields copied back, in declaration order (diag / diag_rows are not)
 
 void host_sizes(const plq_problem_t* p, size_t* in_sz, size_t* out_sz) {
   const size_t B = p->B, T = p->T, n = p->n, m = p->m, J = p->J;

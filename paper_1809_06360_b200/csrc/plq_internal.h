@@ -104,6 +104,12 @@ struct SweepArgs {
   long long* repair_list;      // (B*J)
   double* rank_scratch;
   int64_t rank_scratch_doubles;
+  // collect_diagnostics (StageDiagnostics, endpoint.py:108-115): force_repair
+  // sends every endpoint segment to the repair launch, which has the singular
+  // vectors and writes the defects / row counts here
+  int force_repair;
+  double* diag;          // (B,J,2)
+  int32_t* diag_rows;    // (B,J)
 };
 
 // internal status: segment awaits the rank-revealing repair pass (never

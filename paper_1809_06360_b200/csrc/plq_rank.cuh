@@ -148,7 +148,7 @@ __device__ inline void cta_jacobi_svd(double* A, double* V, double* sig, int* pe
 template <class SAt>
 __device__ int rank_tail_solve(int k, int m, int r, int W, int ldw, SAt sat, double* H, const double* Pp,
                                const double* Mp, int ldm, double nu_scale, double rank_tol, double* G,
-                               const RankScratch& s, double* red) {
+                               const RankScratch& s, double* red, double* defects = nullptr) {
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int idx = tid; idx < k * k; idx += nt) {
     const int c = idx / k, i = idx % k;
@@ -167,6 +167,48 @@ __device__ int rank_tail_solve(int k, int m, int r, int W, int ldw, SAt sat, dou
     s.UP[i * k + c] = s.A[col * k + i] / s.sig[col];
   }
   __syncthreads();
+  if (defects != nullptr) {
+    // StageDiagnostics (endpoint.py:258-276), thread-uniform maxima:
+    // basis: |V V' - I| of the k x k right singular basis ([Py | Zw] in these
+    // coordinates; zero by definition when p = 0); projector: P = I - U_p U_p',
+    // P P - P = U_p (U_p'U_p - I) U_p'
+    double bd = 0.0, pd = 0.0;
+    if (p > 0) {
+      for (int idx = tid; idx < k * k; idx += nt) {
+        const int i = idx / k, c = idx % k;
+        double v = (i == c) ? -1.0 : 0.0;
+        for (int l = 0; l < k; ++l) v += s.V[l * k + i] * s.V[l * k + c];
+        bd = fmax(bd, fabs(v));
+      }
+      // E = U_p'U_p - I in T1 (p x p), then U_p E U_p'
+      for (int idx = tid; idx < p * p; idx += nt) {
+        const int a = idx / p, c = idx % p;
+        double v = (a == c) ? -1.0 : 0.0;
+        for (int i = 0; i < k; ++i) v += s.UP[i * k + a] * s.UP[i * k + c];
+        s.T1[idx] = v;
+      }
+      __syncthreads();
+      // F = E U_p' (p x k) in C (free until the next product), then U_p F
+      for (int idx = tid; idx < p * k; idx += nt) {
+        const int a = idx / k, c = idx % k;
+        double t = 0.0;
+        for (int e = 0; e < p; ++e) t += s.T1[a * p + e] * s.UP[c * k + e];
+        s.C[idx] = t;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < k * k; idx += nt) {
+        const int i = idx / k, c = idx % k;
+        double v = 0.0;
+        for (int a = 0; a < p; ++a) v += s.UP[i * k + a] * s.C[a * k + c];
+        pd = fmax(pd, fabs(v));
+      }
+    }
+    bd = block_max(bd, red);
+    pd = block_max(pd, red);
+    defects[0] = fmax(defects[0], bd);
+    defects[1] = fmax(defects[1], pd);
+    __syncthreads();
+  }
   cta_gemm<true, false, 1, 1>(p, W, k, s.UP, k, H, ldw, [&](int c, int w, double acc) {
     s.C[c * ldw + w] = acc / s.sig[s.perm[c]];
   });

@@ -286,6 +286,21 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
     }
   }
   int r = serial ? 0 : n;
+  // collect_diagnostics: worst defects over the constrained stages (thread-uniform),
+  // largest constraint-to-go row count (endpoint.py:200, 298-299)
+  double defects[2] = {0.0, 0.0};
+  int max_rows = r;
+  if constexpr (!REPAIR) {
+    if (a.force_repair && !serial) {
+      // every endpoint segment goes to the rank-revealing launch (it has the singular vectors)
+      if (tid == 0) {
+        a.status[b * J + j] = PLQ_STATUS_RANK_REPAIR;
+        push_repair(a, b, j);
+      }
+      __syncthreads();
+      return;
+    }
+  }
   __syncthreads();
 
 #ifdef PLQ_PHASE_PROFILE
@@ -535,7 +550,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
           const double* Rv = VF + n;
           const int pr = rank_tail_solve(
               m, m, r, W, ldw, [&](int i, int c) { return c > i ? Rv[i * Fw + c] : (c == i ? rdiag[i] : 0.0); }, H, P,
-              Muu, m, nu_scale, p.rank_tol, G, rsc, red);
+              Muu, m, nu_scale, p.rank_tol, G, rsc, red, a.diag ? defects : nullptr);
           if (pr < 0) {
             if (tid == 0) *sflag = 1 + s;
             __syncthreads();
@@ -625,7 +640,7 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
         cta_apply_q(X, m, r, r, tau, Pp, W, ldw, false);
         const int pr = rank_tail_solve(
             r, m, r, W, ldw, [&](int i, int c) { return c < i ? X[c * r + i] : (c == i ? rdiag[i] : 0.0); }, H, Pp,
-            Mp, m, nu_scale, p.rank_tol, G, rsc, red);
+            Mp, m, nu_scale, p.rank_tol, G, rsc, red, a.diag ? defects : nullptr);
         if (pr < 0) {
           if (tid == 0) *sflag = 1 + s;
           __syncthreads();
@@ -808,6 +823,11 @@ __device__ void sweep_segment(const SweepArgs& a, const Bufs& bf, int64_t b, int
       const int i = idx / (2 * n + 1), c = idx % (2 * n + 1);
       dst[idx] = H[i * ldw + c];
     }
+  }
+  if (a.diag != nullptr && tid == 0) {
+    a.diag[(b * J + j) * 2] = defects[0];
+    a.diag[(b * J + j) * 2 + 1] = defects[1];
+    a.diag_rows[b * J + j] = max_rows;
   }
   if (tid == 0) {
     int st = *sflag;

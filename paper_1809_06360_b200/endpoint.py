@@ -15,7 +15,9 @@ and the evaluation at concrete endpoints all run on the device
   multipliers from the value-function gradient and the stationarity recursion
   (``gradient_duals``, ``endpoint.py:566-587``) on the device; the rows in
   ``constraints[0]`` are an orthonormal rotation of the reference's;
-* ``collect_diagnostics`` raises ``NotImplementedError`` (SVD defects).
+* ``collect_diagnostics=True`` routes the backward pass through the
+  rank-revealing kernel and returns its singular-vector defects as the
+  reference's ``StageDiagnostics`` (include/parlqr_b200.h).
 """
 
 from __future__ import annotations
@@ -113,7 +115,7 @@ class EndpointBatch:
     objective and KKT residual at concrete endpoints (stream-ordered; call
     ``raise_for_status`` to synchronize and map failures)."""
 
-    def __init__(self, B, T, n, m, tolerances=DEFAULT_TOLERANCES, device=None):
+    def __init__(self, B, T, n, m, tolerances=DEFAULT_TOLERANCES, device=None, diagnostics=False):
         torch = _torch()
         self.torch = torch
         self.lib = _native.lib()
@@ -135,13 +137,16 @@ class EndpointBatch:
                 "feas": torch.zeros((B, n, W), **f64),
                 "feas_rows": torch.zeros((B,), dtype=torch.int32, device=self.device),
             }
+            if diagnostics:
+                self.out["diag"] = torch.zeros((B, 2), **f64)
+                self.out["diag_rows"] = torch.zeros((B,), dtype=torch.int32, device=self.device)
             self.point = {
                 "x": torch.empty((B, T + 1, n), **f64), "u": torch.empty((B, T, m), **f64),
                 "lam": torch.empty((B, T + 1, n), **f64), "mu": torch.empty((B, n), **f64),
                 "objective": torch.empty((B,), **f64), "kkt_inf": torch.empty((B,), **f64),
                 "feas_residual": torch.zeros((B,), **f64),
             }
-        self._outs = _native.PlqEndpointOutputs(**{f: _ptr(self.out[f]) for f in _native.ENDPOINT_FIELDS})
+        self._outs = _native.PlqEndpointOutputs(**{f: _ptr(self.out.get(f)) for f in _native.ENDPOINT_FIELDS})
         P = self._problem_struct(None)
         with torch.cuda.device(self.device):
             self.ws_bytes = int(self.lib.plq_endpoint_workspace_bytes(ctypes.byref(P)))
@@ -237,6 +242,9 @@ class EndpointAffineSolution:
         self.multipliers = None if (int(o["gram_status"]) or r) else MultiplierMaps(
             L[:, :, :n], L[:, :, n:2 * n], L[:, :, 2 * n], E[:, :n], E[:, n:2 * n], E[:, 2 * n])
         self.diagnostics = None
+        if "diag" in o:
+            from .parallel import _segment_diagnostics
+            self.diagnostics = _segment_diagnostics({"diag": o["diag"][None], "diag_rows": o["diag_rows"][None]}, 2)[0]
         self._batch, self._index, self._problem = batch, index, problem
 
     @property
@@ -275,12 +283,12 @@ class EndpointAffineSolution:
                            mu=o["mu"], x_term=np.asarray(x_term, dtype=np.float64))
 
 
-def _batch_for(problem, tolerances, device):
+def _batch_for(problem, tolerances, device, diagnostics=False):
     torch = _torch()
     a = stack_problem(problem)
     T, n = a["qx1"].shape
     m = a["qu1"].shape[1]
-    batch = EndpointBatch(1, T, n, m, tolerances=tolerances, device=device)
+    batch = EndpointBatch(1, T, n, m, tolerances=tolerances, device=device, diagnostics=diagnostics)
     inputs = _to_device({f: a[f][None] for f in INPUT_FIELDS}, batch.device, torch)
     with torch.cuda.device(batch.device):
         batch.affine(inputs)
@@ -290,9 +298,7 @@ def _batch_for(problem, tolerances, device):
 def solve_endpoint_affine(problem, tolerances=DEFAULT_TOLERANCES, collect_diagnostics=False,
                           require_multipliers=False, *, device=None):
     """Drop-in for ``parlqr.endpoint.solve_endpoint_affine`` (endpoint.py:603-636)."""
-    if collect_diagnostics:
-        raise NotImplementedError("collect_diagnostics is not computed by the GPU path")
-    batch = _batch_for(problem, tolerances, device)
+    batch = _batch_for(problem, tolerances, device, diagnostics=bool(collect_diagnostics))
     batch.raise_for_status(require_multipliers="strict" if require_multipliers else False)
     return EndpointAffineSolution(problem, batch)
 

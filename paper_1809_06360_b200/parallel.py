@@ -167,7 +167,7 @@ class BatchSolver:
     the per-segment status to the reference's exceptions."""
 
     def __init__(self, B, T, n, m, J=None, partition=None, tolerances=DEFAULT_TOLERANCES,
-                 device=None, keep_unfolded=False, degenerate=True):
+                 device=None, keep_unfolded=False, degenerate=True, diagnostics=False):
         torch = _torch()
         self.torch = torch
         self.lib = _native.lib()
@@ -206,6 +206,9 @@ class BatchSolver:
                 "feas": torch.empty((B, J, n, 2 * n + 1), **dev) if degenerate else None,
                 "feas_rows": torch.zeros((B, J), dtype=torch.int32, device=self.device) if degenerate else None,
                 "feas_residual": torch.zeros((B, J), **dev) if degenerate else None,
+                # collect_diagnostics (StageDiagnostics, endpoint.py:108-115): defects, max rows
+                "diag": torch.zeros((B, J, 2), **dev) if diagnostics else None,
+                "diag_rows": torch.zeros((B, J), dtype=torch.int32, device=self.device) if diagnostics else None,
             }
         self._outs = _native.PlqOutputs(**{f: _ptr(self.out[f]) for f in _native.OUTPUT_FIELDS})
         self._prob = self._problem_struct(None)
@@ -379,7 +382,7 @@ def _symmetrize_blocks(inputs, torch, chunk=1 << 24):
 
 
 def solve_parallel_batch(arrays, J=None, partition=None, tolerances=DEFAULT_TOLERANCES, device=None,
-                         keep_unfolded=False, check=True, symmetrize=True):
+                         keep_unfolded=False, check=True, symmetrize=True, diagnostics=False):
     """Solve ``B`` stacked problems (dict of ``(B, T, ...)`` arrays or
     tensors).  Returns the :class:`BatchSolver` whose ``out`` dict holds the
     device results.  ``symmetrize`` applies the reference constructors'
@@ -389,7 +392,7 @@ def solve_parallel_batch(arrays, J=None, partition=None, tolerances=DEFAULT_TOLE
     B, T, n = (int(s) for s in arrays["qx1"].shape)
     m = int(arrays["qu1"].shape[2])
     solver = BatchSolver(B, T, n, m, J=J, partition=partition, tolerances=tolerances, device=device,
-                         keep_unfolded=keep_unfolded)
+                         keep_unfolded=keep_unfolded, diagnostics=diagnostics)
     inputs = _to_device(arrays, solver.device, torch)
     solver.check_inputs(inputs)
     if symmetrize:
@@ -411,9 +414,6 @@ def solve_parallel(problem, J, workers=None, tolerances=DEFAULT_TOLERANCES, coll
     which equals the reference's value-gradient form ``-(Vxx x + vx1)``
     (serial.py:86-88) up to rounding.
     """
-    if collect_diagnostics:
-        raise NotImplementedError("collect_diagnostics (SVD basis/projector defects) is not computed "
-                                  "by the GPU path")
     T = len(problem.stages)
     if partition is not None:
         partition = _check_partition(partition, T)
@@ -422,9 +422,32 @@ def solve_parallel(problem, J, workers=None, tolerances=DEFAULT_TOLERANCES, coll
         partition = make_partition(T, J)
     a = stack_problem(problem)
     batch = {f: a[f][None] for f in INPUT_FIELDS}
-    solver = solve_parallel_batch(batch, partition=partition, tolerances=tolerances, device=device)
+    solver = solve_parallel_batch(batch, partition=partition, tolerances=tolerances, device=device,
+                                  diagnostics=bool(collect_diagnostics))
     o = {k: (v.cpu().numpy()[0] if v is not None else None) for k, v in solver.out.items()}
     return solution_from_outputs(o, partition)
+
+
+@dataclasses.dataclass(eq=False, repr=False)
+class _StageDiagnostics:
+    """endpoint.py:108-115 (stand-in when ``parlqr`` is not importable)."""
+
+    basis_defect: float = 0.0
+    projector_defect: float = 0.0
+    max_rows: int = 0
+
+
+def _segment_diagnostics(o, Jp):
+    """``details.segment_diagnostics``: one ``StageDiagnostics`` per endpoint
+    segment (``None`` for the last, serial one, and for every segment without
+    ``collect_diagnostics``; parallel.py:239, 549).  The defects come from the
+    rank-revealing kernel's singular vectors (include/parlqr_b200.h)."""
+    if o.get("diag") is None:
+        return tuple(None for _ in range(Jp))
+    ref = compat.reference_module("endpoint")
+    cls = ref.StageDiagnostics if ref is not None else _StageDiagnostics
+    return tuple(cls(basis_defect=float(o["diag"][j][0]), projector_defect=float(o["diag"][j][1]),
+                     max_rows=int(o["diag_rows"][j])) if j < Jp - 1 else None for j in range(Jp))
 
 
 def solution_from_outputs(o, partition):
@@ -470,7 +493,7 @@ def solution_from_outputs(o, partition):
         feasibility_residuals=tuple(float(fres[j]) if fres is not None and int(rows[j]) else 0.0
                                     for j in range(Jp)),
         degenerate=bool(np.any(rows[:Jp - 1] > 0)),
-        segment_diagnostics=tuple(None for _ in range(Jp)),
+        segment_diagnostics=_segment_diagnostics(o, Jp),
     )
     return LqrSolution(
         states=o["x"], controls=o["u"], lambdas=o["lam"],

@@ -37,10 +37,10 @@ def test_library_exports_all_declared_symbols():
 def test_abi_version_and_struct_layout():
     from paper_1809_06360_b200 import _native
     lib = _native.lib()
-    assert lib.plq_abi_version() == 1
+    assert lib.plq_abi_version() == 2
     # plq_problem_t: int64 + 5 int32 + 4 pad + 12 pointers + 2 doubles
     assert ctypes.sizeof(_native.PlqProblem) == 8 + 20 + 4 + 12 * 8 + 16
-    assert ctypes.sizeof(_native.PlqOutputs) == 19 * 8
+    assert ctypes.sizeof(_native.PlqOutputs) == 21 * 8
 
 
 def test_argument_errors_without_gpu():

@@ -242,3 +242,21 @@ def test_endpoint_exactness_over_many_targets():
         assert np.abs(sol.states[-1] - z).max() <= 1e-8 * (1 + np.abs(z).max())
         assert np.abs(sol.states[0] - x0).max() <= 1e-12 * (1 + np.abs(x0).max())
         assert sol.kkt_residual_inf <= 1e-8 * _scale(a) * (1 + np.abs(z).max() + np.abs(x0).max())
+
+
+def test_endpoint_collect_diagnostics():
+    """solve_endpoint_affine(collect_diagnostics=True): StageDiagnostics from the
+    rank-revealing kernel (bounds of test_endpoint.py:73-78), same solution."""
+    import paper_1809_06360_b200 as plq
+    from conftest import load_stored
+    a, _, _ = load_stored("small_random")[5]
+    prob = plq.problem_from_arrays(a)
+    base = plq.solve_endpoint_affine(prob)
+    aff = plq.solve_endpoint_affine(prob, collect_diagnostics=True)
+    assert base.diagnostics is None
+    d = aff.diagnostics
+    assert d.max_rows == a["x_init"].shape[0]
+    assert 0.0 <= d.basis_defect <= 1e-10 and 0.0 <= d.projector_defect <= 1e-12
+    for t in (0, len(aff.policies) - 1):
+        assert rel_err(aff.policies[t].Kx, base.policies[t].Kx) <= 1e-8
+    assert rel_err(aff.maps.Ra, base.maps.Ra) <= 1e-8

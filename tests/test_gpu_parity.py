@@ -449,3 +449,35 @@ def test_chain_link_solve_equals_cyclic_reduction(n, m, T, J, B, monkeypatch):
     st = s.out["status"].cpu().numpy()
     assert st[1, 0] == _native.PLQ_STATUS_LINK_SINGULAR and (np.delete(st, 1, axis=0) == 0).all()
     assert rel_err(s.out["links"][0].cpu().numpy(), outs["chain"]["links"][0]) == 0.0
+
+
+@pytest.mark.parametrize("cfg_id,T,J", [(1, 64, 8), (2, 128, 4), (4, 64, 2), (0, 40, 4)])
+def test_collect_diagnostics(cfg_id, T, J):
+    """collect_diagnostics=True (endpoint.py:258-299, parallel.py:239, 549): the
+    endpoint segments go through the rank-revealing kernel, which has the
+    singular vectors; the solution equals the default path's, every endpoint
+    segment reports defects within the reference's own acceptance bounds
+    (test_endpoint.py:73-78: basis <= 1e-10, projector <= 1e-12) and
+    max_rows = n, the serial segment reports None."""
+    import paper_1809_06360_b200 as plq
+    from paper_1809_06360_b200 import synth
+    cfg = synth.CONFIGS[cfg_id].scaled(T=T, J=J)
+    a = synth.generate_one(cfg.n, cfg.m, T, 21, cfg.a_scale, cfg.q_eps, cfg.r_eps)
+    prob = plq.problem_from_arrays(a)
+    base = plq.solve_parallel(prob, J)
+    sol = plq.solve_parallel(prob, J, collect_diagnostics=True)
+    assert base.details.segment_diagnostics == tuple(None for _ in range(J))
+    sd = sol.details.segment_diagnostics
+    assert len(sd) == J and sd[-1] is None
+    st = {f: a[f] for f in O.STAGE_FIELDS}
+    splits = sol.details.partition.split_times
+    for j in range(J - 1):
+        ref = O.endpoint_sweep({f: st[f][splits[j]:splits[j + 1]] for f in st})["diagnostics"]
+        assert sd[j].max_rows == ref["max_rows"] == cfg.n
+        assert 0.0 <= sd[j].basis_defect <= 1e-10 and 0.0 <= sd[j].projector_defect <= 1e-12
+        assert sd[j].basis_defect > 0.0 or ref["basis_defect"] == 0.0
+    fl = _floor(a, J, O.solve(a, J=J))
+    for got, want, key in ((sol.states, base.states, "states"), (sol.controls, base.controls, "controls"),
+                           (sol.lambdas, base.lambdas, "lambdas")):
+        _gate(key, rel_err(got, want), fl.get(key, 0.0))
+    assert abs(sol.objective - base.objective) <= 1e-9 * abs(base.objective)

@@ -48,6 +48,27 @@ SCRIPT = textwrap.dedent(r'''
     assert type(sol.details) is parlqr.parallel.ParallelDetails
     assert type(sol.details.partition) is parlqr.parallel.Partition
     assert type(sol.policies[0]) is parlqr.AffinePolicy and sol.policies[0](np.ones(n)).shape == (m,)
+    assert sol.details.segment_diagnostics == (None, None)
+
+    # 2b. collect_diagnostics: the reference's StageDiagnostics per endpoint segment, None for the last
+    import parlqr.endpoint
+    od = dict(o, diag=np.array([[1e-16, 2e-16], [0.0, 0.0]]), diag_rows=np.array([n, 0], dtype=np.int32))
+    sd = solution_from_outputs(od, plq.make_partition(T, J)).details.segment_diagnostics
+    assert type(sd[0]) is parlqr.endpoint.StageDiagnostics and sd[1] is None
+    assert (sd[0].basis_defect, sd[0].projector_defect, sd[0].max_rows) == (1e-16, 2e-16, n)
+
+    # 2c. the oracle's restatement of the diagnostics equals the reference's (endpoint.py:258-299)
+    sys.path.insert(0, os.environ["PLQ_REPO_ROOT"])
+    from oracle import parlqr_oracle as O
+    from parlqr.generate import generate
+    for (dn, dm, dT, seed) in [(5, 2, 9, 3), (6, 3, 8, 4), (4, 1, 10, 5)]:
+        pr = generate(dn, dm, dT, seed=seed)
+        bw = parlqr.endpoint.backward_pass(pr.stages, None, collect_diagnostics=True)
+        arr = plq.parallel.stack_problem(pr)
+        d = O.endpoint_sweep({f: arr[f] for f in O.STAGE_FIELDS})["diagnostics"]
+        assert d["basis_defect"] == bw.diagnostics.basis_defect
+        assert d["projector_defect"] == bw.diagnostics.projector_defect
+        assert d["max_rows"] == bw.diagnostics.max_rows
 
     # 3. status codes -> the reference's exception classes
     cases = [(np.array([[0, 3]]), parlqr.errors.CholeskyFailure, "stage", 2),
@@ -84,7 +105,7 @@ SCRIPT = textwrap.dedent(r'''
 
 @pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not mounted (GPU box)")
 def test_reference_types_and_error_contract():
-    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF_SRC, ROOT]), PYTHONDONTWRITEBYTECODE="1")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF_SRC, ROOT]), PYTHONDONTWRITEBYTECODE="1", PLQ_REPO_ROOT=ROOT)
     env.pop("PLQ_NO_PARLQR", None)
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr

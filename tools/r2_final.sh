@@ -32,4 +32,8 @@ done
 python tools/run_sweep.py --config 3 --reps 2 > $o/plain3.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 2 -c 1 -o $o/cfg3_sweep python tools/run_sweep.py --config 3 --reps 2 > $o/ncu3.log 2>&1
 echo "ncu3 $?"
-ls -la $o | head -60
+# summaries on the box (details CSV, raw-metric summary, per-source-line stalls); the .ncu-rep files stay there
+# (gpurun_out is capped at 64 MiB)
+python tools/process_refresh.py $o $o/processed > $o/process.log 2>&1
+rm -f $o/*.ncu-rep
+du -sh $o
