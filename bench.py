@@ -289,12 +289,13 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
     cfg = synth.CONFIGS[args.config]
-    if cfg.B % world and cfg.B > 1:
-        raise SystemExit(f"batch {cfg.B} does not shard over {world} ranks")
     sharded = cfg.B == 1 and world > 1
     if cfg.B > 1:
-        B_loc = cfg.B // world
-        first = rank * B_loc
+        from paper_1809_06360_b200.sharded import batch_shard
+        try:
+            first, B_loc = batch_shard(cfg.B, world, rank)
+        except ValueError as exc:
+            raise SystemExit(str(exc))
     else:
         B_loc, first = 1, 0          # single horizon: segments sharded across ranks
     scaling = "strong"

@@ -35,6 +35,16 @@ def shard_range(J, world, rank):
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def batch_shard(B, world, rank):
+    """Problems ``[first, first + count)`` of a batch of ``B`` owned by ``rank``:
+    independent problems shard with no data-path collective (cfg1, cfg4;
+    SURVEY.md 8e).  Equal shares; ``B`` must divide over the ranks."""
+    if B % world:
+        raise ValueError(f"batch {B} does not shard over {world} ranks")
+    count = B // world
+    return rank * count, count
+
+
 def _gather_rows(dist, group, local, J, world, torch):
     """All-gather per-segment rows.
 
@@ -301,5 +311,5 @@ def sharded_solve_device(inputs, J=None, partition=None, dist=None, group=None, 
     return solver, res
 
 
-__all__ = ["shard_range", "solve_sharded", "raise_sharded_status", "DeviceBackend", "stage_window",
+__all__ = ["batch_shard", "shard_range", "solve_sharded", "raise_sharded_status", "DeviceBackend", "stage_window",
            "sharded_solve_device", "NcclComm", "solve_sharded_native"]

@@ -202,3 +202,46 @@ def test_shard_range_partitions_segments():
             assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
             sizes = [hi - lo for lo, hi in ranges]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _batch_worker(rank, world, port, cfg_id, B, T, J, outdir):
+    """Batch sharding as bench.py does it for cfg1 / cfg4: rank r generates and
+    solves problems [first, first + count) only; no data-path collective; the
+    step time is the max over ranks (an all-reduce of one scalar)."""
+    from paper_1809_06360_b200.sharded import batch_shard
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        cfg = synth.CONFIGS[cfg_id].scaled(B=B, T=T, J=J)
+        first, count = batch_shard(cfg.B, world, rank)
+        batch = synth.generate_batch(cfg, seed=9, count=count, first=first)
+        sols = O.solve_batch(batch, J=J)
+        t = torch.tensor([float(rank + 1)], dtype=torch.float64)       # stand-in for this rank's step time
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        obj = torch.tensor([s["objective"] for s in sols], dtype=torch.float64)
+        allobj = torch.empty(world * count, dtype=torch.float64)
+        dist.all_gather_into_tensor(allobj, obj)                        # optional gather of outputs
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), first=first, count=count, tmax=float(t),
+                 objective=allobj.numpy(), x0=np.stack([s["states"] for s in sols]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cfg_id,B,T,J", [(2, 1, 6, 16, 4), (3, 1, 6, 16, 4)])
+def test_batch_sharding_covers_the_batch(world, cfg_id, B, T, J):
+    cfg = synth.CONFIGS[cfg_id].scaled(B=B, T=T, J=J)
+    ref = O.solve_batch(synth.generate_batch(cfg, seed=9, count=B), J=J)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_batch_worker, args=(world, _free_port(), cfg_id, B, T, J, d), nprocs=world, join=True)
+        outs = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
+    owned = []
+    for r, o in enumerate(outs):
+        first, count = int(o["first"]), int(o["count"])
+        owned += list(range(first, first + count))
+        assert float(o["tmax"]) == float(world)                         # max over ranks, same on every rank
+        assert np.array_equal(o["objective"], np.array([s["objective"] for s in ref]))
+        for i in range(count):
+            assert np.array_equal(o["x0"][i], ref[first + i]["states"])  # same problems as the unsharded batch
+    assert owned == list(range(B))                                       # every problem exactly once
+    from paper_1809_06360_b200.sharded import batch_shard
+    with pytest.raises(ValueError):
+        batch_shard(7, 2, 0)
