@@ -70,13 +70,31 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 2)
       const double* right = left + vs;
       const bool has_r = i + 1 < K;
       // ---- assemble P_i = D_i - S_{i-1} X_{i-1} and [S_i' | g_i]
-      for (int idx = tid; idx < nn; idx += CHAIN_THREADS) {
-        const int r = idx / n, c = idx % n;
-        double pv = left[2 * nn + idx] + right[idx];
-        if (i > 0) pv -= Gs[idx];
-        Pm[r * ldl + c] = pv;
-        // S_i' (r, c) = Vzx0_{i+1}[c][r]: read row-major (coalesced), store transposed
-        Wm[c * ldw + r] = has_r ? right[nn + idx] : 0.0;
+      // (four elements per thread and trip, all twelve / sixteen loads issued before the
+      // stores: the value blocks stream from HBM / L2, one latency per trip)
+      for (int idx0 = tid; idx0 < nn; idx0 += 4 * CHAIN_THREADS) {
+        double vz[4], vx[4], gs[4], sv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int64_t idx = idx0 + (int64_t)e * CHAIN_THREADS;
+          const bool in = idx < nn;
+          vz[e] = in ? left[2 * nn + idx] : 0.0;
+          vx[e] = in ? right[idx] : 0.0;
+          gs[e] = (in && i > 0) ? Gs[idx] : 0.0;
+          sv[e] = (in && has_r) ? right[nn + idx] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int idx = idx0 + e * CHAIN_THREADS;
+          if (idx < nn) {
+            const int r = idx / n, c = idx % n;
+            double pv = vz[e] + vx[e];
+            if (i > 0) pv -= gs[e];
+            Pm[r * ldl + c] = pv;
+            // S_i' (r, c) = Vzx0_{i+1}[c][r]: read row-major (coalesced), store transposed
+            Wm[c * ldw + r] = sv[e];
+          }
+        }
       }
       for (int r = tid; r < n; r += CHAIN_THREADS) {
         double g = -left[3 * nn + n + r] + -right[3 * nn + r];
@@ -130,11 +148,23 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 2)
     __syncthreads();
     for (int i = K - 2; i >= 0; --i) {
       const double* Xi = Xg + (int64_t)i * nn;
-      for (int r = warp; r < n; r += CHAIN_THREADS / 32) {
-        double t = 0.0;
-        for (int c = lane; c < n; c += 32) t += Xi[r * n + c] * xa[c];
-        t = warp_sum(t);
-        if (lane == 0) xb[r] = dg[(int64_t)i * n + r] - t;
+      constexpr int NWP = CHAIN_THREADS / 32;
+      for (int r0 = warp; r0 < n; r0 += 4 * NWP) {   // four rows per trip: one latency for four rows
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int c = lane; c < n; c += 32) {
+          const double xv = xa[c];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = r0 + e * NWP;
+            t[e] += (r < n ? Xi[r * n + c] : 0.0) * xv;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = r0 + e * NWP;
+          const double ts = warp_sum(t[e]);
+          if (lane == 0 && r < n) xb[r] = dg[(int64_t)i * n + r] - ts;
+        }
       }
       __syncthreads();
       for (int r = tid; r < n; r += CHAIN_THREADS) {
@@ -164,14 +194,30 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 2)
         gv[r] = t;
       }
       __syncthreads();
-      for (int r = warp; r < n; r += CHAIN_THREADS / 32) {
-        double t = 0.0;
+      constexpr int NWP = CHAIN_THREADS / 32;
+      for (int r0 = warp; r0 < n; r0 += 4 * NWP) {
+        double tt[4] = {0.0, 0.0, 0.0, 0.0};
         for (int c = lane; c < n; c += 32) {
-          t += (left[2 * nn + r * n + c] + right[r * n + c]) * xb[c];
-          if (has_l) t += left[nn + r * n + c] * xa[c];
+          double d0[4], d1[4], d2[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {   // loads of four rows first
+            const int r = r0 + e * NWP;
+            const bool in = r < n;
+            d0[e] = in ? left[2 * nn + r * n + c] : 0.0;
+            d1[e] = in ? right[r * n + c] : 0.0;
+            d2[e] = (in && has_l) ? left[nn + r * n + c] : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            tt[e] += (d0[e] + d1[e]) * xb[c];
+            if (has_l) tt[e] += d2[e] * xa[c];
+          }
         }
-        t = warp_sum(t);
-        if (lane == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+        const int r = r0 + e * NWP;
+        const double t = warp_sum(tt[e]);
+        if (lane == 0 && r < n) {
           double g = -left[3 * nn + n + r] + -right[3 * nn + r];
           if (i == 0) {
             double s = 0.0;
@@ -179,6 +225,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 2)
             g += -s;
           }
           worst = fmax(worst, fabs(t + gv[r] - g));
+        }
         }
       }
       __syncthreads();
