@@ -454,10 +454,26 @@ __device__ __forceinline__ void small_segment(const SweepArgs& a, double* sm, in
     if (wrow) {
       const double* vr = Vxx + gt * LDN;
       double w2 = 0.0;
+      if constexpr (N % 16 == 0) {
+        // The row stride (= 4 mod 8 doubles, chosen for the DMMA fragment loads)
+        // puts lanes l and l + 4 of a plain vr[k] load on the same banks (8-way
+        // conflict).  16-byte loads starting at column pair (c - l) spread every
+        // quarter-warp over all eight 16-byte bank groups.
+        const double2* v2 = reinterpret_cast<const double2*>(vr);
+        const double2* f2 = reinterpret_cast<const double2*>(sm + S::SF1);
+#pragma unroll 8
+        for (int c = 0; c < N / 2; ++c) {
+          const int k2 = (c - gt) & (N / 2 - 1);
+          const double2 av = v2[k2], fv = f2[k2];
+          wcol += av.x * fv.x;
+          w2 += av.y * fv.y;
+        }
+      } else {
 #pragma unroll
-      for (int k = 0; k < N; k += 2) {
-        wcol += vr[k] * sm[S::SF1 + k];
-        w2 += vr[k + 1] * sm[S::SF1 + k + 1];
+        for (int k = 0; k < N; k += 2) {
+          wcol += vr[k] * sm[S::SF1 + k];
+          w2 += vr[k + 1] * sm[S::SF1 + k + 1];
+        }
       }
       wcol += w2;
     }
