@@ -1,5 +1,5 @@
 """Run the sweep phase (plq_sweep_segments) of a config a few times -- the
-command profiled by ncu (tools/r2_ncu_sweep.sh).
+command profiled by ncu (tools/r2_final.sh).
 
     python tools/run_sweep.py --config 4 --B 148 --reps 2
 """
