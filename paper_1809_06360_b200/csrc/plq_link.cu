@@ -536,22 +536,31 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
       v[r] = Ws[r * w + 2 * n] - t;
     }
   } else if (n > 64) {
-    // stage the factor (coalesced) for the blocked solve below; v by one
-    // warp per row with the lanes over the (coalesced) columns of W
+    // The factor (row stride n + 2: 16-byte rows for the bulk copies; its
+    // column reads below are at worst 4-way conflicted and every element is
+    // read once) and the diagonal-block inverses come by bulk copies issued
+    // up front, one memory latency overlapped with the v rows; v by one warp
+    // per row with the lanes over the (coalesced) columns of W
+    const int ldb = n + 2, nbk8 = (n + 7) / 8;
     double* Lsb = v + ((n + 16) & ~1);
-    // (eight loads in flight per thread: the factor comes from L2)
-    for (int idx0 = threadIdx.x; idx0 < nn; idx0 += 8 * blockDim.x) {
-      double lv[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int64_t idx = idx0 + (int64_t)e * blockDim.x;
-        lv[e] = idx < nn ? Lc[idx] : 0.0;
+    double* Lis = Lsb + (size_t)n * ldb;
+    const double* Lig = L.Linv + (b * E + o) * nbk8 * 64;
+    __shared__ __align__(8) uint64_t bbar;
+    const bool tma = (n % 2) == 0;
+    if (threadIdx.x == 0) mbar_init(&bbar, 1);
+    __syncthreads();
+    if (tma) {
+      if (threadIdx.x < 32) {
+        const int ln = threadIdx.x;
+        fence_proxy_async();
+        if (ln == 0) mbar_arrive_tx(&bbar, 8u * (uint32_t)(nn + nbk8 * 64));
+        __syncwarp();
+        for (int r = ln; r < n; r += 32) bulk_g2s(Lsb + (size_t)r * ldb, Lc + (size_t)r * n, 8u * n, &bbar);
+        if (ln == 0) bulk_g2s(Lis, Lig, 8u * nbk8 * 64, &bbar);
       }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int64_t idx = idx0 + (int64_t)e * blockDim.x;
-        if (idx < nn) Lsb[(idx / n) * (n + 1) + idx % n] = lv[e];
-      }
+    } else {
+      for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lsb[(idx / n) * ldb + idx % n] = Lc[idx];
+      for (int idx = threadIdx.x; idx < nbk8 * 64; idx += blockDim.x) Lis[idx] = Lig[idx];
     }
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     // four rows of W per warp trip (independent loads, one latency for four rows)
@@ -575,6 +584,7 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
         if (lane == 0 && r < n) v[r] = Wm[r * w + 2 * n] - ts;
       }
     }
+    if (tma) mbar_wait(&bbar, 0u);
   } else {
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
       double s = Wm[r * w + 2 * n];
@@ -606,15 +616,16 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
     // elimination: per 8-row block, warp j reduces row k0 + j over the solved
     // rows, then x_k = Linv_k' r
     const int nbk = (n + 7) / 8, lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    const double* Li = L.Linv + (b * E + o) * nbk * 64;
-    const double* Lsb = v + ((n + 16) & ~1);   // staged factor, stride n + 1
+    const int ldb = n + 2;
+    const double* Lsb = v + ((n + 16) & ~1);   // staged factor, stride n + 2
+    const double* Li = Lsb + (size_t)n * ldb;   // staged diagonal-block inverses
     double* rr = v + n;   // 8 doubles (v has n + 2 + ...)
     for (int kb = nbk - 1; kb >= 0; --kb) {
       const int k0 = kb * 8, rb = min(8, n - k0);
       for (int jj = wp; jj < rb; jj += blockDim.x >> 5) {
         const int j = k0 + jj;
         double t = 0.0;
-        for (int c = k0 + rb + lane; c < n; c += 32) t += Lsb[c * (n + 1) + j] * v[c];
+        for (int c = k0 + rb + lane; c < n; c += 32) t += Lsb[c * ldb + j] * v[c];
         t = warp_sum(t);
         if (lane == 0) rr[jj] = v[j] - t;
       }
@@ -738,7 +749,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
     const LinkLevel& C = P.lv[l + 1 < (int)P.lv.size() ? l + 1 : l];
     const size_t bsm = sizeof(double) * (p.n + 10 + (p.n <= 64 ? (size_t)p.n * (p.n + 1) + 4 + (size_t)p.n * p.n +
                                                               (size_t)p.n * (2 * p.n + 1) + 2 * p.n + 2
-                                                          : (size_t)p.n * (p.n + 1) + 8));
+                                                          : (size_t)p.n * (p.n + 2) + (size_t)((p.n + 7) / 8) * 64 + 16));
     if (bsm > 48 * 1024) cudaFuncSetAttribute(link_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     link_backsub<<<B * P.lv[l].K, threads, bsm, s>>>(p, P.lv[l], C, l + 1 < (int)P.lv.size());
     ++nl;
