@@ -662,6 +662,49 @@ __global__ void link_residual_part(plq_problem_t p, LinkLevel L, double* rpart) 
   const double* D = L.D + (b * K + i) * nn;
   const double* x = L.x + b * K * n;
   double worst = 0.0;
+  if (n > 64) {
+    // large blocks: the row products with lanes over the (coalesced) columns,
+    // four rows per warp trip; the transposed term S_i' x_{i+1} thread per
+    // column (coalesced across threads), staged in shared memory first
+    __shared__ double tr[128];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool has_l = i >= 1, has_r = i + 1 < K;
+    const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;
+    const double* Sr = has_r ? L.S + (b * (K - 1) + i) * nn : nullptr;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double t0 = 0.0, t1 = 0.0;
+      if (has_r) {
+        int c = 0;
+        for (; c + 1 < n; c += 2) {
+          t0 += Sr[c * n + r] * x[(i + 1) * n + c];
+          t1 += Sr[(c + 1) * n + r] * x[(i + 1) * n + c + 1];
+        }
+        if (c < n) t0 += Sr[c * n + r] * x[(i + 1) * n + c];
+      }
+      tr[r] = t0 + t1;
+    }
+    __syncthreads();
+    for (int r0 = wp; r0 < n; r0 += 4 * nw) {
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int c = lane; c < n; c += 32) {
+        const double xi_ = x[i * n + c], xl_ = has_l ? x[(i - 1) * n + c] : 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = r0 + e * nw;
+          if (r < n) {
+            t[e] += D[r * n + c] * xi_;
+            if (has_l) t[e] += Sl[r * n + c] * xl_;
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = r0 + e * nw;
+        const double ts = warp_sum(t[e]);
+        if (lane == 0 && r < n) worst = fmax(worst, fabs(ts + tr[r] - L.rhs[(b * K + i) * n + r]));
+      }
+    }
+  } else {
   for (int r = threadIdx.x; r < n; r += blockDim.x) {
     double s = 0.0;
     for (int c = 0; c < n; ++c) s += D[r * n + c] * x[i * n + c];
@@ -674,6 +717,7 @@ __global__ void link_residual_part(plq_problem_t p, LinkLevel L, double* rpart) 
       for (int c = 0; c < n; ++c) s += S[c * n + r] * x[(i + 1) * n + c];
     }
     worst = fmax(worst, fabs(s - L.rhs[(b * K + i) * n + r]));
+  }
   }
   worst = block_max(worst, red);
   if (threadIdx.x == 0) rpart[b * K + i] = worst;
@@ -708,7 +752,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   const int threads = link_threads(p.n);
   const unsigned B = (unsigned)p.B;
   int nl = 0;
-  link_assemble0<<<B * P.lv[0].K, threads, 0, s>>>(p, vf0, P.lv[0]);
+  link_assemble0<<<B * P.lv[0].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, vf0, P.lv[0]);
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
     const int w = 2 * p.n + 1, ldw = ((w + 3) / 8) * 8 + 4;
