@@ -291,17 +291,22 @@ __global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
 // only a few blocks (cfg3: 127, 64, ..., 1 of n = 128), so for n > 64 each
 // block's elimination runs as three kernels: the blocked Cholesky (one CTA
 // per block), the forward solve W = L^{-1}[A(i,i-1) | A(i,i+1) | b_i] in
-// column slabs (LINK_SLABS CTAs per block), and the Gram products in 64 x 64
+// column slabs (link_slabs() CTAs per block), and the Gram products in 64 x 64
 // tiles (LINK_GRAM_TILES CTAs per block).  Same arithmetic as link_eliminate.
-constexpr int LINK_SLABS = 4;        // column slabs of W (w = 2n+1 columns)
 constexpr int LINK_SLAB_LD = 76;     // widest slab: ceil(w/32)*8 <= 72 for n <= 128, stride = 4 (mod 8)
+
+// Column slabs of W (w = 2n+1 columns) per eliminated block: four CTAs while
+// the level has enough blocks to fill the GPU, eight at the deep levels (few
+// blocks: the slab solve is a latency chain of n/8 block steps whose length
+// per step is the number of 8-column tiles a warp owns)
+__host__ __device__ inline int link_slabs(int64_t blocks) { return blocks * 4 <= 74 ? 8 : 4; }
 
 __host__ __device__ inline int link_ldl_big(int n) { return n + ((12 - n % 8) % 8); }   // = 4 (mod 8)
 
-__host__ __device__ inline void link_slab(int w, int sidx, int* c0, int* c1) {
-  const int base = ((w + 31) / 32) * 8;   // multiple of 8 (72, 72, 72, 41 at n = 128)
-  *c0 = sidx * base;
-  *c1 = (sidx == LINK_SLABS - 1) ? w : (sidx + 1) * base;
+__host__ __device__ inline void link_slab(int w, int sidx, int slabs, int* c0, int* c1) {
+  const int base = ((w + 8 * slabs - 1) / (8 * slabs)) * 8;   // multiple of 8 (72 x 3 + 41 or 40 x 6 + 17 at n = 128)
+  *c0 = min(w, sidx * base);
+  *c1 = (sidx == slabs - 1) ? w : min(w, (sidx + 1) * base);
 }
 
 // Stage an n x n row-major global block into shared memory with row stride
@@ -363,13 +368,14 @@ __global__ void __launch_bounds__(256) link_trsm_big(plq_problem_t p, LinkLevel 
   extern __shared__ __align__(16) double dsm[];
   const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1, nbk = (n + 7) / 8;
   const int64_t nn = (int64_t)n * n;
-  const int64_t b = blockIdx.x / (E * LINK_SLABS);
-  const int o = (blockIdx.x / LINK_SLABS) % E;
-  const int sidx = blockIdx.x % LINK_SLABS;
+  const int slabs = link_slabs((int64_t)p.B * E);
+  const int64_t b = blockIdx.x / (E * slabs);
+  const int o = (blockIdx.x / slabs) % E;
+  const int sidx = blockIdx.x % slabs;
   if (status[b * p.J] == PLQ_STATUS_LINK_SINGULAR) return;
   const int i = L.top ? 0 : 2 * o + 1;
   int c0, c1;
-  link_slab(w, sidx, &c0, &c1);
+  link_slab(w, sidx, slabs, &c0, &c1);
   const int sw = c1 - c0;
   const bool has_l = !L.top && i >= 1, has_r = !L.top && i + 1 < K;
   const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;
@@ -773,7 +779,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
       cudaFuncSetAttribute(link_trsm_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
       if (gsm > 48 * 1024) cudaFuncSetAttribute(link_gram_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
       link_factor_big<<<B * Lv.E, 256, fsm, s>>>(p, Lv, status);
-      link_trsm_big<<<B * Lv.E * LINK_SLABS, 256, rsm, s>>>(p, Lv, status);
+      link_trsm_big<<<B * Lv.E * link_slabs((int64_t)B * Lv.E), 256, rsm, s>>>(p, Lv, status);
       nl += 2;
       if (!Lv.top) {
         link_gram_big<<<B * Lv.E * (3 * nt * nt + 1), 256, gsm, s>>>(p, Lv, status);
