@@ -333,7 +333,8 @@ __device__ __forceinline__ void stage_rows(double* dst, int ld, const double* sr
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) link_factor_big(plq_problem_t p, LinkLevel L, int32_t* status) {
+// (16 warps: the trailing update of a 128 x 128 block has up to 120 tiles per block step)
+__global__ void __launch_bounds__(512) link_factor_big(plq_problem_t p, LinkLevel L, int32_t* status) {
   __shared__ int flag;
   extern __shared__ __align__(16) double dsm[];
   __shared__ __align__(8) uint64_t bar;
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(256) link_factor_big(plq_problem_t p, LinkLeve
   __syncthreads();
   uint32_t phase = 0;
   stage_rows(Lc, ldl, D, n, nullptr, nullptr, 0, &bar, phase);
-  if (!gchol8<8>(Lc, n, ldl, Linv, &flag, threadIdx.x, [] { __syncthreads(); }, Ld)) {
+  if (!gchol8<16>(Lc, n, ldl, Linv, &flag, threadIdx.x, [] { __syncthreads(); }, Ld)) {
     flag_singular(p, status, b);
     return;
   }
@@ -778,7 +779,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
       cudaFuncSetAttribute(link_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
       cudaFuncSetAttribute(link_trsm_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
       if (gsm > 48 * 1024) cudaFuncSetAttribute(link_gram_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
-      link_factor_big<<<B * Lv.E, 256, fsm, s>>>(p, Lv, status);
+      link_factor_big<<<B * Lv.E, 512, fsm, s>>>(p, Lv, status);
       link_trsm_big<<<B * Lv.E * link_slabs((int64_t)B * Lv.E), 256, rsm, s>>>(p, Lv, status);
       nl += 2;
       if (!Lv.top) {
