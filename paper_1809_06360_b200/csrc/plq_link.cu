@@ -173,7 +173,7 @@ __host__ __device__ inline size_t link_elim_blocked_doubles(int n) { return 2 * 
 // eliminate the odd blocks of one level (or the single top block).  For
 // n <= 64 the pivot block and W live in shared memory; the factor and W are
 // written back to global once for the back-substitution.
-__global__ void link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
+__global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
   __shared__ int flag;
   extern __shared__ __align__(16) double dsm[];
   const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1;
