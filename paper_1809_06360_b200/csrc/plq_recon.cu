@@ -99,7 +99,7 @@ struct ReconSmem {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(NT) recon_kernel(ReconArgs A) {
+__global__ void __launch_bounds__(NT, (NT == 512 ? 2 : 1)) recon_kernel(ReconArgs A) {
   extern __shared__ __align__(16) double sm[];
   const plq_problem_t& p = A.p;
   const int n = p.n, m = p.m, J = p.J, T = p.T, nn = n * n;
