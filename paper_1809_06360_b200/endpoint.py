@@ -8,7 +8,8 @@ and the evaluation at concrete endpoints all run on the device
 (``csrc/plq_endpoint.cu``).  Differences a caller can observe:
 
 * ``values`` / ``constraints`` hold the t = 0 entries only (the ones
-  ``evaluate`` needs; ``values[0].const`` is not computed);
+  ``evaluate`` needs); ``values[0].const`` is taken lazily from one device
+  evaluation at a feasible endpoint pair;
 * problems whose endpoint cannot be reached in every direction (feasibility
   rows, e.g. ``T m < n``) are solved like the reference does: no multiplier
   maps, ``evaluate`` checks the rows (``Infeasible``) and takes the
@@ -33,22 +34,34 @@ from .parallel import INPUT_FIELDS, _ptr, _to_device, _torch, stack_problem
 from .problem import DEFAULT_TOLERANCES, AffinePolicy, LqrSolution
 
 
-@dataclasses.dataclass(frozen=True, eq=False, repr=False)
 class ValueFunction:
-    """endpoint.py:61-83 (``const`` not computed on the GPU path)."""
+    """endpoint.py:61-83: ``value(x, z) = 1/2 x'Vxx x + z'Vzx x + 1/2 z'Vzz z
+    + vx1'x + vz1'z + const``.  The sweep kernels do not carry ``const``;
+    it is taken on first use from one device evaluation at a feasible endpoint
+    pair (``const`` may be given as a callable returning it)."""
 
-    Vxx: np.ndarray
-    Vzx: np.ndarray
-    Vzz: np.ndarray
-    vx1: np.ndarray
-    vz1: np.ndarray
-    const: float = None
+    def __init__(self, Vxx, Vzx, Vzz, vx1, vz1, const=0.0):
+        self.Vxx, self.Vzx, self.Vzz, self.vx1, self.vz1 = Vxx, Vzx, Vzz, vx1, vz1
+        self._const = const
+
+    @property
+    def const(self):
+        if callable(self._const):
+            self._const = float(self._const())
+        return self._const
 
     def gradient_x(self, x, z):
         return self.Vxx @ x + self.Vzx.T @ z + self.vx1
 
     def gradient_z(self, x, z):
         return self.Vzx @ x + self.Vzz @ z + self.vz1
+
+    def _quadratic(self, x, z):
+        return float(0.5 * x @ (self.Vxx @ x) + z @ (self.Vzx @ x) + 0.5 * z @ (self.Vzz @ z)
+                     + self.vx1 @ x + self.vz1 @ z)
+
+    def value(self, x, z):
+        return self._quadratic(x, z) + self.const
 
 
 @dataclasses.dataclass(frozen=True, eq=False, repr=False)
@@ -232,7 +245,8 @@ class EndpointAffineSolution:
         self.policies = tuple(AffinePolicy(o["Kx"][t], o["Kz"][t], o["k1"][t]) for t in range(T))
         v = o["value0"]
         self.values = (ValueFunction(v[:nn].reshape(n, n), v[nn:2 * nn].reshape(n, n),
-                                     v[2 * nn:3 * nn].reshape(n, n), v[3 * nn:3 * nn + n], v[3 * nn + n:]),)
+                                     v[2 * nn:3 * nn].reshape(n, n), v[3 * nn:3 * nn + n], v[3 * nn + n:],
+                                     const=self._const0),)
         r = int(o["feas_rows"])
         Hf = o["feas"][:r]
         self.constraints = (ConstraintToGo(Hf[:, :n].copy(), Hf[:, n:2 * n].copy(), Hf[:, 2 * n].copy()),)
@@ -250,6 +264,30 @@ class EndpointAffineSolution:
     @property
     def feasibility(self):
         return self.constraints[0]
+
+    def _const0(self):
+        """``values[0].const`` (endpoint.py:283-284, 296): the objective of one device
+        evaluation at a feasible endpoint pair minus the value function's other terms
+        there -- (0, 0) when every endpoint is reachable, else the least-norm pair on
+        the feasibility rows."""
+        c = self.feasibility
+        n = self._batch.n
+        xz = np.zeros(2 * n)
+        if c.rows:
+            xz = np.linalg.lstsq(np.concatenate([c.Hx, c.Hz], axis=1), -c.h1, rcond=None)[0]
+        x, z = xz[:n], xz[n:]
+        return self._objective_at(x, z) - self.values[0]._quadratic(x, z)
+
+    def _objective_at(self, x_init, x_term):
+        torch = self._batch.torch
+        B, n, dev = self._batch.B, self._batch.n, self._batch.device
+        xi = torch.zeros((B, n), dtype=torch.float64, device=dev)
+        xt = torch.zeros((B, n), dtype=torch.float64, device=dev)
+        xi[self._index] = torch.from_numpy(np.asarray(x_init, dtype=np.float64))
+        xt[self._index] = torch.from_numpy(np.asarray(x_term, dtype=np.float64))
+        with torch.cuda.device(dev):
+            pt = self._batch.evaluate(xt, xi)
+        return float(pt["objective"][self._index].cpu())
 
     def feasibility_residual(self, x_init, x_term):
         res = self.feasibility.residual(np.asarray(x_init, float), np.asarray(x_term, float))

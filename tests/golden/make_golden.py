@@ -200,6 +200,7 @@ def endpoint_case(a, seed):
         "Kx": np.stack([p.Kx for p in aff.policies]), "Kz": np.stack([p.Kz for p in aff.policies]),
         "k1": np.stack([p.k1 for p in aff.policies]),
         "Vxx0": v0.Vxx, "Vzx0": v0.Vzx, "Vzz0": v0.Vzz, "vx10": v0.vx1, "vz10": v0.vz1,
+        "const0": np.float64(v0.const),
         "X": np.concatenate([mp.Ra, mp.Rz, mp.r1[:, :, None]], axis=2),
         "S": np.concatenate([mp.Sa, mp.Sz, mp.s1[:, :, None]], axis=2),
         "Lam": np.concatenate([mm.La, mm.Lz, mm.l1[:, :, None]], axis=2),
@@ -264,6 +265,7 @@ def endpoint_unreachable_goldens():
             "Kx": np.stack([p.Kx for p in aff.policies]), "Kz": np.stack([p.Kz for p in aff.policies]),
             "k1": np.stack([p.k1 for p in aff.policies]),
             "Vxx0": v0.Vxx, "Vzx0": v0.Vzx, "Vzz0": v0.Vzz, "vx10": v0.vx1, "vz10": v0.vz1,
+            "const0": np.float64(v0.const),
             "X": np.concatenate([mp.Ra, mp.Rz, mp.r1[:, :, None]], axis=2),
             "S": np.concatenate([mp.Sa, mp.Sz, mp.s1[:, :, None]], axis=2),
             "feas_rows": np.int64(aff.feasibility.rows),

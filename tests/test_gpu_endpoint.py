@@ -260,3 +260,28 @@ def test_endpoint_collect_diagnostics():
     for t in (0, len(aff.policies) - 1):
         assert rel_err(aff.policies[t].Kx, base.policies[t].Kx) <= 1e-8
     assert rel_err(aff.maps.Ra, base.maps.Ra) <= 1e-8
+
+
+def test_initial_value_constant_and_objective_identity():
+    """``values[0].const`` (endpoint.py:283-284, 296) against the reference's own
+    goldens -- reachable problems (taken at the pair (0, 0)) and problems with
+    feasibility rows (least-norm pair on the rows) -- and test_endpoint.py:223-231
+    restated: the objective at a reachable endpoint equals ``values[0].value``."""
+    import paper_1809_06360_b200 as plq
+    for name in ("endpoint_small", "endpoint_unreachable"):
+        z = np.load(os.path.join(GOLDEN, name + ".npz"))
+        for i in range(int(z["num"])):
+            a = {k.split("/")[-1]: z[k] for k in z.files if k.startswith(f"{i}/in/")}
+            o = {k.split("/")[-1]: z[k] for k in z.files if k.startswith(f"{i}/out/")}
+            prob = plq.problem_from_arrays(a)
+            aff = plq.solve_endpoint_affine(prob)
+            v0 = aff.values[0]
+            sc = _scale(a)
+            for k, mine in (("Vxx0", v0.Vxx), ("Vzx0", v0.Vzx), ("Vzz0", v0.Vzz), ("vx10", v0.vx1), ("vz10", v0.vz1)):
+                assert rel_err(mine, o[k]) <= 1e-8 * sc, (name, i, k, rel_err(mine, o[k]))
+            quad = abs(float(o["objective"])) + abs(float(o["const0"])) + 1.0
+            assert abs(v0.const - float(o["const0"])) <= 1e-8 * sc * quad, (name, i, v0.const, float(o["const0"]))
+            sol = aff.evaluate(a["x_init"], o["x_term"])
+            val = v0.value(a["x_init"], o["x_term"])
+            assert sol.objective == pytest.approx(val, rel=1e-8 * sc, abs=1e-8 * sc * (1 + abs(val)))
+            assert val == pytest.approx(float(o["objective"]), rel=1e-8 * sc, abs=1e-8 * sc * (1 + abs(val)))
