@@ -20,6 +20,7 @@
 #include "plq_internal.h"
 #include "plq_tma.cuh"
 
+#include <cstdlib>
 #include <vector>
 
 namespace plq {
@@ -173,14 +174,53 @@ __host__ __device__ inline size_t link_elim_blocked_doubles(int n) { return 2 * 
 // eliminate the odd blocks of one level (or the single top block).  For
 // n <= 64 the pivot block and W live in shared memory; the factor and W are
 // written back to global once for the back-substitution.
-__global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLevel L, int32_t* status) {
+//
+// FUSED (levels >= 1, n <= 64): the level's system is not assembled by a
+// separate launch.  The grid has one CTA per block of the level: CTA k builds
+// block k from the previous level's even block 2k and its eliminated
+// neighbours' Schur terms (D = D'_{2k} - CR'_{k-1} - CL'_k, A(k+1,k) = -X'_k,
+// rhs likewise) -- kept (even) blocks are written out for the next level and
+// the CTA exits, odd blocks (and the top block) are assembled straight into
+// the factor / W buffers and eliminated.  One launch and one ~12 us
+// dependent-latency step less per level; the S blocks of levels >= 1 are
+// never materialized (only odd blocks read them).
+template <bool FUSED>
+__global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLevel L, LinkLevel Pv, int32_t* status) {
   __shared__ int flag;
   extern __shared__ __align__(16) double dsm[];
   const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1;
   const int64_t nn = (int64_t)n * n;
-  const int64_t b = blockIdx.x / E;
-  const int o = blockIdx.x % E;
-  const int i = L.top ? 0 : 2 * o + 1;
+  const int per = FUSED ? K : E;
+  const int64_t b = blockIdx.x / per;
+  const int kb = blockIdx.x % per;
+  const int o = FUSED ? kb / 2 : kb;
+  const int i = L.top ? 0 : (FUSED ? kb : 2 * o + 1);
+  // previous level's pieces of block i (FUSED)
+  const int Kp = Pv.K, Ep = Pv.E;
+  const bool pl = FUSED && i >= 1, pr = FUSED && 2 * i + 1 < Kp;
+  const double* pD = FUSED ? Pv.D + (b * Kp + 2 * i) * nn : nullptr;
+  const double* pCR = pl ? Pv.CR + (b * Ep + (i - 1)) * nn : nullptr;
+  const double* pCL = pr ? Pv.CL + (b * Ep + i) * nn : nullptr;
+  const double* prh = FUSED ? Pv.rhs + (b * Kp + 2 * i) * n : nullptr;
+  const double* pcR = pl ? Pv.cR + (b * Ep + (i - 1)) * n : nullptr;
+  const double* pcL = pr ? Pv.cL + (b * Ep + i) * n : nullptr;
+  if (FUSED && !L.top && (kb & 1) == 0) {
+    // kept block: next level's input
+    double* Dn = L.D + (b * K + i) * nn;
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+      double v = pD[idx];
+      if (pl) v -= pCR[idx];
+      if (pr) v -= pCL[idx];
+      Dn[idx] = v;
+    }
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double v = prh[r];
+      if (pl) v -= pcR[r];
+      if (pr) v -= pcL[r];
+      L.rhs[(b * K + i) * n + r] = v;
+    }
+    return;
+  }
   const bool sm = n <= 64;     // factor and right-hand sides on chip
   const bool lsm = n <= 128;   // the factor on chip (n <= 128: 132 KB), W in L2
   const int ldl = lsm ? n + 1 : n;
@@ -190,11 +230,13 @@ __global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLe
   double* Lc = lsm ? dsm : gLc;
   double* Wm = sm ? dsm + n * ldl : gWm;
   double* tiles = sm ? nullptr : dsm + (lsm ? ((n * ldl + 1) & ~1) : 0);
-  const double* D = L.D + (b * K + i) * nn;
+  const double* D = FUSED ? pD : L.D + (b * K + i) * nn;
   const bool has_l = i >= 1, has_r = i + 1 < K;
-  const double* Sl = has_l ? L.S + (b * (K - 1) + (i - 1)) * nn : nullptr;   // A(i,i-1)
-  const double* Sr = has_r ? L.S + (b * (K - 1) + i) * nn : nullptr;         // A(i+1,i) -> A(i,i+1) = Sr'
-  const double* rh = L.rhs + (b * K + i) * n;
+  // A(i,i-1) and A(i+1,i) (A(i,i+1) = Sr'); FUSED: minus the previous level's X blocks
+  const double* Sl = has_l ? (FUSED ? Pv.X + (b * Ep + (i - 1)) * nn : L.S + (b * (K - 1) + (i - 1)) * nn) : nullptr;
+  const double* Sr = has_r ? (FUSED ? Pv.X + (b * Ep + i) * nn : L.S + (b * (K - 1) + i) * nn) : nullptr;
+  const double* rh = FUSED ? prh : L.rhs + (b * K + i) * n;
+  const double ssign = FUSED ? -1.0 : 1.0;
   if (sm) {
     // bulk-stage D, S_l, S_r, rhs behind the factor / W buffers, assemble in smem
     __shared__ __align__(8) uint64_t bar;
@@ -208,16 +250,24 @@ __global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLe
     if (has_r) bs.add(st + 2 * nn, Sr, (int)nn);
     bs.add(st + 3 * nn, rh, n);
     bulk_stage(bs, &bar, phase);
-    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) Lc[(idx / n) * ldl + idx % n] = st[idx];
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+      double v = st[idx];
+      if (pl) v -= pCR[idx];
+      if (pr) v -= pCL[idx];
+      Lc[(idx / n) * ldl + idx % n] = v;
+    }
     for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) {
       const int r = idx / w, c = idx % w;
       double v;
       if (c < n)
-        v = has_l ? st[nn + r * n + c] : 0.0;
+        v = has_l ? ssign * st[nn + r * n + c] : 0.0;
       else if (c < 2 * n)
-        v = has_r ? st[2 * nn + (c - n) * n + r] : 0.0;
-      else
+        v = has_r ? ssign * st[2 * nn + (c - n) * n + r] : 0.0;
+      else {
         v = st[3 * nn + r];
+        if (pl) v -= pcR[r];
+        if (pr) v -= pcL[r];
+      }
       Wm[r * ldw + c] = v;
     }
   } else {
@@ -759,6 +809,12 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   const int threads = link_threads(p.n);
   const unsigned B = (unsigned)p.B;
   int nl = 0;
+  // n <= 64: levels >= 1 assemble their own blocks inside the elimination (PLQ_LINK_FUSE=0: separate launches)
+  static const bool fuse_env = [] {
+    const char* e = getenv("PLQ_LINK_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  const bool fuse = fuse_env && p.n <= 64;
   link_assemble0<<<B * P.lv[0].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, vf0, P.lv[0]);
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
@@ -787,11 +843,18 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
         ++nl;
       }
     } else {
-      if (tsm > 48 * 1024) cudaFuncSetAttribute(link_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-      link_eliminate<<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], status);
+      if (l > 0 && fuse) {
+        if (tsm > 48 * 1024)
+          cudaFuncSetAttribute(link_eliminate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        link_eliminate<true><<<B * P.lv[l].K, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l - 1], status);
+      } else {
+        if (tsm > 48 * 1024)
+          cudaFuncSetAttribute(link_eliminate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        link_eliminate<false><<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l], status);
+      }
       ++nl;
     }
-    if (!P.lv[l].top) {
+    if (!P.lv[l].top && !fuse) {
       link_assemble_next<<<B * P.lv[l + 1].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, P.lv[l], P.lv[l + 1]);
       ++nl;
     }
