@@ -132,11 +132,12 @@ __device__ __forceinline__ void bulk_stage(BulkSet& bs, uint64_t* bar, uint32_t&
 // level-0 system from the segment-start value blocks (parallel.py:286-319):
 // D_i = Vzz0_i + Vxx0_{i+1},  A(i+1,i) = Vzx0_{i+1},
 // b_i = -vz1_i - vx1_{i+1} (- Vzx0_0 x_init for i = 0).
-__global__ void link_assemble0(plq_problem_t p, const double* vf0, LinkLevel L) {
+__global__ void link_assemble0(plq_problem_t p, const double* vf0, LinkLevel L, double* link_residual) {
   const int n = p.n, J = p.J, K = L.K;
   const int64_t nn = (int64_t)n * n, vsz = 3 * nn + 2 * n;
   const int64_t b = blockIdx.x / K;
   const int i = blockIdx.x % K;
+  if (i == 0 && threadIdx.x == 0) link_residual[b] = 0.0;   // link_residual_part accumulates the maximum
   const double* left = vf0 + (b * J + i) * vsz;
   const double* right = vf0 + (b * J + i + 1) * vsz;
   double* D = L.D + (b * K + i) * nn;
@@ -308,7 +309,25 @@ __global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLe
     for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) gLc[idx] = Lc[(idx / n) * ldl + idx % n];
   if (sm)
     for (int idx = threadIdx.x; idx < n * w; idx += blockDim.x) gWm[idx] = Wm[(idx / w) * ldw + idx % w];
-  if (L.top) return;
+  if (L.top) {
+    // top block: nothing left to couple to -- finish x = L^{-T} W_b here
+    // (n <= 64: the factor and W are on chip), no back-substitution launch
+    if (sm) {
+      double* v = dsm + ((n * ldl + n * ldw + 1) & ~1);   // staging area, dead
+      __syncthreads();
+      for (int r = threadIdx.x; r < n; r += blockDim.x) v[r] = Wm[r * ldw + 2 * n];
+      __syncthreads();
+      for (int r = n - 1; r >= 0; --r) {
+        if (threadIdx.x == 0) v[r] /= Lc[r * ldl + r];
+        __syncthreads();
+        const double xr_ = v[r];
+        for (int k = threadIdx.x; k < r; k += blockDim.x) v[k] -= Lc[r * ldl + k] * xr_;
+        __syncthreads();
+      }
+      for (int r = threadIdx.x; r < n; r += blockDim.x) L.x[b * K * n + r] = v[r];
+    }
+    return;
+  }
   double* CL = L.CL + (b * E + o) * nn;
   double* CR = L.CR + (b * E + o) * nn;
   double* X = L.X + (b * E + o) * nn;
@@ -709,8 +728,11 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
   for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = v[r];
 }
 
-// residual of the level-0 equations at the solved links (parallel.py:273-282)
-__global__ void link_residual_part(plq_problem_t p, LinkLevel L, double* rpart) {
+// residual of the level-0 equations at the solved links (parallel.py:273-282):
+// CTA i takes block row i, copies x_i out as link i and folds its maximum into
+// link_residual[b] (zeroed by link_assemble0; the maximum of non-negative
+// doubles = the maximum of their bit patterns, exact in any order)
+__global__ void link_residual_part(plq_problem_t p, LinkLevel L, double* links, double* link_residual) {
   __shared__ double red[32];
   const int n = p.n, K = L.K;
   const int64_t nn = (int64_t)n * n;
@@ -776,20 +798,10 @@ __global__ void link_residual_part(plq_problem_t p, LinkLevel L, double* rpart) 
     worst = fmax(worst, fabs(s - L.rhs[(b * K + i) * n + r]));
   }
   }
+  for (int r = threadIdx.x; r < n; r += blockDim.x) links[(b * K + i) * n + r] = x[i * n + r];
   worst = block_max(worst, red);
-  if (threadIdx.x == 0) rpart[b * K + i] = worst;
-}
-
-__global__ void link_residual_reduce(plq_problem_t p, const double* rpart, const double* x0, double* links,
-                                     double* link_residual) {
-  __shared__ double red[32];
-  const int64_t b = blockIdx.x;
-  const int K = p.J - 1, n = p.n;
-  for (int64_t idx = threadIdx.x; idx < (int64_t)K * n; idx += blockDim.x) links[b * K * n + idx] = x0[b * K * n + idx];
-  double w = 0.0;
-  for (int i = threadIdx.x; i < K; i += blockDim.x) w = fmax(w, rpart[b * K + i]);
-  w = block_max(w, red);
-  if (threadIdx.x == 0) link_residual[b] = w;
+  if (threadIdx.x == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(link_residual + b), (unsigned long long)__double_as_longlong(worst));
 }
 
 int link_threads(int n) {
@@ -815,7 +827,7 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
     return !(e && e[0] == '0');
   }();
   const bool fuse = fuse_env && p.n <= 64;
-  link_assemble0<<<B * P.lv[0].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, vf0, P.lv[0]);
+  link_assemble0<<<B * P.lv[0].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, vf0, P.lv[0], link_residual);
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
     const int w = 2 * p.n + 1, ldw = ((w + 3) / 8) * 8 + 4;
@@ -865,12 +877,12 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
                                                               (size_t)p.n * (2 * p.n + 1) + 2 * p.n + 2
                                                           : (size_t)p.n * (p.n + 2) + (size_t)((p.n + 7) / 8) * 64 + 16));
     if (bsm > 48 * 1024) cudaFuncSetAttribute(link_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+    if (P.lv[l].top && p.n <= 64) continue;   // solved inside the top elimination
     link_backsub<<<B * P.lv[l].K, threads, bsm, s>>>(p, P.lv[l], C, l + 1 < (int)P.lv.size());
     ++nl;
   }
-  link_residual_part<<<B * P.lv[0].K, threads, 0, s>>>(p, P.lv[0], P.rpart);
-  link_residual_reduce<<<B, 1024, 0, s>>>(p, P.rpart, P.lv[0].x, links, link_residual);
-  nl += 2;
+  link_residual_part<<<B * P.lv[0].K, threads, 0, s>>>(p, P.lv[0], links, link_residual);
+  ++nl;
   if (launches) *launches += nl;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -44,7 +44,15 @@ __global__ void __launch_bounds__(LF_NT) link_feas_kernel(LinkFeasArgs a) {
   for (int64_t base = (int64_t)blockIdx.x * LF_NT; base < p.B; base += (int64_t)gridDim.x * LF_NT) {
     if (tid == 0) cnt = 0;
     __syncthreads();
-    {
+    if (J >= 128) {
+      // long chains (few problems): a warp sums one problem's row counts
+      for (int q = warp; q < LF_NT && base + q < p.B; q += LF_NT / 32) {
+        int R = 0;
+        for (int j = lane; j < J; j += 32) R += a.feas_rows[(base + q) * J + j];
+        R = __reduce_add_sync(0xffffffffu, R);
+        if (lane == 0 && R > 0) list[atomicAdd(&cnt, 1)] = q;
+      }
+    } else {
       const int64_t bt = base + tid;
       int R = 0;
       if (bt < p.B)
