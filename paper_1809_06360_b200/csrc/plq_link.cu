@@ -822,11 +822,8 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   const unsigned B = (unsigned)p.B;
   int nl = 0;
   // n <= 64: levels >= 1 assemble their own blocks inside the elimination (PLQ_LINK_FUSE=0: separate launches)
-  static const bool fuse_env = [] {
-    const char* e = getenv("PLQ_LINK_FUSE");
-    return !(e && e[0] == '0');
-  }();
-  const bool fuse = fuse_env && p.n <= 64;
+  const char* fe = getenv("PLQ_LINK_FUSE");
+  const bool fuse = !(fe && fe[0] == '0') && p.n <= 64;
   link_assemble0<<<B * P.lv[0].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, vf0, P.lv[0], link_residual);
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {

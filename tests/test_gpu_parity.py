@@ -451,6 +451,32 @@ def test_chain_link_solve_equals_cyclic_reduction(n, m, T, J, B, monkeypatch):
     assert rel_err(s.out["links"][0].cpu().numpy(), outs["chain"]["links"][0]) == 0.0
 
 
+@pytest.mark.parametrize("n,m,T,J,B", [(32, 8, 192, 24, 2), (64, 32, 72, 9, 2), (20, 6, 85, 17, 3), (12, 4, 130, 65, 2),
+                                       (32, 8, 16, 2, 2), (24, 6, 24, 3, 2)])
+def test_cyclic_reduction_fused_levels_bitwise(n, m, T, J, B, monkeypatch):
+    """Block cyclic reduction with the levels' assembly fused into the elimination
+    launch (one CTA per block of the level, plq_link.cu) does the same arithmetic in
+    the same order as the separate assembly launches (PLQ_LINK_FUSE=0): links and
+    link residuals bitwise equal, fewer launches, and both within the parity gate
+    of the oracle (parallel.py:264-319, endpoint.py:410-438).  Odd and even block
+    counts at several depths, the two-segment (single top block) case included."""
+    from paper_1809_06360_b200 import synth
+    cfg = synth.Config(f"bcr_n{n}", B, n, m, T, J, cross=0.3)
+    batch = synth.generate_batch(cfg, seed=23, count=B)
+    monkeypatch.setenv("PLQ_LINK", "bcr")
+    outs, launches = {}, {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PLQ_LINK_FUSE", mode)
+        outs[mode], s = _gpu_batch(batch, J=J)
+        launches[mode] = s.launches
+    for k in ("links", "link_residual", "x", "u", "lam", "objective"):
+        assert np.array_equal(outs["0"][k], outs["1"][k]), k
+    if J > 2:
+        assert launches["1"] < launches["0"]
+    ref = O.solve(O.problem_slice(batch, B - 1), J=J)
+    assert rel_err(outs["1"]["links"][B - 1], ref["links"]) <= 1e-7
+
+
 @pytest.mark.parametrize("cfg_id,T,J", [(1, 64, 8), (2, 128, 4), (4, 64, 2), (0, 40, 4)])
 def test_collect_diagnostics(cfg_id, T, J):
     """collect_diagnostics=True (endpoint.py:258-299, parallel.py:239, 549): the
