@@ -451,7 +451,7 @@ def test_chain_link_solve_equals_cyclic_reduction(n, m, T, J, B, monkeypatch):
     assert rel_err(s.out["links"][0].cpu().numpy(), outs["chain"]["links"][0]) == 0.0
 
 
-@pytest.mark.parametrize("n,m,T,J,B", [(32, 8, 192, 24, 2), (64, 32, 72, 9, 2), (20, 6, 85, 17, 3), (12, 4, 130, 65, 2),
+@pytest.mark.parametrize("n,m,T,J,B", [(32, 8, 192, 24, 2), (64, 32, 72, 9, 2), (20, 6, 85, 17, 3), (12, 4, 260, 65, 2),
                                        (32, 8, 16, 2, 2), (24, 6, 24, 3, 2)])
 def test_cyclic_reduction_fused_levels_bitwise(n, m, T, J, B, monkeypatch):
     """Block cyclic reduction with the levels' assembly fused into the elimination
@@ -473,8 +473,10 @@ def test_cyclic_reduction_fused_levels_bitwise(n, m, T, J, B, monkeypatch):
         assert np.array_equal(outs["0"][k], outs["1"][k]), k
     if J > 2:
         assert launches["1"] < launches["0"]
-    ref = O.solve(O.problem_slice(batch, B - 1), J=J)
-    assert rel_err(outs["1"]["links"][B - 1], ref["links"]) <= 1e-7
+    prob = O.problem_slice(batch, B - 1)
+    ref = O.solve(prob, J=J)
+    gate = max(1e-9, 10 * _floor(prob, J, ref)["links"])
+    assert rel_err(outs["1"]["links"][B - 1], ref["links"]) <= gate
 
 
 @pytest.mark.parametrize("cfg_id,T,J", [(1, 64, 8), (2, 128, 4), (4, 64, 2), (0, 40, 4)])
