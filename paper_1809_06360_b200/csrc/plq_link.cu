@@ -186,7 +186,8 @@ __host__ __device__ inline size_t link_elim_blocked_doubles(int n) { return 2 * 
 // dependent-latency step less per level; the S blocks of levels >= 1 are
 // never materialized (only odd blocks read them).
 template <bool FUSED>
-__global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLevel L, LinkLevel Pv, int32_t* status) {
+__global__ void __launch_bounds__(256, 2)
+    link_eliminate(plq_problem_t p, LinkLevel L, LinkLevel Pv, int32_t* status, int fused_solve) {
   __shared__ int flag;
   extern __shared__ __align__(16) double dsm[];
   const int n = p.n, K = L.K, E = L.E, w = 2 * n + 1;
@@ -293,13 +294,19 @@ __global__ void __launch_bounds__(256, 2) link_eliminate(plq_problem_t p, LinkLe
   double* bsc = dsm + link_elim_blocked_off(n, sm, lsm, ldl, ldw, blockDim.x);
   auto csync = [] { __syncthreads(); };
   const int nbk = (n + 7) / 8;
-  const bool ok = blocked ? gchol8<8>(Lc, n, ldl, bsc, &flag, threadIdx.x, csync, bsc + nbk * 64)
+  // W on chip: the forward solve W <- L^{-1} W rides in the factorization's
+  // trailing phases (block row k of W next to step k's Schur tiles: n/8
+  // group barriers less than a separate gtrsm8)
+  const bool fsolve = blocked && sm && fused_solve;
+  const bool ok = blocked ? gchol8<8>(Lc, n, ldl, bsc, &flag, threadIdx.x, csync, bsc + nbk * 64,
+                                      fsolve ? Wm : nullptr, w, ldw, bsc + 2 * nbk * 64)
                           : cta_cholesky(Lc, n, ldl, &flag);
   if (!ok) {
     flag_singular(p, status, b);
     return;
   }
-  if (blocked)
+  if (fsolve) {
+  } else if (blocked)
     gtrsm8<0, 8>(Lc, n, ldl, bsc, Wm, w, ldw, bsc + 2 * nbk * 64, threadIdx.x, csync);
   else if (n >= 16)
     cta_trsm_lower_blocked(Lc, n, ldl, Wm, w, ldw);
@@ -824,6 +831,8 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
   // n <= 64: levels >= 1 assemble their own blocks inside the elimination (PLQ_LINK_FUSE=0: separate launches)
   const char* fe = getenv("PLQ_LINK_FUSE");
   const bool fuse = !(fe && fe[0] == '0') && p.n <= 64;
+  const char* fs = getenv("PLQ_LINK_FSOLVE");   // 0: separate forward solve after the factorization (measurement)
+  const int fsolve = !(fs && fs[0] == '0');
   link_assemble0<<<B * P.lv[0].K, p.n > 64 ? 1024 : threads, 0, s>>>(p, vf0, P.lv[0], link_residual);
   ++nl;
   for (size_t l = 0; l < P.lv.size(); ++l) {
@@ -855,11 +864,11 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
       if (l > 0 && fuse) {
         if (tsm > 48 * 1024)
           cudaFuncSetAttribute(link_eliminate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-        link_eliminate<true><<<B * P.lv[l].K, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l - 1], status);
+        link_eliminate<true><<<B * P.lv[l].K, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l - 1], status, fsolve);
       } else {
         if (tsm > 48 * 1024)
           cudaFuncSetAttribute(link_eliminate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-        link_eliminate<false><<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l], status);
+        link_eliminate<false><<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l], status, fsolve);
       }
       ++nl;
     }
