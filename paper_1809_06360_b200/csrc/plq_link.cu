@@ -185,8 +185,11 @@ __host__ __device__ inline size_t link_elim_blocked_doubles(int n) { return 2 * 
 // the factor / W buffers and eliminated.  One launch and one ~12 us
 // dependent-latency step less per level; the S blocks of levels >= 1 are
 // never materialized (only odd blocks read them).
-template <bool FUSED>
-__global__ void __launch_bounds__(256, 2)
+// MINB: resident CTAs per SM the register allocation is bounded for -- 2 (128
+// registers) for the wide levels, 1 (no cap) for levels with at most one CTA
+// per SM anyway.
+template <bool FUSED, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     link_eliminate(plq_problem_t p, LinkLevel L, LinkLevel Pv, int32_t* status, int fused_solve) {
   __shared__ int flag;
   extern __shared__ __align__(16) double dsm[];
@@ -861,15 +864,13 @@ int launch_link_solve(const plq_problem_t& p, const double* vf0, double* links, 
         ++nl;
       }
     } else {
-      if (l > 0 && fuse) {
-        if (tsm > 48 * 1024)
-          cudaFuncSetAttribute(link_eliminate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-        link_eliminate<true><<<B * P.lv[l].K, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l - 1], status, fsolve);
-      } else {
-        if (tsm > 48 * 1024)
-          cudaFuncSetAttribute(link_eliminate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-        link_eliminate<false><<<B * P.lv[l].E, ethreads, tsm, s>>>(p, P.lv[l], P.lv[l], status, fsolve);
-      }
+      const bool fl = l > 0 && fuse;
+      const unsigned grid = B * (unsigned)(fl ? P.lv[l].K : P.lv[l].E);
+      const bool deep = grid <= 148;   // one CTA per SM at most: no register cap
+      auto kern = fl ? (deep ? link_eliminate<true, 1> : link_eliminate<true, 2>)
+                     : (deep ? link_eliminate<false, 1> : link_eliminate<false, 2>);
+      if (tsm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      kern<<<grid, ethreads, tsm, s>>>(p, P.lv[l], fl ? P.lv[l - 1] : P.lv[l], status, fsolve);
       ++nl;
     }
     if (!P.lv[l].top && !fuse) {
