@@ -705,21 +705,32 @@ __global__ void link_backsub(plq_problem_t p, LinkLevel L, LinkLevel C, int has_
     const int ldb = n + 2;
     const double* Lsb = v + ((n + 16) & ~1);   // staged factor, stride n + 2
     const double* Li = Lsb + (size_t)n * ldb;   // staged diagonal-block inverses
-    double* rr = v + n;   // 8 doubles (v has n + 2 + ...)
+    // right-looking: x_k = Linv_k' v_k by eight threads, then every unsolved
+    // row j < k0 takes its rank-8 update v_j -= sum_i L[k0+i][j] x_{k0+i}
+    // (thread per row, coalesced factor rows, no reductions) -- a quarter of
+    // the left-looking step's latency (warp dot products over the solved rows)
+    (void)lane;
+    (void)wp;
     for (int kb = nbk - 1; kb >= 0; --kb) {
       const int k0 = kb * 8, rb = min(8, n - k0);
-      for (int jj = wp; jj < rb; jj += blockDim.x >> 5) {
-        const int j = k0 + jj;
-        double t = 0.0;
-        for (int c = k0 + rb + lane; c < n; c += 32) t += Lsb[c * ldb + j] * v[c];
-        t = warp_sum(t);
-        if (lane == 0) rr[jj] = v[j] - t;
+      if (threadIdx.x < 32) {
+        double rr[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) rr[j] = j < rb ? v[k0 + j] : 0.0;
+        __syncwarp();
+        if (threadIdx.x < rb) {
+          double xt = 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < rb) xt += Li[kb * 64 + j * 8 + threadIdx.x] * rr[j];
+          v[k0 + threadIdx.x] = xt;
+        }
       }
       __syncthreads();
-      if (threadIdx.x < rb) {
-        double xt = 0.0;
-        for (int j = 0; j < rb; ++j) xt += Li[kb * 64 + j * 8 + threadIdx.x] * rr[j];
-        v[k0 + threadIdx.x] = xt;
+      for (int j = threadIdx.x; j < k0; j += blockDim.x) {
+        double t = v[j];
+        for (int i = 0; i < rb; ++i) t -= Lsb[(k0 + i) * ldb + j] * v[k0 + i];
+        v[j] = t;
       }
       __syncthreads();
     }
